@@ -1,0 +1,69 @@
+"""Seeded synthetic inputs and workload shapes (shared by oracle tests and the CUDA path).
+
+This module holds NO method arithmetic: only the configuration table of
+BASELINE.json (C0-C4) and the seeded random draws of
+DESIGN.md reading R11 (numpy PCG64, ``default_rng(seed)``; lam drawn first,
+uniform [0.9, 1.1]; then the right-hand side, uniform (-1, 1); for C1 then x
+and u the same way).  All arrays are fp64, layer-major ``[nz][n]``.
+
+The paper's own workload (81,920 cells = ref 6 x 64 layers) is a
+synthetic gravity-wave step whose right-hand side it does not print; no public
+dataset is involved.  White-noise right-hand sides excite every mode.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def ncells(ref: int) -> int:
+    """Icosahedral cells at refinement ``ref``: 20 * 4**ref."""
+    return 20 * 4 ** ref
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    fine_ref: int
+    coarsest_ref: int
+    nz: int
+    thickness: float
+    w2: float
+    seed: int = 0
+
+    @property
+    def n(self) -> int:
+        return ncells(self.fine_ref)
+
+    @property
+    def ndofs(self) -> int:
+        return self.n * self.nz
+
+
+# BASELINE.json configs; C2 carries the three anisotropy settings.
+CONFIGS = {
+    "C0": Config("C0", 2, 0, 8, 0.01, 1e-4),
+    "C1": Config("C1", 5, 4, 64, 0.01, 1e-4),
+    "C2a": Config("C2a", 7, 0, 64, 0.01, 1e-4),
+    "C2b": Config("C2b", 7, 0, 64, 0.001, 1e-5),
+    "C2c": Config("C2c", 7, 0, 64, 1e-4, 1e-6),
+    "C4": Config("C4", 8, 0, 128, 0.001, 1e-5),
+}
+
+
+def make_inputs(cfg: Config, seed: int | None = None, extra: int = 0):
+    """Return (lam, b, *extras): lam ~ U[0.9,1.1], b ~ U(-1,1), then ``extra``
+    more U(-1,1) vectors (C1 uses 2: x, u).  Shapes [nz][n], fp64."""
+    rng = np.random.default_rng(cfg.seed if seed is None else seed)
+    shape = (cfg.nz, cfg.n)
+    lam = rng.uniform(0.9, 1.1, shape)
+    out = [lam, rng.uniform(-1.0, 1.0, shape)]
+    for _ in range(extra):
+        out.append(rng.uniform(-1.0, 1.0, shape))
+    return tuple(out)
+
+
+def uniform_vector(shape, seed: int) -> np.ndarray:
+    """An extra seeded U(-1,1) vector (test vectors, not part of a config)."""
+    return np.random.default_rng(seed).uniform(-1.0, 1.0, shape)
