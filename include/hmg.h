@@ -1,0 +1,167 @@
+/*
+ * hmg.h -- C-ABI of the B200-native tensor-product multigrid Helmholtz solver
+ * (hot path of arXiv:1605.00492, Mitchell & Mueller).
+ *
+ * Problem (Eq. 8 and P:626): solve  H^ P = R  for the DG0 pressure
+ * P on an extruded icosahedral prism mesh of a thin spherical shell, with
+ *   H^ = M3 + w_c^2 (Dh Minv_h Dh^T + Dz Minv_z Dz^T / (1 + w_N^2))
+ * assembled with lumped two-point couplings (readings R1-R4):
+ *   vertical   coupling  w2 * area * lamf / dz
+ *   horizontal coupling  w2 * edge_len * dz * lamf / centroid_dist
+ *   diagonal             prism volume + sum of couplings
+ * by CG preconditioned with the tensor-product multigrid V-cycle of
+ * Alg. 1 and Sec. 4.2.1: damped vertical line-Jacobi
+ * smoother (Eq. 10/13), horizontal-only coarsening down the
+ * icosahedral hierarchy (MeshHierarchy) with 4-child sum
+ * restriction and injection prolongation.
+ *
+ * Conventions for every entry point
+ *  - Return value: hmg_status; HMG_OK = 0.  On error a message naming the
+ *    offending argument (or the singular column) is available from
+ *    hmg_last_error() (thread-local, valid until the next call on the thread).
+ *  - Vectors are fp64, LAYER-MAJOR [nlayers][ld] (cells contiguous within a
+ *    layer), where ld is the level's leading dimension from hmg_level_info
+ *    (ld = number of cells rounded up to a multiple of 32).  Entries with
+ *    cell index >= ncells are padding: never read, never written.
+ *  - Device pointers (everything except *_host arguments) are caller-owned
+ *    CUDA device memory on the hierarchy's device; host pointers are plain
+ *    host memory.  The library never frees caller memory.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Calls enqueue work on `stream` and return without
+ *    synchronising unless stated otherwise.  A hierarchy is not re-entrant:
+ *    do not use one hierarchy from two streams concurrently.
+ *  - Input and output vectors of one call must not alias unless stated.
+ *  - Cell numbering: the 20 icosahedron faces in the fixed order of reading
+ *    R1; children of cell p at the next refinement are 4p+0..4p+3.
+ */
+#ifndef HMG_H
+#define HMG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HMG_OK = 0,
+    HMG_ERR_INVALID_ARG = 1,     /* message names the argument */
+    HMG_ERR_CUDA = 2,            /* CUDA runtime error (message has cudaGetErrorString) */
+    HMG_ERR_NCCL = 3,            /* reserved for the multi-GPU layer */
+    HMG_ERR_SINGULAR_COLUMN = 4, /* a Thomas pivot was <= 0 or non-finite: "ref r column c" */
+    HMG_ERR_NOT_CONVERGED = 5,   /* PCG hit maxit; outputs are still filled in */
+    HMG_ERR_OOM = 6              /* device or host allocation failed */
+} hmg_status;
+
+/* Opaque hierarchy: owns every level's neighbour table, geometry, bands and
+ * V-cycle workspaces (device memory), plus the PCG workspace. */
+typedef struct hmg_hierarchy hmg_hierarchy;
+
+/* Multigrid parameters.  The defaults of BASELINE.json are
+ * {nu_pre = 2, nu_post = 2, n_coarse = 20, omega = 0.8}; the paper's own run
+ * uses {1, 1, 2, 0.8}. */
+typedef struct {
+    int nu_pre;    /* presmoothing sweeps per level (>= 0) */
+    int nu_post;   /* postsmoothing sweeps per level (>= 0) */
+    int n_coarse;  /* sweeps from zero on the coarsest level (>= 1) */
+    double omega;  /* damping of the line-Jacobi correction (reading R7) */
+} hmg_mg_params;
+
+/* Build the hierarchy ref fine_ref -> coarsest_ref (setup; synchronous).
+ *  fine_ref      0..10, refinement of the icosahedron (20*4^fine_ref cells)
+ *  coarsest_ref  0..fine_ref, coarsest multigrid level
+ *  nlayers       >= 1 uniform layers; dz = thickness / nlayers
+ *  thickness     > 0 shell thickness (unit sphere radius)
+ *  w2            >= 0 coupling scale (w_c^2 of Eq. 8)
+ *  lam_host      HOST array [nlayers][20*4^fine_ref] (dense, no padding) of
+ *                per-dof coefficients, each finite and > 0; copied, not kept
+ *  device        CUDA device ordinal
+ *  out           receives the hierarchy; *out = NULL on failure
+ * Coarse coefficients are the 4-child means (reading R3); every level is
+ * rediscretised, not Galerkin. */
+hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, double thickness,
+                               double w2, const double* lam_host, int device, hmg_hierarchy** out);
+
+/* Free all device and host storage of the hierarchy (NULL is a no-op). */
+hmg_status hmg_free_hierarchy(hmg_hierarchy* h);
+
+/* Size of level `ref`: number of cells and leading dimension of vectors. */
+hmg_status hmg_level_info(const hmg_hierarchy* h, int ref, int64_t* ncells, int64_t* ld);
+
+/* y = H^ x on level `ref` (Eq. 8; "v = H^ u = H^_z u + H^_h u").
+ * x, y: device [nlayers][ld].  Row order of reading R5. */
+hmg_status hmg_apply_helmholtz(const hmg_hierarchy* h, int ref, const double* x, double* y,
+                               void* stream);
+
+/* nsweeps damped line-Jacobi sweeps on level `ref` (Eq. 10 read with Eq. 13,
+ * reading R7):  u <- u + omega * T^{-1} (b - H^ u),  T = the column-block
+ * (tridiagonal) part of H^ (Eq. 9), solved per column by the Thomas
+ * algorithm.  If u_is_zero != 0 the incoming u is taken as zero
+ * and the first sweep is u = omega * T^{-1} b (its content is ignored).
+ * b, u: device [nlayers][ld]; u is updated in place (ping-pong is internal).
+ * A non-positive or non-finite pivot -> HMG_ERR_SINGULAR_COLUMN (this call
+ * synchronises `stream` to report it). */
+hmg_status hmg_line_smooth(const hmg_hierarchy* h, int ref, const double* b, double* u,
+                           int nsweeps, double omega, int u_is_zero, void* stream);
+
+/* b_c = R r_f: 4-child sum restriction from fine_ref to fine_ref-1
+ * (reading R8).  r_f: [nlayers][ld_fine], b_c: [nlayers][ld_coarse]. */
+hmg_status hmg_restrict(const hmg_hierarchy* h, int fine_ref, const double* r_f, double* b_c,
+                        void* stream);
+
+/* b_c = R (b - H^ u): fused residual + restriction on level fine_ref. */
+hmg_status hmg_residual_restrict(const hmg_hierarchy* h, int fine_ref, const double* b,
+                                 const double* u, double* b_c, void* stream);
+
+/* u_f += P u_c: injection prolongation ("natural embedding"). */
+hmg_status hmg_prolong_add(const hmg_hierarchy* h, int fine_ref, const double* u_c, double* u_f,
+                           void* stream);
+
+/* z = B b: one V-cycle (Alg. 1 recursively; reading R9) from the finest level
+ * with zero initial guess.  b, z: device [nlayers][ld_fine]. */
+hmg_status hmg_vcycle(const hmg_hierarchy* h, const hmg_mg_params* p, const double* b, double* z,
+                      void* stream);
+
+/* Solve H^ x = b by CG preconditioned with one V-cycle per iteration
+ * (reading R10/R12), x0 = 0, stopping when ||r_k||_2 <= rtol ||b||_2 on the
+ * recursively updated residual.  b, x: device [nlayers][ld_fine].
+ *  iters   number of H^ applications performed
+ *  relres  final ||r||/||b||
+ * Synchronises `stream` once per iteration (8-byte convergence read).
+ * Returns HMG_ERR_NOT_CONVERGED (x, iters, relres filled) after maxit. */
+hmg_status hmg_pcg_solve(const hmg_hierarchy* h, const hmg_mg_params* p, const double* b, double* x,
+                         double rtol, int maxit, int* iters, double* relres, void* stream);
+
+/* As hmg_pcg_solve with HOST buffers b_host / x_host of shape
+ * [nlayers][ncells_fine] (dense, no padding): copies b in, solves, copies x
+ * out; synchronous.  The end-to-end entry point. */
+hmg_status hmg_pcg_solve_host(const hmg_hierarchy* h, const hmg_mg_params* p, const double* b_host,
+                              double* x_host, double rtol, int maxit, int* iters, double* relres,
+                              void* stream);
+
+/* Same as hmg_pcg_solve but preconditioned by `nsweeps` line-Jacobi sweeps
+ * from zero on the finest level: the paper's single-level method
+ * ("two iterations of Block-Jacobi vertical line relaxation"). */
+hmg_status hmg_pcg_solve_single_level(const hmg_hierarchy* h, int nsweeps, double omega,
+                                      const double* b, double* x, double rtol, int maxit,
+                                      int* iters, double* relres, void* stream);
+
+/* Export one level to HOST buffers (tests; synchronous; any pointer may be NULL):
+ *  nbr   int32 [ncells][3]     cell across edge (v_j, v_{j+1}) of the cell
+ *  geom  double [7][ncells]    area, len_0..2, cd_0..2 (reading R2)
+ *  bands double [5][nlayers][ncells]  D, U, H_0, H_1, H_2 (U[k] couples k,k+1)
+ *  lam   double [nlayers][ncells]      the level's coefficient */
+hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, double* geom,
+                            double* bands, double* lam);
+
+/* Kernel launches issued by the library since the hierarchy was built
+ * (diagnostic counter used by the benchmark's gpu_launches claim). */
+int64_t hmg_launch_count(const hmg_hierarchy* h);
+
+/* Message for the last error on this thread ("" if none). */
+const char* hmg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HMG_H */

@@ -1,0 +1,235 @@
+"""ctypes binding of the C-ABI in include/hmg.h (argument marshalling only).
+
+Device vectors are torch float64 CUDA tensors of shape (nlayers, ld) (layer-
+major, see ``Hierarchy.level_info``); host vectors are numpy float64 arrays of
+shape (nlayers, ncells).  Calls are enqueued on torch's current CUDA stream.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libhmg.so")
+_lib = None
+
+STATUS = {0: "HMG_OK", 1: "HMG_ERR_INVALID_ARG", 2: "HMG_ERR_CUDA", 3: "HMG_ERR_NCCL",
+          4: "HMG_ERR_SINGULAR_COLUMN", 5: "HMG_ERR_NOT_CONVERGED", 6: "HMG_ERR_OOM"}
+
+
+class HmgError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+        self.status = STATUS.get(code, str(code))
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("nu_pre", ctypes.c_int), ("nu_post", ctypes.c_int), ("n_coarse", ctypes.c_int),
+                ("omega", ctypes.c_double)]
+
+
+@dataclass(frozen=True)
+class MGParams:
+    """V-cycle parameters; defaults are BASELINE.json's V(2,2), 20 coarse sweeps, omega 0.8."""
+    nu_pre: int = 2
+    nu_post: int = 2
+    n_coarse: int = 20
+    omega: float = 0.8
+
+    def c(self) -> _Params:
+        return _Params(self.nu_pre, self.nu_post, self.n_coarse, self.omega)
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load libhmg.so; raises if it is missing (no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"CUDA library {_LIB_PATH} not built: run __graft_entry__.build() "
+                          "(python -m paper_1605_00492_b200.build)")
+    lib = ctypes.CDLL(_LIB_PATH)
+    P, I, D, I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_int64
+    pI, pD, pI64 = ctypes.POINTER(I), ctypes.POINTER(D), ctypes.POINTER(I64)
+    pP = ctypes.POINTER(_Params)
+    sig = {
+        "hmg_build_hierarchy": [I, I, I, D, D, P, I, ctypes.POINTER(P)],
+        "hmg_free_hierarchy": [P],
+        "hmg_level_info": [P, I, pI64, pI64],
+        "hmg_apply_helmholtz": [P, I, P, P, P],
+        "hmg_line_smooth": [P, I, P, P, I, D, I, P],
+        "hmg_restrict": [P, I, P, P, P],
+        "hmg_residual_restrict": [P, I, P, P, P, P],
+        "hmg_prolong_add": [P, I, P, P, P],
+        "hmg_vcycle": [P, pP, P, P, P],
+        "hmg_pcg_solve": [P, pP, P, P, D, I, pI, pD, P],
+        "hmg_pcg_solve_host": [P, pP, P, P, D, I, pI, pD, P],
+        "hmg_pcg_solve_single_level": [P, I, D, P, P, D, I, pI, pD, P],
+        "hmg_export_level": [P, I, P, P, P, P],
+    }
+    for name, args in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    lib.hmg_launch_count.argtypes = [P]
+    lib.hmg_launch_count.restype = I64
+    lib.hmg_last_error.argtypes = []
+    lib.hmg_last_error.restype = ctypes.c_char_p
+    _lib = lib
+    return lib
+
+
+def _check(code: int, allow=()):
+    if code != 0 and code not in allow:
+        raise HmgError(code, load_library().hmg_last_error().decode())
+    return code
+
+
+def _stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _dptr(t, name: str):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous float64 CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+class Hierarchy:
+    """Device hierarchy ref ``fine_ref`` -> ``coarsest_ref`` (hmg_build_hierarchy)."""
+
+    def __init__(self, fine_ref: int, coarsest_ref: int, nlayers: int, thickness: float, w2: float,
+                 lam, device: int = 0):
+        lib = load_library()
+        lam = np.ascontiguousarray(np.asarray(lam, dtype=np.float64))
+        h = ctypes.c_void_p()
+        _check(lib.hmg_build_hierarchy(fine_ref, coarsest_ref, nlayers, thickness, w2,
+                                       lam.ctypes.data_as(ctypes.c_void_p), device, ctypes.byref(h)))
+        self._h = h
+        self.fine_ref, self.coarsest_ref, self.nz = fine_ref, coarsest_ref, nlayers
+        self.thickness, self.w2, self.device = thickness, w2, device
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().hmg_free_hierarchy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- shapes and tensors -------------------------------------------------
+    def level_info(self, ref: int):
+        n, ld = ctypes.c_int64(), ctypes.c_int64()
+        _check(load_library().hmg_level_info(self._h, ref, ctypes.byref(n), ctypes.byref(ld)))
+        return n.value, ld.value
+
+    def empty(self, ref: int):
+        import torch
+        _, ld = self.level_info(ref)
+        return torch.zeros((self.nz, ld), dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def to_device(self, ref: int, a):
+        """numpy [nz][n] -> padded CUDA tensor [nz][ld]."""
+        import torch
+        n, ld = self.level_info(ref)
+        t = self.empty(ref)
+        t[:, :n] = torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(t.device)
+        return t
+
+    def to_host(self, ref: int, t) -> np.ndarray:
+        n, _ = self.level_info(ref)
+        return t[:, :n].cpu().numpy().copy()
+
+    @property
+    def launches(self) -> int:
+        return int(load_library().hmg_launch_count(self._h))
+
+    # -- the C-ABI calls -----------------------------------------------------
+    def apply_helmholtz(self, ref: int, x, y=None):
+        y = self.empty(ref) if y is None else y
+        _check(load_library().hmg_apply_helmholtz(self._h, ref, _dptr(x, "x"), _dptr(y, "y"), _stream()))
+        return y
+
+    def line_smooth(self, ref: int, b, u, nsweeps: int = 1, omega: float = 0.8, u_is_zero: bool = False):
+        _check(load_library().hmg_line_smooth(self._h, ref, _dptr(b, "b"), _dptr(u, "u"), nsweeps, omega,
+                                              int(u_is_zero), _stream()))
+        return u
+
+    def restrict(self, fine_ref: int, r_f, b_c=None):
+        b_c = self.empty(fine_ref - 1) if b_c is None else b_c
+        _check(load_library().hmg_restrict(self._h, fine_ref, _dptr(r_f, "r_f"), _dptr(b_c, "b_c"), _stream()))
+        return b_c
+
+    def residual_restrict(self, fine_ref: int, b, u, b_c=None):
+        b_c = self.empty(fine_ref - 1) if b_c is None else b_c
+        _check(load_library().hmg_residual_restrict(self._h, fine_ref, _dptr(b, "b"), _dptr(u, "u"),
+                                                    _dptr(b_c, "b_c"), _stream()))
+        return b_c
+
+    def prolong_add(self, fine_ref: int, u_c, u_f):
+        _check(load_library().hmg_prolong_add(self._h, fine_ref, _dptr(u_c, "u_c"), _dptr(u_f, "u_f"), _stream()))
+        return u_f
+
+    def vcycle(self, b, z=None, params: MGParams = MGParams()):
+        z = self.empty(self.fine_ref) if z is None else z
+        p = params.c()
+        _check(load_library().hmg_vcycle(self._h, ctypes.byref(p), _dptr(b, "b"), _dptr(z, "z"), _stream()))
+        return z
+
+    def pcg_solve(self, b, x=None, rtol: float = 1e-8, maxit: int = 200, params: MGParams = MGParams()):
+        """Returns (x, iters, relres, status_name)."""
+        x = self.empty(self.fine_ref) if x is None else x
+        p = params.c()
+        it, rr = ctypes.c_int(0), ctypes.c_double(0.0)
+        code = _check(load_library().hmg_pcg_solve(self._h, ctypes.byref(p), _dptr(b, "b"), _dptr(x, "x"), rtol,
+                                                   maxit, ctypes.byref(it), ctypes.byref(rr), _stream()),
+                      allow=(5,))
+        return x, it.value, rr.value, STATUS[code]
+
+    def pcg_solve_single_level(self, b, x=None, nsweeps: int = 2, omega: float = 0.8, rtol: float = 1e-8,
+                               maxit: int = 500):
+        x = self.empty(self.fine_ref) if x is None else x
+        it, rr = ctypes.c_int(0), ctypes.c_double(0.0)
+        code = _check(load_library().hmg_pcg_solve_single_level(self._h, nsweeps, omega, _dptr(b, "b"),
+                                                                _dptr(x, "x"), rtol, maxit, ctypes.byref(it),
+                                                                ctypes.byref(rr), _stream()), allow=(5,))
+        return x, it.value, rr.value, STATUS[code]
+
+    def pcg_solve_host(self, b: np.ndarray, x: np.ndarray | None = None, rtol: float = 1e-8, maxit: int = 200,
+                       params: MGParams = MGParams()):
+        """End-to-end entry point: host arrays [nz][n] in and out."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        x = np.empty_like(b) if x is None else x
+        p = params.c()
+        it, rr = ctypes.c_int(0), ctypes.c_double(0.0)
+        code = _check(load_library().hmg_pcg_solve_host(self._h, ctypes.byref(p), b.ctypes.data_as(ctypes.c_void_p),
+                                                        x.ctypes.data_as(ctypes.c_void_p), rtol, maxit,
+                                                        ctypes.byref(it), ctypes.byref(rr), _stream()), allow=(5,))
+        return x, it.value, rr.value, STATUS[code]
+
+    def export_level(self, ref: int) -> dict:
+        n, _ = self.level_info(ref)
+        nz = self.nz
+        nbr = np.empty((n, 3), np.int32)
+        geom = np.empty((7, n))
+        bands = np.empty((5, nz, n))
+        lam = np.empty((nz, n))
+        _check(load_library().hmg_export_level(self._h, ref, nbr.ctypes.data_as(ctypes.c_void_p),
+                                               geom.ctypes.data_as(ctypes.c_void_p),
+                                               bands.ctypes.data_as(ctypes.c_void_p),
+                                               lam.ctypes.data_as(ctypes.c_void_p)))
+        return dict(nbr=nbr, area=geom[0], len=geom[1:4].T.copy(), cd=geom[4:7].T.copy(), lam=lam,
+                    D=bands[0], U=bands[1], H=bands[2:5])

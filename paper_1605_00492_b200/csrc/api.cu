@@ -1,0 +1,517 @@
+// C-ABI of the B200 Helmholtz multigrid library (include/hmg.h): argument
+// validation, hierarchy construction, the V-cycle driver (Alg. 1)
+// and the PCG driver.  Every step of the path runs in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "hmg_internal.h"
+#include "mesh.h"
+
+using namespace hmg;
+
+namespace {
+
+thread_local std::string g_err;
+
+hmg_status fail(hmg_status st, const std::string& msg) {
+    g_err = msg;
+    return st;
+}
+
+#define HMG_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(e_ == cudaErrorMemoryAllocation ? HMG_ERR_OOM : HMG_ERR_CUDA,          \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+    } while (0)
+
+#define HMG_TRY(expr)                      \
+    do {                                   \
+        hmg_status s_ = (expr);            \
+        if (s_ != HMG_OK) return s_;       \
+    } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int64_t round_up32(int64_t n) { return (n + 31) & ~int64_t(31); }
+
+hmg_status check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(HMG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    return HMG_OK;
+}
+
+hmg_status check_h(const hmg_hierarchy* h) {
+    if (!h) return fail(HMG_ERR_INVALID_ARG, "h: null hierarchy");
+    return HMG_OK;
+}
+
+const Hierarchy& HH(const hmg_hierarchy* h) { return *reinterpret_cast<const Hierarchy*>(h); }
+
+hmg_status check_level(const Hierarchy& H, int ref, const char* name) {
+    if (ref < H.coarsest_ref || ref > H.fine_ref)
+        return fail(HMG_ERR_INVALID_ARG, std::string(name) + ": level " + std::to_string(ref) +
+                                             " outside hierarchy [" + std::to_string(H.coarsest_ref) + ", " +
+                                             std::to_string(H.fine_ref) + "]");
+    return HMG_OK;
+}
+
+hmg_status check_ptr(const void* p, const char* name) {
+    if (!p) return fail(HMG_ERR_INVALID_ARG, std::string(name) + ": null pointer");
+    return HMG_OK;
+}
+
+hmg_status check_params(const hmg_mg_params* p) {
+    if (!p) return fail(HMG_ERR_INVALID_ARG, "p: null parameters");
+    if (p->nu_pre < 0) return fail(HMG_ERR_INVALID_ARG, "p->nu_pre: must be >= 0");
+    if (p->nu_post < 0) return fail(HMG_ERR_INVALID_ARG, "p->nu_post: must be >= 0");
+    if (p->n_coarse < 1) return fail(HMG_ERR_INVALID_ARG, "p->n_coarse: must be >= 1");
+    if (!std::isfinite(p->omega)) return fail(HMG_ERR_INVALID_ARG, "p->omega: must be finite");
+    return HMG_OK;
+}
+
+// Reads the device singular-pivot flag (synchronises the stream).
+hmg_status check_bad(const Hierarchy& H, cudaStream_t s) {
+    unsigned long long bad = 0;
+    HMG_CUDA(cudaMemcpyAsync(&bad, &H.scal->bad, sizeof(bad), cudaMemcpyDeviceToHost, s));
+    HMG_CUDA(cudaStreamSynchronize(s));
+    if (bad != ~0ull) {
+        const unsigned long long reset = ~0ull;
+        HMG_CUDA(cudaMemcpy(&H.scal->bad, &reset, sizeof(reset), cudaMemcpyHostToDevice));
+        return fail(HMG_ERR_SINGULAR_COLUMN, "singular column: ref " + std::to_string(bad >> 40) + " column " +
+                                                 std::to_string(bad & ((1ull << 40) - 1)));
+    }
+    return HMG_OK;
+}
+
+void free_hierarchy(Hierarchy* H) {
+    if (!H) return;
+    cudaSetDevice(H->device);
+    for (auto& L : H->lev) {
+        cudaFree(L.nbr); cudaFree(L.geom); cudaFree(L.lam); cudaFree(L.bands);
+        cudaFree(L.wa); cudaFree(L.wb); cudaFree(L.b); cudaFree(L.u);
+    }
+    cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q);
+    cudaFree(H->partials); cudaFree(H->scal); cudaFree(H->hb); cudaFree(H->hx);
+    if (H->scal_host) cudaFreeHost(H->scal_host);
+    delete H;
+}
+
+// -------------------------------------------------------------------------
+// Sweeps on one level: `count` sweeps from `uin` (nullptr = zero guess),
+// the first one adding P uc if uc != nullptr; intermediate iterates ping-pong
+// through the level's wa/wb (never aliasing uin), the last lands in `out`.
+// -------------------------------------------------------------------------
+void run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
+                int count, double* out, double omega, cudaStream_t s) {
+    const double* cur = uin;
+    for (int i = 0; i < count; ++i) {
+        double* dst;
+        if (i == count - 1) {
+            dst = out;
+        } else {
+            // a work buffer that is neither the sweep's input nor the final output
+            // (callers never pass cur/out = {wa, wb} together)
+            dst = (cur != L.wa && out != L.wa) ? L.wa : L.wb;
+        }
+        launch_sweep(H, L, b, cur, i == 0 ? uc : nullptr, dst, omega, s);
+        cur = dst;
+    }
+}
+
+// Alg. 1 recursively (reading R9): z_l = V_l(b_l) with zero initial guess.
+void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const double* b, double* out,
+                  cudaStream_t s) {
+    const DevLevel& L = H.lev[ref];
+    if (ref == H.coarsest_ref) {
+        run_sweeps(H, L, b, nullptr, nullptr, p.n_coarse, out, p.omega, s);
+        return;
+    }
+    const DevLevel& C = H.lev[ref - 1];
+    // M1 presmooth: the final presmoothed iterate lands in wa/wb (kept through M3)
+    const double* cur = nullptr;
+    if (p.nu_pre > 0) {
+        double* pre_out = L.wa;
+        if (out == L.wa) pre_out = L.wb;
+        run_sweeps(H, L, b, nullptr, nullptr, p.nu_pre, pre_out, p.omega, s);
+        cur = pre_out;
+    }
+    // M2 restrict the residual
+    if (cur)
+        launch_resid_restrict(H, L, b, cur, C.b, s);
+    else
+        launch_restrict(H, L, b, C.b, s);
+    // M3 coarse correction
+    vcycle_level(H, ref - 1, p, C.b, C.u, s);
+    // M4 + M5: prolongation fused into the first postsmoothing sweep
+    if (!cur) {
+        double* zero = (out == L.wa) ? L.wb : L.wa;
+        cudaMemsetAsync(zero, 0, sizeof(double) * H.nz * L.ld, s);
+        cur = zero;
+    }
+    if (p.nu_post > 0) {
+        // keep `cur` intact while ping-ponging: run_sweeps avoids aliasing uin
+        run_sweeps(H, L, b, cur, C.u, p.nu_post, out, p.omega, s);
+    } else {
+        launch_prolong_add(H, L, cur, C.u, out, s);
+    }
+}
+
+hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweeps, double single_omega,
+                    const double* b, double* x, double rtol, int maxit, int* iters, double* relres,
+                    cudaStream_t s) {
+    const DevLevel& F = H.lev[H.fine_ref];
+    const size_t bytes = sizeof(double) * H.nz * F.ld;
+    *iters = 0;
+    *relres = 0.0;
+    auto precond = [&](const double* r, double* z) {
+        if (p)
+            vcycle_level(H, H.fine_ref, *p, r, z, s);
+        else
+            run_sweeps(H, F, r, nullptr, nullptr, single_sweeps, z, single_omega, s);
+    };
+    // r = b (internal r keeps zero padding), x = 0
+    launch_copy_pad(H, F, b, F.ld, H.r, F.ld, s);
+    HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
+    launch_dot(H, F, H.r, H.r, s);
+    launch_finalize(H, kFinBB, s);
+    HMG_TRY(check_launch());
+    HMG_CUDA(cudaMemcpyAsync(H.scal_host, H.scal, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+    HMG_CUDA(cudaStreamSynchronize(s));
+    const double bn = std::sqrt(H.scal_host->bb);
+    if (bn == 0.0) return HMG_OK;
+    precond(H.r, H.z);
+    launch_dot(H, F, H.r, H.z, s);
+    launch_finalize(H, kFinRhoInit, s);
+    HMG_CUDA(cudaMemcpyAsync(H.p, H.z, bytes, cudaMemcpyDeviceToDevice, s));
+    for (int it = 1; it <= maxit; ++it) {
+        launch_apply_dot(H, F, H.p, H.q, s);       // q = H^ p, alpha = rho / <p, q>
+        launch_update_xr(H, F, x, s);              // x += alpha p, r -= alpha q, partial <r, r>
+        launch_finalize(H, kFinRR, s);
+        HMG_TRY(check_launch());
+        HMG_CUDA(cudaMemcpyAsync(H.scal_host, H.scal, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
+        HMG_CUDA(cudaStreamSynchronize(s));
+        if (H.scal_host->bad != ~0ull) return check_bad(H, s);
+        const double rn = std::sqrt(H.scal_host->rr);
+        *iters = it;
+        *relres = rn / bn;
+        if (rn <= rtol * bn) return HMG_OK;
+        precond(H.r, H.z);
+        launch_dot(H, F, H.r, H.z, s);
+        launch_finalize(H, kFinRZ, s);             // beta = rho' / rho, rho = rho'
+        launch_update_p(H, F, s);                  // p = z + beta p
+    }
+    return fail(HMG_ERR_NOT_CONVERGED, "not converged after " + std::to_string(maxit) +
+                                           " iterations (relres " + std::to_string(*relres) + ")");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hmg_last_error(void) { return g_err.c_str(); }
+
+hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
+                               const double* lam_host, int device, hmg_hierarchy** out) {
+    g_err.clear();
+    if (!out) return fail(HMG_ERR_INVALID_ARG, "out: null pointer");
+    *out = nullptr;
+    if (fine_ref < 0 || fine_ref > kMaxRef)
+        return fail(HMG_ERR_INVALID_ARG, "fine_ref: must be in [0, 10], got " + std::to_string(fine_ref));
+    if (coarsest_ref < 0 || coarsest_ref > fine_ref)
+        return fail(HMG_ERR_INVALID_ARG, "coarsest_ref: must be in [0, fine_ref], got " + std::to_string(coarsest_ref));
+    if (nlayers < 1 || nlayers > kMaxLayers)
+        return fail(HMG_ERR_INVALID_ARG, "nlayers: must be in [1, 256], got " + std::to_string(nlayers));
+    if (!(thickness > 0) || !std::isfinite(thickness)) return fail(HMG_ERR_INVALID_ARG, "thickness: must be > 0 and finite");
+    if (!(w2 >= 0) || !std::isfinite(w2)) return fail(HMG_ERR_INVALID_ARG, "w2: must be >= 0 and finite");
+    if (!lam_host) return fail(HMG_ERR_INVALID_ARG, "lam_host: null pointer");
+    const int64_t nfine = 20 * (int64_t(1) << (2 * fine_ref));
+    for (int64_t i = 0; i < nfine * nlayers; ++i)
+        if (!(lam_host[i] > 0) || !std::isfinite(lam_host[i]))
+            return fail(HMG_ERR_INVALID_ARG, "lam_host: entry " + std::to_string(i) + " is not finite and > 0");
+    int ndev = 0;
+    HMG_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(HMG_ERR_INVALID_ARG, "device: no CUDA device " + std::to_string(device));
+    HMG_CUDA(cudaSetDevice(device));
+
+    Hierarchy* H = new (std::nothrow) Hierarchy();
+    if (!H) return fail(HMG_ERR_OOM, "host allocation");
+    H->device = device;
+    H->fine_ref = fine_ref;
+    H->coarsest_ref = coarsest_ref;
+    H->nz = nlayers;
+    H->thickness = thickness;
+    H->w2 = w2;
+    H->dz = thickness / nlayers;
+    auto cleanup = [&](hmg_status s2) { free_hierarchy(H); return s2; };
+
+    std::vector<HostLevel> host;
+    try {
+        host = build_icosahedral_levels(fine_ref);
+    } catch (const std::exception& e) {
+        return cleanup(fail(HMG_ERR_INVALID_ARG, std::string("mesh: ") + e.what()));
+    }
+    H->lev.resize(fine_ref + 1);
+    cudaStream_t s = nullptr;
+#define BCUDA(call)                                                                         \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return cleanup(fail(e_ == cudaErrorMemoryAllocation ? HMG_ERR_OOM : HMG_ERR_CUDA, \
+                                std::string(#call) + ": " + cudaGetErrorString(e_)));      \
+    } while (0)
+    for (int r = coarsest_ref; r <= fine_ref; ++r) {
+        DevLevel& L = H->lev[r];
+        const HostLevel& HL = host[r];
+        L.ref = r;
+        L.n = HL.n;
+        L.ld = round_up32(HL.n);
+        const size_t vb = sizeof(double) * nlayers * L.ld;
+        // SoA neighbour table and geometry, padded entries point at cell 0 / are zero
+        std::vector<int32_t> nbr(3 * L.ld, 0);
+        std::vector<double> geom(7 * L.ld, 0.0);
+        for (int64_t c = 0; c < L.n; ++c) {
+            geom[c] = HL.area[c];
+            for (int j = 0; j < 3; ++j) {
+                nbr[j * L.ld + c] = HL.nbr[c * 3 + j];
+                geom[(1 + j) * L.ld + c] = HL.len[c * 3 + j];
+                geom[(4 + j) * L.ld + c] = HL.cd[c * 3 + j];
+            }
+        }
+        BCUDA(cudaMalloc(&L.nbr, sizeof(int32_t) * 3 * L.ld));
+        BCUDA(cudaMalloc(&L.geom, sizeof(double) * 7 * L.ld));
+        BCUDA(cudaMalloc(&L.lam, vb));
+        BCUDA(cudaMalloc(&L.bands, 5 * vb));
+        BCUDA(cudaMalloc(&L.wa, vb));
+        BCUDA(cudaMalloc(&L.wb, vb));
+        BCUDA(cudaMemset(L.lam, 0, vb));
+        BCUDA(cudaMemset(L.bands, 0, 5 * vb));
+        BCUDA(cudaMemset(L.wa, 0, vb));
+        BCUDA(cudaMemset(L.wb, 0, vb));
+        if (r < fine_ref) {
+            BCUDA(cudaMalloc(&L.b, vb));
+            BCUDA(cudaMalloc(&L.u, vb));
+            BCUDA(cudaMemset(L.b, 0, vb));
+            BCUDA(cudaMemset(L.u, 0, vb));
+        }
+        BCUDA(cudaMemcpy(L.nbr, nbr.data(), sizeof(int32_t) * 3 * L.ld, cudaMemcpyHostToDevice));
+        BCUDA(cudaMemcpy(L.geom, geom.data(), sizeof(double) * 7 * L.ld, cudaMemcpyHostToDevice));
+    }
+    host.clear();
+    // fine coefficients (dense host rows -> padded device rows), coarse by 4-child means
+    DevLevel& F = H->lev[fine_ref];
+    BCUDA(cudaMemcpy2D(F.lam, sizeof(double) * F.ld, lam_host, sizeof(double) * F.n, sizeof(double) * F.n, nlayers,
+                       cudaMemcpyHostToDevice));
+    for (int r = fine_ref - 1; r >= coarsest_ref; --r) launch_coarsen_lam(*H, H->lev[r + 1], H->lev[r], s);
+    for (int r = coarsest_ref; r <= fine_ref; ++r) launch_assemble(*H, H->lev[r], s);
+    // PCG workspace
+    const size_t fb = sizeof(double) * nlayers * F.ld;
+    for (double** v : {&H->r, &H->z, &H->p, &H->q}) {
+        BCUDA(cudaMalloc(v, fb));
+        BCUDA(cudaMemset(*v, 0, fb));
+    }
+    H->npartials = partials_needed(F.n);
+    BCUDA(cudaMalloc(&H->partials, sizeof(double) * H->npartials));
+    BCUDA(cudaMalloc(&H->scal, sizeof(PcgScalars)));
+    BCUDA(cudaMallocHost(&H->scal_host, sizeof(PcgScalars)));
+    PcgScalars init{};
+    init.bad = ~0ull;
+    BCUDA(cudaMemcpy(H->scal, &init, sizeof(init), cudaMemcpyHostToDevice));
+    BCUDA(cudaGetLastError());
+    BCUDA(cudaDeviceSynchronize());
+#undef BCUDA
+    *out = reinterpret_cast<hmg_hierarchy*>(H);
+    return HMG_OK;
+}
+
+hmg_status hmg_free_hierarchy(hmg_hierarchy* h) {
+    free_hierarchy(reinterpret_cast<Hierarchy*>(h));
+    return HMG_OK;
+}
+
+hmg_status hmg_level_info(const hmg_hierarchy* h, int ref, int64_t* ncells, int64_t* ld) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    if (ref < 0 || ref > H.fine_ref) return fail(HMG_ERR_INVALID_ARG, "ref: outside [0, fine_ref]");
+    const int64_t n = 20 * (int64_t(1) << (2 * ref));
+    if (ncells) *ncells = n;
+    if (ld) *ld = round_up32(n);
+    return HMG_OK;
+}
+
+hmg_status hmg_apply_helmholtz(const hmg_hierarchy* h, int ref, const double* x, double* y, void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_level(H, ref, "ref"));
+    HMG_TRY(check_ptr(x, "x"));
+    HMG_TRY(check_ptr(y, "y"));
+    if (x == y) return fail(HMG_ERR_INVALID_ARG, "y: must not alias x");
+    launch_apply(H, H.lev[ref], x, y, S(stream));
+    return check_launch();
+}
+
+hmg_status hmg_line_smooth(const hmg_hierarchy* h, int ref, const double* b, double* u, int nsweeps, double omega,
+                           int u_is_zero, void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_level(H, ref, "ref"));
+    HMG_TRY(check_ptr(b, "b"));
+    HMG_TRY(check_ptr(u, "u"));
+    if (nsweeps < 0) return fail(HMG_ERR_INVALID_ARG, "nsweeps: must be >= 0");
+    if (!std::isfinite(omega)) return fail(HMG_ERR_INVALID_ARG, "omega: must be finite");
+    if (b == u) return fail(HMG_ERR_INVALID_ARG, "u: must not alias b");
+    if (nsweeps == 0) {
+        if (u_is_zero)
+            HMG_CUDA(cudaMemset2DAsync(u, sizeof(double) * H.lev[ref].ld, 0, sizeof(double) * H.lev[ref].n, H.nz,
+                                       S(stream)));
+        return HMG_OK;
+    }
+    const DevLevel& L = H.lev[ref];
+    if (u_is_zero) {
+        run_sweeps(H, L, b, nullptr, nullptr, nsweeps, u, omega, S(stream));
+    } else {
+        // Jacobi semantics need the old iterate intact: sweep out of place, copy back
+        run_sweeps(H, L, b, u, nullptr, nsweeps, L.wa, omega, S(stream));
+        HMG_CUDA(cudaMemcpy2DAsync(u, sizeof(double) * L.ld, L.wa, sizeof(double) * L.ld, sizeof(double) * L.n, H.nz,
+                                   cudaMemcpyDeviceToDevice, S(stream)));
+    }
+    HMG_TRY(check_launch());
+    return check_bad(H, S(stream));
+}
+
+hmg_status hmg_restrict(const hmg_hierarchy* h, int fine_ref, const double* r_f, double* b_c, void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_level(H, fine_ref, "fine_ref"));
+    if (fine_ref == H.coarsest_ref) return fail(HMG_ERR_INVALID_ARG, "fine_ref: no coarser level in hierarchy");
+    HMG_TRY(check_ptr(r_f, "r_f"));
+    HMG_TRY(check_ptr(b_c, "b_c"));
+    launch_restrict(H, H.lev[fine_ref], r_f, b_c, S(stream));
+    return check_launch();
+}
+
+hmg_status hmg_residual_restrict(const hmg_hierarchy* h, int fine_ref, const double* b, const double* u, double* b_c,
+                                 void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_level(H, fine_ref, "fine_ref"));
+    if (fine_ref == H.coarsest_ref) return fail(HMG_ERR_INVALID_ARG, "fine_ref: no coarser level in hierarchy");
+    HMG_TRY(check_ptr(b, "b"));
+    HMG_TRY(check_ptr(u, "u"));
+    HMG_TRY(check_ptr(b_c, "b_c"));
+    launch_resid_restrict(H, H.lev[fine_ref], b, u, b_c, S(stream));
+    return check_launch();
+}
+
+hmg_status hmg_prolong_add(const hmg_hierarchy* h, int fine_ref, const double* u_c, double* u_f, void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_level(H, fine_ref, "fine_ref"));
+    if (fine_ref == H.coarsest_ref) return fail(HMG_ERR_INVALID_ARG, "fine_ref: no coarser level in hierarchy");
+    HMG_TRY(check_ptr(u_c, "u_c"));
+    HMG_TRY(check_ptr(u_f, "u_f"));
+    launch_prolong_add(H, H.lev[fine_ref], u_f, u_c, u_f, S(stream));
+    return check_launch();
+}
+
+hmg_status hmg_vcycle(const hmg_hierarchy* h, const hmg_mg_params* p, const double* b, double* z, void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_params(p));
+    HMG_TRY(check_ptr(b, "b"));
+    HMG_TRY(check_ptr(z, "z"));
+    if (b == z) return fail(HMG_ERR_INVALID_ARG, "z: must not alias b");
+    vcycle_level(H, H.fine_ref, *p, b, z, S(stream));
+    return check_launch();
+}
+
+hmg_status hmg_pcg_solve(const hmg_hierarchy* h, const hmg_mg_params* p, const double* b, double* x, double rtol,
+                         int maxit, int* iters, double* relres, void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_params(p));
+    HMG_TRY(check_ptr(b, "b"));
+    HMG_TRY(check_ptr(x, "x"));
+    HMG_TRY(check_ptr(iters, "iters"));
+    HMG_TRY(check_ptr(relres, "relres"));
+    if (b == x) return fail(HMG_ERR_INVALID_ARG, "x: must not alias b");
+    if (!(rtol >= 0)) return fail(HMG_ERR_INVALID_ARG, "rtol: must be >= 0");
+    if (maxit < 0) return fail(HMG_ERR_INVALID_ARG, "maxit: must be >= 0");
+    return pcg_impl(H, p, 0, 0.0, b, x, rtol, maxit, iters, relres, S(stream));
+}
+
+hmg_status hmg_pcg_solve_single_level(const hmg_hierarchy* h, int nsweeps, double omega, const double* b, double* x,
+                                      double rtol, int maxit, int* iters, double* relres, void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    if (nsweeps < 1) return fail(HMG_ERR_INVALID_ARG, "nsweeps: must be >= 1");
+    if (!std::isfinite(omega)) return fail(HMG_ERR_INVALID_ARG, "omega: must be finite");
+    HMG_TRY(check_ptr(b, "b"));
+    HMG_TRY(check_ptr(x, "x"));
+    HMG_TRY(check_ptr(iters, "iters"));
+    HMG_TRY(check_ptr(relres, "relres"));
+    if (b == x) return fail(HMG_ERR_INVALID_ARG, "x: must not alias b");
+    if (!(rtol >= 0)) return fail(HMG_ERR_INVALID_ARG, "rtol: must be >= 0");
+    if (maxit < 0) return fail(HMG_ERR_INVALID_ARG, "maxit: must be >= 0");
+    return pcg_impl(H, nullptr, nsweeps, omega, b, x, rtol, maxit, iters, relres, S(stream));
+}
+
+hmg_status hmg_pcg_solve_host(const hmg_hierarchy* h, const hmg_mg_params* p, const double* b_host, double* x_host,
+                              double rtol, int maxit, int* iters, double* relres, void* stream) {
+    HMG_TRY(check_h(h));
+    Hierarchy& H = const_cast<Hierarchy&>(HH(h));
+    HMG_TRY(check_ptr(b_host, "b_host"));
+    HMG_TRY(check_ptr(x_host, "x_host"));
+    const DevLevel& F = H.lev[H.fine_ref];
+    const size_t vb = sizeof(double) * H.nz * F.ld;
+    if (!H.hb) {
+        HMG_CUDA(cudaMalloc(&H.hb, vb));
+        HMG_CUDA(cudaMalloc(&H.hx, vb));
+    }
+    cudaStream_t s = S(stream);
+    HMG_CUDA(cudaMemcpy2DAsync(H.hb, sizeof(double) * F.ld, b_host, sizeof(double) * F.n, sizeof(double) * F.n, H.nz,
+                               cudaMemcpyHostToDevice, s));
+    hmg_status st = hmg_pcg_solve(h, p, H.hb, H.hx, rtol, maxit, iters, relres, stream);
+    if (st != HMG_OK && st != HMG_ERR_NOT_CONVERGED) return st;
+    std::string msg = g_err;
+    HMG_CUDA(cudaMemcpy2DAsync(x_host, sizeof(double) * F.n, H.hx, sizeof(double) * F.ld, sizeof(double) * F.n, H.nz,
+                               cudaMemcpyDeviceToHost, s));
+    HMG_CUDA(cudaStreamSynchronize(s));
+    g_err = msg;
+    return st;
+}
+
+hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, double* geom, double* bands, double* lam) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_level(H, ref, "ref"));
+    const DevLevel& L = H.lev[ref];
+    HMG_CUDA(cudaSetDevice(H.device));
+    HMG_CUDA(cudaDeviceSynchronize());
+    if (nbr) {
+        std::vector<int32_t> t(3 * L.ld);
+        HMG_CUDA(cudaMemcpy(t.data(), L.nbr, sizeof(int32_t) * 3 * L.ld, cudaMemcpyDeviceToHost));
+        for (int64_t c = 0; c < L.n; ++c)
+            for (int j = 0; j < 3; ++j) nbr[c * 3 + j] = t[j * L.ld + c];
+    }
+    if (geom)
+        HMG_CUDA(cudaMemcpy2D(geom, sizeof(double) * L.n, L.geom, sizeof(double) * L.ld, sizeof(double) * L.n, 7,
+                              cudaMemcpyDeviceToHost));
+    if (bands)
+        HMG_CUDA(cudaMemcpy2D(bands, sizeof(double) * L.n, L.bands, sizeof(double) * L.ld, sizeof(double) * L.n,
+                              5 * H.nz, cudaMemcpyDeviceToHost));
+    if (lam)
+        HMG_CUDA(cudaMemcpy2D(lam, sizeof(double) * L.n, L.lam, sizeof(double) * L.ld, sizeof(double) * L.n, H.nz,
+                              cudaMemcpyDeviceToHost));
+    return HMG_OK;
+}
+
+int64_t hmg_launch_count(const hmg_hierarchy* h) { return h ? HH(h).launches : -1; }
+
+}  // extern "C"

@@ -1,0 +1,94 @@
+// Internal types of the CUDA path (not part of the C-ABI).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/hmg.h"
+
+namespace hmg {
+
+constexpr int kMaxLayers = 256;   // Thomas state for a column lives in shared memory
+constexpr int kMaxRef = 10;
+
+// Read-only view of one level's operator, passed by value to kernels.
+// Bands are layer-major [nz][ld]; the neighbour table is SoA [3][ld].
+struct LevelView {
+    int64_t n;          // cells
+    int64_t ld;         // leading dimension (multiple of 32)
+    int nz;
+    const int32_t* __restrict__ nbr;   // [3][ld]
+    const double* __restrict__ D;
+    const double* __restrict__ U;      // U[k] couples layers k and k+1; U[nz-1] = 0
+    const double* __restrict__ H0;
+    const double* __restrict__ H1;
+    const double* __restrict__ H2;
+};
+
+struct DevLevel {
+    int ref = 0;
+    int64_t n = 0, ld = 0;
+    int32_t* nbr = nullptr;     // [3][ld]
+    double* geom = nullptr;     // [7][ld]: area, len0..2, cd0..2
+    double* lam = nullptr;      // [nz][ld]
+    double* bands = nullptr;    // [5][nz][ld]: D, U, H0, H1, H2
+    double* wa = nullptr;       // V-cycle ping-pong work [nz][ld]
+    double* wb = nullptr;
+    double* b = nullptr;        // coarse-level right-hand side
+    double* u = nullptr;        // coarse-level output (coarse correction)
+    LevelView view(int nz) const {
+        const int64_t s = (int64_t)nz * ld;
+        return LevelView{n, ld, nz, nbr, bands, bands + s, bands + 2 * s, bands + 3 * s, bands + 4 * s};
+    }
+};
+
+// Device-resident PCG scalars: one struct so a single 64-byte D2H read per
+// iteration returns the residual norm and the singular-pivot flag together.
+struct PcgScalars {
+    double rho, alpha, beta, pq, rr, rz, bb;
+    unsigned long long bad;     // encoded (ref << 40 | column) of the first bad pivot, or ~0
+};
+
+struct Hierarchy {
+    int device = 0;
+    int fine_ref = 0, coarsest_ref = 0, nz = 0;
+    double thickness = 0, w2 = 0, dz = 0;
+    std::vector<DevLevel> lev;  // index = ref
+    // PCG workspace on the finest level
+    double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+    double* partials = nullptr; // per-block partial sums (deterministic reductions)
+    int npartials = 0;
+    PcgScalars* scal = nullptr; // device
+    PcgScalars* scal_host = nullptr;  // pinned
+    double *hb = nullptr, *hx = nullptr;  // device staging for the host entry point
+    mutable int64_t launches = 0;
+};
+
+// kernels.cu
+void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
+void launch_coarsen_lam(const Hierarchy& H, const DevLevel& F, const DevLevel& C, cudaStream_t s);
+void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s);
+void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, double* y,
+                      cudaStream_t s);   // partial sums of x.y into H.partials
+// One sweep: uout = uin(+P uc) + omega T^{-1}(b - H^ uin(+P uc)); uin == nullptr -> zero guess.
+void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin,
+                  const double* uc, double* uout, double omega, cudaStream_t s);
+void launch_restrict(const Hierarchy& H, const DevLevel& F, const double* r, double* bc, cudaStream_t s);
+void launch_resid_restrict(const Hierarchy& H, const DevLevel& F, const double* b, const double* u,
+                           double* bc, cudaStream_t s);
+void launch_prolong_add(const Hierarchy& H, const DevLevel& F, const double* uin, const double* uc,
+                        double* uout, cudaStream_t s);
+// PCG vector kernels (scalars read from H.scal on the device)
+void launch_dot(const Hierarchy& H, const DevLevel& L, const double* a, const double* b, cudaStream_t s);
+void launch_finalize(const Hierarchy& H, int op, cudaStream_t s);
+void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, cudaStream_t s);
+void launch_update_p(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
+void launch_copy_pad(const Hierarchy& H, const DevLevel& L, const double* src, int64_t src_ld,
+                     double* dst, int64_t dst_ld, cudaStream_t s);
+int partials_needed(int64_t n);
+
+enum FinalizeOp { kFinPQ = 0, kFinRR = 1, kFinRZ = 2, kFinRhoInit = 3, kFinBB = 4 };
+
+}  // namespace hmg

@@ -1,0 +1,464 @@
+// sm_100a kernels of the tensor-product multigrid Helmholtz path.
+//
+// All kernels are fp64 and HBM-bound (no tensor cores: nothing here is a
+// dense contraction).  Layout: layer-major [nz][ld], cells contiguous, so a
+// warp walking 32 adjacent columns reads and writes 256-byte coalesced rows
+// at every layer.  Arithmetic follows the canonical operation order of
+// DESIGN.md (readings R4-R10) with no FMA contraction (-fmad=false), so the
+// V-cycle path is bitwise equal to the oracle.
+#include <cfloat>
+
+#include "hmg_internal.h"
+
+namespace hmg {
+namespace {
+
+constexpr int kApplyBlock = 128;
+constexpr int kVecBlock = 256;
+constexpr int kVecPerThread = 4;                  // consecutive cells per thread in vector kernels
+constexpr int kVecCells = kVecBlock * kVecPerThread;
+constexpr int kFinThreads = 1024;
+
+__device__ __forceinline__ bool pivot_ok(double den) { return den > 0.0 && den <= DBL_MAX; }
+
+// Deterministic block sum: fixed shuffle tree per warp, then warp partials
+// summed in warp order by thread 0.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+    for (int off = 16; off > 0; off >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, off);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+        const int nw = blockDim.x >> 5;
+        for (int w = 0; w < nw; ++w) s = s + red[w];
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------------------
+// Setup: coefficient coarsening (reading R3) and band assembly (reading R4,
+// Eq. 8 with lumped two-point couplings; u.n = 0 at top and bottom).
+// ---------------------------------------------------------------------------
+__global__ void k_coarsen_lam(const double* __restrict__ lf, int64_t ldf, double* __restrict__ lc,
+                              int64_t ldc, int64_t nc) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (p >= nc) return;
+    const double* l = lf + k * ldf + 4 * p;
+    lc[k * ldc + p] = 0.25 * (((l[0] + l[1]) + l[2]) + l[3]);
+}
+
+__global__ void k_assemble(int64_t n, int64_t ld, int nz, const int32_t* __restrict__ nbr,
+                           const double* __restrict__ geom, const double* __restrict__ lam,
+                           double w2, double dz, double* __restrict__ bands) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (c >= n) return;
+    const int64_t s = (int64_t)nz * ld, i = k * ld + c;
+    const double area = geom[c];
+    const double vol = area * dz;
+    const double lk = lam[i];
+    double vdn = 0.0, vup = 0.0;
+    if (k > 0) vdn = ((w2 * area) * (0.5 * (lam[i - ld] + lk))) / dz;
+    if (k < nz - 1) vup = ((w2 * area) * (0.5 * (lk + lam[i + ld]))) / dz;
+    double hc[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        const int32_t o = nbr[j * ld + c];
+        const double lamf = 0.5 * (lk + lam[k * ld + o]);
+        hc[j] = (((w2 * geom[(1 + j) * ld + c]) * dz) * lamf) / geom[(4 + j) * ld + c];
+    }
+    double d = vol;
+    if (k > 0) d = d + vdn;
+    if (k < nz - 1) d = d + vup;
+    d = d + hc[0];
+    d = d + hc[1];
+    d = d + hc[2];
+    bands[i] = d;
+    bands[s + i] = (k < nz - 1) ? -vup : 0.0;
+    bands[2 * s + i] = -hc[0];
+    bands[3 * s + i] = -hc[1];
+    bands[4 * s + i] = -hc[2];
+}
+
+// ---------------------------------------------------------------------------
+// Operator apply y = H^ x (reading R5).  One thread per column walks
+// the layers with a sliding window (x[k-1], x[k], x[k+1], U[k-1] in
+// registers); the three face neighbours are gathered from the same layer row.
+// DOT additionally accumulates x.y for the CG step (fused <p, H^ p>).
+// ---------------------------------------------------------------------------
+template <bool DOT>
+__global__ void __launch_bounds__(kApplyBlock) k_apply(LevelView L, const double* __restrict__ x,
+                                                       double* __restrict__ y, double* __restrict__ partial) {
+    __shared__ double red[kApplyBlock / 32];
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    double dot = 0.0;
+    if (c < L.n) {
+        const int64_t ld = L.ld;
+        const int nz = L.nz;
+        const int32_t n0 = L.nbr[c], n1 = L.nbr[ld + c], n2 = L.nbr[2 * ld + c];
+        double xm = 0.0, xk = x[c], Um = 0.0;
+        for (int k = 0; k < nz; ++k) {
+            const int64_t row = k * ld, i = row + c;
+            const double xp = (k + 1 < nz) ? x[i + ld] : 0.0;
+            const double Uk = L.U[i];
+            double acc = L.D[i] * xk;
+            if (k > 0) acc = acc + Um * xm;
+            if (k < nz - 1) acc = acc + Uk * xp;
+            acc = acc + L.H0[i] * x[row + n0];
+            acc = acc + L.H1[i] * x[row + n1];
+            acc = acc + L.H2[i] * x[row + n2];
+            y[i] = acc;
+            if (DOT) dot = dot + xk * acc;
+            xm = xk;
+            xk = xp;
+            Um = Uk;
+        }
+    }
+    if (DOT) {
+        const double s = block_sum(dot, red);
+        if (threadIdx.x == 0) partial[blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused damped line-Jacobi sweep (Eq. 10 read with Eq. 13; readings R6/R7):
+//   r = b - H^ u;  delta = T^{-1} r (Thomas);  u' = u + omega delta
+// One thread per column.  Forward pass computes the residual row and the
+// Thomas elimination; the (z_k, g_k) state of the column sits in shared
+// memory, then back substitution writes u'.  ZERO: u = 0 (u' = omega T^-1 b,
+// P:992-995 "before the pre-smoother application the solution is zero").
+// PROLONG: the incoming u is u + P u_c (the prolongation M4 of Alg. 1 fused
+// into the first post-smoothing sweep; identical arithmetic).
+// ---------------------------------------------------------------------------
+template <bool ZERO, bool PROLONG>
+__global__ void k_sweep(LevelView L, const double* __restrict__ b, const double* __restrict__ uin,
+                        const double* __restrict__ uc, int64_t ldc, double* __restrict__ uout,
+                        double omega, int ref, unsigned long long* __restrict__ bad) {
+    extern __shared__ double sm[];
+    const int T = blockDim.x, t = threadIdx.x;
+    double* zs = sm;
+    double* gs = sm + L.nz * T;
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + t;
+    if (c >= L.n) return;
+    const int64_t ld = L.ld;
+    const int nz = L.nz;
+    int32_t n0 = 0, n1 = 0, n2 = 0;
+    if (!ZERO) { n0 = L.nbr[c]; n1 = L.nbr[ld + c]; n2 = L.nbr[2 * ld + c]; }
+    auto U_IN = [&](int k, int64_t cell) -> double {
+        if (PROLONG) return uin[k * ld + cell] + uc[k * ldc + (cell >> 2)];
+        return uin[k * ld + cell];
+    };
+    double um = 0.0, uk = 0.0, Um = 0.0, den = 0.0, zprev = 0.0;
+    if (!ZERO) uk = U_IN(0, c);
+    bool ok = true;
+    for (int k = 0; k < nz; ++k) {
+        const int64_t i = k * ld + c;
+        const double Dk = L.D[i];
+        const double Uk = L.U[i];
+        double r;
+        double up = 0.0;
+        if (ZERO) {
+            r = b[i];
+        } else {
+            if (k < nz - 1) up = U_IN(k + 1, c);
+            double acc = Dk * uk;
+            if (k > 0) acc = acc + Um * um;
+            if (k < nz - 1) acc = acc + Uk * up;
+            acc = acc + L.H0[i] * U_IN(k, n0);
+            acc = acc + L.H1[i] * U_IN(k, n1);
+            acc = acc + L.H2[i] * U_IN(k, n2);
+            r = b[i] - acc;
+        }
+        double z;
+        if (k == 0) {
+            den = Dk;
+            z = r / den;
+        } else {
+            const double g = Um / den;
+            gs[(k - 1) * T + t] = g;
+            den = Dk - Um * g;
+            z = (r - Um * zprev) / den;
+        }
+        ok = ok && pivot_ok(den);
+        zs[k * T + t] = z;
+        zprev = z;
+        um = uk;
+        uk = up;
+        Um = Uk;
+    }
+    if (!ok) atomicMin(bad, ((unsigned long long)ref << 40) | (unsigned long long)c);
+    double dl = zs[(nz - 1) * T + t];
+    {
+        const int64_t i = (int64_t)(nz - 1) * ld + c;
+        uout[i] = ZERO ? omega * dl : U_IN(nz - 1, c) + omega * dl;
+    }
+    for (int k = nz - 2; k >= 0; --k) {
+        dl = zs[k * T + t] - gs[k * T + t] * dl;
+        const int64_t i = k * ld + c;
+        uout[i] = ZERO ? omega * dl : U_IN(k, c) + omega * dl;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Transfers (reading R8): restriction b_c = ((r0 + r1) + r2) + r3 over the
+// children 4p..4p+3 (R = P^T); prolongation u_f = u_f + u_c[c >> 2].
+// ---------------------------------------------------------------------------
+__global__ void k_restrict(const double* __restrict__ r, int64_t ldf, double* __restrict__ bc,
+                           int64_t ldc, int64_t nc) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (p >= nc) return;
+    const double2* q = reinterpret_cast<const double2*>(r + k * ldf + 4 * p);
+    const double2 a = q[0], b = q[1];
+    bc[k * ldc + p] = ((a.x + a.y) + b.x) + b.y;
+}
+
+// Residual of the current iterate restricted to the coarse level: each lane
+// computes r = b - H^ u for its column; groups of 4 lanes (the 4 children of
+// one parent) combine in child order through shuffles.
+__global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, const double* __restrict__ b,
+                                                                const double* __restrict__ u,
+                                                                double* __restrict__ bc, int64_t ldc) {
+    const int64_t cc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool valid = cc < L.n;          // n is a multiple of 4: groups are all-valid or all-invalid
+    const int64_t c = valid ? cc : L.n - 1;
+    const int64_t ld = L.ld;
+    const int nz = L.nz;
+    const int32_t n0 = L.nbr[c], n1 = L.nbr[ld + c], n2 = L.nbr[2 * ld + c];
+    const int lane = threadIdx.x & 31;
+    double um = 0.0, uk = u[c], Um = 0.0;
+    for (int k = 0; k < nz; ++k) {
+        const int64_t row = k * ld, i = row + c;
+        const double up = (k + 1 < nz) ? u[i + ld] : 0.0;
+        const double Uk = L.U[i];
+        double acc = L.D[i] * uk;
+        if (k > 0) acc = acc + Um * um;
+        if (k < nz - 1) acc = acc + Uk * up;
+        acc = acc + L.H0[i] * u[row + n0];
+        acc = acc + L.H1[i] * u[row + n1];
+        acc = acc + L.H2[i] * u[row + n2];
+        const double r = b[i] - acc;
+        const double r1 = __shfl_down_sync(0xffffffffu, r, 1);
+        const double r2 = __shfl_down_sync(0xffffffffu, r, 2);
+        const double r3 = __shfl_down_sync(0xffffffffu, r, 3);
+        if (valid && (lane & 3) == 0) bc[k * ldc + (cc >> 2)] = ((r + r1) + r2) + r3;
+        um = uk;
+        uk = up;
+        Um = Uk;
+    }
+}
+
+__global__ void k_prolong_add(const double* __restrict__ uin, const double* __restrict__ uc,
+                              double* __restrict__ uout, int64_t ld, int64_t ldc, int64_t n) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (c >= n) return;
+    uout[k * ld + c] = uin[k * ld + c] + uc[k * ldc + (c >> 2)];
+}
+
+// ---------------------------------------------------------------------------
+// CG vector kernels (reading R10).  Each block owns kVecCells consecutive
+// cells of every layer; per-block partial sums are reduced by k_finalize in a
+// fixed order, so dots are deterministic (not equal in rounding to the
+// oracle's sequential sum; see DESIGN.md parity contract).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kVecBlock) k_dot(const double* __restrict__ a, const double* __restrict__ b,
+                                                   int64_t n, int64_t ld, int nz, double* __restrict__ partial) {
+    __shared__ double red[kVecBlock / 32];
+    const int64_t c0 = blockIdx.x * (int64_t)kVecCells + threadIdx.x;
+    double s = 0.0;
+    for (int k = 0; k < nz; ++k)
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+            const int64_t c = c0 + j * kVecBlock;
+            if (c < n) s = s + a[k * ld + c] * b[k * ld + c];
+        }
+    const double tot = block_sum(s, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x, double* __restrict__ r,
+                                                         const double* __restrict__ p, const double* __restrict__ q,
+                                                         int64_t n, int64_t ld, int nz, const PcgScalars* __restrict__ sc,
+                                                         double* __restrict__ partial) {
+    __shared__ double red[kVecBlock / 32];
+    const double alpha = sc->alpha;
+    const int64_t c0 = blockIdx.x * (int64_t)kVecCells + threadIdx.x;
+    double s = 0.0;
+    for (int k = 0; k < nz; ++k)
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+            const int64_t c = c0 + j * kVecBlock;
+            if (c < n) {
+                const int64_t i = k * ld + c;
+                x[i] = x[i] + alpha * p[i];
+                const double rn = r[i] - alpha * q[i];
+                r[i] = rn;
+                s = s + rn * rn;
+            }
+        }
+    const double tot = block_sum(s, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(kVecBlock) k_update_p(double* __restrict__ p, const double* __restrict__ z,
+                                                        int64_t n, int64_t ld, int nz,
+                                                        const PcgScalars* __restrict__ sc) {
+    const double beta = sc->beta;
+    const int64_t c0 = blockIdx.x * (int64_t)kVecCells + threadIdx.x;
+    for (int k = 0; k < nz; ++k)
+#pragma unroll
+        for (int j = 0; j < kVecPerThread; ++j) {
+            const int64_t c = c0 + j * kVecBlock;
+            if (c < n) {
+                const int64_t i = k * ld + c;
+                p[i] = z[i] + beta * p[i];
+            }
+        }
+}
+
+__global__ void __launch_bounds__(kFinThreads) k_finalize(const double* __restrict__ partial, int np, int op,
+                                                          PcgScalars* __restrict__ sc) {
+    __shared__ double red[kFinThreads / 32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < np; i += kFinThreads) s = s + partial[i];
+    const double S = block_sum(s, red);
+    if (threadIdx.x != 0) return;
+    switch (op) {
+        case kFinPQ: sc->pq = S; sc->alpha = sc->rho / S; break;
+        case kFinRR: sc->rr = S; break;
+        case kFinRZ: sc->rz = S; sc->beta = S / sc->rho; sc->rho = S; break;
+        case kFinRhoInit: sc->rho = S; break;
+        case kFinBB: sc->bb = S; break;
+    }
+}
+
+__global__ void k_copy_rows(const double* __restrict__ src, int64_t sld, double* __restrict__ dst, int64_t dld,
+                            int64_t n) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (c < n) dst[k * dld + c] = src[k * sld + c];
+}
+
+inline unsigned blocks(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
+
+int sweep_block(int nz) {
+    int t = 4096 / nz;             // 2 * nz * t * 8 B = 64 KB of Thomas state per block
+    t = t < 32 ? 32 : (t > 128 ? 128 : t);
+    return t & ~31;
+}
+
+template <bool Z, bool P>
+void set_smem_attr() {
+    static bool done = false;
+    if (!done) {
+        cudaFuncSetAttribute(k_sweep<Z, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        done = true;
+    }
+}
+
+}  // namespace
+
+int partials_needed(int64_t n) {
+    const int a = (int)blocks(n, kApplyBlock), v = (int)blocks(n, kVecCells);
+    return a > v ? a : v;
+}
+
+void launch_coarsen_lam(const Hierarchy& H, const DevLevel& F, const DevLevel& C, cudaStream_t s) {
+    dim3 g(blocks(C.n, 256), H.nz);
+    k_coarsen_lam<<<g, 256, 0, s>>>(F.lam, F.ld, C.lam, C.ld, C.n);
+    ++H.launches;
+}
+
+void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
+    dim3 g(blocks(L.n, 256), H.nz);
+    k_assemble<<<g, 256, 0, s>>>(L.n, L.ld, H.nz, L.nbr, L.geom, L.lam, H.w2, H.dz, L.bands);
+    ++H.launches;
+}
+
+void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
+    k_apply<false><<<blocks(L.n, kApplyBlock), kApplyBlock, 0, s>>>(L.view(H.nz), x, y, nullptr);
+    ++H.launches;
+}
+
+void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
+    k_apply<true><<<blocks(L.n, kApplyBlock), kApplyBlock, 0, s>>>(L.view(H.nz), x, y, H.partials);
+    ++H.launches;
+    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)blocks(L.n, kApplyBlock), kFinPQ, H.scal);
+    ++H.launches;
+}
+
+void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin,
+                  const double* uc, double* uout, double omega, cudaStream_t s) {
+    const int T = sweep_block(H.nz);
+    const size_t smem = (size_t)2 * H.nz * T * sizeof(double);
+    const unsigned g = blocks(L.n, T);
+    unsigned long long* bad = &H.scal->bad;
+    const int64_t ldc = uc ? H.lev[L.ref - 1].ld : 0;
+    if (!uin) {
+        set_smem_attr<true, false>();
+        k_sweep<true, false><<<g, T, smem, s>>>(L.view(H.nz), b, nullptr, nullptr, 0, uout, omega, L.ref, bad);
+    } else if (uc) {
+        set_smem_attr<false, true>();
+        k_sweep<false, true><<<g, T, smem, s>>>(L.view(H.nz), b, uin, uc, ldc, uout, omega, L.ref, bad);
+    } else {
+        set_smem_attr<false, false>();
+        k_sweep<false, false><<<g, T, smem, s>>>(L.view(H.nz), b, uin, nullptr, 0, uout, omega, L.ref, bad);
+    }
+    ++H.launches;
+}
+
+void launch_restrict(const Hierarchy& H, const DevLevel& F, const double* r, double* bc, cudaStream_t s) {
+    const DevLevel& C = H.lev[F.ref - 1];
+    dim3 g(blocks(C.n, 256), H.nz);
+    k_restrict<<<g, 256, 0, s>>>(r, F.ld, bc, C.ld, C.n);
+    ++H.launches;
+}
+
+void launch_resid_restrict(const Hierarchy& H, const DevLevel& F, const double* b, const double* u,
+                           double* bc, cudaStream_t s) {
+    const DevLevel& C = H.lev[F.ref - 1];
+    k_resid_restrict<<<blocks(F.n, kApplyBlock), kApplyBlock, 0, s>>>(F.view(H.nz), b, u, bc, C.ld);
+    ++H.launches;
+}
+
+void launch_prolong_add(const Hierarchy& H, const DevLevel& F, const double* uin, const double* uc,
+                        double* uout, cudaStream_t s) {
+    const DevLevel& C = H.lev[F.ref - 1];
+    dim3 g(blocks(F.n, 256), H.nz);
+    k_prolong_add<<<g, 256, 0, s>>>(uin, uc, uout, F.ld, C.ld, F.n);
+    ++H.launches;
+}
+
+void launch_dot(const Hierarchy& H, const DevLevel& L, const double* a, const double* b, cudaStream_t s) {
+    k_dot<<<blocks(L.n, kVecCells), kVecBlock, 0, s>>>(a, b, L.n, L.ld, H.nz, H.partials);
+    ++H.launches;
+}
+
+void launch_finalize(const Hierarchy& H, int op, cudaStream_t s) {
+    const DevLevel& L = H.lev[H.fine_ref];
+    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)blocks(L.n, kVecCells), op, H.scal);
+    ++H.launches;
+}
+
+void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, cudaStream_t s) {
+    k_update_xr<<<blocks(L.n, kVecCells), kVecBlock, 0, s>>>(x, H.r, H.p, H.q, L.n, L.ld, H.nz, H.scal,
+                                                             H.partials);
+    ++H.launches;
+}
+
+void launch_update_p(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
+    k_update_p<<<blocks(L.n, kVecCells), kVecBlock, 0, s>>>(H.p, H.z, L.n, L.ld, H.nz, H.scal);
+    ++H.launches;
+}
+
+void launch_copy_pad(const Hierarchy& H, const DevLevel& L, const double* src, int64_t src_ld, double* dst,
+                     int64_t dst_ld, cudaStream_t s) {
+    dim3 g(blocks(L.n, 256), H.nz);
+    k_copy_rows<<<g, 256, 0, s>>>(src, src_ld, dst, dst_ld, L.n);
+    ++H.launches;
+}
+
+}  // namespace hmg

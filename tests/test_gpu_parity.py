@@ -1,0 +1,218 @@
+"""GPU path == oracle, through the C-ABI (libhmg.so), on seeded inputs.
+
+Parity contract: the V-cycle path (assembly, apply,
+sweeps, transfers, V-cycle) reproduces the oracle's operation order with no
+FMA contraction, so it must be BITWISE equal; the tests assert the
+BASELINE.json tolerances (relative 1e-12 on applies/sweeps/transfers, 1e-10
+on the V-cycle, max-norm relative) and additionally bitwise equality.  PCG
+differs only in the order of its dot-product sums and must reach the same
+iteration count for relative residual 1e-8.
+"""
+import numpy as np
+import pytest
+
+import hmg_inputs as hi
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_1605_00492_b200 import Hierarchy, HmgError, MGParams  # noqa: E402
+
+
+def rel(a, b):
+    d = np.max(np.abs(a - b))
+    s = np.max(np.abs(b))
+    return d / s if s > 0 else d
+
+
+CASES = {
+    "C0": hi.CONFIGS["C0"],
+    "C1": hi.CONFIGS["C1"],
+    "C2a_r4": hi.Config("C2a_r4", 4, 0, 64, 0.01, 1e-4),
+    "C2b_r4": hi.Config("C2b_r4", 4, 0, 64, 0.001, 1e-5),
+    "C2c_r4": hi.Config("C2c_r4", 4, 0, 64, 1e-4, 1e-6),
+    "C4_r3": hi.Config("C4_r3", 3, 0, 128, 0.001, 1e-5),
+    "nz1": hi.Config("nz1", 3, 0, 1, 0.01, 1e-4),
+    "nz3_r1": hi.Config("nz3_r1", 1, 0, 3, 0.01, 1e-4),
+    "w2zero": hi.Config("w2zero", 2, 0, 8, 0.01, 0.0),
+}
+
+
+@pytest.fixture(scope="module", params=list(CASES))
+def pair(request):
+    cfg = CASES[request.param]
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    o = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    yield cfg, g, o, lam, b
+    g.close()
+    o.close()
+
+
+def levels(cfg):
+    return range(cfg.coarsest_ref, cfg.fine_ref + 1)
+
+
+def test_hierarchy_bitwise(pair):
+    """P7: the two independent builders produce identical neighbour tables and
+    bitwise-identical geometry, coefficients and bands on every level."""
+    cfg, g, o, lam, b = pair
+    for r in levels(cfg):
+        G, O = g.export_level(r), o.level(r)
+        assert np.array_equal(G["nbr"], O["nbr"]), f"ref {r} neighbours"
+        for k in ("area", "len", "cd", "lam", "D", "U", "H"):
+            assert np.array_equal(G[k], O[k]), f"ref {r} {k}"
+
+
+def test_apply(pair):
+    cfg, g, o, lam, b = pair
+    for r in levels(cfg):
+        x = hi.uniform_vector(o.shape(r), 100 + r)
+        y = g.to_host(r, g.apply_helmholtz(r, g.to_device(r, x)))
+        ref = o.apply(r, x)
+        assert rel(y, ref) <= 1e-12
+        assert np.array_equal(y, ref), f"ref {r}: not bitwise ({rel(y, ref):.2e})"
+
+
+def test_sweeps(pair):
+    cfg, g, o, lam, b = pair
+    for r in levels(cfg):
+        bb = hi.uniform_vector(o.shape(r), 200 + r)
+        u0 = hi.uniform_vector(o.shape(r), 300 + r)
+        for ns, zero in ((1, True), (1, False), (3, False), (2, True)):
+            u = g.to_device(r, u0)
+            g.line_smooth(r, g.to_device(r, bb), u, ns, 0.8, zero)
+            got = g.to_host(r, u)
+            ref = o.sweep(r, bb, None if zero else u0, ns, 0.8)
+            assert rel(got, ref) <= 1e-12
+            assert np.array_equal(got, ref), f"ref {r} ns {ns} zero {zero}"
+
+
+def test_transfers(pair):
+    cfg, g, o, lam, b = pair
+    for r in levels(cfg):
+        if r == cfg.coarsest_ref:
+            continue
+        rf = hi.uniform_vector(o.shape(r), 400 + r)
+        uc = hi.uniform_vector(o.shape(r - 1), 500 + r)
+        uf = hi.uniform_vector(o.shape(r), 600 + r)
+        got = g.to_host(r - 1, g.restrict(r, g.to_device(r, rf)))
+        assert np.array_equal(got, o.restrict(r, rf))
+        ud = g.to_device(r, uf)
+        g.prolong_add(r, g.to_device(r - 1, uc), ud)
+        assert np.array_equal(g.to_host(r, ud), o.prolong_add(r, uc, uf))
+        # fused residual + restriction
+        got = g.to_host(r - 1, g.residual_restrict(r, g.to_device(r, rf), g.to_device(r, uf)))
+        ref = o.restrict(r, o.residual(r, rf, uf))
+        assert rel(got, ref) <= 1e-12
+        assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("params", [MGParams(), MGParams(1, 1, 2, 0.8), MGParams(0, 2, 5, 0.8),
+                                    MGParams(2, 0, 3, 0.8), MGParams(3, 1, 20, 1.0)])
+def test_vcycle(pair, params):
+    cfg, g, o, lam, b = pair
+    z = g.to_host(cfg.fine_ref, g.vcycle(g.to_device(cfg.fine_ref, b), params=params))
+    ref = o.vcycle(b, params.nu_pre, params.nu_post, params.n_coarse, params.omega)
+    assert rel(z, ref) <= 1e-10
+    assert np.array_equal(z, ref), f"V-cycle not bitwise ({rel(z, ref):.2e})"
+
+
+def test_pcg_iterations(pair):
+    cfg, g, o, lam, b = pair
+    x, it, rr, st = g.pcg_solve(g.to_device(cfg.fine_ref, b), rtol=1e-8, maxit=200)
+    xo, it_o, rr_o, hist, st_o = o.pcg(b, rtol=1e-8, maxit=200)
+    assert st == "HMG_OK" and st_o == 0
+    assert it == it_o, f"iterations {it} vs oracle {it_o} (oracle history tail {hist[-3:]})"
+    assert rr <= 1e-8
+    assert rel(g.to_host(cfg.fine_ref, x), xo) <= 1e-6
+
+
+def test_single_level_pcg(pair):
+    """NEXT-1: the paper's single-level preconditioner (2 line sweeps) in the same PCG."""
+    cfg, g, o, lam, b = pair
+    x, it, rr, st = g.pcg_solve_single_level(g.to_device(cfg.fine_ref, b), nsweeps=2, rtol=1e-8, maxit=500)
+    _, it_o, _, _, st_o = o.pcg(b, precond="single", nu_pre=2, rtol=1e-8, maxit=500)
+    assert st == "HMG_OK" and st_o == 0 and it == it_o
+
+
+def test_host_entry_point(pair):
+    cfg, g, o, lam, b = pair
+    x, it, rr, st = g.pcg_solve_host(b)
+    xd, itd, rrd, std = g.pcg_solve(g.to_device(cfg.fine_ref, b))
+    assert st == std == "HMG_OK" and it == itd
+    assert np.array_equal(x, g.to_host(cfg.fine_ref, xd))
+
+
+def test_padding_untouched_and_ignored():
+    """ref 0 (20 cells, ld 32) and ref 1 (80 cells, ld 96): padding entries are
+    never read (NaN there changes nothing) and never written."""
+    cfg = hi.Config("pad", 1, 0, 4, 0.01, 1e-3)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(1, 0, 4, 0.01, 1e-3, lam)
+    o = oracle.Hierarchy(1, 0, 4, 0.01, 1e-3, lam)
+    for r in (0, 1):
+        n, ld = g.level_info(r)
+        assert ld % 32 == 0 and ld >= n
+        x = g.to_device(r, hi.uniform_vector((4, n), 7))
+        x[:, n:] = float("nan")
+        y = g.empty(r)
+        y[:, n:] = 12345.0
+        g.apply_helmholtz(r, x, y)
+        assert np.array_equal(g.to_host(r, y), o.apply(r, x[:, :n].cpu().numpy()))
+        assert torch.all(y[:, n:] == 12345.0)
+    bd = g.to_device(1, b)
+    bd[:, 80:] = float("nan")
+    z = g.empty(1)
+    z[:, 80:] = 7.0
+    g.vcycle(bd, z)
+    assert np.array_equal(g.to_host(1, z), o.vcycle(b))
+    assert torch.all(z[:, 80:] == 7.0)
+    x, it, rr, st = g.pcg_solve(bd)
+    assert st == "HMG_OK" and it == o.pcg(b)[1]
+
+
+def test_errors_name_arguments():
+    cfg = hi.CONFIGS["C0"]
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(2, 0, 8, 0.01, 1e-4, lam)
+    x = g.empty(2)
+    with pytest.raises(HmgError, match="ref"):
+        g.apply_helmholtz(3, x, g.empty(2))
+    with pytest.raises(HmgError, match="alias"):
+        g.apply_helmholtz(2, x, x)
+    with pytest.raises(HmgError, match="n_coarse"):
+        g.vcycle(x, params=MGParams(2, 2, 0, 0.8))
+    with pytest.raises(HmgError, match="coarser"):
+        g.restrict(0, g.empty(0))
+    x, it, rr, st = g.pcg_solve(g.to_device(2, b), rtol=1e-30, maxit=2)
+    assert st == "HMG_ERR_NOT_CONVERGED" and it == 2
+    x, it, rr, st = g.pcg_solve(g.empty(2))
+    assert st == "HMG_OK" and it == 0 and float(x.abs().max()) == 0.0
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C2a", "C2b", "C2c"])
+def test_full_size_c2(name):
+    """BASELINE.json config C2 at full size (ref 7 x 64 = 20.97M dofs), in the
+    launch configuration bench.py times: V-cycle bitwise equal to the oracle,
+    apply bitwise, and the same PCG iteration count."""
+    cfg = hi.CONFIGS[name]
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    o = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    r = cfg.fine_ref
+    bd = g.to_device(r, b)
+    assert np.array_equal(g.to_host(r, g.apply_helmholtz(r, bd)), o.apply(r, b))
+    z = g.to_host(r, g.vcycle(bd))
+    zo = o.vcycle(b)
+    assert rel(z, zo) <= 1e-10 and np.array_equal(z, zo)
+    _, it, rr, st = g.pcg_solve(bd)
+    _, it_o, _, _, st_o = o.pcg(b)
+    assert st == "HMG_OK" and st_o == 0 and it == it_o
+    g.close()
+    o.close()
