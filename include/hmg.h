@@ -22,7 +22,9 @@
  *  - Vectors are fp64, LAYER-MAJOR [nlayers][ld] (cells contiguous within a
  *    layer), where ld is the level's leading dimension from hmg_level_info
  *    (ld = number of cells rounded up to a multiple of 32).  Entries with
- *    cell index >= ncells are padding: never read, never written.
+ *    cell index >= ncells are padding: their values never affect a result
+ *    (they may be read by row-block copies) and they are never written.
+ *    Device vector pointers must be 16-byte aligned (HMG_ERR_INVALID_ARG).
  *  - Device pointers (everything except *_host arguments) are caller-owned
  *    CUDA device memory on the hierarchy's device; host pointers are plain
  *    host memory.  The library never frees caller memory.
@@ -157,6 +159,12 @@ hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, doubl
 /* Kernel launches issued by the library since the hierarchy was built
  * (diagnostic counter used by the benchmark's gpu_launches claim). */
 int64_t hmg_launch_count(const hmg_hierarchy* h);
+
+/* Diagnostic: for device arrays a, b of length n, writes fast[i] = the
+ * shared-reciprocal division the sweep kernel uses and ref[i] = a[i] / b[i]
+ * (the compiler's div.rn.f64).  The two must be bitwise equal. */
+hmg_status hmg_selftest_div(const double* a, const double* b, double* fast, double* ref, int64_t n,
+                            void* stream);
 
 /* Message for the last error on this thread ("" if none). */
 const char* hmg_last_error(void);

@@ -74,6 +74,7 @@ def load_library():
         "hmg_pcg_solve_host": [P, pP, P, P, D, I, pI, pD, P],
         "hmg_pcg_solve_single_level": [P, I, D, P, P, D, I, pI, pD, P],
         "hmg_export_level": [P, I, P, P, P, P],
+        "hmg_selftest_div": [P, P, P, P, I64, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -103,6 +104,15 @@ def _dptr(t, name: str):
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
         raise TypeError(f"{name}: expected a contiguous float64 CUDA tensor")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def selftest_div(a, b):
+    """(fast, ref) device tensors: the sweep kernel's division vs the '/' operator."""
+    import torch
+    fast, ref = torch.empty_like(a), torch.empty_like(a)
+    _check(load_library().hmg_selftest_div(_dptr(a, "a"), _dptr(b, "b"), _dptr(fast, "fast"), _dptr(ref, "ref"),
+                                           a.numel(), _stream()))
+    return fast, ref
 
 
 class Hierarchy:

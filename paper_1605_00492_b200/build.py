@@ -14,8 +14,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhmg.so")
-SOURCES = ["api.cu", "kernels.cu", "mesh.cpp"]
-HEADERS = ["hmg_internal.h", "mesh.h", os.path.join("..", "..", "include", "hmg.h")]
+SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "mesh.cpp"]
+HEADERS = ["hmg_internal.h", "mesh.h", "sm100_ptx.cuh", os.path.join("..", "..", "include", "hmg.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",

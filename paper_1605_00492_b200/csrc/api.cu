@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <cstdlib>
 #include <new>
 #include <string>
 
@@ -42,6 +44,7 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 int64_t round_up32(int64_t n) { return (n + 31) & ~int64_t(31); }
 
 hmg_status check_launch() {
+    if (const char* m = take_launch_error()) return fail(HMG_ERR_CUDA, m);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(HMG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
     return HMG_OK;
@@ -64,6 +67,8 @@ hmg_status check_level(const Hierarchy& H, int ref, const char* name) {
 
 hmg_status check_ptr(const void* p, const char* name) {
     if (!p) return fail(HMG_ERR_INVALID_ARG, std::string(name) + ": null pointer");
+    if (reinterpret_cast<uintptr_t>(p) % 16 != 0)
+        return fail(HMG_ERR_INVALID_ARG, std::string(name) + ": must be 16-byte aligned");
     return HMG_OK;
 }
 
@@ -96,6 +101,7 @@ void free_hierarchy(Hierarchy* H) {
     for (auto& L : H->lev) {
         cudaFree(L.nbr); cudaFree(L.geom); cudaFree(L.lam); cudaFree(L.bands);
         cudaFree(L.wa); cudaFree(L.wb); cudaFree(L.b); cudaFree(L.u);
+        cudaFree(L.halo_cells); cudaFree(L.halo_count); cudaFree(L.halo_loc);
     }
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q);
     cudaFree(H->partials); cudaFree(H->scal); cudaFree(H->hb); cudaFree(H->hx);
@@ -104,28 +110,26 @@ void free_hierarchy(Hierarchy* H) {
 }
 
 // -------------------------------------------------------------------------
-// Sweeps on one level: `count` sweeps from `uin` (nullptr = zero guess),
-// the first one adding P uc if uc != nullptr; intermediate iterates ping-pong
-// through the level's wa/wb (never aliasing uin), the last lands in `out`.
+// Sweeps on one level: `count` sweeps from `uin` (nullptr = zero guess), the
+// first one adding P uc if uc != nullptr.  Intermediate iterates ping-pong
+// through the level's wa/wb, always avoiding the sweep's own input (Jacobi
+// semantics: every column must read the OLD neighbour values).  The last
+// sweep writes `out` if given (it must not be wa/wb), else wa or wb.
+// Returns the buffer holding the result.
 // -------------------------------------------------------------------------
-void run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
-                int count, double* out, double omega, cudaStream_t s) {
+const double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
+                         int count, double* out, double omega, cudaStream_t s) {
     const double* cur = uin;
     for (int i = 0; i < count; ++i) {
-        double* dst;
-        if (i == count - 1) {
-            dst = out;
-        } else {
-            // a work buffer that is neither the sweep's input nor the final output
-            // (callers never pass cur/out = {wa, wb} together)
-            dst = (cur != L.wa && out != L.wa) ? L.wa : L.wb;
-        }
+        double* dst = (i == count - 1 && out) ? out : (cur == L.wa ? L.wb : L.wa);
         launch_sweep(H, L, b, cur, i == 0 ? uc : nullptr, dst, omega, s);
         cur = dst;
     }
+    return cur;
 }
 
-// Alg. 1 recursively (reading R9): z_l = V_l(b_l) with zero initial guess.
+// Alg. 1 recursively (reading R9): out = V_l(b_l) with zero initial guess.
+// `out` is never the level's wa/wb (it is the coarse level's u or the caller's z).
 void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const double* b, double* out,
                   cudaStream_t s) {
     const DevLevel& L = H.lev[ref];
@@ -134,15 +138,10 @@ void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const dou
         return;
     }
     const DevLevel& C = H.lev[ref - 1];
-    // M1 presmooth: the final presmoothed iterate lands in wa/wb (kept through M3)
+    // M1 presmooth from zero: the iterate stays in wa/wb through M2-M3
     const double* cur = nullptr;
-    if (p.nu_pre > 0) {
-        double* pre_out = L.wa;
-        if (out == L.wa) pre_out = L.wb;
-        run_sweeps(H, L, b, nullptr, nullptr, p.nu_pre, pre_out, p.omega, s);
-        cur = pre_out;
-    }
-    // M2 restrict the residual
+    if (p.nu_pre > 0) cur = run_sweeps(H, L, b, nullptr, nullptr, p.nu_pre, nullptr, p.omega, s);
+    // M2 restrict the residual (b itself when u = 0)
     if (cur)
         launch_resid_restrict(H, L, b, cur, C.b, s);
     else
@@ -151,16 +150,13 @@ void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const dou
     vcycle_level(H, ref - 1, p, C.b, C.u, s);
     // M4 + M5: prolongation fused into the first postsmoothing sweep
     if (!cur) {
-        double* zero = (out == L.wa) ? L.wb : L.wa;
-        cudaMemsetAsync(zero, 0, sizeof(double) * H.nz * L.ld, s);
-        cur = zero;
+        cudaMemsetAsync(L.wa, 0, sizeof(double) * H.nz * L.ld, s);
+        cur = L.wa;
     }
-    if (p.nu_post > 0) {
-        // keep `cur` intact while ping-ponging: run_sweeps avoids aliasing uin
+    if (p.nu_post > 0)
         run_sweeps(H, L, b, cur, C.u, p.nu_post, out, p.omega, s);
-    } else {
+    else
         launch_prolong_add(H, L, cur, C.u, out, s);
-    }
 }
 
 hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweeps, double single_omega,
@@ -249,6 +245,11 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
     H->thickness = thickness;
     H->w2 = w2;
     H->dz = thickness / nlayers;
+    if (const char* e = std::getenv("HMG_SWEEP")) H->use_tc_sweep = std::string(e) != "simple";
+    if (H->use_tc_sweep && !tensor_maps_available()) {
+        delete H;
+        return fail(HMG_ERR_CUDA, "cuTensorMapEncodeTiled not available from the CUDA driver");
+    }
     auto cleanup = [&](hmg_status s2) { free_hierarchy(H); return s2; };
 
     std::vector<HostLevel> host;
@@ -302,6 +303,51 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
         }
         BCUDA(cudaMemcpy(L.nbr, nbr.data(), sizeof(int32_t) * 3 * L.ld, cudaMemcpyHostToDevice));
         BCUDA(cudaMemcpy(L.geom, geom.data(), sizeof(double) * 7 * L.ld, cudaMemcpyHostToDevice));
+        // tile halos for the streamed sweep (sweep_tc.cu)
+        {
+            const int64_t ntiles = (L.n + kSweepTile - 1) / kSweepTile;
+            std::vector<int32_t> hcells(ntiles * kHaloMax, 0), hcount(ntiles, 0);
+            std::vector<uint32_t> loc(L.ld, 0);
+            bool fits = true;
+            for (int64_t t = 0; t < ntiles && fits; ++t) {
+                const int64_t a = t * kSweepTile, e = std::min<int64_t>(L.n, a + kSweepTile);
+                std::vector<int32_t> out;
+                for (int64_t c = a; c < e; ++c)
+                    for (int j = 0; j < 3; ++j) {
+                        const int32_t o = HL.nbr[c * 3 + j];
+                        if (o < a || o >= e) out.push_back(o);
+                    }
+                std::sort(out.begin(), out.end());
+                out.erase(std::unique(out.begin(), out.end()), out.end());
+                if ((int)out.size() > kHaloMax) { fits = false; break; }
+                hcount[t] = (int32_t)out.size();
+                std::copy(out.begin(), out.end(), hcells.begin() + t * kHaloMax);
+                for (int64_t c = a; c < e; ++c) {
+                    uint32_t packed = 0;
+                    for (int j = 0; j < 3; ++j) {
+                        const int32_t o = HL.nbr[c * 3 + j];
+                        uint32_t slot;
+                        if (o >= a && o < e)
+                            slot = (uint32_t)(o - a);
+                        else
+                            slot = kSweepTile + (uint32_t)(std::lower_bound(out.begin(), out.end(), o) - out.begin());
+                        packed |= slot << (8 * j);
+                    }
+                    loc[c] = packed;
+                }
+            }
+            if (fits) {
+                BCUDA(cudaMalloc(&L.halo_cells, sizeof(int32_t) * hcells.size()));
+                BCUDA(cudaMalloc(&L.halo_count, sizeof(int32_t) * hcount.size()));
+                BCUDA(cudaMalloc(&L.halo_loc, sizeof(uint32_t) * loc.size()));
+                BCUDA(cudaMemcpy(L.halo_cells, hcells.data(), sizeof(int32_t) * hcells.size(), cudaMemcpyHostToDevice));
+                BCUDA(cudaMemcpy(L.halo_count, hcount.data(), sizeof(int32_t) * hcount.size(), cudaMemcpyHostToDevice));
+                BCUDA(cudaMemcpy(L.halo_loc, loc.data(), sizeof(uint32_t) * loc.size(), cudaMemcpyHostToDevice));
+                L.halo.cells = L.halo_cells;
+                L.halo.count = L.halo_count;
+                L.halo.loc = L.halo_loc;
+            }
+        }
     }
     host.clear();
     // fine coefficients (dense host rows -> padded device rows), coarse by 4-child means
@@ -377,8 +423,8 @@ hmg_status hmg_line_smooth(const hmg_hierarchy* h, int ref, const double* b, dou
         run_sweeps(H, L, b, nullptr, nullptr, nsweeps, u, omega, S(stream));
     } else {
         // Jacobi semantics need the old iterate intact: sweep out of place, copy back
-        run_sweeps(H, L, b, u, nullptr, nsweeps, L.wa, omega, S(stream));
-        HMG_CUDA(cudaMemcpy2DAsync(u, sizeof(double) * L.ld, L.wa, sizeof(double) * L.ld, sizeof(double) * L.n, H.nz,
+        const double* res = run_sweeps(H, L, b, u, nullptr, nsweeps, nullptr, omega, S(stream));
+        HMG_CUDA(cudaMemcpy2DAsync(u, sizeof(double) * L.ld, res, sizeof(double) * L.ld, sizeof(double) * L.n, H.nz,
                                    cudaMemcpyDeviceToDevice, S(stream)));
     }
     HMG_TRY(check_launch());
@@ -513,5 +559,16 @@ hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, doubl
 }
 
 int64_t hmg_launch_count(const hmg_hierarchy* h) { return h ? HH(h).launches : -1; }
+
+hmg_status hmg_selftest_div(const double* a, const double* b, double* fast, double* ref, int64_t n, void* stream) {
+    HMG_TRY(check_ptr(a, "a"));
+    HMG_TRY(check_ptr(b, "b"));
+    HMG_TRY(check_ptr(fast, "fast"));
+    HMG_TRY(check_ptr(ref, "ref"));
+    if (n < 0) return fail(HMG_ERR_INVALID_ARG, "n: must be >= 0");
+    if (n == 0) return HMG_OK;
+    launch_selftest_div(n, a, b, fast, ref, S(stream));
+    return check_launch();
+}
 
 }  // extern "C"

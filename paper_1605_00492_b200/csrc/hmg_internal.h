@@ -12,6 +12,18 @@ namespace hmg {
 
 constexpr int kMaxLayers = 256;   // Thomas state for a column lives in shared memory
 constexpr int kMaxRef = 10;
+constexpr int kSweepTile = 128;   // columns per CTA of the TMA/TMEM sweep (sweep_tc.cu)
+constexpr int kHaloMax = 64;      // max off-tile neighbour cells per tile (51 observed at ref >= 2)
+
+// Per-level tile halo for the streamed sweep: for tile t (cells
+// [t*kSweepTile, (t+1)*kSweepTile)), the sorted distinct neighbour cells
+// outside the tile, and per cell the 3 neighbours' local slots packed in
+// bytes (slot < kSweepTile: in-tile offset; else kSweepTile + halo index).
+struct TileHalo {
+    const int32_t* cells = nullptr;   // [ntiles][kHaloMax]
+    const int32_t* count = nullptr;   // [ntiles]
+    const uint32_t* loc = nullptr;    // [ld]
+};
 
 // Read-only view of one level's operator, passed by value to kernels.
 // Bands are layer-major [nz][ld]; the neighbour table is SoA [3][ld].
@@ -38,6 +50,10 @@ struct DevLevel {
     double* wb = nullptr;
     double* b = nullptr;        // coarse-level right-hand side
     double* u = nullptr;        // coarse-level output (coarse correction)
+    int32_t* halo_cells = nullptr;
+    int32_t* halo_count = nullptr;
+    uint32_t* halo_loc = nullptr;
+    TileHalo halo;
     LevelView view(int nz) const {
         const int64_t s = (int64_t)nz * ld;
         return LevelView{n, ld, nz, nbr, bands, bands + s, bands + 2 * s, bands + 3 * s, bands + 4 * s};
@@ -64,6 +80,7 @@ struct Hierarchy {
     PcgScalars* scal_host = nullptr;  // pinned
     double *hb = nullptr, *hx = nullptr;  // device staging for the host entry point
     mutable int64_t launches = 0;
+    bool use_tc_sweep = true;   // HMG_SWEEP=simple selects the reference-layout kernel (diagnostics)
 };
 
 // kernels.cu
@@ -88,6 +105,15 @@ void launch_update_p(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
 void launch_copy_pad(const Hierarchy& H, const DevLevel& L, const double* src, int64_t src_ld,
                      double* dst, int64_t dst_ld, cudaStream_t s);
 int partials_needed(int64_t n);
+// sweep_tc.cu: TMA-streamed, TMEM-state sweep (same arithmetic as launch_sweep's kernel)
+bool sweep_tc_supported(const Hierarchy& H, const DevLevel& L);
+void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
+                     double* uout, double omega, cudaStream_t s);
+
+// Error raised on the host side of a launch (tensor-map encoding); nullptr if none.
+const char* take_launch_error();
+bool tensor_maps_available();
+void launch_selftest_div(int64_t n, const double* a, const double* b, double* fast, double* ref, cudaStream_t s);
 
 enum FinalizeOp { kFinPQ = 0, kFinRR = 1, kFinRZ = 2, kFinRhoInit = 3, kFinBB = 4 };
 

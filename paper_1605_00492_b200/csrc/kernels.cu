@@ -392,6 +392,10 @@ void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, do
 
 void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin,
                   const double* uc, double* uout, double omega, cudaStream_t s) {
+    if (H.use_tc_sweep && sweep_tc_supported(H, L)) {
+        launch_sweep_tc(H, L, b, uin, uc, uout, omega, s);
+        return;
+    }
     const int T = sweep_block(H.nz);
     const size_t smem = (size_t)2 * H.nz * T * sizeof(double);
     const unsigned g = blocks(L.n, T);

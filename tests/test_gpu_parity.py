@@ -188,7 +188,7 @@ def test_errors_name_arguments():
     with pytest.raises(HmgError, match="n_coarse"):
         g.vcycle(x, params=MGParams(2, 2, 0, 0.8))
     with pytest.raises(HmgError, match="coarser"):
-        g.restrict(0, g.empty(0))
+        g.restrict(0, g.empty(0), g.empty(0))
     x, it, rr, st = g.pcg_solve(g.to_device(2, b), rtol=1e-30, maxit=2)
     assert st == "HMG_ERR_NOT_CONVERGED" and it == 2
     x, it, rr, st = g.pcg_solve(g.empty(2))
@@ -216,3 +216,26 @@ def test_full_size_c2(name):
     assert st == "HMG_OK" and st_o == 0 and it == it_o
     g.close()
     o.close()
+
+
+def test_shared_reciprocal_division_is_bitwise_ieee():
+    """The sweep's shared-reciprocal division equals the compiler's a / b bit
+    for bit: 2^24 random pairs over a wide exponent range plus special values."""
+    from paper_1605_00492_b200.binding import selftest_div
+    rng = np.random.default_rng(5)
+    n = 1 << 24
+    a = rng.uniform(-1, 1, n) * 10.0 ** rng.uniform(-300, 300, n)
+    b = rng.uniform(0, 1, n) * 10.0 ** rng.uniform(-300, 300, n)
+    special = np.array([0.0, -0.0, 1.0, -1.0, np.inf, -np.inf, np.nan, 5e-324, -5e-324, 2.2250738585072014e-308,
+                        1.7976931348623157e308, 1e-310, 3.0, 7.0])
+    sa, sb = np.meshgrid(special, special)
+    a = np.concatenate([a, sa.ravel(), rng.uniform(1e-8, 1e4, 1 << 20)])
+    b = np.concatenate([b, sb.ravel(), rng.uniform(1e-8, 1e4, 1 << 20)])
+    fast, ref = selftest_div(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda())
+    f, r = fast.cpu().numpy(), ref.cpu().numpy()
+    both_nan = np.isnan(f) & np.isnan(r)
+    assert np.array_equal(f.view(np.int64)[~both_nan], r.view(np.int64)[~both_nan])
+    assert np.array_equal(np.isnan(f), np.isnan(r))
+    ok = ~np.isnan(r) & (b != 0) & np.isfinite(a) & np.isfinite(b)
+    # and the compiler's division is the IEEE quotient numpy computes
+    assert np.array_equal(r[ok].view(np.int64), (a[ok] / b[ok]).view(np.int64))
