@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 tensor-product multigrid Helmholtz solver (arXiv:1605.00492 hot path).
+
+One step = one full solve of BASELINE.json config C2 (anisotropy C2a: ref 7 x 64
+layers = 20,971,520 fp64 dofs, hierarchy ref 7 -> 0, PCG preconditioned by one
+V(2,2) cycle per iteration, damped line-Jacobi omega = 0.8, 20 coarse sweeps,
+relative residual 1e-8).  Every row of SURVEY.md 8(a) runs inside the step:
+operator apply, fused sweeps, residual+restriction, prolongation, the coarse
+solve, the V-cycle driver and the PCG vector/dot kernels.
+
+Metric (BASELINE.json): fp64 Helmholtz dofs/s per V-cycle = fine dofs x
+V-cycles executed in the step / step time (the PCG's own apply and vector
+work is included in the time, so this under-states the bare V-cycle rate,
+which is reported as `vcycle_only`).  Also reported: PCG solve time, the
+dominant kernel's achieved HBM GB/s against MEASURED_PEAKS.json, the oracle on
+the host cores, and an end-to-end number through the host-buffer entry point.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Multi-GPU (torchrun, N > 1): each rank solves its own C2a-sized problem
+(weak scaling, replicas): the NCCL halo layer of SURVEY 8(e) is not built yet.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import hmg_inputs as hi  # noqa: E402
+
+METRIC = "fp64 Helmholtz dofs/s per V-cycle"
+UNIT = "dof/s"
+# Algorithmic bytes per dof of each kernel class
+BYTES_PER_DOF = {"sweep": 64.0, "sweep_zero": 32.0, "sweep_prolong": 66.0, "apply": 56.0, "resid_restrict": 58.0}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hmg", choices=["hmg", "reference"])
+    ap.add_argument("--config", default="C2a", choices=["C2a", "C2b", "C2c", "C0", "C1"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as fh:
+            return json.load(fh).get(kernel)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clock and throttle reasons during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id, self.lines, self.proc = gpu_id, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def oracle_sample(cfg, lam, b, threads: int):
+    """Bounded oracle sample: the oracle's PCG on the same workload, truncated
+    at 2 iterations (2 V-cycles, 2 operator applies, the CG vector work)."""
+    os.environ["OMP_NUM_THREADS"] = str(threads)
+    import oracle
+    h = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    t0 = time.perf_counter()
+    _, it, _, _, _ = h.pcg(b, rtol=1e-30, maxit=2)
+    dt = time.perf_counter() - t0
+    h.close()
+    nv = it  # V-cycles executed: 1 at setup + (it - 1) inside the loop
+    return cfg.ndofs * nv / dt, dt, nv
+
+
+def run_reference(args, ws, rank):
+    """--impl reference: the oracle (the paper-defined CPU program of this
+    repo, oracle/) timed as it stands on the host cores; rank 0 only."""
+    if rank != 0:
+        return
+    cfg = hi.CONFIGS[args.config]
+    lam, b = hi.make_inputs(cfg)
+    cores = len(os.sched_getaffinity(0))
+    os.environ["OMP_NUM_THREADS"] = str(cores)
+    import oracle
+    h = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    for _ in range(args.warmup):
+        h.pcg(b, rtol=1e-30, maxit=2)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        _, it, _, _, _ = h.pcg(b, rtol=1e-30, maxit=2)
+        times.append(time.perf_counter() - t0)
+    h.close()
+    t = float(np.mean(times))
+    value = cfg.ndofs * it / t
+    sample = f"oracle PCG on {cfg.name} truncated at 2 iterations (2 V-cycles + 2 applies) per step"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: ref {cfg.fine_ref}->0 x {cfg.nz} layers, {cfg.ndofs} dofs, "
+                               f"t={cfg.thickness}, w2={cfg.w2}", "params": "V(2,2) omega 0.8, 20 coarse sweeps"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def run_hmg(args, ws, rank, local):
+    import torch
+    import torch.distributed as dist
+    from paper_1605_00492_b200 import Hierarchy, MGParams
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA GPU (no CPU fallback exists)")
+    torch.cuda.set_device(local)
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    cfg = hi.CONFIGS[args.config]
+    lam, b = hi.make_inputs(cfg, seed=cfg.seed + rank)
+    t0 = time.perf_counter()
+    h = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, device=local)
+    setup_s = time.perf_counter() - t0
+    r = cfg.fine_ref
+    bd = h.to_device(r, b)
+    x = h.empty(r)
+    params = MGParams()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if ws == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- warm-up ------------------------------------------------------------
+    iters = None
+    for _ in range(max(args.warmup, 3)):
+        _, iters, relres, st = h.pcg_solve(bd, x, rtol=1e-8, maxit=200, params=params)
+    assert st == "HMG_OK", st
+    nv = iters  # V-cycles per solve: 1 before the loop + 1 per non-final iteration
+
+    # ---- timed region: K full solves, CUDA events on the launching stream ----
+    props = torch.cuda.get_device_properties(local)
+    gpu_id = f"GPU-{props.uuid}" if hasattr(props, "uuid") else str(local)
+    launches0 = h.launches
+    h.profile_begin()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(gpu_id) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            _, it, relres, st = h.pcg_solve(bd, x, rtol=1e-8, maxit=200, params=params)
+            assert it == iters and st == "HMG_OK"
+        e1.record(stream)
+        barrier()
+    h.profile_end()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    launches = h.launches - launches0
+    value = ws * cfg.ndofs * nv / (ms * 1e-3)
+
+    # ---- dominant kernel: the fused line-Jacobi sweep on the finest level ----
+    n_sw, ms_sw = h.profile_query("sweep", r)
+    avg_sw = ms_sw / max(n_sw, 1)
+    bytes_sw = BYTES_PER_DOF["sweep"] * cfg.ndofs
+    peak, peak_note = measured_peak()
+    achieved = bytes_sw / (avg_sw * 1e-3) / 1e9
+    shares = {}
+    for k in ("sweep", "sweep_zero", "sweep_prolong", "apply", "resid_restrict", "restrict", "prolong", "vector"):
+        n_k, ms_k = h.profile_query(k, -1)
+        shares[k] = round(ms_k / (ms * args.steps), 4)
+    fine = {}
+    for k in ("sweep", "sweep_zero", "sweep_prolong", "apply", "resid_restrict"):
+        n_k, ms_k = h.profile_query(k, r)
+        if n_k:
+            avg = ms_k / n_k
+            fine[k] = {"us": round(avg * 1e3, 2), "GB/s": round(BYTES_PER_DOF[k] * cfg.ndofs / (avg * 1e-3) / 1e9, 1)}
+
+    # ---- V-cycle alone -------------------------------------------------------
+    z = h.empty(r)
+    for _ in range(3):
+        h.vcycle(bd, z, params)
+    barrier()
+    e0.record(stream)
+    nvc = 20
+    for _ in range(nvc):
+        h.vcycle(bd, z, params)
+    e1.record(stream)
+    barrier()
+    ms_vc = max_over_ranks(e0.elapsed_time(e1) / nvc)
+
+    # ---- end to end: host buffers through hmg_pcg_solve_host ----------------
+    n = cfg.n
+    hb = torch.from_numpy(b).pin_memory()
+    hx = torch.empty_like(hb).pin_memory()
+    bnp, xnp = hb.numpy(), hx.numpy()
+    h.pcg_solve_host(bnp, xnp)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        _, it_e, _, st_e = h.pcg_solve_host(bnp, xnp)
+    e1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    e2e_value = ws * cfg.ndofs * nv / (ms_e2e * 1e-3)
+
+    # ---- oracle on the host cores (rank 0, N = 1 only) -----------------------
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        v, dt, nvo = oracle_sample(cfg, lam, b, cores)
+        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"oracle PCG on {cfg.name} truncated at 2 iterations ({nvo} V-cycles, 2 applies): {dt:.2f} s"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{cfg.name}: PCG + V(2,2) solve to 1e-8, ref {cfg.fine_ref}->0 x {cfg.nz} layers",
+                       "dofs_per_gpu": cfg.ndofs, "thickness": cfg.thickness, "w2": cfg.w2,
+                       "pcg_iterations": iters, "vcycles_per_step": nv, "final_relres": relres,
+                       "parallelism": "replicas" if ws > 1 else "single GPU",
+                       "cache": "inputs larger than L2 (bands 840 MB + vectors per level)"},
+            "pcg_solve_ms": ms,
+            "vcycle_only": {"value": ws * cfg.ndofs / (ms_vc * 1e-3), "unit": UNIT, "ms": ms_vc},
+            "setup_s": setup_s,
+            "roofline": {"kernel": "k_sweep_tc (fused residual + Thomas line sweep, finest level)",
+                         "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic("k_sweep_tc<0, 0, 2>"),
+                         "algorithmic_bytes_per_launch": bytes_sw, "avg_launch_us": avg_sw * 1e3,
+                         "launches_timed": n_sw, "peak_source": peak_note},
+            "fine_level_kernels": fine,
+            "time_share": shares,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * cfg.nz * n),
+                    "d2h_bytes_per_step": int(8 * cfg.nz * n), "ms_per_step": ms_e2e},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(out))
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_hmg(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

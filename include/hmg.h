@@ -160,6 +160,17 @@ hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, doubl
  * (diagnostic counter used by the benchmark's gpu_launches claim). */
 int64_t hmg_launch_count(const hmg_hierarchy* h);
 
+/* Diagnostics: CUDA-event timing of the library's kernel launches.
+ * hmg_profile_begin clears and enables recording (an event pair on the
+ * launching stream around every kernel), hmg_profile_end disables it, and
+ * hmg_profile_query sums the recorded durations (synchronising on them) for
+ * one kernel class on level `ref` (ref < 0: all levels).  Classes:
+ * 0 apply, 1 zero-guess sweep, 2 sweep, 3 sweep with fused prolongation,
+ * 4 residual+restriction, 5 restriction, 6 prolongation, 7 CG vector kernels. */
+hmg_status hmg_profile_begin(hmg_hierarchy* h);
+hmg_status hmg_profile_end(hmg_hierarchy* h);
+hmg_status hmg_profile_query(const hmg_hierarchy* h, int kernel_class, int ref, int64_t* count, double* total_ms);
+
 /* Diagnostic: for device arrays a, b of length n, writes fast[i] = the
  * shared-reciprocal division the sweep kernel uses and ref[i] = a[i] / b[i]
  * (the compiler's div.rn.f64).  The two must be bitwise equal. */

@@ -75,6 +75,9 @@ def load_library():
         "hmg_pcg_solve_single_level": [P, I, D, P, P, D, I, pI, pD, P],
         "hmg_export_level": [P, I, P, P, P, P],
         "hmg_selftest_div": [P, P, P, P, I64, P],
+        "hmg_profile_begin": [P],
+        "hmg_profile_end": [P],
+        "hmg_profile_query": [P, I, I, pI64, pD],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -229,6 +232,23 @@ class Hierarchy:
                                                         x.ctypes.data_as(ctypes.c_void_p), rtol, maxit,
                                                         ctypes.byref(it), ctypes.byref(rr), _stream()), allow=(5,))
         return x, it.value, rr.value, STATUS[code]
+
+    # -- diagnostics -----------------------------------------------------------
+    KERNEL_CLASSES = {"apply": 0, "sweep_zero": 1, "sweep": 2, "sweep_prolong": 3, "resid_restrict": 4,
+                      "restrict": 5, "prolong": 6, "vector": 7}
+
+    def profile_begin(self):
+        _check(load_library().hmg_profile_begin(self._h))
+
+    def profile_end(self):
+        _check(load_library().hmg_profile_end(self._h))
+
+    def profile_query(self, kernel_class: str, ref: int = -1):
+        """(launch count, total ms) of one kernel class recorded since profile_begin."""
+        n, ms = ctypes.c_int64(), ctypes.c_double()
+        _check(load_library().hmg_profile_query(self._h, self.KERNEL_CLASSES[kernel_class], ref, ctypes.byref(n),
+                                                ctypes.byref(ms)))
+        return n.value, ms.value
 
     def export_level(self, ref: int) -> dict:
         n, _ = self.level_info(ref)

@@ -56,6 +56,7 @@ hmg_status check_h(const hmg_hierarchy* h) {
 }
 
 const Hierarchy& HH(const hmg_hierarchy* h) { return *reinterpret_cast<const Hierarchy*>(h); }
+Hierarchy& HH(hmg_hierarchy* h) { return *reinterpret_cast<Hierarchy*>(h); }
 
 hmg_status check_level(const Hierarchy& H, int ref, const char* name) {
     if (ref < H.coarsest_ref || ref > H.fine_ref)
@@ -106,6 +107,7 @@ void free_hierarchy(Hierarchy* H) {
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q);
     cudaFree(H->partials); cudaFree(H->scal); cudaFree(H->hb); cudaFree(H->hx);
     if (H->scal_host) cudaFreeHost(H->scal_host);
+    for (cudaEvent_t e : H->prof.pool) cudaEventDestroy(e);
     delete H;
 }
 
@@ -559,6 +561,41 @@ hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, doubl
 }
 
 int64_t hmg_launch_count(const hmg_hierarchy* h) { return h ? HH(h).launches : -1; }
+
+hmg_status hmg_profile_begin(hmg_hierarchy* h) {
+    HMG_TRY(check_h(h));
+    Profiler& P = HH(h).prof;
+    P.on = true;
+    P.used = 0;
+    P.cls.clear();
+    P.ref.clear();
+    return HMG_OK;
+}
+
+hmg_status hmg_profile_end(hmg_hierarchy* h) {
+    HMG_TRY(check_h(h));
+    HH(h).prof.on = false;
+    return HMG_OK;
+}
+
+hmg_status hmg_profile_query(const hmg_hierarchy* h, int kernel_class, int ref, int64_t* count, double* total_ms) {
+    HMG_TRY(check_h(h));
+    HMG_TRY(check_ptr(count, "count"));
+    HMG_TRY(check_ptr(total_ms, "total_ms"));
+    if (kernel_class < 0 || kernel_class >= kKNumClasses) return fail(HMG_ERR_INVALID_ARG, "kernel_class: unknown");
+    const Profiler& P = HH(h).prof;
+    *count = 0;
+    *total_ms = 0.0;
+    for (size_t i = 0; i < P.cls.size(); ++i) {
+        if (P.cls[i] != kernel_class || (ref >= 0 && P.ref[i] != ref)) continue;
+        float ms = 0.f;
+        HMG_CUDA(cudaEventSynchronize(P.pool[2 * i + 1]));
+        HMG_CUDA(cudaEventElapsedTime(&ms, P.pool[2 * i], P.pool[2 * i + 1]));
+        *count += 1;
+        *total_ms += ms;
+    }
+    return HMG_OK;
+}
 
 hmg_status hmg_selftest_div(const double* a, const double* b, double* fast, double* ref, int64_t n, void* stream) {
     HMG_TRY(check_ptr(a, "a"));

@@ -67,6 +67,19 @@ struct PcgScalars {
     unsigned long long bad;     // encoded (ref << 40 | column) of the first bad pivot, or ~0
 };
 
+// Optional per-launch CUDA-event timing (hmg_profile_*): each instrumented
+// launch records an event pair on its own stream; totals are read back per
+// (kernel class, level).  Off by default; the benchmark turns it on for the
+// timed region to report the dominant kernel's live duration.
+enum KernelClass { kKApply = 0, kKSweepZero, kKSweep, kKSweepProlong, kKResidRestrict, kKRestrict, kKProlong,
+                   kKVector, kKNumClasses };
+struct Profiler {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;   // pairs
+    size_t used = 0;                 // events in use
+    std::vector<int> cls, ref;       // per pair
+};
+
 struct Hierarchy {
     int device = 0;
     int fine_ref = 0, coarsest_ref = 0, nz = 0;
@@ -80,6 +93,7 @@ struct Hierarchy {
     PcgScalars* scal_host = nullptr;  // pinned
     double *hb = nullptr, *hx = nullptr;  // device staging for the host entry point
     mutable int64_t launches = 0;
+    mutable Profiler prof;
     bool use_tc_sweep = true;   // HMG_SWEEP=simple selects the reference-layout kernel (diagnostics)
 };
 
@@ -114,6 +128,15 @@ void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, con
 const char* take_launch_error();
 bool tensor_maps_available();
 void launch_selftest_div(int64_t n, const double* a, const double* b, double* fast, double* ref, cudaStream_t s);
+
+// RAII event pair around one launch when profiling is on.
+struct ProfScope {
+    const Hierarchy& H;
+    cudaStream_t s;
+    cudaEvent_t stop = nullptr;
+    ProfScope(const Hierarchy& h, int cls, int ref, cudaStream_t st);
+    ~ProfScope();
+};
 
 enum FinalizeOp { kFinPQ = 0, kFinRR = 1, kFinRZ = 2, kFinRhoInit = 3, kFinBB = 4 };
 

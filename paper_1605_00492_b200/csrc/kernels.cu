@@ -361,6 +361,28 @@ void set_smem_attr() {
 
 }  // namespace
 
+ProfScope::ProfScope(const Hierarchy& h, int cls, int ref, cudaStream_t st) : H(h), s(st) {
+    Profiler& P = H.prof;
+    if (!P.on) return;
+    if (P.used + 2 > P.pool.size()) {
+        for (int i = 0; i < 256; ++i) {
+            cudaEvent_t e;
+            if (cudaEventCreate(&e) != cudaSuccess) return;
+            P.pool.push_back(e);
+        }
+    }
+    cudaEvent_t start = P.pool[P.used];
+    stop = P.pool[P.used + 1];
+    P.used += 2;
+    P.cls.push_back(cls);
+    P.ref.push_back(ref);
+    cudaEventRecord(start, s);
+}
+
+ProfScope::~ProfScope() {
+    if (stop) cudaEventRecord(stop, s);
+}
+
 int partials_needed(int64_t n) {
     const int a = (int)blocks(n, kApplyBlock), v = (int)blocks(n, kVecCells);
     return a > v ? a : v;
@@ -379,11 +401,13 @@ void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
 }
 
 void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
+    ProfScope ps(H, kKApply, L.ref, s);
     k_apply<false><<<blocks(L.n, kApplyBlock), kApplyBlock, 0, s>>>(L.view(H.nz), x, y, nullptr);
     ++H.launches;
 }
 
 void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
+    ProfScope ps(H, kKApply, L.ref, s);
     k_apply<true><<<blocks(L.n, kApplyBlock), kApplyBlock, 0, s>>>(L.view(H.nz), x, y, H.partials);
     ++H.launches;
     k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)blocks(L.n, kApplyBlock), kFinPQ, H.scal);
@@ -392,6 +416,7 @@ void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, do
 
 void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin,
                   const double* uc, double* uout, double omega, cudaStream_t s) {
+    ProfScope ps(H, !uin ? kKSweepZero : (uc ? kKSweepProlong : kKSweep), L.ref, s);
     if (H.use_tc_sweep && sweep_tc_supported(H, L)) {
         launch_sweep_tc(H, L, b, uin, uc, uout, omega, s);
         return;
@@ -415,6 +440,7 @@ void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const 
 }
 
 void launch_restrict(const Hierarchy& H, const DevLevel& F, const double* r, double* bc, cudaStream_t s) {
+    ProfScope ps(H, kKRestrict, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
     dim3 g(blocks(C.n, 256), H.nz);
     k_restrict<<<g, 256, 0, s>>>(r, F.ld, bc, C.ld, C.n);
@@ -423,6 +449,7 @@ void launch_restrict(const Hierarchy& H, const DevLevel& F, const double* r, dou
 
 void launch_resid_restrict(const Hierarchy& H, const DevLevel& F, const double* b, const double* u,
                            double* bc, cudaStream_t s) {
+    ProfScope ps(H, kKResidRestrict, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
     k_resid_restrict<<<blocks(F.n, kApplyBlock), kApplyBlock, 0, s>>>(F.view(H.nz), b, u, bc, C.ld);
     ++H.launches;
@@ -430,6 +457,7 @@ void launch_resid_restrict(const Hierarchy& H, const DevLevel& F, const double* 
 
 void launch_prolong_add(const Hierarchy& H, const DevLevel& F, const double* uin, const double* uc,
                         double* uout, cudaStream_t s) {
+    ProfScope ps(H, kKProlong, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
     dim3 g(blocks(F.n, 256), H.nz);
     k_prolong_add<<<g, 256, 0, s>>>(uin, uc, uout, F.ld, C.ld, F.n);
@@ -437,6 +465,7 @@ void launch_prolong_add(const Hierarchy& H, const DevLevel& F, const double* uin
 }
 
 void launch_dot(const Hierarchy& H, const DevLevel& L, const double* a, const double* b, cudaStream_t s) {
+    ProfScope ps(H, kKVector, H.fine_ref, s);
     k_dot<<<blocks(L.n, kVecCells), kVecBlock, 0, s>>>(a, b, L.n, L.ld, H.nz, H.partials);
     ++H.launches;
 }
@@ -448,12 +477,14 @@ void launch_finalize(const Hierarchy& H, int op, cudaStream_t s) {
 }
 
 void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, cudaStream_t s) {
+    ProfScope ps(H, kKVector, H.fine_ref, s);
     k_update_xr<<<blocks(L.n, kVecCells), kVecBlock, 0, s>>>(x, H.r, H.p, H.q, L.n, L.ld, H.nz, H.scal,
                                                              H.partials);
     ++H.launches;
 }
 
 void launch_update_p(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
+    ProfScope ps(H, kKVector, H.fine_ref, s);
     k_update_p<<<blocks(L.n, kVecCells), kVecBlock, 0, s>>>(H.p, H.z, L.n, L.ld, H.nz, H.scal);
     ++H.launches;
 }
