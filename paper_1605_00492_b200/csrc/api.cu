@@ -103,6 +103,7 @@ void free_hierarchy(Hierarchy* H) {
         cudaFree(L.nbr); cudaFree(L.geom); cudaFree(L.lam); cudaFree(L.bands);
         cudaFree(L.wa); cudaFree(L.wb); cudaFree(L.b); cudaFree(L.u);
         cudaFree(L.halo_cells); cudaFree(L.halo_count); cudaFree(L.halo_loc);
+        cudaFree(L.fden);
     }
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q);
     cudaFree(H->partials); cudaFree(H->scal); cudaFree(H->hb); cudaFree(H->hx);
@@ -135,8 +136,16 @@ const double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b,
 void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const double* b, double* out,
                   cudaStream_t s) {
     const DevLevel& L = H.lev[ref];
+    if (ref == H.tail_ref) {                    // levels <= tail_ref: one launch
+        launch_coarse_tail(H, p, b, out, s);
+        return;
+    }
     if (ref == H.coarsest_ref) {
-        run_sweeps(H, L, b, nullptr, nullptr, p.n_coarse, out, p.omega, s);
+        // whole coarsest level in one CTA's shared memory when it fits (ref 0: 20 columns)
+        if (L.fden && L.n <= 128 && coarsest_smem_bytes(H.nz, L.n, (int)((L.n + 31) / 32 * 32)) <= 200 * 1024)
+            launch_coarsest(H, L, b, out, p.n_coarse, p.omega, s);
+        else
+            run_sweeps(H, L, b, nullptr, nullptr, p.n_coarse, out, p.omega, s);
         return;
     }
     const DevLevel& C = H.lev[ref - 1];
@@ -248,6 +257,16 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
     H->w2 = w2;
     H->dz = thickness / nlayers;
     if (const char* e = std::getenv("HMG_SWEEP")) H->use_tc_sweep = std::string(e) != "simple";
+    {
+        int tail = -1;   // default: per-level kernels (HMG_TAIL_REF=r enables the one-launch tail)
+        if (const char* e = std::getenv("HMG_TAIL_REF")) tail = std::atoi(e);
+        if (tail < 0) {
+            H->tail_ref = -1;
+        } else {
+            tail = std::max(tail, coarsest_ref);
+            H->tail_ref = std::min(tail, fine_ref);
+        }
+    }
     if (H->use_tc_sweep && !tensor_maps_available()) {
         delete H;
         return fail(HMG_ERR_CUDA, "cuTensorMapEncodeTiled not available from the CUDA driver");
@@ -364,13 +383,33 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
         BCUDA(cudaMalloc(v, fb));
         BCUDA(cudaMemset(*v, 0, fb));
     }
-    H->npartials = partials_needed(F.n);
+    H->npartials = partials_needed(F.n, nlayers);
     BCUDA(cudaMalloc(&H->partials, sizeof(double) * H->npartials));
     BCUDA(cudaMalloc(&H->scal, sizeof(PcgScalars)));
     BCUDA(cudaMallocHost(&H->scal_host, sizeof(PcgScalars)));
     PcgScalars init{};
     init.bad = ~0ull;
     BCUDA(cudaMemcpy(H->scal, &init, sizeof(init), cudaMemcpyHostToDevice));
+    // Thomas factors (matrix-only; computed once) for the coarse-tail levels and
+    // for every level too small to fill the GPU (latency-bound sweeps)
+    for (int r = coarsest_ref; r <= fine_ref; ++r) {
+        DevLevel& L = H->lev[r];
+        if (!(r <= H->tail_ref || L.n <= kFactMaxCells)) continue;
+        const size_t vb = sizeof(double) * nlayers * L.ld;
+        BCUDA(cudaMalloc(&L.fden, 3 * vb));          // [3][nz][ld]: den, y, g (one TMA box)
+        L.fy = L.fden + (size_t)nlayers * L.ld;
+        L.fg = L.fy + (size_t)nlayers * L.ld;
+        launch_factor(*H, L, s);
+    }
+    BCUDA(cudaGetLastError());
+    BCUDA(cudaDeviceSynchronize());
+    {
+        unsigned long long bad = 0;
+        BCUDA(cudaMemcpy(&bad, &H->scal->bad, sizeof(bad), cudaMemcpyDeviceToHost));
+        if (bad != ~0ull)
+            return cleanup(fail(HMG_ERR_SINGULAR_COLUMN, "singular column: ref " + std::to_string(bad >> 40) +
+                                                             " column " + std::to_string(bad & ((1ull << 40) - 1))));
+    }
     BCUDA(cudaGetLastError());
     BCUDA(cudaDeviceSynchronize());
 #undef BCUDA

@@ -13,7 +13,8 @@ namespace hmg {
 constexpr int kMaxLayers = 256;   // Thomas state for a column lives in shared memory
 constexpr int kMaxRef = 10;
 constexpr int kSweepTile = 128;   // columns per CTA of the TMA/TMEM sweep (sweep_tc.cu)
-constexpr int kHaloMax = 64;      // max off-tile neighbour cells per tile (51 observed at ref >= 2)
+constexpr int kHaloMax = 64;
+constexpr int64_t kFactMaxCells = 148 * 128;  // levels up to this size stream precomputed Thomas pivots      // max off-tile neighbour cells per tile (51 observed at ref >= 2)
 
 // Per-level tile halo for the streamed sweep: for tile t (cells
 // [t*kSweepTile, (t+1)*kSweepTile)), the sorted distinct neighbour cells
@@ -54,10 +55,29 @@ struct DevLevel {
     int32_t* halo_count = nullptr;
     uint32_t* halo_loc = nullptr;
     TileHalo halo;
+    // Thomas factors (coarse-tail levels only): pivots, refined reciprocals, multipliers
+    double* fden = nullptr;
+    double* fy = nullptr;
+    double* fg = nullptr;
     LevelView view(int nz) const {
         const int64_t s = (int64_t)nz * ld;
         return LevelView{n, ld, nz, nbr, bands, bands + s, bands + 2 * s, bands + 3 * s, bands + 4 * s};
     }
+};
+
+// One level as seen by the coarse-tail kernel (coarse_tail.cu).
+struct TailLevel {
+    LevelView V;
+    double *wa, *wb, *b, *u;
+    const double *den, *y, *g;
+    int64_t ldc;                // coarse leading dimension for the fused prolongation (set in-kernel)
+};
+struct TailParams {
+    TailLevel lev[kMaxRef + 1];
+    int nz, top, coarsest, nu_pre, nu_post, n_coarse;
+    double omega;
+    const double* b_top;
+    double* out_top;
 };
 
 // Device-resident PCG scalars: one struct so a single 64-byte D2H read per
@@ -72,7 +92,7 @@ struct PcgScalars {
 // (kernel class, level).  Off by default; the benchmark turns it on for the
 // timed region to report the dominant kernel's live duration.
 enum KernelClass { kKApply = 0, kKSweepZero, kKSweep, kKSweepProlong, kKResidRestrict, kKRestrict, kKProlong,
-                   kKVector, kKNumClasses };
+                   kKVector, kKCoarseTail, kKNumClasses };
 struct Profiler {
     bool on = false;
     std::vector<cudaEvent_t> pool;   // pairs
@@ -92,6 +112,7 @@ struct Hierarchy {
     PcgScalars* scal = nullptr; // device
     PcgScalars* scal_host = nullptr;  // pinned
     double *hb = nullptr, *hx = nullptr;  // device staging for the host entry point
+    int tail_ref = -1;          // levels <= tail_ref run in one coarse-tail launch (-1: off)
     mutable int64_t launches = 0;
     mutable Profiler prof;
     bool use_tc_sweep = true;   // HMG_SWEEP=simple selects the reference-layout kernel (diagnostics)
@@ -118,12 +139,19 @@ void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, cudaStre
 void launch_update_p(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
 void launch_copy_pad(const Hierarchy& H, const DevLevel& L, const double* src, int64_t src_ld,
                      double* dst, int64_t dst_ld, cudaStream_t s);
-int partials_needed(int64_t n);
+int partials_needed(int64_t n, int nz);
 // sweep_tc.cu: TMA-streamed, TMEM-state sweep (same arithmetic as launch_sweep's kernel)
 bool sweep_tc_supported(const Hierarchy& H, const DevLevel& L);
 void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                      double* uout, double omega, cudaStream_t s);
 
+// coarse_tail.cu
+void launch_factor(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
+void launch_coarse_tail(const Hierarchy& H, const hmg_mg_params& p, const double* b_top, double* out_top,
+                        cudaStream_t s);
+size_t coarsest_smem_bytes(int nz, int64_t n, int threads);
+void launch_coarsest(const Hierarchy& H, const DevLevel& L, const double* b, double* out, int n_coarse, double omega,
+                     cudaStream_t s);
 // Error raised on the host side of a launch (tensor-map encoding); nullptr if none.
 const char* take_launch_error();
 bool tensor_maps_available();

@@ -93,13 +93,18 @@ __global__ void __launch_bounds__(kApplyBlock) k_apply(LevelView L, const double
                                                        double* __restrict__ y, double* __restrict__ partial) {
     __shared__ double red[kApplyBlock / 32];
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    // vertical chunk of this thread (gridDim.y chunks; 1 on fine levels)
+    const int nz = L.nz;
+    const int kc = (nz + gridDim.y - 1) / gridDim.y;
+    const int k0 = blockIdx.y * kc, k1 = min(nz, k0 + kc);
     double dot = 0.0;
-    if (c < L.n) {
+    if (c < L.n && k0 < k1) {
         const int64_t ld = L.ld;
-        const int nz = L.nz;
         const int32_t n0 = L.nbr[c], n1 = L.nbr[ld + c], n2 = L.nbr[2 * ld + c];
-        double xm = 0.0, xk = x[c], Um = 0.0;
-        for (int k = 0; k < nz; ++k) {
+        double xm = k0 > 0 ? x[(int64_t)(k0 - 1) * ld + c] : 0.0;
+        double Um = k0 > 0 ? L.U[(int64_t)(k0 - 1) * ld + c] : 0.0;
+        double xk = x[(int64_t)k0 * ld + c];
+        for (int k = k0; k < k1; ++k) {
             const int64_t row = k * ld, i = row + c;
             const double xp = (k + 1 < nz) ? x[i + ld] : 0.0;
             const double Uk = L.U[i];
@@ -118,7 +123,7 @@ __global__ void __launch_bounds__(kApplyBlock) k_apply(LevelView L, const double
     }
     if (DOT) {
         const double s = block_sum(dot, red);
-        if (threadIdx.x == 0) partial[blockIdx.x] = s;
+        if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
     }
 }
 
@@ -226,10 +231,15 @@ __global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, con
     const int64_t c = valid ? cc : L.n - 1;
     const int64_t ld = L.ld;
     const int nz = L.nz;
+    const int kc = (nz + gridDim.y - 1) / gridDim.y;
+    const int k0 = blockIdx.y * kc, k1 = min(nz, k0 + kc);
     const int32_t n0 = L.nbr[c], n1 = L.nbr[ld + c], n2 = L.nbr[2 * ld + c];
     const int lane = threadIdx.x & 31;
-    double um = 0.0, uk = u[c], Um = 0.0;
-    for (int k = 0; k < nz; ++k) {
+    if (k0 >= k1) return;                 // uniform across the block
+    double um = k0 > 0 ? u[(int64_t)(k0 - 1) * ld + c] : 0.0;
+    double Um = k0 > 0 ? L.U[(int64_t)(k0 - 1) * ld + c] : 0.0;
+    double uk = u[(int64_t)k0 * ld + c];
+    for (int k = k0; k < k1; ++k) {
         const int64_t row = k * ld, i = row + c;
         const double up = (k + 1 < nz) ? u[i + ld] : 0.0;
         const double Uk = L.U[i];
@@ -344,6 +354,16 @@ __global__ void k_copy_rows(const double* __restrict__ src, int64_t sld, double*
 
 inline unsigned blocks(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 
+// Vertical chunks for the column kernels: 1 on levels with enough columns to
+// fill the GPU; on small (coarse) levels split the layers so that the
+// sequential per-thread loop is short (these levels are latency-bound).
+unsigned vchunks(int64_t n, int nz) {
+    const int64_t target = 148LL * 1024;
+    int64_t c = (target + n - 1) / n;
+    if (c > nz / 4) c = nz / 4;
+    return c < 1 ? 1u : (unsigned)c;
+}
+
 int sweep_block(int nz) {
     int t = 4096 / nz;             // 2 * nz * t * 8 B = 64 KB of Thomas state per block
     t = t < 32 ? 32 : (t > 128 ? 128 : t);
@@ -383,8 +403,8 @@ ProfScope::~ProfScope() {
     if (stop) cudaEventRecord(stop, s);
 }
 
-int partials_needed(int64_t n) {
-    const int a = (int)blocks(n, kApplyBlock), v = (int)blocks(n, kVecCells);
+int partials_needed(int64_t n, int nz) {
+    const int a = (int)(blocks(n, kApplyBlock) * vchunks(n, nz)), v = (int)blocks(n, kVecCells);
     return a > v ? a : v;
 }
 
@@ -402,15 +422,17 @@ void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
 
 void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
     ProfScope ps(H, kKApply, L.ref, s);
-    k_apply<false><<<blocks(L.n, kApplyBlock), kApplyBlock, 0, s>>>(L.view(H.nz), x, y, nullptr);
+    dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
+    k_apply<false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, nullptr);
     ++H.launches;
 }
 
 void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
     ProfScope ps(H, kKApply, L.ref, s);
-    k_apply<true><<<blocks(L.n, kApplyBlock), kApplyBlock, 0, s>>>(L.view(H.nz), x, y, H.partials);
+    dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
+    k_apply<true><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, H.partials);
     ++H.launches;
-    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)blocks(L.n, kApplyBlock), kFinPQ, H.scal);
+    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)(g.x * g.y), kFinPQ, H.scal);
     ++H.launches;
 }
 
@@ -451,7 +473,8 @@ void launch_resid_restrict(const Hierarchy& H, const DevLevel& F, const double* 
                            double* bc, cudaStream_t s) {
     ProfScope ps(H, kKResidRestrict, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
-    k_resid_restrict<<<blocks(F.n, kApplyBlock), kApplyBlock, 0, s>>>(F.view(H.nz), b, u, bc, C.ld);
+    dim3 g(blocks(F.n, kApplyBlock), vchunks(F.n, H.nz));
+    k_resid_restrict<<<g, kApplyBlock, 0, s>>>(F.view(H.nz), b, u, bc, C.ld);
     ++H.launches;
 }
 

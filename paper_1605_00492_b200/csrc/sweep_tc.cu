@@ -44,8 +44,14 @@ constexpr int kThreads = kTile + 32;
 __device__ __forceinline__ bool pivot_ok(double den) { return den > 0.0 && den <= DBL_MAX; }
 
 // Tensor maps of one launch: bands (per level) + vectors (per call).
+// The band planes D, U, H0, H1, H2 are contiguous ([5][nz][ld]), and so are the
+// precomputed factors ([3][nz][ld]): one 3-D box moves every band (or factor)
+// of G layers in a single TMA instruction -- per-instruction latency, not
+// bytes, limits a CTA's TMA stream, so fewer, larger copies matter.
 struct SweepMaps {
-    CUtensorMap a[6];   // rows streamed through the ring: D, U, H0, H1, H2, b  (ZERO: D, U, b)
+    CUtensorMap bands;  // 3-D (cell, layer, band), box kTile x G x nb  (nb = 2: D, U; 5: D..H2)
+    CUtensorMap b;      // right-hand side, box kTile x G
+    CUtensorMap fact;   // 3-D factors den, y, g, box kTile x G x 3 (FACT only)
     CUtensorMap u;      // incoming iterate (box kTile x G)
     CUtensorMap uc;     // coarse correction (box kTile/4 x G), PROLONG only
 };
@@ -55,10 +61,10 @@ struct SweepSmem {
     size_t off_u, off_uc, off_stage, total;
 };
 
-__host__ __device__ inline SweepSmem sweep_layout(int nz, bool zero, bool prolong, int S, int G) {
+__host__ __device__ inline SweepSmem sweep_layout(int nz, bool zero, bool prolong, bool fact, int S, int G) {
     SweepSmem L;
     L.S = S;
-    L.nrows = zero ? 3 : 6;
+    L.nrows = (zero ? 3 : 6) + (fact ? 3 : 0);
     L.rows_pad = ((nz + G - 1) / G) * G;
     L.stage_doubles = L.nrows * G * kTile + (zero ? 0 : G * kHaloMax) + (prolong ? G * kHaloMax : 0);
     size_t off = 1024;  // barriers + TMEM slot
@@ -72,18 +78,27 @@ __host__ __device__ inline SweepSmem sweep_layout(int nz, bool zero, bool prolon
     return L;
 }
 
-template <bool ZERO, bool PROLONG, int G>
+#ifdef HMG_TIMING
+__device__ long long g_tc_timing[16];
+#define TSTAMP(i) do { if (blockIdx.x == 0 && (threadIdx.x == 0 || threadIdx.x == 128)) g_tc_timing[i] = clock64(); } while (0)
+#else
+#define TSTAMP(i) do {} while (0)
+#endif
+
+template <bool ZERO, bool PROLONG, bool FACT, int G>
 __global__ void __launch_bounds__(kThreads, 2)
-    k_sweep_tc(const __grid_constant__ SweepMaps maps, LevelView L, TileHalo th, const double* __restrict__ uin,
-               const double* __restrict__ uc, int64_t ldc, double* __restrict__ uout, double omega, int ref,
-               unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols) {
+    k_sweep_tc(const __grid_constant__ SweepMaps maps, LevelView L, TileHalo th, const double* __restrict__ bvec,
+               const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc,
+               const double* __restrict__ fdp, const double* __restrict__ fgp, double* __restrict__ uout,
+               double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     const int nz = L.nz;
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t c0 = (int64_t)blockIdx.x * kTile;
-    const SweepSmem lay = sweep_layout(nz, ZERO, PROLONG, S, G);
+    const SweepSmem lay = sweep_layout(nz, ZERO, PROLONG, FACT, S, G);
+    constexpr int kFactRow = ZERO ? 3 : 6;                            // den, y, g rows (FACT)
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
     uint64_t* empty = full + S;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + S);
@@ -92,6 +107,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     double* stages = reinterpret_cast<double*>(smraw + lay.off_stage);
     const int row_block = G * kTile;                                  // doubles per array per stage
 
+    TSTAMP(0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -104,6 +120,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    TSTAMP(1);
 
     if (warp == kConsumerWarps) {
         // ======================= producer warp =======================
@@ -141,13 +158,16 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             __syncwarp();
             if (lane == 0) {
-                uint32_t bytes = (uint32_t)lay.nrows * ublock;
+                uint32_t bytes = (uint32_t)lay.nrows * ublock;   // bands + b (+ factors)
                 const bool u0 = !ZERO && gi == 0;
                 const bool unext = !ZERO && gi + 1 < ngroups;
                 if (u0) bytes += ublock + (PROLONG ? ucblock : 0);
                 if (unext) bytes += ublock + (PROLONG ? ucblock : 0);
                 ptx::mbar_arrive_expect_tx(&full[s], bytes);
-                for (int a = 0; a < lay.nrows; ++a) ptx::tma_load_2d(st + a * row_block, &maps.a[a], x, gi * G, &full[s]);
+                constexpr int nb = ZERO ? 2 : 5;
+                ptx::tma_load_3d(st, &maps.bands, x, gi * G, 0, &full[s]);
+                ptx::tma_load_2d(st + nb * row_block, &maps.b, x, gi * G, &full[s]);
+                if (FACT) ptx::tma_load_3d(st + (nb + 1) * row_block, &maps.fact, x, gi * G, 0, &full[s]);
                 if (u0) {
                     ptx::tma_load_2d(utile, &maps.u, x, 0, &full[s]);
                     if (PROLONG) ptx::tma_load_2d(uctile, &maps.uc, xc, 0, &full[s]);
@@ -185,13 +205,51 @@ __global__ void __launch_bounds__(kThreads, 2)
 
         // Thomas forward elimination, reading R6 order: den_0 = D_0; for k >= 1
         // den_k = D_k - U_{k-1} g_{k-1}; z_k = (r_k - U_{k-1} z_{k-1}) / den_k;
-        // g_k = U_k / den_k.
+        // g_k = U_k / den_k.  One layer of it, from already-loaded operands;
+        // EXACT selects the '/' operator, otherwise the shared-reciprocal
+        // division whose rare invalid cases are flagged in `slow` (the whole
+        // column is then redone exactly, below, so the hot loop has no branch).
         double um = 0.0, uk = 0.0, Um = 0.0, gprev = 0.0, zprev = 0.0;
-        bool ok = true;
+        bool ok = true, slow = false;
+        auto layer = [&](int k, double Dk, double Uk, double r, double fden, double fy, double fg, bool exact) {
+            const double num = (k == 0) ? r : r - Um * zprev;
+            const bool has_g = k < nz - 1;
+            double den, z, g = 0.0;
+            if (FACT) {                           // pivots precomputed at setup (matrix-only)
+                den = fden;
+                g = fg;
+                z = exact ? num / den : div_fast(num, den, fy, slow);
+            } else {
+                den = (k == 0) ? Dk : Dk - Um * gprev;
+                if (exact) {
+                    z = num / den;
+                    if (has_g) g = Uk / den;
+                } else {
+                    const double y = div_recip(den);
+                    z = div_fast(num, den, y, slow);
+                    if (has_g) g = div_fast(Uk, den, y, slow);
+                }
+                ok = ok && pivot_ok(den);
+            }
+            ptx::tmem_st_f64(tl + 2u * (uint32_t)k, z);
+            if (has_g) ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, g);
+            zprev = z;
+            gprev = g;
+        };
         int s = 0;
         uint32_t phase = 0;
+#ifdef HMG_TIMING
+        long long wait_acc = 0;
+#endif
         for (int gi = 0; gi < ngroups; ++gi, (++s == S ? (s = 0, phase ^= 1u) : 0)) {
+#ifdef HMG_TIMING
+            long long tw0 = clock64();
+#endif
             ptx::mbar_wait(&full[s], phase);
+#ifdef HMG_TIMING
+            wait_acc += clock64() - tw0;
+#endif
+            if (gi == 0) TSTAMP(2);
             const double* st = stages + (size_t)s * lay.stage_doubles;
 #pragma unroll
             for (int kk = 0; kk < G; ++kk) {
@@ -205,7 +263,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (ZERO) {
                     r = sr[2 * row_block];
                 } else {
-                    const double* hu = st + 6 * row_block + kk * kHaloMax;
+                    const double* hu = st + lay.nrows * row_block + kk * kHaloMax;
                     if (k == 0) uk = UV(0, j);
                     if (k < nz - 1) up = UV(k + 1, j);
                     double acc = Dk * uk;
@@ -216,23 +274,13 @@ __global__ void __launch_bounds__(kThreads, 2)
                     acc = acc + sr[4 * row_block] * NBR(k, l2, hu);
                     r = sr[5 * row_block] - acc;
                 }
-                const double den = (k == 0) ? Dk : Dk - Um * gprev;
-                const double num = (k == 0) ? r : r - Um * zprev;
-                const double y = div_recip(den);
-                bool slow = false;
-                double z = div_fast(num, den, y, slow);
-                double g = 0.0;
-                const bool has_g = k < nz - 1;
-                if (has_g) g = div_fast(Uk, den, y, slow);
-                if (slow) {
-                    z = num / den;
-                    if (has_g) g = Uk / den;
+                double fden = 0.0, fy = 0.0, fg = 0.0;
+                if (FACT) {
+                    fden = sr[kFactRow * row_block];
+                    fy = sr[(kFactRow + 1) * row_block];
+                    fg = sr[(kFactRow + 2) * row_block];
                 }
-                ok = ok && pivot_ok(den);
-                ptx::tmem_st_f64(tl + 2u * (uint32_t)k, z);
-                if (has_g) ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, g);
-                zprev = z;
-                gprev = g;
+                layer(k, Dk, Uk, r, fden, fy, fg, false);
                 um = uk;
                 uk = up;
                 Um = Uk;
@@ -240,8 +288,48 @@ __global__ void __launch_bounds__(kThreads, 2)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&empty[s]);
         }
+        TSTAMP(3);
+#ifdef HMG_TIMING
+        if (blockIdx.x == 0 && threadIdx.x == 0) g_tc_timing[8] = wait_acc;
+#endif
+        // Rare: a quotient left the fast path's exact range (e.g. a zero
+        // numerator).  The warp recomputes its columns' forward pass from
+        // global memory with the '/' operator (TMEM stores are warp-wide).
+        if (__any_sync(0xffffffffu, slow && valid)) {
+            const int64_t ce = valid ? c : L.n - 1;
+            const int32_t g0 = ZERO ? 0 : L.nbr[ce], g1 = ZERO ? 0 : L.nbr[ld + ce], g2 = ZERO ? 0 : L.nbr[2 * ld + ce];
+            auto GU = [&](int kk, int64_t cell) -> double {
+                double v = uin[(int64_t)kk * ld + cell];
+                if (PROLONG) v = v + uc[(int64_t)kk * ldc + (cell >> 2)];
+                return v;
+            };
+            um = uk = Um = gprev = zprev = 0.0;
+            if (!ZERO) uk = GU(0, ce);
+            for (int k = 0; k < nz; ++k) {
+                const int64_t i = (int64_t)k * ld + ce;
+                const double Dk = L.D[i], Uk = L.U[i];
+                double r, up = 0.0;
+                if (ZERO) {
+                    r = bvec[i];
+                } else {
+                    if (k < nz - 1) up = GU(k + 1, ce);
+                    double acc = Dk * uk;
+                    if (k > 0) acc = acc + Um * um;
+                    if (k < nz - 1) acc = acc + Uk * up;
+                    acc = acc + L.H0[i] * GU(k, g0);
+                    acc = acc + L.H1[i] * GU(k, g1);
+                    acc = acc + L.H2[i] * GU(k, g2);
+                    r = bvec[i] - acc;
+                }
+                layer(k, Dk, Uk, r, FACT ? fdp[i] : 0.0, 0.0, FACT ? fgp[i] : 0.0, true);
+                um = uk;
+                uk = up;
+                Um = Uk;
+            }
+        }
         if (valid && !ok) atomicMin(bad, ((unsigned long long)ref << 40) | (unsigned long long)c);
         ptx::tmem_wait_st();
+        TSTAMP(4);
 
         // back substitution from the top layer, 8 layers of (z, g) per TMEM load
         double dl = 0.0;
@@ -282,9 +370,11 @@ __global__ void __launch_bounds__(kThreads, 2)
             k = k0 - 1;
         }
     }
+    TSTAMP(5);
     ptx::tc_fence_before();
     __syncthreads();
     if (warp == 0) ptx::tmem_dealloc(tbase, tmem_cols);
+    TSTAMP(6);
 }
 
 __global__ void k_selftest_div(int64_t n, const double* __restrict__ a, const double* __restrict__ b,
@@ -318,20 +408,45 @@ EncodeFn encode_fn() {
     return fn;
 }
 
-// 2-D map over a layer-major [rows][ld] fp64 array; box = box_x cells x G layers.
+// Map over `planes` consecutive layer-major [rows][ld] fp64 arrays (planes = 1:
+// 2-D, else 3-D with plane stride rows*ld); box = box_x cells x G layers x planes.
 // Out-of-range box elements (tail tile, layers >= rows) are zero-filled.
-CUtensorMap make_map(const double* base, int64_t ld, int64_t rows, int box_x, int G) {
+CUtensorMap encode_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
-    const cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
-    const cuuint64_t strides[1] = {(cuuint64_t)(ld * sizeof(double))};
-    const cuuint32_t box[2] = {(cuuint32_t)box_x, (cuuint32_t)G};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box,
-                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+    const cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)rows, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)(ld * sizeof(double)), (cuuint64_t)(rows * ld * sizeof(double))};
+    const cuuint32_t box[3] = {(cuuint32_t)box_x, (cuuint32_t)G, (cuuint32_t)planes};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, planes == 1 ? 2 : 3, const_cast<double*>(base), dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) throw std::runtime_error("cuTensorMapEncodeTiled failed");
     return m;
+}
+
+// Encoding a tensor map costs host microseconds; the V-cycle and PCG reuse the
+// same few buffers every call, so maps are cached by (base, ld, rows, box).
+struct MapKey {
+    const double* base;
+    int64_t ld, rows;
+    int box_x, G, planes;
+    bool operator==(const MapKey& o) const {
+        return base == o.base && ld == o.ld && rows == o.rows && box_x == o.box_x && G == o.G && planes == o.planes;
+    }
+};
+CUtensorMap make_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes = 1) {
+    constexpr int kCache = 128;
+    static thread_local MapKey keys[kCache];
+    static thread_local CUtensorMap maps[kCache];
+    static thread_local int used = 0, next = 0;
+    const MapKey k{base, ld, rows, box_x, G, planes};
+    for (int i = 0; i < used; ++i)
+        if (keys[i] == k) return maps[i];
+    const int slot = used < kCache ? used++ : (next++ % kCache);
+    keys[slot] = k;
+    maps[slot] = encode_map(base, ld, rows, box_x, G, planes);
+    return maps[slot];
 }
 
 uint32_t tmem_cols_for(int nz) {
@@ -340,41 +455,37 @@ uint32_t tmem_cols_for(int nz) {
     return c;
 }
 
-template <bool Z, bool P, int G>
+template <bool Z, bool P, bool F, int G>
 void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                double* uout, double omega, cudaStream_t s) {
     const int nz = H.nz;
     const uint32_t cols = tmem_cols_for(nz);
     // Budget: 2 CTAs per SM when the tile's TMEM share allows it (<= 256 columns).
-    const size_t budget = cols <= 256 ? 110 * 1024 : 220 * 1024;
-    SweepSmem lay = sweep_layout(nz, Z, P, 2, G);
+    const unsigned grid = (unsigned)((L.n + kTile - 1) / kTile);
+    // 2 CTAs per SM when the tile's TMEM share allows it (<= 256 columns) and
+    // the grid fills the GPU; small (coarse) grids get one CTA per SM and a
+    // deeper ring instead (they are latency-bound).
+    const size_t budget = (cols <= 256 && grid > 148) ? 110 * 1024 : 220 * 1024;
+    SweepSmem lay = sweep_layout(nz, Z, P, F, 2, G);
     const size_t per_stage = sizeof(double) * lay.stage_doubles;
     int S = (int)((budget - lay.off_stage) / per_stage);
-    S = S < 2 ? 2 : (S > 16 ? 16 : S);
-    lay = sweep_layout(nz, Z, P, S, G);
+    S = S < 2 ? 2 : (S > 32 ? 32 : S);
+    lay = sweep_layout(nz, Z, P, F, S, G);
     size_t smem = lay.total;
     // never let a third CTA onto an SM (its TMEM allocation would have to wait)
-    const size_t floor_smem = cols <= 256 ? 80 * 1024 : 120 * 1024;
+    const size_t floor_smem = (cols <= 256 && grid > 148) ? 80 * 1024 : 120 * 1024;
     if (smem < floor_smem) smem = floor_smem;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k_sweep_tc<Z, P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_sweep_tc<Z, P, F, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr_done = true;
     }
     SweepMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     const LevelView V = L.view(nz);
-    const double* rows[6];
-    int nrows = 0;
-    rows[nrows++] = V.D;
-    rows[nrows++] = V.U;
-    if (!Z) {
-        rows[nrows++] = V.H0;
-        rows[nrows++] = V.H1;
-        rows[nrows++] = V.H2;
-    }
-    rows[nrows++] = b;
-    for (int a = 0; a < nrows; ++a) maps.a[a] = make_map(rows[a], L.ld, nz, kTile, G);
+    maps.bands = make_map(V.D, L.ld, nz, kTile, G, Z ? 2 : 5);
+    maps.b = make_map(b, L.ld, nz, kTile, G);
+    if (F) maps.fact = make_map(L.fden, L.ld, nz, kTile, G, 3);
     if (!Z) maps.u = make_map(uin, L.ld, nz, kTile, G);
     int64_t ldc = 0;
     if (P) {
@@ -382,12 +493,15 @@ void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const dou
         ldc = C.ld;
         maps.uc = make_map(uc, C.ld, nz, kTile / 4, G);
     }
-    const unsigned grid = (unsigned)((L.n + kTile - 1) / kTile);
-    k_sweep_tc<Z, P, G><<<grid, kThreads, smem, s>>>(maps, V, L.halo, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad,
-                                                     S, cols);
+    k_sweep_tc<Z, P, F, G><<<grid, kThreads, smem, s>>>(maps, V, L.halo, b, uin, uc, ldc, L.fden, L.fg, uout, omega,
+                                                        L.ref, &H.scal->bad, S, cols);
 }
 
 }  // namespace
+
+#ifdef HMG_TIMING
+extern "C" void hmg_debug_tc_timing(long long* out) { cudaMemcpyFromSymbol(out, g_tc_timing, sizeof(long long) * 16); }
+#endif
 
 void launch_selftest_div(int64_t n, const double* a, const double* b, double* fast, double* ref, cudaStream_t s) {
     k_selftest_div<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, a, b, fast, ref);
@@ -418,12 +532,22 @@ bool tensor_maps_available() {
 void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                      double* uout, double omega, cudaStream_t s) {
     try {
-        if (!uin)
-            launch_tc<true, false, 4>(H, L, b, nullptr, nullptr, uout, omega, s);
-        else if (uc)
-            launch_tc<false, true, 2>(H, L, b, uin, uc, uout, omega, s);
-        else
-            launch_tc<false, false, 2>(H, L, b, uin, nullptr, uout, omega, s);
+        const bool fact = L.fden != nullptr;   // small (latency-bound) levels carry precomputed pivots
+        if (fact) {
+            if (!uin)
+                launch_tc<true, false, true, 4>(H, L, b, nullptr, nullptr, uout, omega, s);
+            else if (uc)
+                launch_tc<false, true, true, 2>(H, L, b, uin, uc, uout, omega, s);
+            else
+                launch_tc<false, false, true, 2>(H, L, b, uin, nullptr, uout, omega, s);
+        } else {
+            if (!uin)
+                launch_tc<true, false, false, 4>(H, L, b, nullptr, nullptr, uout, omega, s);
+            else if (uc)
+                launch_tc<false, true, false, 2>(H, L, b, uin, uc, uout, omega, s);
+            else
+                launch_tc<false, false, false, 2>(H, L, b, uin, nullptr, uout, omega, s);
+        }
     } catch (const std::exception& e) {
         g_launch_error = std::string("sweep launch: ") + e.what();
     }

@@ -239,3 +239,42 @@ def test_shared_reciprocal_division_is_bitwise_ieee():
     ok = ~np.isnan(r) & (b != 0) & np.isfinite(a) & np.isfinite(b)
     # and the compiler's division is the IEEE quotient numpy computes
     assert np.array_equal(r[ok].view(np.int64), (a[ok] / b[ok]).view(np.int64))
+
+
+@pytest.mark.parametrize("tail", ["-1", "0", "1", "3", "4"])
+@pytest.mark.parametrize("params", [MGParams(), MGParams(0, 1, 3, 0.8), MGParams(1, 0, 2, 0.9)])
+def test_coarse_tail_settings(monkeypatch, tail, params):
+    """The single-launch coarse tail (levels <= HMG_TAIL_REF) and the per-level
+    kernels give the same bits as the oracle, for any split point."""
+    monkeypatch.setenv("HMG_TAIL_REF", tail)
+    cfg = hi.Config("tail", 4, 0, 16, 0.01, 1e-3)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(4, 0, 16, 0.01, 1e-3, lam)
+    o = oracle.Hierarchy(4, 0, 16, 0.01, 1e-3, lam)
+    z = g.to_host(4, g.vcycle(g.to_device(4, b), params=params))
+    assert np.array_equal(z, o.vcycle(b, params.nu_pre, params.nu_post, params.n_coarse, params.omega))
+    # (V(0,1) / V(1,0) are not symmetric preconditioners: CG need not converge,
+    # but both sides must behave identically)
+    _, it, _, st = g.pcg_solve(g.to_device(4, b), params=params, maxit=60)
+    _, it_o, _, _, st_o = o.pcg(b, nu_pre=params.nu_pre, nu_post=params.nu_post, n_coarse=params.n_coarse,
+                                omega=params.omega, maxit=60)
+    assert it == it_o and (st == "HMG_OK") == (st_o == 0)
+
+
+@pytest.mark.parametrize("ref,fine", [(2, 2), (4, 4), (3, 5)])
+def test_sweep_exact_division_fallback(ref, fine):
+    """Zero numerators leave the shared-reciprocal division's fast range: the
+    sweep must then recompute the column with '/' and still match the oracle
+    bit for bit (zero right-hand-side columns and isolated zero entries)."""
+    cfg = hi.Config("zeros", fine, 0, 16, 0.01, 1e-4)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(fine, 0, 16, 0.01, 1e-4, lam)
+    o = oracle.Hierarchy(fine, 0, 16, 0.01, 1e-4, lam)
+    bb = hi.uniform_vector(o.shape(ref), 77)
+    bb[:, ::7] = 0.0
+    bb[3, 1::5] = 0.0
+    for zero in (True, False):
+        u0 = np.zeros(o.shape(ref)) if zero else hi.uniform_vector(o.shape(ref), 78)
+        u = g.to_device(ref, u0)
+        g.line_smooth(ref, g.to_device(ref, bb), u, 2, 0.8, zero)
+        assert np.array_equal(g.to_host(ref, u), o.sweep(ref, bb, None if zero else u0, 2, 0.8))

@@ -47,3 +47,17 @@ xx, it, rr, st = g.pcg_solve(bd); torch.cuda.synchronize()
 print(f"pcg warm {time.time()-t0:.3f}s it={it} rr={rr:.2e} {st}")
 t = timeit(lambda: g.pcg_solve(bd, xx), reps=3)
 print(f"pcg     {t:8.2f} ms  it={it}")
+
+# per-class, per-level breakdown of one V-cycle (library CUDA events)
+g.profile_begin()
+g.vcycle(bd, z)
+torch.cuda.synchronize()
+g.profile_end()
+tot = 0.0
+for cls in g.KERNEL_CLASSES:
+    for lev in range(cfg.fine_ref, -1, -1):
+        n_, ms_ = g.profile_query(cls, lev)
+        if n_:
+            tot += ms_
+            print(f"  {cls:15s} ref {lev}: {n_:3d} launches {ms_*1e3:9.1f} us")
+print(f"  sum of kernel time {tot*1e3:.1f} us")
