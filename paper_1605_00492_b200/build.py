@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhmg.so")
-SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "coarse_tail.cu", "mesh.cpp"]
+SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "sweep_small.cu", "coarse_tail.cu", "mesh.cpp"]
 HEADERS = ["hmg_internal.h", "mesh.h", "sm100_ptx.cuh", os.path.join("..", "..", "include", "hmg.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

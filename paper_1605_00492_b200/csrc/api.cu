@@ -104,6 +104,7 @@ void free_hierarchy(Hierarchy* H) {
         cudaFree(L.wa); cudaFree(L.wb); cudaFree(L.b); cudaFree(L.u);
         cudaFree(L.halo_cells); cudaFree(L.halo_count); cudaFree(L.halo_loc);
         cudaFree(L.fden);
+        cudaFree(L.small_cells); cudaFree(L.small_count); cudaFree(L.small_loc);
     }
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q);
     cudaFree(H->partials); cudaFree(H->scal); cudaFree(H->hb); cudaFree(H->hx);
@@ -142,7 +143,10 @@ void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const dou
     }
     if (ref == H.coarsest_ref) {
         // whole coarsest level in one CTA's shared memory when it fits (ref 0: 20 columns)
-        if (L.fden && L.n <= 128 && coarsest_smem_bytes(H.nz, L.n, (int)((L.n + 31) / 32 * 32)) <= 200 * 1024)
+        if (H.use_small_sweep && L.n <= kSmallTile && sweep_small_supported(H, L)) {
+            ProfScope ps(H, kKCoarseTail, L.ref, s);
+            launch_sweep_small(H, L, b, nullptr, nullptr, out, p.omega, p.n_coarse, s);
+        } else if (L.fden && L.n <= 128 && coarsest_smem_bytes(H.nz, L.n, (int)((L.n + 31) / 32 * 32)) <= 200 * 1024)
             launch_coarsest(H, L, b, out, p.n_coarse, p.omega, s);
         else
             run_sweeps(H, L, b, nullptr, nullptr, p.n_coarse, out, p.omega, s);
@@ -257,6 +261,7 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
     H->w2 = w2;
     H->dz = thickness / nlayers;
     if (const char* e = std::getenv("HMG_SWEEP")) H->use_tc_sweep = std::string(e) != "simple";
+    if (const char* e = std::getenv("HMG_SMALL")) H->use_small_sweep = std::string(e) != "0";
     {
         int tail = -1;   // default: per-level kernels (HMG_TAIL_REF=r enables the one-launch tail)
         if (const char* e = std::getenv("HMG_TAIL_REF")) tail = std::atoi(e);
@@ -324,14 +329,14 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
         }
         BCUDA(cudaMemcpy(L.nbr, nbr.data(), sizeof(int32_t) * 3 * L.ld, cudaMemcpyHostToDevice));
         BCUDA(cudaMemcpy(L.geom, geom.data(), sizeof(double) * 7 * L.ld, cudaMemcpyHostToDevice));
-        // tile halos for the streamed sweep (sweep_tc.cu)
-        {
-            const int64_t ntiles = (L.n + kSweepTile - 1) / kSweepTile;
-            std::vector<int32_t> hcells(ntiles * kHaloMax, 0), hcount(ntiles, 0);
+        // tile halos: 128-cell tiles of the streamed sweep (sweep_tc.cu) and
+        // 32-cell tiles of the small-level sweep (sweep_small.cu)
+        auto build_halo = [&](int tile, int hmax, int32_t** d_cells, int32_t** d_count, uint32_t** d_loc) -> hmg_status {
+            const int64_t ntiles = (L.n + tile - 1) / tile;
+            std::vector<int32_t> hcells(ntiles * hmax, 0), hcount(ntiles, 0);
             std::vector<uint32_t> loc(L.ld, 0);
-            bool fits = true;
-            for (int64_t t = 0; t < ntiles && fits; ++t) {
-                const int64_t a = t * kSweepTile, e = std::min<int64_t>(L.n, a + kSweepTile);
+            for (int64_t t = 0; t < ntiles; ++t) {
+                const int64_t a = t * tile, e = std::min<int64_t>(L.n, a + tile);
                 std::vector<int32_t> out;
                 for (int64_t c = a; c < e; ++c)
                     for (int j = 0; j < 3; ++j) {
@@ -340,9 +345,9 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
                     }
                 std::sort(out.begin(), out.end());
                 out.erase(std::unique(out.begin(), out.end()), out.end());
-                if ((int)out.size() > kHaloMax) { fits = false; break; }
+                if ((int)out.size() > hmax) return HMG_OK;        // table not usable: kernel not selected
                 hcount[t] = (int32_t)out.size();
-                std::copy(out.begin(), out.end(), hcells.begin() + t * kHaloMax);
+                std::copy(out.begin(), out.end(), hcells.begin() + t * hmax);
                 for (int64_t c = a; c < e; ++c) {
                     uint32_t packed = 0;
                     for (int j = 0; j < 3; ++j) {
@@ -351,22 +356,32 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
                         if (o >= a && o < e)
                             slot = (uint32_t)(o - a);
                         else
-                            slot = kSweepTile + (uint32_t)(std::lower_bound(out.begin(), out.end(), o) - out.begin());
+                            slot = tile + (uint32_t)(std::lower_bound(out.begin(), out.end(), o) - out.begin());
                         packed |= slot << (8 * j);
                     }
                     loc[c] = packed;
                 }
             }
-            if (fits) {
-                BCUDA(cudaMalloc(&L.halo_cells, sizeof(int32_t) * hcells.size()));
-                BCUDA(cudaMalloc(&L.halo_count, sizeof(int32_t) * hcount.size()));
-                BCUDA(cudaMalloc(&L.halo_loc, sizeof(uint32_t) * loc.size()));
-                BCUDA(cudaMemcpy(L.halo_cells, hcells.data(), sizeof(int32_t) * hcells.size(), cudaMemcpyHostToDevice));
-                BCUDA(cudaMemcpy(L.halo_count, hcount.data(), sizeof(int32_t) * hcount.size(), cudaMemcpyHostToDevice));
-                BCUDA(cudaMemcpy(L.halo_loc, loc.data(), sizeof(uint32_t) * loc.size(), cudaMemcpyHostToDevice));
-                L.halo.cells = L.halo_cells;
-                L.halo.count = L.halo_count;
-                L.halo.loc = L.halo_loc;
+            HMG_CUDA(cudaMalloc(d_cells, sizeof(int32_t) * hcells.size()));
+            HMG_CUDA(cudaMalloc(d_count, sizeof(int32_t) * hcount.size()));
+            HMG_CUDA(cudaMalloc(d_loc, sizeof(uint32_t) * loc.size()));
+            HMG_CUDA(cudaMemcpy(*d_cells, hcells.data(), sizeof(int32_t) * hcells.size(), cudaMemcpyHostToDevice));
+            HMG_CUDA(cudaMemcpy(*d_count, hcount.data(), sizeof(int32_t) * hcount.size(), cudaMemcpyHostToDevice));
+            HMG_CUDA(cudaMemcpy(*d_loc, loc.data(), sizeof(uint32_t) * loc.size(), cudaMemcpyHostToDevice));
+            return HMG_OK;
+        };
+        {
+            hmg_status hs = build_halo(kSweepTile, kHaloMax, &L.halo_cells, &L.halo_count, &L.halo_loc);
+            if (hs != HMG_OK) return cleanup(hs);
+            L.halo.cells = L.halo_cells;
+            L.halo.count = L.halo_count;
+            L.halo.loc = L.halo_loc;
+            if (L.n <= kFactMaxCells) {
+                hs = build_halo(kSmallTile, kSmallHaloMax, &L.small_cells, &L.small_count, &L.small_loc);
+                if (hs != HMG_OK) return cleanup(hs);
+                L.small.cells = L.small_cells;
+                L.small.count = L.small_count;
+                L.small.loc = L.small_loc;
             }
         }
     }

@@ -14,7 +14,9 @@ constexpr int kMaxLayers = 256;   // Thomas state for a column lives in shared m
 constexpr int kMaxRef = 10;
 constexpr int kSweepTile = 128;   // columns per CTA of the TMA/TMEM sweep (sweep_tc.cu)
 constexpr int kHaloMax = 64;
-constexpr int64_t kFactMaxCells = 148 * 128;  // levels up to this size stream precomputed Thomas pivots      // max off-tile neighbour cells per tile (51 observed at ref >= 2)
+constexpr int64_t kFactMaxCells = 148 * 128;
+constexpr int kSmallTile = 32;    // columns per CTA of the small-level sweep (sweep_small.cu)
+constexpr int kSmallHaloMax = 32; // off-tile neighbours per 32-cell tile (24 observed)  // levels up to this size stream precomputed Thomas pivots      // max off-tile neighbour cells per tile (51 observed at ref >= 2)
 
 // Per-level tile halo for the streamed sweep: for tile t (cells
 // [t*kSweepTile, (t+1)*kSweepTile)), the sorted distinct neighbour cells
@@ -24,6 +26,13 @@ struct TileHalo {
     const int32_t* cells = nullptr;   // [ntiles][kHaloMax]
     const int32_t* count = nullptr;   // [ntiles]
     const uint32_t* loc = nullptr;    // [ld]
+};
+
+// Same for the 32-column tiles of the small-level sweep.
+struct SmallHalo {
+    const int32_t* cells = nullptr;   // [ntiles][kSmallHaloMax]
+    const int32_t* count = nullptr;   // [ntiles]
+    const uint32_t* loc = nullptr;    // [ld]: slot < 32 in-tile, else 32 + halo index
 };
 
 // Read-only view of one level's operator, passed by value to kernels.
@@ -55,6 +64,10 @@ struct DevLevel {
     int32_t* halo_count = nullptr;
     uint32_t* halo_loc = nullptr;
     TileHalo halo;
+    int32_t* small_cells = nullptr;
+    int32_t* small_count = nullptr;
+    uint32_t* small_loc = nullptr;
+    SmallHalo small;
     // Thomas factors (coarse-tail levels only): pivots, refined reciprocals, multipliers
     double* fden = nullptr;
     double* fy = nullptr;
@@ -115,7 +128,8 @@ struct Hierarchy {
     int tail_ref = -1;          // levels <= tail_ref run in one coarse-tail launch (-1: off)
     mutable int64_t launches = 0;
     mutable Profiler prof;
-    bool use_tc_sweep = true;   // HMG_SWEEP=simple selects the reference-layout kernel (diagnostics)
+    bool use_tc_sweep = true;
+    bool use_small_sweep = true;   // HMG_SMALL=0 disables the small-level kernel (diagnostics)   // HMG_SWEEP=simple selects the reference-layout kernel (diagnostics)
 };
 
 // kernels.cu
@@ -152,6 +166,10 @@ void launch_coarse_tail(const Hierarchy& H, const hmg_mg_params& p, const double
 size_t coarsest_smem_bytes(int nz, int64_t n, int threads);
 void launch_coarsest(const Hierarchy& H, const DevLevel& L, const double* b, double* out, int n_coarse, double omega,
                      cudaStream_t s);
+// sweep_small.cu: small-level sweep (whole tile in shared memory); nsweeps > 1 only for a one-tile level
+bool sweep_small_supported(const Hierarchy& H, const DevLevel& L);
+void launch_sweep_small(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
+                        double* uout, double omega, int nsweeps, cudaStream_t s);
 // Error raised on the host side of a launch (tensor-map encoding); nullptr if none.
 const char* take_launch_error();
 bool tensor_maps_available();

@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(kApplyBlock) k_apply(LevelView L, const double
         double xm = k0 > 0 ? x[(int64_t)(k0 - 1) * ld + c] : 0.0;
         double Um = k0 > 0 ? L.U[(int64_t)(k0 - 1) * ld + c] : 0.0;
         double xk = x[(int64_t)k0 * ld + c];
+#pragma unroll 4
         for (int k = k0; k < k1; ++k) {
             const int64_t row = k * ld, i = row + c;
             const double xp = (k + 1 < nz) ? x[i + ld] : 0.0;
@@ -239,6 +240,7 @@ __global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, con
     double um = k0 > 0 ? u[(int64_t)(k0 - 1) * ld + c] : 0.0;
     double Um = k0 > 0 ? L.U[(int64_t)(k0 - 1) * ld + c] : 0.0;
     double uk = u[(int64_t)k0 * ld + c];
+#pragma unroll 4
     for (int k = k0; k < k1; ++k) {
         const int64_t row = k * ld, i = row + c;
         const double up = (k + 1 < nz) ? u[i + ld] : 0.0;
@@ -439,6 +441,10 @@ void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, do
 void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin,
                   const double* uc, double* uout, double omega, cudaStream_t s) {
     ProfScope ps(H, !uin ? kKSweepZero : (uc ? kKSweepProlong : kKSweep), L.ref, s);
+    if (H.use_small_sweep && sweep_small_supported(H, L)) {
+        launch_sweep_small(H, L, b, uin, uc, uout, omega, 1, s);
+        return;
+    }
     if (H.use_tc_sweep && sweep_tc_supported(H, L)) {
         launch_sweep_tc(H, L, b, uin, uc, uout, omega, s);
         return;

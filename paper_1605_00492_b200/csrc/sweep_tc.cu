@@ -499,6 +499,10 @@ void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const dou
 
 }  // namespace
 
+CUtensorMap make_tensor_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes) {
+    return make_map(base, ld, rows, box_x, G, planes);
+}
+
 #ifdef HMG_TIMING
 extern "C" void hmg_debug_tc_timing(long long* out) { cudaMemcpyFromSymbol(out, g_tc_timing, sizeof(long long) * 16); }
 #endif
