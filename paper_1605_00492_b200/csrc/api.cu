@@ -106,7 +106,7 @@ void free_hierarchy(Hierarchy* H) {
         cudaFree(L.fden);
         cudaFree(L.small_cells); cudaFree(L.small_count); cudaFree(L.small_loc);
     }
-    cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q);
+    cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q); cudaFree(H->p2);
     cudaFree(H->partials); cudaFree(H->scal); cudaFree(H->hb); cudaFree(H->hx);
     if (H->scal_host) cudaFreeHost(H->scal_host);
     for (cudaEvent_t e : H->prof.pool) cudaEventDestroy(e);
@@ -201,9 +201,16 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     launch_dot(H, F, H.r, H.z, s);
     launch_finalize(H, kFinRhoInit, s);
     HMG_CUDA(cudaMemcpyAsync(H.p, H.z, bytes, cudaMemcpyDeviceToDevice, s));
+    double* pc = H.p;                              // current search direction (ping-pong with p2)
     for (int it = 1; it <= maxit; ++it) {
-        launch_apply_dot(H, F, H.p, H.q, s);       // q = H^ p, alpha = rho / <p, q>
-        launch_update_xr(H, F, x, s);              // x += alpha p, r -= alpha q, partial <r, r>
+        if (it == 1) {
+            launch_apply_dot(H, F, pc, H.q, s);    // q = H^ p, alpha = rho / <p, q>
+        } else {                                   // p = z + beta p fused into q = H^ p
+            double* pn = (pc == H.p) ? H.p2 : H.p;
+            launch_apply_pupdate_dot(H, F, H.z, pc, pn, H.q, s);
+            pc = pn;
+        }
+        launch_update_xr(H, F, x, pc, s);          // x += alpha p, r -= alpha q, partial <r, r>
         launch_finalize(H, kFinRR, s);
         HMG_TRY(check_launch());
         HMG_CUDA(cudaMemcpyAsync(H.scal_host, H.scal, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
@@ -215,8 +222,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         if (rn <= rtol * bn) return HMG_OK;
         precond(H.r, H.z);
         launch_dot(H, F, H.r, H.z, s);
-        launch_finalize(H, kFinRZ, s);             // beta = rho' / rho, rho = rho'
-        launch_update_p(H, F, s);                  // p = z + beta p
+        launch_finalize(H, kFinRZ, s);             // beta = rho' / rho, rho = rho' (p updated in the next apply)
     }
     return fail(HMG_ERR_NOT_CONVERGED, "not converged after " + std::to_string(maxit) +
                                            " iterations (relres " + std::to_string(*relres) + ")");
@@ -262,6 +268,7 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
     H->dz = thickness / nlayers;
     if (const char* e = std::getenv("HMG_SWEEP")) H->use_tc_sweep = std::string(e) != "simple";
     if (const char* e = std::getenv("HMG_SMALL")) H->use_small_sweep = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     {
         int tail = -1;   // default: per-level kernels (HMG_TAIL_REF=r enables the one-launch tail)
         if (const char* e = std::getenv("HMG_TAIL_REF")) tail = std::atoi(e);
@@ -394,11 +401,11 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
     for (int r = coarsest_ref; r <= fine_ref; ++r) launch_assemble(*H, H->lev[r], s);
     // PCG workspace
     const size_t fb = sizeof(double) * nlayers * F.ld;
-    for (double** v : {&H->r, &H->z, &H->p, &H->q}) {
+    for (double** v : {&H->r, &H->z, &H->p, &H->q, &H->p2}) {
         BCUDA(cudaMalloc(v, fb));
         BCUDA(cudaMemset(*v, 0, fb));
     }
-    H->npartials = partials_needed(F.n, nlayers);
+    H->npartials = partials_needed(F.n, nlayers) + 148 * 8 + 64;
     BCUDA(cudaMalloc(&H->partials, sizeof(double) * H->npartials));
     BCUDA(cudaMalloc(&H->scal, sizeof(PcgScalars)));
     BCUDA(cudaMallocHost(&H->scal_host, sizeof(PcgScalars)));

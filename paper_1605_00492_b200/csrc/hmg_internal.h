@@ -119,7 +119,7 @@ struct Hierarchy {
     double thickness = 0, w2 = 0, dz = 0;
     std::vector<DevLevel> lev;  // index = ref
     // PCG workspace on the finest level
-    double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr;
+    double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *p2 = nullptr;
     double* partials = nullptr; // per-block partial sums (deterministic reductions)
     int npartials = 0;
     PcgScalars* scal = nullptr; // device
@@ -128,8 +128,13 @@ struct Hierarchy {
     int tail_ref = -1;          // levels <= tail_ref run in one coarse-tail launch (-1: off)
     mutable int64_t launches = 0;
     mutable Profiler prof;
+    // diagnostics switches (environment, read at build time): HMG_SWEEP=simple
+    // selects the reference-layout sweep kernel, HMG_SMALL=0 disables the
+    // small-level kernel, HMG_L2PF sets the streamed sweep's L2 prefetch
+    // distance in ring stages, HMG_TAIL_REF the one-launch coarse tail
     bool use_tc_sweep = true;
-    bool use_small_sweep = true;   // HMG_SMALL=0 disables the small-level kernel (diagnostics)   // HMG_SWEEP=simple selects the reference-layout kernel (diagnostics)
+    bool use_small_sweep = true;
+    int l2_prefetch_groups = 3;
 };
 
 // kernels.cu
@@ -149,8 +154,10 @@ void launch_prolong_add(const Hierarchy& H, const DevLevel& F, const double* uin
 // PCG vector kernels (scalars read from H.scal on the device)
 void launch_dot(const Hierarchy& H, const DevLevel& L, const double* a, const double* b, cudaStream_t s);
 void launch_finalize(const Hierarchy& H, int op, cudaStream_t s);
-void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, cudaStream_t s);
-void launch_update_p(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
+void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, const double* p, cudaStream_t s);
+// q = H^ p_new with p_new = z + beta p_old formed on the fly and stored; partial <p_new, q> -> alpha
+void launch_apply_pupdate_dot(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
+                              double* q, cudaStream_t s);
 void launch_copy_pad(const Hierarchy& H, const DevLevel& L, const double* src, int64_t src_ld,
                      double* dst, int64_t dst_ld, cudaStream_t s);
 int partials_needed(int64_t n, int nz);

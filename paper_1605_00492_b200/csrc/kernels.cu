@@ -88,9 +88,11 @@ __global__ void k_assemble(int64_t n, int64_t ld, int nz, const int32_t* __restr
 // registers); the three face neighbours are gathered from the same layer row.
 // DOT additionally accumulates x.y for the CG step (fused <p, H^ p>).
 // ---------------------------------------------------------------------------
-template <bool DOT>
-__global__ void __launch_bounds__(kApplyBlock) k_apply(LevelView L, const double* __restrict__ x,
-                                                       double* __restrict__ y, double* __restrict__ partial) {
+template <bool DOT, bool PUPD>
+__global__ void __launch_bounds__(kApplyBlock) k_apply_t(LevelView L, const double* __restrict__ xin,
+                                                         double* __restrict__ y, double* __restrict__ partial,
+                                                         const double* __restrict__ zv, double* __restrict__ pnew,
+                                                         const PcgScalars* __restrict__ sc) {
     __shared__ double red[kApplyBlock / 32];
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     // vertical chunk of this thread (gridDim.y chunks; 1 on fine levels)
@@ -98,24 +100,34 @@ __global__ void __launch_bounds__(kApplyBlock) k_apply(LevelView L, const double
     const int kc = (nz + gridDim.y - 1) / gridDim.y;
     const int k0 = blockIdx.y * kc, k1 = min(nz, k0 + kc);
     double dot = 0.0;
+    // PUPD (CG): the operand is p = z + beta p_old, formed on the fly for the
+    // cell and its neighbours (same arithmetic as a separate update) and
+    // written back for the cell -- the p update fused into the operator apply.
+    double beta = 0.0;
+    if (PUPD) beta = sc->beta;
+    auto X = [&](int64_t i) -> double {
+        if (PUPD) return zv[i] + beta * xin[i];
+        return xin[i];
+    };
     if (c < L.n && k0 < k1) {
         const int64_t ld = L.ld;
         const int32_t n0 = L.nbr[c], n1 = L.nbr[ld + c], n2 = L.nbr[2 * ld + c];
-        double xm = k0 > 0 ? x[(int64_t)(k0 - 1) * ld + c] : 0.0;
+        double xm = k0 > 0 ? X((int64_t)(k0 - 1) * ld + c) : 0.0;
         double Um = k0 > 0 ? L.U[(int64_t)(k0 - 1) * ld + c] : 0.0;
-        double xk = x[(int64_t)k0 * ld + c];
+        double xk = X((int64_t)k0 * ld + c);
 #pragma unroll 4
         for (int k = k0; k < k1; ++k) {
             const int64_t row = k * ld, i = row + c;
-            const double xp = (k + 1 < nz) ? x[i + ld] : 0.0;
+            const double xp = (k + 1 < nz) ? X(i + ld) : 0.0;
             const double Uk = L.U[i];
             double acc = L.D[i] * xk;
             if (k > 0) acc = acc + Um * xm;
             if (k < nz - 1) acc = acc + Uk * xp;
-            acc = acc + L.H0[i] * x[row + n0];
-            acc = acc + L.H1[i] * x[row + n1];
-            acc = acc + L.H2[i] * x[row + n2];
+            acc = acc + L.H0[i] * X(row + n0);
+            acc = acc + L.H1[i] * X(row + n1);
+            acc = acc + L.H2[i] * X(row + n2);
             y[i] = acc;
+            if (PUPD) pnew[i] = xk;
             if (DOT) dot = dot + xk * acc;
             xm = xk;
             xk = xp;
@@ -271,24 +283,43 @@ __global__ void k_prolong_add(const double* __restrict__ uin, const double* __re
 }
 
 // ---------------------------------------------------------------------------
-// CG vector kernels (reading R10).  Each block owns kVecCells consecutive
-// cells of every layer; per-block partial sums are reduced by k_finalize in a
-// fixed order, so dots are deterministic (not equal in rounding to the
-// oracle's sequential sum; see DESIGN.md parity contract).
+// CG vector kernels (reading R10).  Block (bx, by) owns kVecCells consecutive
+// cells (2 per 16-byte access, 4 per thread) of the layers [by*kc, by*kc+kc);
+// per-block partial sums are reduced by k_finalize in a fixed order, so dots
+// are deterministic (not equal in rounding to the oracle's sequential sum;
+// see DESIGN.md parity contract).
 // ---------------------------------------------------------------------------
+struct VecRange {
+    int64_t c0;   // first cell of this thread's first pair
+    int k0, k1;   // layers
+};
+__device__ __forceinline__ VecRange vec_range(int nz) {
+    const int kc = (nz + gridDim.y - 1) / gridDim.y;
+    VecRange v;
+    v.c0 = blockIdx.x * (int64_t)kVecCells + 2 * threadIdx.x;
+    v.k0 = blockIdx.y * kc;
+    v.k1 = min(nz, v.k0 + kc);
+    return v;
+}
+
 __global__ void __launch_bounds__(kVecBlock) k_dot(const double* __restrict__ a, const double* __restrict__ b,
                                                    int64_t n, int64_t ld, int nz, double* __restrict__ partial) {
     __shared__ double red[kVecBlock / 32];
-    const int64_t c0 = blockIdx.x * (int64_t)kVecCells + threadIdx.x;
+    const VecRange v = vec_range(nz);
     double s = 0.0;
-    for (int k = 0; k < nz; ++k)
+    for (int k = v.k0; k < v.k1; ++k)
 #pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j) {
-            const int64_t c = c0 + j * kVecBlock;
-            if (c < n) s = s + a[k * ld + c] * b[k * ld + c];
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = v.c0 + h * 2 * kVecBlock;
+            if (c < n) {
+                const double2 x = *reinterpret_cast<const double2*>(a + k * ld + c);
+                const double2 y = *reinterpret_cast<const double2*>(b + k * ld + c);
+                s = s + x.x * y.x;
+                s = s + x.y * y.y;
+            }
         }
     const double tot = block_sum(s, red);
-    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
+    if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = tot;
 }
 
 __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x, double* __restrict__ r,
@@ -297,38 +328,30 @@ __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x,
                                                          double* __restrict__ partial) {
     __shared__ double red[kVecBlock / 32];
     const double alpha = sc->alpha;
-    const int64_t c0 = blockIdx.x * (int64_t)kVecCells + threadIdx.x;
+    const VecRange v = vec_range(nz);
     double s = 0.0;
-    for (int k = 0; k < nz; ++k)
+    for (int k = v.k0; k < v.k1; ++k)
 #pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j) {
-            const int64_t c = c0 + j * kVecBlock;
+        for (int h = 0; h < 2; ++h) {
+            const int64_t c = v.c0 + h * 2 * kVecBlock;
             if (c < n) {
                 const int64_t i = k * ld + c;
-                x[i] = x[i] + alpha * p[i];
-                const double rn = r[i] - alpha * q[i];
-                r[i] = rn;
-                s = s + rn * rn;
+                double2 xx = *reinterpret_cast<const double2*>(x + i);
+                double2 rr = *reinterpret_cast<const double2*>(r + i);
+                const double2 pp = *reinterpret_cast<const double2*>(p + i);
+                const double2 qq = *reinterpret_cast<const double2*>(q + i);
+                xx.x = xx.x + alpha * pp.x;
+                xx.y = xx.y + alpha * pp.y;
+                rr.x = rr.x - alpha * qq.x;
+                rr.y = rr.y - alpha * qq.y;
+                *reinterpret_cast<double2*>(x + i) = xx;
+                *reinterpret_cast<double2*>(r + i) = rr;
+                s = s + rr.x * rr.x;
+                s = s + rr.y * rr.y;
             }
         }
     const double tot = block_sum(s, red);
-    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(kVecBlock) k_update_p(double* __restrict__ p, const double* __restrict__ z,
-                                                        int64_t n, int64_t ld, int nz,
-                                                        const PcgScalars* __restrict__ sc) {
-    const double beta = sc->beta;
-    const int64_t c0 = blockIdx.x * (int64_t)kVecCells + threadIdx.x;
-    for (int k = 0; k < nz; ++k)
-#pragma unroll
-        for (int j = 0; j < kVecPerThread; ++j) {
-            const int64_t c = c0 + j * kVecBlock;
-            if (c < n) {
-                const int64_t i = k * ld + c;
-                p[i] = z[i] + beta * p[i];
-            }
-        }
+    if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = tot;
 }
 
 __global__ void __launch_bounds__(kFinThreads) k_finalize(const double* __restrict__ partial, int np, int op,
@@ -425,14 +448,14 @@ void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
 void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
     ProfScope ps(H, kKApply, L.ref, s);
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
-    k_apply<false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, nullptr);
+    k_apply_t<false, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, nullptr, nullptr, nullptr, nullptr);
     ++H.launches;
 }
 
 void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
     ProfScope ps(H, kKApply, L.ref, s);
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
-    k_apply<true><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, H.partials);
+    k_apply_t<true, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, H.partials, nullptr, nullptr, nullptr);
     ++H.launches;
     k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)(g.x * g.y), kFinPQ, H.scal);
     ++H.launches;
@@ -467,6 +490,16 @@ void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const 
     ++H.launches;
 }
 
+void launch_apply_pupdate_dot(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
+                              double* q, cudaStream_t s) {
+    ProfScope ps(H, kKApply, L.ref, s);
+    dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
+    k_apply_t<true, true><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), pold, q, H.partials, z, pnew, H.scal);
+    ++H.launches;
+    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)(g.x * g.y), kFinPQ, H.scal);
+    ++H.launches;
+}
+
 void launch_restrict(const Hierarchy& H, const DevLevel& F, const double* r, double* bc, cudaStream_t s) {
     ProfScope ps(H, kKRestrict, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
@@ -493,28 +526,30 @@ void launch_prolong_add(const Hierarchy& H, const DevLevel& F, const double* uin
     ++H.launches;
 }
 
+// Grid of the vector kernels: column blocks x layer chunks, ~8 blocks per SM.
+dim3 vec_grid(int64_t n, int nz) {
+    const unsigned gx = blocks(n, kVecCells);
+    unsigned gy = (unsigned)((148 * 8 + gx - 1) / gx);
+    if (gy > (unsigned)nz) gy = (unsigned)nz;
+    return dim3(gx, gy < 1 ? 1 : gy);
+}
+
 void launch_dot(const Hierarchy& H, const DevLevel& L, const double* a, const double* b, cudaStream_t s) {
     ProfScope ps(H, kKVector, H.fine_ref, s);
-    k_dot<<<blocks(L.n, kVecCells), kVecBlock, 0, s>>>(a, b, L.n, L.ld, H.nz, H.partials);
+    k_dot<<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(a, b, L.n, L.ld, H.nz, H.partials);
     ++H.launches;
 }
 
 void launch_finalize(const Hierarchy& H, int op, cudaStream_t s) {
     const DevLevel& L = H.lev[H.fine_ref];
-    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)blocks(L.n, kVecCells), op, H.scal);
+    const dim3 g = vec_grid(L.n, H.nz);
+    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)(g.x * g.y), op, H.scal);
     ++H.launches;
 }
 
-void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, cudaStream_t s) {
+void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, const double* p, cudaStream_t s) {
     ProfScope ps(H, kKVector, H.fine_ref, s);
-    k_update_xr<<<blocks(L.n, kVecCells), kVecBlock, 0, s>>>(x, H.r, H.p, H.q, L.n, L.ld, H.nz, H.scal,
-                                                             H.partials);
-    ++H.launches;
-}
-
-void launch_update_p(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
-    ProfScope ps(H, kKVector, H.fine_ref, s);
-    k_update_p<<<blocks(L.n, kVecCells), kVecBlock, 0, s>>>(H.p, H.z, L.n, L.ld, H.nz, H.scal);
+    k_update_xr<<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(x, H.r, p, H.q, L.n, L.ld, H.nz, H.scal, H.partials);
     ++H.launches;
 }
 

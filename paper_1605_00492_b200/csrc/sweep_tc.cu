@@ -90,7 +90,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     k_sweep_tc(const __grid_constant__ SweepMaps maps, LevelView L, TileHalo th, const double* __restrict__ bvec,
                const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc,
                const double* __restrict__ fdp, const double* __restrict__ fgp, double* __restrict__ uout,
-               double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols) {
+               double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols,
+               int pf_groups) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     const int nz = L.nz;
     const int64_t ld = L.ld;
@@ -157,6 +158,19 @@ __global__ void __launch_bounds__(kThreads, 2)
                 ptx::cp_async_arrive(&full[s]);
             }
             __syncwarp();
+            if (lane == 0 && pf_groups > 0) {
+                // L2 prefetch pf_groups stages ahead: the ring's copies then see
+                // L2 instead of HBM latency (smem caps the ring's depth)
+                const int gp = gi + pf_groups;
+                if (gp < ngroups) {
+                    constexpr int nbp = ZERO ? 2 : 5;
+                    (void)nbp;
+                    ptx::tma_prefetch_3d(&maps.bands, x, gp * G, 0);
+                    ptx::tma_prefetch_2d(&maps.b, x, gp * G);
+                    if (!ZERO) ptx::tma_prefetch_2d(&maps.u, x, (gp + 1) * G);
+                    if (FACT) ptx::tma_prefetch_3d(&maps.fact, x, gp * G, 0);
+                }
+            }
             if (lane == 0) {
                 uint32_t bytes = (uint32_t)lay.nrows * ublock;   // bands + b (+ factors)
                 const bool u0 = !ZERO && gi == 0;
@@ -494,7 +508,7 @@ void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const dou
         maps.uc = make_map(uc, C.ld, nz, kTile / 4, G);
     }
     k_sweep_tc<Z, P, F, G><<<grid, kThreads, smem, s>>>(maps, V, L.halo, b, uin, uc, ldc, L.fden, L.fg, uout, omega,
-                                                        L.ref, &H.scal->bad, S, cols);
+                                                        L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
 }
 
 }  // namespace

@@ -5,7 +5,7 @@ B._LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhmg_t
 import torch, hmg_inputs as hi
 from paper_1605_00492_b200 import Hierarchy
 lib = B.load_library()
-for ref in (0, 3, 7):
+for ref in (5, 6, 7):
     cfg = hi.Config("s", ref, ref, 64, 0.01, 1e-4); lam, b = hi.make_inputs(cfg)
     g = Hierarchy(ref, ref, 64, 0.01, 1e-4, lam); bd = g.to_device(ref, b); u = g.empty(ref)
     for zero in (True, False):
