@@ -1,10 +1,12 @@
 #!/usr/bin/env python
 """Benchmark of the B200 tensor-product multigrid Helmholtz solver (arXiv:1605.00492 hot path).
 
-One step = one full solve of BASELINE.json config C2 (anisotropy C2a: ref 7 x 64
-layers = 20,971,520 fp64 dofs, hierarchy ref 7 -> 0, PCG preconditioned by one
-V(2,2) cycle per iteration, damped line-Jacobi omega = 0.8, 20 coarse sweeps,
-relative residual 1e-8).  Every row of SURVEY.md 8(a) runs inside the step:
+One step = one full solve of BASELINE.json config C2 (anisotropy C2b: ref 7 x 64
+layers = 20,971,520 fp64 dofs, thickness 0.001, w2 1e-5, hierarchy ref 7 -> 0,
+PCG preconditioned by one V(2,2) cycle per iteration, damped line-Jacobi
+omega = 0.8, 20 coarse sweeps, relative residual 1e-8).  C2b is the C2
+anisotropy that BASELINE.json's weak-scaling config C4 (thickness 0.001) pairs
+with.  Every row of SURVEY.md 8(a) runs inside the step:
 operator apply, fused sweeps, residual+restriction, prolongation, the coarse
 solve, the V-cycle driver and the PCG vector/dot kernels.
 
@@ -16,8 +18,12 @@ dominant kernel's achieved HBM GB/s against MEASURED_PEAKS.json, the oracle on
 the host cores, and an end-to-end number through the host-buffer entry point.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-Multi-GPU (torchrun, N > 1): each rank solves its own C2a-sized problem
-(weak scaling, replicas): the NCCL halo layer of SURVEY 8(e) is not built yet.
+Multi-GPU (torchrun, N > 1): ONE distributed solve over NCCL (SURVEY 8(e):
+horizontal partition by ref-2 blocks, one-ring halo exchange on every
+distributed level, all-reduced CG inner products, coarse gather at ref 3).
+Weak scaling at 20,971,520 dofs per GPU, thickness 0.001, w2 1e-5:
+N=1 ref 7 x 64 (C2b), N=2 ref 7 x 128, N=4 ref 8 x 64, N=8 ref 8 x 128 (C4);
+other N divide C2b (strong scaling).
 """
 from __future__ import annotations
 
@@ -45,10 +51,11 @@ BYTES_PER_DOF = {"sweep": 64.0, "sweep_zero": 32.0, "sweep_prolong": 66.0, "appl
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="hmg", choices=["hmg", "reference"])
-    ap.add_argument("--config", default="C2a", choices=["C2a", "C2b", "C2c", "C0", "C1"])
+    ap.add_argument("--config", default="C2b", choices=["C2a", "C2b", "C2c", "C0", "C1"])
+    ap.add_argument("--gather-ref", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -91,7 +98,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -179,20 +186,44 @@ def run_reference(args, ws, rank):
     }))
 
 
+WEAK = {1: (7, 64), 2: (7, 128), 4: (8, 64), 8: (8, 128)}   # (fine ref, layers): 20,971,520 dofs per GPU
+
+
+def workload(args, ws):
+    base = hi.CONFIGS[args.config]
+    if ws == 1:
+        return base, "weak"
+    if ws in WEAK and args.config == "C2b":
+        ref, nz = WEAK[ws]
+        return hi.Config(f"C2b-weak-x{ws}" if ws != 8 else "C4", ref, 0, nz, 0.001, 1e-5), "weak"
+    return base, "strong"
+
+
 def run_hmg(args, ws, rank, local):
     import torch
     import torch.distributed as dist
-    from paper_1605_00492_b200 import Hierarchy, MGParams
+    from paper_1605_00492_b200 import Hierarchy, MGParams, nccl_unique_id
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA GPU (no CPU fallback exists)")
     torch.cuda.set_device(local)
     if ws > 1 and not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    cfg = hi.CONFIGS[args.config]
-    lam, b = hi.make_inputs(cfg, seed=cfg.seed + rank)
+    cfg, scaling = workload(args, ws)
+    lam, b = hi.make_inputs(cfg)                 # the global problem (seeded); each rank keeps its part
     t0 = time.perf_counter()
-    h = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, device=local)
+    if ws == 1:
+        h = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, device=local)
+    else:
+        nid = torch.zeros(128, dtype=torch.uint8, device=f"cuda:{local}")
+        if rank == 0:
+            nid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(nid, 0)
+        per = cfg.n // ws
+        own = slice(rank * per, (rank + 1) * per)
+        lam, b = np.ascontiguousarray(lam[:, own]), np.ascontiguousarray(b[:, own])
+        h = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, device=local,
+                      dist=(rank, ws, bytes(nid.cpu().numpy()), min(args.gather_ref, cfg.fine_ref)))
     setup_s = time.perf_counter() - t0
     r = cfg.fine_ref
     bd = h.to_device(r, b)
@@ -236,12 +267,13 @@ def run_hmg(args, ws, rank, local):
     h.profile_end()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     launches = h.launches - launches0
-    value = ws * cfg.ndofs * nv / (ms * 1e-3)
+    value = cfg.ndofs * nv / (ms * 1e-3)        # cfg is the global problem
 
     # ---- dominant kernel: the fused line-Jacobi sweep on the finest level ----
     n_sw, ms_sw = h.profile_query("sweep", r)
     avg_sw = ms_sw / max(n_sw, 1)
-    bytes_sw = BYTES_PER_DOF["sweep"] * cfg.ndofs
+    dofs_local = cfg.ndofs // ws
+    bytes_sw = BYTES_PER_DOF["sweep"] * dofs_local
     peak, peak_note = measured_peak()
     achieved = bytes_sw / (avg_sw * 1e-3) / 1e9
     shares = {}
@@ -253,7 +285,7 @@ def run_hmg(args, ws, rank, local):
         n_k, ms_k = h.profile_query(k, r)
         if n_k:
             avg = ms_k / n_k
-            fine[k] = {"us": round(avg * 1e3, 2), "GB/s": round(BYTES_PER_DOF[k] * cfg.ndofs / (avg * 1e-3) / 1e9, 1)}
+            fine[k] = {"us": round(avg * 1e3, 2), "GB/s": round(BYTES_PER_DOF[k] * dofs_local / (avg * 1e-3) / 1e9, 1)}
 
     # ---- V-cycle alone -------------------------------------------------------
     z = h.empty(r)
@@ -267,9 +299,9 @@ def run_hmg(args, ws, rank, local):
     e1.record(stream)
     barrier()
     ms_vc = max_over_ranks(e0.elapsed_time(e1) / nvc)
+    n = cfg.n // ws
 
     # ---- end to end: host buffers through hmg_pcg_solve_host ----------------
-    n = cfg.n
     hb = torch.from_numpy(b).pin_memory()
     hx = torch.empty_like(hb).pin_memory()
     bnp, xnp = hb.numpy(), hx.numpy()
@@ -281,7 +313,7 @@ def run_hmg(args, ws, rank, local):
     e1.record(stream)
     barrier()
     ms_e2e = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    e2e_value = ws * cfg.ndofs * nv / (ms_e2e * 1e-3)
+    e2e_value = cfg.ndofs * nv / (ms_e2e * 1e-3)
 
     # ---- oracle on the host cores (rank 0, N = 1 only) -----------------------
     cpu = None
@@ -294,15 +326,16 @@ def run_hmg(args, ws, rank, local):
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: PCG + V(2,2) solve to 1e-8, ref {cfg.fine_ref}->0 x {cfg.nz} layers",
-                       "dofs_per_gpu": cfg.ndofs, "thickness": cfg.thickness, "w2": cfg.w2,
+                       "dofs": cfg.ndofs, "dofs_per_gpu": cfg.ndofs // ws, "thickness": cfg.thickness, "w2": cfg.w2,
                        "pcg_iterations": iters, "vcycles_per_step": nv, "final_relres": relres,
-                       "parallelism": "replicas" if ws > 1 else "single GPU",
+                       "parallelism": (f"domain decomposition x{ws} (NCCL halos, all-reduce, coarse gather at ref "
+                                       f"{min(args.gather_ref, cfg.fine_ref)})") if ws > 1 else "single GPU",
                        "cache": "inputs larger than L2 (bands 840 MB + vectors per level)"},
             "pcg_solve_ms": ms,
-            "vcycle_only": {"value": ws * cfg.ndofs / (ms_vc * 1e-3), "unit": UNIT, "ms": ms_vc},
+            "vcycle_only": {"value": cfg.ndofs / (ms_vc * 1e-3), "unit": UNIT, "ms": ms_vc},
             "setup_s": setup_s,
             "roofline": {"kernel": "k_sweep_tc (fused residual + Thomas line sweep, finest level)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -312,8 +345,8 @@ def run_hmg(args, ws, rank, local):
             "fine_level_kernels": fine,
             "time_share": shares,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * cfg.nz * n),
-                    "d2h_bytes_per_step": int(8 * cfg.nz * n), "ms_per_step": ms_e2e},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * cfg.nz * n * ws),
+                    "d2h_bytes_per_step": int(8 * cfg.nz * n * ws), "ms_per_step": ms_e2e},
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }

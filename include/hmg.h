@@ -49,7 +49,7 @@ typedef enum {
     HMG_OK = 0,
     HMG_ERR_INVALID_ARG = 1,     /* message names the argument */
     HMG_ERR_CUDA = 2,            /* CUDA runtime error (message has cudaGetErrorString) */
-    HMG_ERR_NCCL = 3,            /* reserved for the multi-GPU layer */
+    HMG_ERR_NCCL = 3,            /* NCCL missing or a collective failed (multi-GPU) */
     HMG_ERR_SINGULAR_COLUMN = 4, /* a Thomas pivot was <= 0 or non-finite: "ref r column c" */
     HMG_ERR_NOT_CONVERGED = 5,   /* PCG hit maxit; outputs are still filled in */
     HMG_ERR_OOM = 6              /* device or host allocation failed */
@@ -83,6 +83,49 @@ typedef struct {
  * rediscretised, not Galerkin. */
 hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, double thickness,
                                double w2, const double* lam_host, int device, hmg_hierarchy** out);
+
+/* Multi-GPU (one process per GPU, the paper's horizontal domain
+ * decomposition with halo exchanges).  Rank r of nranks
+ * (nranks must divide 320) owns the ref-2 cells [r*320/nranks,
+ * (r+1)*320/nranks) and, because children of p are 4p..4p+3, the contiguous
+ * global cells [r*n/nranks, (r+1)*n/nranks) on every level ref > gather_ref.
+ * Levels ref <= gather_ref (gather_ref in [max(2, coarsest_ref), fine_ref])
+ * are replicated: their right-hand side is all-gathered and every rank runs
+ * them redundantly (the coarse gather).  Vectors of a distributed level are
+ * [nlayers][ld] with the owned cells first, in global order (local c = global
+ * off + c), then the halo cells; halo slots are library scratch, written by
+ * the library before it reads them (so inputs are written there too).
+ * Transport: NCCL (libnccl.so.2 resolved at run time) -- grouped send/recv of
+ * packed halos, all-reduce of CG inner products, all-gather at gather_ref. */
+typedef struct {
+    int rank;
+    int nranks;
+    const unsigned char* nccl_id;   /* 128 bytes from hmg_nccl_unique_id on rank 0, same on all ranks */
+    int gather_ref;
+} hmg_dist;
+
+/* As hmg_build_hierarchy for one rank of a distributed hierarchy.  lam_host is
+ * this rank's owned part of the finest level, [nlayers][20*4^fine_ref/nranks],
+ * when gather_ref < fine_ref (else the whole finest level).  Collective: all
+ * ranks must call it. */
+hmg_status hmg_build_hierarchy_dist(int fine_ref, int coarsest_ref, int nlayers, double thickness,
+                                    double w2, const double* lam_host, int device,
+                                    const hmg_dist* dist, hmg_hierarchy** out);
+
+/* ncclGetUniqueId into id_out[128] (call on rank 0, broadcast the bytes). */
+hmg_status hmg_nccl_unique_id(unsigned char* id_out);
+
+/* Host-only query of the partition plan of level `ref` for `rank` (no GPU;
+ * used by tests).  Pass NULL arrays to get the sizes first.  Outputs: global
+ * offset and count of the owned cells, halo size, number of peers, total
+ * send count; halo_gid[n_halo] (global ids, grouped by owner rank, ascending),
+ * nbr_local[n_own][3] (local numbering), per peer: rank, send count, receive
+ * offset/count (halo slots relative to n_own); send_local (concatenated owned
+ * local indices each peer needs, ascending global id). */
+hmg_status hmg_partition_plan(int fine_ref, int ref, int rank, int nranks, int64_t* off, int64_t* n_own,
+                              int64_t* n_halo, int* npeers, int64_t* send_total, int64_t* halo_gid,
+                              int32_t* nbr_local, int32_t* peer_rank, int64_t* send_count,
+                              int64_t* recv_offset, int64_t* recv_count, int32_t* send_local);
 
 /* Free all device and host storage of the hierarchy (NULL is a no-op). */
 hmg_status hmg_free_hierarchy(hmg_hierarchy* h);

@@ -6,6 +6,8 @@ of ``include/hmg.h``; this package is a thin ctypes binding (argument
 marshalling only).  There is no CPU fallback: importing works without a GPU,
 but every call that computes needs the CUDA library and a device.
 """
-from .binding import (HmgError, Hierarchy, MGParams, STATUS, lib_path, load_library)
+from .binding import (HmgError, Hierarchy, MGParams, STATUS, lib_path, load_library, nccl_unique_id,
+                      partition_plan)
 
-__all__ = ["HmgError", "Hierarchy", "MGParams", "STATUS", "lib_path", "load_library"]
+__all__ = ["HmgError", "Hierarchy", "MGParams", "STATUS", "lib_path", "load_library", "nccl_unique_id",
+           "partition_plan"]

@@ -27,6 +27,11 @@ class HmgError(RuntimeError):
         self.status = STATUS.get(code, str(code))
 
 
+class _Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("nranks", ctypes.c_int), ("nccl_id", ctypes.c_void_p),
+                ("gather_ref", ctypes.c_int)]
+
+
 class _Params(ctypes.Structure):
     _fields_ = [("nu_pre", ctypes.c_int), ("nu_post", ctypes.c_int), ("n_coarse", ctypes.c_int),
                 ("omega", ctypes.c_double)]
@@ -78,6 +83,9 @@ def load_library():
         "hmg_profile_begin": [P],
         "hmg_profile_end": [P],
         "hmg_profile_query": [P, I, I, pI64, pD],
+        "hmg_build_hierarchy_dist": [I, I, I, D, D, P, I, P, ctypes.POINTER(P)],
+        "hmg_nccl_unique_id": [P],
+        "hmg_partition_plan": [I, I, I, I, pI64, pI64, pI64, pI, pI64, P, P, P, P, P, P, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -109,6 +117,37 @@ def _dptr(t, name: str):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes) for hmg_build_hierarchy_dist; call on rank 0 and broadcast."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().hmg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def partition_plan(fine_ref: int, ref: int, rank: int, nranks: int) -> dict:
+    """Host-only partition plan of one level for one rank (hmg_partition_plan)."""
+    lib = load_library()
+    off, n_own, n_halo, send_total = (ctypes.c_int64() for _ in range(4))
+    npeers = ctypes.c_int()
+    _check(lib.hmg_partition_plan(fine_ref, ref, rank, nranks, ctypes.byref(off), ctypes.byref(n_own),
+                                  ctypes.byref(n_halo), ctypes.byref(npeers), ctypes.byref(send_total),
+                                  *([None] * 7)))
+    halo = np.empty(n_halo.value, np.int64)
+    nbr = np.empty((n_own.value, 3), np.int32)
+    prank = np.empty(npeers.value, np.int32)
+    scount, roff, rcount = (np.empty(npeers.value, np.int64) for _ in range(3))
+    slocal = np.empty(send_total.value, np.int32)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _check(lib.hmg_partition_plan(fine_ref, ref, rank, nranks, None, None, None, None, None, ptr(halo), ptr(nbr),
+                                  ptr(prank), ptr(scount), ptr(roff), ptr(rcount), ptr(slocal)))
+    peers, pos = [], 0
+    for i in range(npeers.value):
+        peers.append(dict(rank=int(prank[i]), send_local=slocal[pos:pos + scount[i]].copy(),
+                          recv_offset=int(roff[i]), recv_count=int(rcount[i])))
+        pos += int(scount[i])
+    return dict(off=off.value, n_own=n_own.value, halo_gid=halo, nbr_local=nbr, peers=peers)
+
+
 def selftest_div(a, b):
     """(fast, ref) device tensors: the sweep kernel's division vs the '/' operator."""
     import torch
@@ -122,12 +161,24 @@ class Hierarchy:
     """Device hierarchy ref ``fine_ref`` -> ``coarsest_ref`` (hmg_build_hierarchy)."""
 
     def __init__(self, fine_ref: int, coarsest_ref: int, nlayers: int, thickness: float, w2: float,
-                 lam, device: int = 0):
+                 lam, device: int = 0, dist=None):
+        """dist = (rank, nranks, nccl_id_bytes, gather_ref) for one rank of a
+        distributed hierarchy; lam is then this rank's owned part of the finest
+        level when gather_ref < fine_ref."""
         lib = load_library()
         lam = np.ascontiguousarray(np.asarray(lam, dtype=np.float64))
         h = ctypes.c_void_p()
-        _check(lib.hmg_build_hierarchy(fine_ref, coarsest_ref, nlayers, thickness, w2,
-                                       lam.ctypes.data_as(ctypes.c_void_p), device, ctypes.byref(h)))
+        if dist is None:
+            _check(lib.hmg_build_hierarchy(fine_ref, coarsest_ref, nlayers, thickness, w2,
+                                           lam.ctypes.data_as(ctypes.c_void_p), device, ctypes.byref(h)))
+        else:
+            rank, nranks, nid, gref = dist
+            self._nid = ctypes.create_string_buffer(bytes(nid), 128)
+            d = _Dist(rank, nranks, ctypes.cast(self._nid, ctypes.c_void_p), gref)
+            _check(lib.hmg_build_hierarchy_dist(fine_ref, coarsest_ref, nlayers, thickness, w2,
+                                                lam.ctypes.data_as(ctypes.c_void_p), device, ctypes.byref(d),
+                                                ctypes.byref(h)))
+        self.dist = dist
         self._h = h
         self.fine_ref, self.coarsest_ref, self.nz = fine_ref, coarsest_ref, nlayers
         self.thickness, self.w2, self.device = thickness, w2, device

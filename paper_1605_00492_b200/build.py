@@ -14,8 +14,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhmg.so")
-SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "sweep_small.cu", "coarse_tail.cu", "mesh.cpp"]
-HEADERS = ["hmg_internal.h", "mesh.h", "sm100_ptx.cuh", os.path.join("..", "..", "include", "hmg.h")]
+SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "sweep_small.cu", "coarse_tail.cu", "mesh.cpp", "dist.cpp", "nccl_dyn.cpp"]
+HEADERS = ["hmg_internal.h", "mesh.h", "sm100_ptx.cuh", "dist.h", "nccl_dyn.h", os.path.join("..", "..", "include", "hmg.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
@@ -34,7 +34,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+    cmd = [NVCC, *ARCH, *FLAGS, "-shared", *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp, "-ldl"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(HERE, "build.log"), "w") as fh:
         fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)

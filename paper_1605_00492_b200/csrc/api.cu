@@ -8,9 +8,11 @@
 #include <cstring>
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <new>
 #include <string>
 
+#include "dist.h"
 #include "hmg_internal.h"
 #include "mesh.h"
 
@@ -43,8 +45,15 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int64_t round_up32(int64_t n) { return (n + 31) & ~int64_t(31); }
 
+std::string& nccl_err_ref();
+
 hmg_status check_launch() {
     if (const char* m = take_launch_error()) return fail(HMG_ERR_CUDA, m);
+    if (!nccl_err_ref().empty()) {
+        std::string m = nccl_err_ref();
+        nccl_err_ref().clear();
+        return fail(HMG_ERR_NCCL, m);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(HMG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
     return HMG_OK;
@@ -105,13 +114,76 @@ void free_hierarchy(Hierarchy* H) {
         cudaFree(L.halo_cells); cudaFree(L.halo_count); cudaFree(L.halo_loc);
         cudaFree(L.fden);
         cudaFree(L.small_cells); cudaFree(L.small_count); cudaFree(L.small_loc);
+        cudaFree(L.dist.send_idx); cudaFree(L.dist.sendbuf); cudaFree(L.dist.recvbuf);
     }
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q); cudaFree(H->p2);
     cudaFree(H->partials); cudaFree(H->scal); cudaFree(H->hb); cudaFree(H->hx);
     if (H->scal_host) cudaFreeHost(H->scal_host);
     for (cudaEvent_t e : H->prof.pool) cudaEventDestroy(e);
+    cudaFree(H->gbuf_send); cudaFree(H->gbuf_recv);
+    if (H->comm) {
+        std::string err;
+        if (const Nccl* N = nccl(&err)) N->CommDestroy(H->comm);
+    }
     delete H;
 }
+
+// -------------------------------------------------------------------------
+// Multi-GPU exchange.  NCCL errors are sticky: recorded here and
+// reported by the next check_launch().
+// -------------------------------------------------------------------------
+thread_local std::string g_nccl_err;
+std::string& nccl_err_ref() { return g_nccl_err; }
+
+void nccl_check(int r, const char* what) {
+    if (r == kNcclSuccess || !g_nccl_err.empty()) return;
+    std::string err;
+    const Nccl* N = nccl(&err);
+    g_nccl_err = std::string(what) + ": " + (N ? N->GetErrorString(r) : err);
+}
+
+// Fill the halo slots of vector v on a distributed level from the owners:
+// pack my owned cells each peer needs, grouped send/recv, unpack.
+void halo_exchange(const Hierarchy& H, const DevLevel& L, const double* v_const, cudaStream_t s) {
+    const DistLevel& D = L.dist;
+    if (!D.on || D.peer_rank.empty()) return;
+    double* v = const_cast<double*>(v_const);     // halo slots are library scratch (include/hmg.h)
+    const Nccl* N = nccl(nullptr);
+    launch_halo_pack(H, L, v, s);
+    const int nz = H.nz;
+    nccl_check(N->GroupStart(), "ncclGroupStart");
+    for (size_t i = 0; i < D.peer_rank.size(); ++i) {
+        if (D.send_cnt[i])
+            nccl_check(N->Send(D.sendbuf + D.send_off[i] * nz, (size_t)(D.send_cnt[i] * nz), kNcclFloat64, D.peer_rank[i],
+                               H.comm, s), "ncclSend");
+        if (D.recv_cnt[i])
+            nccl_check(N->Recv(D.recvbuf + D.recv_off[i] * nz, (size_t)(D.recv_cnt[i] * nz), kNcclFloat64, D.peer_rank[i],
+                               H.comm, s), "ncclRecv");
+    }
+    nccl_check(N->GroupEnd(), "ncclGroupEnd");
+    launch_halo_unpack(H, L, v, s);
+}
+
+// Coarse gather at gather_ref: every rank holds its owned part (global
+// numbering) of vector v of the replicated level C; all-gather the rest.
+void coarse_gather(const Hierarchy& H, const DevLevel& C, double* v, cudaStream_t s) {
+    if (H.nranks == 1 && !H.force_coll) return;
+    const int64_t cnt = C.n / H.nranks;
+    launch_gather_pack(H, C, v, (int64_t)H.rank * cnt, cnt, s);
+    const Nccl* N = nccl(nullptr);
+    nccl_check(N->AllGather(H.gbuf_send, H.gbuf_recv, (size_t)(cnt * H.nz), kNcclFloat64, H.comm, s), "ncclAllGather");
+    launch_gather_unpack(H, C, v, cnt, s);
+}
+
+}  // namespace
+
+void hmg::dist_allreduce_tmp(const Hierarchy& H, cudaStream_t s) {
+    const Nccl* N = nccl(nullptr);
+    double* t = &H.scal->tmp;
+    nccl_check(N->AllReduce(t, t, 1, kNcclFloat64, kNcclSum, H.comm, s), "ncclAllReduce");
+}
+
+namespace {
 
 // -------------------------------------------------------------------------
 // Sweeps on one level: `count` sweeps from `uin` (nullptr = zero guess), the
@@ -126,6 +198,7 @@ const double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b,
     const double* cur = uin;
     for (int i = 0; i < count; ++i) {
         double* dst = (i == count - 1 && out) ? out : (cur == L.wa ? L.wb : L.wa);
+        if (cur) halo_exchange(H, L, cur, s);      // neighbours' old values (Jacobi)
         launch_sweep(H, L, b, cur, i == 0 ? uc : nullptr, dst, omega, s);
         cur = dst;
     }
@@ -157,21 +230,31 @@ void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const dou
     const double* cur = nullptr;
     if (p.nu_pre > 0) cur = run_sweeps(H, L, b, nullptr, nullptr, p.nu_pre, nullptr, p.omega, s);
     // M2 restrict the residual (b itself when u = 0)
-    if (cur)
+    if (cur) {
+        halo_exchange(H, L, cur, s);
         launch_resid_restrict(H, L, b, cur, C.b, s);
-    else
+    } else {
         launch_restrict(H, L, b, C.b, s);
+    }
+    if (L.dist.on && !C.dist.on) coarse_gather(H, C, C.b, s);   // distributed -> replicated levels
     // M3 coarse correction
     vcycle_level(H, ref - 1, p, C.b, C.u, s);
-    // M4 + M5: prolongation fused into the first postsmoothing sweep
+    // M4 + M5: prolongation fused into the first postsmoothing sweep (single
+    // GPU); on a distributed level the prolonged iterate is formed first and its
+    // halo exchanged, because halo cells' parents live on other ranks
     if (!cur) {
         cudaMemsetAsync(L.wa, 0, sizeof(double) * H.nz * L.ld, s);
         cur = L.wa;
     }
-    if (p.nu_post > 0)
+    if (p.nu_post > 0 && !L.dist.on) {
         run_sweeps(H, L, b, cur, C.u, p.nu_post, out, p.omega, s);
-    else
+    } else if (p.nu_post > 0) {
+        double* pro = (cur == L.wa) ? L.wb : L.wa;
+        launch_prolong_add(H, L, cur, C.u, pro, s);
+        run_sweeps(H, L, b, pro, nullptr, p.nu_post, out, p.omega, s);
+    } else {
         launch_prolong_add(H, L, cur, C.u, out, s);
+    }
 }
 
 hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweeps, double single_omega,
@@ -203,7 +286,11 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     HMG_CUDA(cudaMemcpyAsync(H.p, H.z, bytes, cudaMemcpyDeviceToDevice, s));
     double* pc = H.p;                              // current search direction (ping-pong with p2)
     for (int it = 1; it <= maxit; ++it) {
-        if (it == 1) {
+        if (F.dist.on) {                           // multi-GPU: p update, halo exchange, apply
+            if (it > 1) launch_update_p(H, F, pc, H.z, s);
+            halo_exchange(H, F, pc, s);
+            launch_apply_dot(H, F, pc, H.q, s);
+        } else if (it == 1) {
             launch_apply_dot(H, F, pc, H.q, s);    // q = H^ p, alpha = rho / <p, q>
         } else {                                   // p = z + beta p fused into q = H^ p
             double* pn = (pc == H.p) ? H.p2 : H.p;
@@ -228,14 +315,12 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
                                            " iterations (relres " + std::to_string(*relres) + ")");
 }
 
-}  // namespace
 
-extern "C" {
-
-const char* hmg_last_error(void) { return g_err.c_str(); }
-
-hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
-                               const double* lam_host, int device, hmg_hierarchy** out) {
+// ---------------------------------------------------------------------------
+// Hierarchy construction (single GPU, or one rank of a distributed hierarchy).
+// ---------------------------------------------------------------------------
+hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
+                      const double* lam_host, int device, const hmg_dist* dist, hmg_hierarchy** out) {
     g_err.clear();
     if (!out) return fail(HMG_ERR_INVALID_ARG, "out: null pointer");
     *out = nullptr;
@@ -248,8 +333,24 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
     if (!(thickness > 0) || !std::isfinite(thickness)) return fail(HMG_ERR_INVALID_ARG, "thickness: must be > 0 and finite");
     if (!(w2 >= 0) || !std::isfinite(w2)) return fail(HMG_ERR_INVALID_ARG, "w2: must be >= 0 and finite");
     if (!lam_host) return fail(HMG_ERR_INVALID_ARG, "lam_host: null pointer");
+    int rank = 0, nranks = 1, gather_ref = fine_ref;
+    if (dist) {
+        rank = dist->rank;
+        nranks = dist->nranks;
+        gather_ref = dist->gather_ref;
+        if (nranks < 1 || 320 % nranks != 0) return fail(HMG_ERR_INVALID_ARG, "dist->nranks: must divide 320");
+        if (rank < 0 || rank >= nranks) return fail(HMG_ERR_INVALID_ARG, "dist->rank: must be in [0, nranks)");
+        if (!dist->nccl_id) return fail(HMG_ERR_INVALID_ARG, "dist->nccl_id: null pointer");
+        if (gather_ref < std::max(2, coarsest_ref) || gather_ref > fine_ref)
+            return fail(HMG_ERR_INVALID_ARG, "dist->gather_ref: must be in [max(2, coarsest_ref), fine_ref]");
+    }
+    // lam_host: the finest level, [nlayers][20*4^fine_ref] (single GPU) or this
+    // rank's owned cells [nlayers][20*4^fine_ref/nranks] (distributed, when
+    // gather_ref < fine_ref) -- see include/hmg.h
     const int64_t nfine = 20 * (int64_t(1) << (2 * fine_ref));
-    for (int64_t i = 0; i < nfine * nlayers; ++i)
+    const bool dist_fine = dist && gather_ref < fine_ref;
+    const int64_t nlam = dist_fine ? nfine / nranks : nfine;
+    for (int64_t i = 0; i < nlam * nlayers; ++i)
         if (!(lam_host[i] > 0) || !std::isfinite(lam_host[i]))
             return fail(HMG_ERR_INVALID_ARG, "lam_host: entry " + std::to_string(i) + " is not finite and > 0");
     int ndev = 0;
@@ -266,6 +367,10 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
     H->thickness = thickness;
     H->w2 = w2;
     H->dz = thickness / nlayers;
+    H->rank = rank;
+    H->nranks = nranks;
+    H->gather_ref = dist ? gather_ref : -1;
+    if (const char* e = std::getenv("HMG_FORCE_COLLECTIVES")) H->force_coll = dist && std::string(e) == "1";
     if (const char* e = std::getenv("HMG_SWEEP")) H->use_tc_sweep = std::string(e) != "simple";
     if (const char* e = std::getenv("HMG_SMALL")) H->use_small_sweep = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
@@ -276,7 +381,7 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
             H->tail_ref = -1;
         } else {
             tail = std::max(tail, coarsest_ref);
-            H->tail_ref = std::min(tail, fine_ref);
+            H->tail_ref = std::min(tail, dist ? gather_ref : fine_ref);   // the tail never spans distributed levels
         }
     }
     if (H->use_tc_sweep && !tensor_maps_available()) {
@@ -284,15 +389,6 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
         return fail(HMG_ERR_CUDA, "cuTensorMapEncodeTiled not available from the CUDA driver");
     }
     auto cleanup = [&](hmg_status s2) { free_hierarchy(H); return s2; };
-
-    std::vector<HostLevel> host;
-    try {
-        host = build_icosahedral_levels(fine_ref);
-    } catch (const std::exception& e) {
-        return cleanup(fail(HMG_ERR_INVALID_ARG, std::string("mesh: ") + e.what()));
-    }
-    H->lev.resize(fine_ref + 1);
-    cudaStream_t s = nullptr;
 #define BCUDA(call)                                                                         \
     do {                                                                                    \
         cudaError_t e_ = (call);                                                            \
@@ -300,22 +396,86 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
             return cleanup(fail(e_ == cudaErrorMemoryAllocation ? HMG_ERR_OOM : HMG_ERR_CUDA, \
                                 std::string(#call) + ": " + cudaGetErrorString(e_)));      \
     } while (0)
+    if (dist) {
+        std::string err;
+        const Nccl* N = nccl(&err);
+        if (!N) return cleanup(fail(HMG_ERR_NCCL, err));
+        NcclUniqueId id;
+        std::memcpy(id.internal, dist->nccl_id, sizeof(id.internal));
+        const int r = N->CommInitRank(&H->comm, nranks, id, rank);
+        if (r != kNcclSuccess) return cleanup(fail(HMG_ERR_NCCL, std::string("ncclCommInitRank: ") + N->GetErrorString(r)));
+    }
+
+    std::vector<HostLevel> host;
+    try {
+        host = build_icosahedral_levels(fine_ref);
+    } catch (const std::exception& e) {
+        return cleanup(fail(HMG_ERR_INVALID_ARG, std::string("mesh: ") + e.what()));
+    }
+    // Distributed: all levels' coefficients on the host (4-child means, reading
+    // R3, same formula), because halo cells need their neighbours' values.
+    std::vector<std::vector<double>> lam_levels;
+    if (dist) {
+        lam_levels.resize(fine_ref + 1);
+        lam_levels[fine_ref].assign(lam_host, lam_host + nlam * nlayers);
+        if (dist_fine) {
+            // the fine level arrives distributed: gather it (host staging through the device)
+            const int64_t per = nfine / nranks;
+            std::vector<double> full((size_t)nfine * nlayers);
+            double *dsend = nullptr, *drecv = nullptr;
+            BCUDA(cudaMalloc(&dsend, sizeof(double) * per * nlayers));
+            BCUDA(cudaMalloc(&drecv, sizeof(double) * nfine * nlayers));
+            BCUDA(cudaMemcpy(dsend, lam_host, sizeof(double) * per * nlayers, cudaMemcpyHostToDevice));
+            std::string err;
+            const Nccl* N = nccl(&err);
+            const int r = N->AllGather(dsend, drecv, (size_t)per * nlayers, kNcclFloat64, H->comm, nullptr);
+            if (r != kNcclSuccess) return cleanup(fail(HMG_ERR_NCCL, std::string("ncclAllGather: ") + N->GetErrorString(r)));
+            BCUDA(cudaDeviceSynchronize());
+            std::vector<double> stage((size_t)nfine * nlayers);
+            BCUDA(cudaMemcpy(stage.data(), drecv, sizeof(double) * nfine * nlayers, cudaMemcpyDeviceToHost));
+            cudaFree(dsend);
+            cudaFree(drecv);
+            for (int q = 0; q < nranks; ++q)            // [q][nz][per] -> [nz][nfine]
+                for (int k = 0; k < nlayers; ++k)
+                    std::memcpy(&full[(size_t)k * nfine + (size_t)q * per], &stage[((size_t)q * nlayers + k) * per],
+                                sizeof(double) * per);
+            lam_levels[fine_ref] = std::move(full);
+        }
+        for (int r = fine_ref - 1; r >= coarsest_ref; --r) {
+            const int64_t nf = host[r + 1].n, nc = host[r].n;
+            lam_levels[r].resize((size_t)nc * nlayers);
+            for (int k = 0; k < nlayers; ++k)
+                for (int64_t p = 0; p < nc; ++p) {
+                    const double* l = &lam_levels[r + 1][(size_t)k * nf + 4 * p];
+                    lam_levels[r][(size_t)k * nc + p] = 0.25 * (((l[0] + l[1]) + l[2]) + l[3]);
+                }
+        }
+    }
+    H->lev.resize(fine_ref + 1);
+    cudaStream_t s = nullptr;
     for (int r = coarsest_ref; r <= fine_ref; ++r) {
         DevLevel& L = H->lev[r];
         const HostLevel& HL = host[r];
         L.ref = r;
-        L.n = HL.n;
-        L.ld = round_up32(HL.n);
+        const bool distributed = dist && r > gather_ref;
+        LevelPlan plan;
+        if (distributed) plan = plan_level(r, HL.nbr, rank, nranks);
+        const int64_t off = distributed ? plan.off : 0;
+        L.n = distributed ? plan.n_own : HL.n;
+        const int64_t nh = distributed ? plan.n_halo() : 0;
+        L.ld = round_up32(L.n + nh);
+        const std::vector<int32_t>& nbl = distributed ? plan.nbr_local : HL.nbr;
         const size_t vb = sizeof(double) * nlayers * L.ld;
-        // SoA neighbour table and geometry, padded entries point at cell 0 / are zero
+        // SoA neighbour table and geometry of the owned cells; padding points at cell 0 / is zero
         std::vector<int32_t> nbr(3 * L.ld, 0);
         std::vector<double> geom(7 * L.ld, 0.0);
         for (int64_t c = 0; c < L.n; ++c) {
-            geom[c] = HL.area[c];
+            const int64_t g = off + c;
+            geom[c] = HL.area[g];
             for (int j = 0; j < 3; ++j) {
-                nbr[j * L.ld + c] = HL.nbr[c * 3 + j];
-                geom[(1 + j) * L.ld + c] = HL.len[c * 3 + j];
-                geom[(4 + j) * L.ld + c] = HL.cd[c * 3 + j];
+                nbr[j * L.ld + c] = nbl[c * 3 + j];
+                geom[(1 + j) * L.ld + c] = HL.len[g * 3 + j];
+                geom[(4 + j) * L.ld + c] = HL.cd[g * 3 + j];
             }
         }
         BCUDA(cudaMalloc(&L.nbr, sizeof(int32_t) * 3 * L.ld));
@@ -336,6 +496,39 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
         }
         BCUDA(cudaMemcpy(L.nbr, nbr.data(), sizeof(int32_t) * 3 * L.ld, cudaMemcpyHostToDevice));
         BCUDA(cudaMemcpy(L.geom, geom.data(), sizeof(double) * 7 * L.ld, cudaMemcpyHostToDevice));
+        if (dist) {      // coefficients: owned + halo cells from the host copy
+            std::vector<double> lam((size_t)nlayers * L.ld, 1.0);
+            const std::vector<double>& G = lam_levels[r];
+            for (int k = 0; k < nlayers; ++k) {
+                for (int64_t c = 0; c < L.n; ++c) lam[(size_t)k * L.ld + c] = G[(size_t)k * HL.n + off + c];
+                for (int64_t h = 0; h < nh; ++h) lam[(size_t)k * L.ld + L.n + h] = G[(size_t)k * HL.n + plan.halo_gid[h]];
+            }
+            BCUDA(cudaMemcpy(L.lam, lam.data(), vb, cudaMemcpyHostToDevice));
+        }
+        if (distributed) {
+            DistLevel& D = L.dist;
+            D.on = true;
+            D.off = off;
+            D.n_halo = nh;
+            std::vector<int32_t> sidx;
+            for (const PeerPlan& q : plan.peers) {
+                D.peer_rank.push_back(q.rank);
+                D.send_off.push_back((int64_t)sidx.size());
+                D.send_cnt.push_back((int64_t)q.send_local.size());
+                D.recv_off.push_back(q.recv_offset);
+                D.recv_cnt.push_back(q.recv_count);
+                sidx.insert(sidx.end(), q.send_local.begin(), q.send_local.end());
+            }
+            D.send_total = (int64_t)sidx.size();
+            if (D.send_total) {
+                BCUDA(cudaMalloc(&D.send_idx, sizeof(int32_t) * sidx.size()));
+                BCUDA(cudaMemcpy(D.send_idx, sidx.data(), sizeof(int32_t) * sidx.size(), cudaMemcpyHostToDevice));
+                BCUDA(cudaMalloc(&D.sendbuf, sizeof(double) * D.send_total * nlayers));
+            }
+            if (nh) BCUDA(cudaMalloc(&D.recvbuf, sizeof(double) * nh * nlayers));
+            // coarser level replicated: its vectors use global numbering
+            D.coff = (r - 1 <= gather_ref) ? off / 4 : 0;
+        }
         // tile halos: 128-cell tiles of the streamed sweep (sweep_tc.cu) and
         // 32-cell tiles of the small-level sweep (sweep_small.cu)
         auto build_halo = [&](int tile, int hmax, int32_t** d_cells, int32_t** d_count, uint32_t** d_loc) -> hmg_status {
@@ -344,26 +537,26 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
             std::vector<uint32_t> loc(L.ld, 0);
             for (int64_t t = 0; t < ntiles; ++t) {
                 const int64_t a = t * tile, e = std::min<int64_t>(L.n, a + tile);
-                std::vector<int32_t> out;
+                std::vector<int32_t> outs;
                 for (int64_t c = a; c < e; ++c)
                     for (int j = 0; j < 3; ++j) {
-                        const int32_t o = HL.nbr[c * 3 + j];
-                        if (o < a || o >= e) out.push_back(o);
+                        const int32_t o = nbl[c * 3 + j];
+                        if (o < a || o >= e) outs.push_back(o);
                     }
-                std::sort(out.begin(), out.end());
-                out.erase(std::unique(out.begin(), out.end()), out.end());
-                if ((int)out.size() > hmax) return HMG_OK;        // table not usable: kernel not selected
-                hcount[t] = (int32_t)out.size();
-                std::copy(out.begin(), out.end(), hcells.begin() + t * hmax);
+                std::sort(outs.begin(), outs.end());
+                outs.erase(std::unique(outs.begin(), outs.end()), outs.end());
+                if ((int)outs.size() > hmax) return HMG_OK;        // table not usable: kernel not selected
+                hcount[t] = (int32_t)outs.size();
+                std::copy(outs.begin(), outs.end(), hcells.begin() + t * hmax);
                 for (int64_t c = a; c < e; ++c) {
                     uint32_t packed = 0;
                     for (int j = 0; j < 3; ++j) {
-                        const int32_t o = HL.nbr[c * 3 + j];
+                        const int32_t o = nbl[c * 3 + j];
                         uint32_t slot;
                         if (o >= a && o < e)
                             slot = (uint32_t)(o - a);
                         else
-                            slot = tile + (uint32_t)(std::lower_bound(out.begin(), out.end(), o) - out.begin());
+                            slot = tile + (uint32_t)(std::lower_bound(outs.begin(), outs.end(), o) - outs.begin());
                         packed |= slot << (8 * j);
                     }
                     loc[c] = packed;
@@ -393,11 +586,13 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
         }
     }
     host.clear();
-    // fine coefficients (dense host rows -> padded device rows), coarse by 4-child means
     DevLevel& F = H->lev[fine_ref];
-    BCUDA(cudaMemcpy2D(F.lam, sizeof(double) * F.ld, lam_host, sizeof(double) * F.n, sizeof(double) * F.n, nlayers,
-                       cudaMemcpyHostToDevice));
-    for (int r = fine_ref - 1; r >= coarsest_ref; --r) launch_coarsen_lam(*H, H->lev[r + 1], H->lev[r], s);
+    if (!dist) {
+        // fine coefficients (dense host rows -> padded device rows), coarse by 4-child means
+        BCUDA(cudaMemcpy2D(F.lam, sizeof(double) * F.ld, lam_host, sizeof(double) * F.n, sizeof(double) * F.n, nlayers,
+                           cudaMemcpyHostToDevice));
+        for (int r = fine_ref - 1; r >= coarsest_ref; --r) launch_coarsen_lam(*H, H->lev[r + 1], H->lev[r], s);
+    }
     for (int r = coarsest_ref; r <= fine_ref; ++r) launch_assemble(*H, H->lev[r], s);
     // PCG workspace
     const size_t fb = sizeof(double) * nlayers * F.ld;
@@ -412,6 +607,12 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
     PcgScalars init{};
     init.bad = ~0ull;
     BCUDA(cudaMemcpy(H->scal, &init, sizeof(init), cudaMemcpyHostToDevice));
+    if (dist && gather_ref < fine_ref) {      // coarse-gather staging at gather_ref
+        const DevLevel& C = H->lev[gather_ref];
+        const int64_t cnt = C.n / nranks;
+        BCUDA(cudaMalloc(&H->gbuf_send, sizeof(double) * cnt * nlayers));
+        BCUDA(cudaMalloc(&H->gbuf_recv, sizeof(double) * C.n * nlayers));
+    }
     // Thomas factors (matrix-only; computed once) for the coarse-tail levels and
     // for every level too small to fill the GPU (latency-bound sweeps)
     for (int r = coarsest_ref; r <= fine_ref; ++r) {
@@ -432,10 +633,70 @@ hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, doub
             return cleanup(fail(HMG_ERR_SINGULAR_COLUMN, "singular column: ref " + std::to_string(bad >> 40) +
                                                              " column " + std::to_string(bad & ((1ull << 40) - 1))));
     }
-    BCUDA(cudaGetLastError());
-    BCUDA(cudaDeviceSynchronize());
 #undef BCUDA
     *out = reinterpret_cast<hmg_hierarchy*>(H);
+    return HMG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hmg_last_error(void) { return g_err.c_str(); }
+
+hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
+                               const double* lam_host, int device, hmg_hierarchy** out) {
+    return build_impl(fine_ref, coarsest_ref, nlayers, thickness, w2, lam_host, device, nullptr, out);
+}
+
+hmg_status hmg_build_hierarchy_dist(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
+                                    const double* lam_host, int device, const hmg_dist* dist, hmg_hierarchy** out) {
+    if (!dist) return fail(HMG_ERR_INVALID_ARG, "dist: null pointer");
+    return build_impl(fine_ref, coarsest_ref, nlayers, thickness, w2, lam_host, device, dist, out);
+}
+
+hmg_status hmg_nccl_unique_id(unsigned char* id_out) {
+    if (!id_out) return fail(HMG_ERR_INVALID_ARG, "id_out: null pointer");
+    std::string err;
+    const Nccl* N = nccl(&err);
+    if (!N) return fail(HMG_ERR_NCCL, err);
+    NcclUniqueId id;
+    const int r = N->GetUniqueId(&id);
+    if (r != kNcclSuccess) return fail(HMG_ERR_NCCL, std::string("ncclGetUniqueId: ") + N->GetErrorString(r));
+    std::memcpy(id_out, id.internal, sizeof(id.internal));
+    return HMG_OK;
+}
+
+hmg_status hmg_partition_plan(int fine_ref, int ref, int rank, int nranks, int64_t* off, int64_t* n_own,
+                              int64_t* n_halo, int* npeers, int64_t* send_total, int64_t* halo_gid,
+                              int32_t* nbr_local, int32_t* peer_rank, int64_t* send_count, int64_t* recv_offset,
+                              int64_t* recv_count, int32_t* send_local) {
+    g_err.clear();
+    if (fine_ref < 2 || fine_ref > kMaxRef) return fail(HMG_ERR_INVALID_ARG, "fine_ref: must be in [2, 10]");
+    if (ref < 2 || ref > fine_ref) return fail(HMG_ERR_INVALID_ARG, "ref: must be in [2, fine_ref]");
+    if (nranks < 1 || 320 % nranks != 0) return fail(HMG_ERR_INVALID_ARG, "nranks: must divide 320");
+    if (rank < 0 || rank >= nranks) return fail(HMG_ERR_INVALID_ARG, "rank: must be in [0, nranks)");
+    std::vector<HostLevel> host = build_icosahedral_levels(ref);
+    LevelPlan P = plan_level(ref, host[ref].nbr, rank, nranks);
+    if (off) *off = P.off;
+    if (n_own) *n_own = P.n_own;
+    if (n_halo) *n_halo = P.n_halo();
+    if (npeers) *npeers = (int)P.peers.size();
+    int64_t tot = 0;
+    for (const PeerPlan& q : P.peers) tot += (int64_t)q.send_local.size();
+    if (send_total) *send_total = tot;
+    if (halo_gid) std::copy(P.halo_gid.begin(), P.halo_gid.end(), halo_gid);
+    if (nbr_local) std::copy(P.nbr_local.begin(), P.nbr_local.end(), nbr_local);
+    int64_t pos = 0;
+    for (size_t i = 0; i < P.peers.size(); ++i) {
+        const PeerPlan& q = P.peers[i];
+        if (peer_rank) peer_rank[i] = q.rank;
+        if (send_count) send_count[i] = (int64_t)q.send_local.size();
+        if (recv_offset) recv_offset[i] = q.recv_offset;
+        if (recv_count) recv_count[i] = q.recv_count;
+        if (send_local) std::copy(q.send_local.begin(), q.send_local.end(), send_local + pos);
+        pos += (int64_t)q.send_local.size();
+    }
     return HMG_OK;
 }
 
@@ -448,6 +709,11 @@ hmg_status hmg_level_info(const hmg_hierarchy* h, int ref, int64_t* ncells, int6
     HMG_TRY(check_h(h));
     const Hierarchy& H = HH(h);
     if (ref < 0 || ref > H.fine_ref) return fail(HMG_ERR_INVALID_ARG, "ref: outside [0, fine_ref]");
+    if (ref >= H.coarsest_ref) {
+        if (ncells) *ncells = H.lev[ref].n;
+        if (ld) *ld = H.lev[ref].ld;
+        return HMG_OK;
+    }
     const int64_t n = 20 * (int64_t(1) << (2 * ref));
     if (ncells) *ncells = n;
     if (ld) *ld = round_up32(n);
@@ -461,6 +727,7 @@ hmg_status hmg_apply_helmholtz(const hmg_hierarchy* h, int ref, const double* x,
     HMG_TRY(check_ptr(x, "x"));
     HMG_TRY(check_ptr(y, "y"));
     if (x == y) return fail(HMG_ERR_INVALID_ARG, "y: must not alias x");
+    halo_exchange(H, H.lev[ref], x, S(stream));
     launch_apply(H, H.lev[ref], x, y, S(stream));
     return check_launch();
 }

@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../../include/hmg.h"
+#include "nccl_dyn.h"
 
 namespace hmg {
 
@@ -49,6 +50,21 @@ struct LevelView {
     const double* __restrict__ H2;
 };
 
+// Distribution of one level: owned cells [0, n) in global order
+// (global id off + c), halo slots [n, n + n_halo) grouped by owner rank.
+struct DistLevel {
+    bool on = false;                 // distributed level; false: single GPU or replicated level
+    int64_t off = 0;                 // global id of local cell 0
+    int64_t n_halo = 0;
+    int64_t coff = 0;                // offset added to (c >> 2) to index the coarser level's vectors
+    std::vector<int> peer_rank;
+    std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;   // cells
+    int64_t send_total = 0;
+    int32_t* send_idx = nullptr;     // device, concatenated per peer
+    double* sendbuf = nullptr;       // device [send_total][nz]
+    double* recvbuf = nullptr;       // device [n_halo][nz]
+};
+
 struct DevLevel {
     int ref = 0;
     int64_t n = 0, ld = 0;
@@ -72,6 +88,7 @@ struct DevLevel {
     double* fden = nullptr;
     double* fy = nullptr;
     double* fg = nullptr;
+    DistLevel dist;
     LevelView view(int nz) const {
         const int64_t s = (int64_t)nz * ld;
         return LevelView{n, ld, nz, nbr, bands, bands + s, bands + 2 * s, bands + 3 * s, bands + 4 * s};
@@ -96,7 +113,7 @@ struct TailParams {
 // Device-resident PCG scalars: one struct so a single 64-byte D2H read per
 // iteration returns the residual norm and the singular-pivot flag together.
 struct PcgScalars {
-    double rho, alpha, beta, pq, rr, rz, bb;
+    double rho, alpha, beta, pq, rr, rz, bb, tmp;
     unsigned long long bad;     // encoded (ref << 40 | column) of the first bad pivot, or ~0
 };
 
@@ -126,6 +143,11 @@ struct Hierarchy {
     PcgScalars* scal_host = nullptr;  // pinned
     double *hb = nullptr, *hx = nullptr;  // device staging for the host entry point
     int tail_ref = -1;          // levels <= tail_ref run in one coarse-tail launch (-1: off)
+    // multi-GPU (hmg_build_hierarchy_dist): levels > gather_ref are distributed
+    int rank = 0, nranks = 1, gather_ref = -1;
+    ncclComm_t comm = nullptr;
+    bool force_coll = false;   // HMG_FORCE_COLLECTIVES=1: run the collectives even with one rank (tests)
+    double *gbuf_send = nullptr, *gbuf_recv = nullptr;   // coarse-gather staging
     mutable int64_t launches = 0;
     mutable Profiler prof;
     // diagnostics switches (environment, read at build time): HMG_SWEEP=simple
@@ -192,5 +214,17 @@ struct ProfScope {
 };
 
 enum FinalizeOp { kFinPQ = 0, kFinRR = 1, kFinRZ = 2, kFinRhoInit = 3, kFinBB = 4 };
+
+// multi-GPU helpers (kernels.cu)
+void launch_halo_pack(const Hierarchy& H, const DevLevel& L, const double* v, cudaStream_t s);
+void launch_halo_unpack(const Hierarchy& H, const DevLevel& L, double* v, cudaStream_t s);
+void launch_gather_pack(const Hierarchy& H, const DevLevel& C, const double* v, int64_t off, int64_t cnt, cudaStream_t s);
+void launch_gather_unpack(const Hierarchy& H, const DevLevel& C, double* v, int64_t cnt, cudaStream_t s);
+void launch_update_p(const Hierarchy& H, const DevLevel& L, double* p, const double* z, cudaStream_t s);
+// finalize of a dot when its partial sums are rank-local: local total into scal->tmp
+void launch_finalize_local(const Hierarchy& H, int nparts, cudaStream_t s);
+void launch_scalar_op(const Hierarchy& H, int op, cudaStream_t s);   // op on scal->tmp as the (global) sum
+// api.cu: all-reduce (sum) of scal->tmp across the ranks on stream s
+void dist_allreduce_tmp(const Hierarchy& H, cudaStream_t s);
 
 }  // namespace hmg

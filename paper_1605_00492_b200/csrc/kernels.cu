@@ -224,13 +224,13 @@ __global__ void k_sweep(LevelView L, const double* __restrict__ b, const double*
 // children 4p..4p+3 (R = P^T); prolongation u_f = u_f + u_c[c >> 2].
 // ---------------------------------------------------------------------------
 __global__ void k_restrict(const double* __restrict__ r, int64_t ldf, double* __restrict__ bc,
-                           int64_t ldc, int64_t nc) {
+                           int64_t ldc, int64_t nc, int64_t coff) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int k = blockIdx.y;
     if (p >= nc) return;
     const double2* q = reinterpret_cast<const double2*>(r + k * ldf + 4 * p);
     const double2 a = q[0], b = q[1];
-    bc[k * ldc + p] = ((a.x + a.y) + b.x) + b.y;
+    bc[k * ldc + coff + p] = ((a.x + a.y) + b.x) + b.y;
 }
 
 // Residual of the current iterate restricted to the coarse level: each lane
@@ -238,7 +238,7 @@ __global__ void k_restrict(const double* __restrict__ r, int64_t ldf, double* __
 // one parent) combine in child order through shuffles.
 __global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, const double* __restrict__ b,
                                                                 const double* __restrict__ u,
-                                                                double* __restrict__ bc, int64_t ldc) {
+                                                                double* __restrict__ bc, int64_t ldc, int64_t coff) {
     const int64_t cc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const bool valid = cc < L.n;          // n is a multiple of 4: groups are all-valid or all-invalid
     const int64_t c = valid ? cc : L.n - 1;
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, con
         const double r1 = __shfl_down_sync(0xffffffffu, r, 1);
         const double r2 = __shfl_down_sync(0xffffffffu, r, 2);
         const double r3 = __shfl_down_sync(0xffffffffu, r, 3);
-        if (valid && (lane & 3) == 0) bc[k * ldc + (cc >> 2)] = ((r + r1) + r2) + r3;
+        if (valid && (lane & 3) == 0) bc[k * ldc + coff + (cc >> 2)] = ((r + r1) + r2) + r3;
         um = uk;
         uk = up;
         Um = Uk;
@@ -275,11 +275,58 @@ __global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, con
 }
 
 __global__ void k_prolong_add(const double* __restrict__ uin, const double* __restrict__ uc,
-                              double* __restrict__ uout, int64_t ld, int64_t ldc, int64_t n) {
+                              double* __restrict__ uout, int64_t ld, int64_t ldc, int64_t n, int64_t coff) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int k = blockIdx.y;
     if (c >= n) return;
-    uout[k * ld + c] = uin[k * ld + c] + uc[k * ldc + (c >> 2)];
+    uout[k * ld + c] = uin[k * ld + c] + uc[k * ldc + coff + (c >> 2)];
+}
+
+// ---------------------------------------------------------------------------
+// Multi-GPU staging.  Halo send buffer: [send_total][nz] (cell
+// major, so each peer's segment is contiguous); receive buffer: [n_halo][nz],
+// each peer's run of halo slots contiguous.  Coarse gather: owned segment of
+// every layer packed [nz][cnt]; the all-gather result is [nranks][nz][cnt].
+// ---------------------------------------------------------------------------
+__global__ void k_halo_pack(const double* __restrict__ v, int64_t ld, int nz, const int32_t* __restrict__ idx,
+                            int64_t total, double* __restrict__ buf) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= total * nz) return;
+    const int64_t i = t / nz;
+    const int k = (int)(t - i * nz);
+    buf[t] = v[k * ld + idx[i]];
+}
+
+__global__ void k_halo_unpack(const double* __restrict__ buf, int64_t n_halo, int nz, double* __restrict__ v,
+                              int64_t ld, int64_t n_own) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_halo * nz) return;
+    const int64_t h = t / nz;
+    const int k = (int)(t - h * nz);
+    v[k * ld + n_own + h] = buf[t];
+}
+
+__global__ void k_gather_pack(const double* __restrict__ v, int64_t ld, int64_t off, int64_t cnt,
+                              double* __restrict__ buf) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (i < cnt) buf[k * cnt + i] = v[k * ld + off + i];
+}
+
+__global__ void k_gather_unpack(const double* __restrict__ buf, int64_t cnt, int nz, double* __restrict__ v,
+                                int64_t ld) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y, q = blockIdx.z;
+    if (i < cnt) v[k * ld + q * cnt + i] = buf[((int64_t)q * nz + k) * cnt + i];
+}
+
+__global__ void k_update_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, int64_t ld,
+                           const PcgScalars* __restrict__ sc) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (c >= n) return;
+    const int64_t i = k * ld + c;
+    p[i] = z[i] + sc->beta * p[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -354,13 +401,7 @@ __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x,
     if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = tot;
 }
 
-__global__ void __launch_bounds__(kFinThreads) k_finalize(const double* __restrict__ partial, int np, int op,
-                                                          PcgScalars* __restrict__ sc) {
-    __shared__ double red[kFinThreads / 32];
-    double s = 0.0;
-    for (int i = threadIdx.x; i < np; i += kFinThreads) s = s + partial[i];
-    const double S = block_sum(s, red);
-    if (threadIdx.x != 0) return;
+__device__ __forceinline__ void scalar_op(PcgScalars* sc, int op, double S) {
     switch (op) {
         case kFinPQ: sc->pq = S; sc->alpha = sc->rho / S; break;
         case kFinRR: sc->rr = S; break;
@@ -369,6 +410,22 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(const double* __restri
         case kFinBB: sc->bb = S; break;
     }
 }
+
+__global__ void __launch_bounds__(kFinThreads) k_finalize(const double* __restrict__ partial, int np, int op,
+                                                          PcgScalars* __restrict__ sc) {
+    __shared__ double red[kFinThreads / 32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < np; i += kFinThreads) s = s + partial[i];
+    const double S = block_sum(s, red);
+    if (threadIdx.x != 0) return;
+    if (op < 0) {                 // rank-local total, to be all-reduced
+        sc->tmp = S;
+        return;
+    }
+    scalar_op(sc, op, S);
+}
+
+__global__ void k_scalar_op(PcgScalars* __restrict__ sc, int op) { scalar_op(sc, op, sc->tmp); }
 
 __global__ void k_copy_rows(const double* __restrict__ src, int64_t sld, double* __restrict__ dst, int64_t dld,
                             int64_t n) {
@@ -428,6 +485,21 @@ ProfScope::~ProfScope() {
     if (stop) cudaEventRecord(stop, s);
 }
 
+// Sum of the per-block partials into the PCG scalar `op`; across ranks
+// (multi-GPU) the rank-local totals are all-reduced first.
+void finalize_parts(const Hierarchy& H, int nparts, int op, cudaStream_t s) {
+    if (!H.comm || (H.nranks == 1 && !H.force_coll)) {
+        k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, op, H.scal);
+        ++H.launches;
+        return;
+    }
+    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, -1, H.scal);
+    ++H.launches;
+    dist_allreduce_tmp(H, s);
+    k_scalar_op<<<1, 1, 0, s>>>(H.scal, op);
+    ++H.launches;
+}
+
 int partials_needed(int64_t n, int nz) {
     const int a = (int)(blocks(n, kApplyBlock) * vchunks(n, nz)), v = (int)blocks(n, kVecCells);
     return a > v ? a : v;
@@ -457,8 +529,7 @@ void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, do
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
     k_apply_t<true, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, H.partials, nullptr, nullptr, nullptr);
     ++H.launches;
-    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)(g.x * g.y), kFinPQ, H.scal);
-    ++H.launches;
+    finalize_parts(H, (int)(g.x * g.y), kFinPQ, s);
 }
 
 void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin,
@@ -496,15 +567,14 @@ void launch_apply_pupdate_dot(const Hierarchy& H, const DevLevel& L, const doubl
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
     k_apply_t<true, true><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), pold, q, H.partials, z, pnew, H.scal);
     ++H.launches;
-    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)(g.x * g.y), kFinPQ, H.scal);
-    ++H.launches;
+    finalize_parts(H, (int)(g.x * g.y), kFinPQ, s);
 }
 
 void launch_restrict(const Hierarchy& H, const DevLevel& F, const double* r, double* bc, cudaStream_t s) {
     ProfScope ps(H, kKRestrict, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
-    dim3 g(blocks(C.n, 256), H.nz);
-    k_restrict<<<g, 256, 0, s>>>(r, F.ld, bc, C.ld, C.n);
+    dim3 g(blocks(F.n / 4, 256), H.nz);
+    k_restrict<<<g, 256, 0, s>>>(r, F.ld, bc, C.ld, F.n / 4, F.dist.coff);
     ++H.launches;
 }
 
@@ -513,7 +583,7 @@ void launch_resid_restrict(const Hierarchy& H, const DevLevel& F, const double* 
     ProfScope ps(H, kKResidRestrict, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
     dim3 g(blocks(F.n, kApplyBlock), vchunks(F.n, H.nz));
-    k_resid_restrict<<<g, kApplyBlock, 0, s>>>(F.view(H.nz), b, u, bc, C.ld);
+    k_resid_restrict<<<g, kApplyBlock, 0, s>>>(F.view(H.nz), b, u, bc, C.ld, F.dist.coff);
     ++H.launches;
 }
 
@@ -522,7 +592,7 @@ void launch_prolong_add(const Hierarchy& H, const DevLevel& F, const double* uin
     ProfScope ps(H, kKProlong, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
     dim3 g(blocks(F.n, 256), H.nz);
-    k_prolong_add<<<g, 256, 0, s>>>(uin, uc, uout, F.ld, C.ld, F.n);
+    k_prolong_add<<<g, 256, 0, s>>>(uin, uc, uout, F.ld, C.ld, F.n, F.dist.coff);
     ++H.launches;
 }
 
@@ -543,7 +613,51 @@ void launch_dot(const Hierarchy& H, const DevLevel& L, const double* a, const do
 void launch_finalize(const Hierarchy& H, int op, cudaStream_t s) {
     const DevLevel& L = H.lev[H.fine_ref];
     const dim3 g = vec_grid(L.n, H.nz);
-    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, (int)(g.x * g.y), op, H.scal);
+    finalize_parts(H, (int)(g.x * g.y), op, s);
+}
+
+void launch_finalize_local(const Hierarchy& H, int nparts, cudaStream_t s) {
+    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, -1, H.scal);
+    ++H.launches;
+}
+
+void launch_scalar_op(const Hierarchy& H, int op, cudaStream_t s) {
+    k_scalar_op<<<1, 1, 0, s>>>(H.scal, op);
+    ++H.launches;
+}
+
+void launch_halo_pack(const Hierarchy& H, const DevLevel& L, const double* v, cudaStream_t s) {
+    const int64_t tot = L.dist.send_total * H.nz;
+    if (tot == 0) return;
+    k_halo_pack<<<blocks(tot, 256), 256, 0, s>>>(v, L.ld, H.nz, L.dist.send_idx, L.dist.send_total, L.dist.sendbuf);
+    ++H.launches;
+}
+
+void launch_halo_unpack(const Hierarchy& H, const DevLevel& L, double* v, cudaStream_t s) {
+    const int64_t tot = L.dist.n_halo * H.nz;
+    if (tot == 0) return;
+    k_halo_unpack<<<blocks(tot, 256), 256, 0, s>>>(L.dist.recvbuf, L.dist.n_halo, H.nz, v, L.ld, L.n);
+    ++H.launches;
+}
+
+void launch_gather_pack(const Hierarchy& H, const DevLevel& C, const double* v, int64_t off, int64_t cnt,
+                        cudaStream_t s) {
+    dim3 g(blocks(cnt, 256), H.nz);
+    k_gather_pack<<<g, 256, 0, s>>>(v, C.ld, off, cnt, H.gbuf_send);
+    ++H.launches;
+}
+
+void launch_gather_unpack(const Hierarchy& H, const DevLevel& C, double* v, int64_t cnt, cudaStream_t s) {
+    dim3 g(blocks(cnt, 256), H.nz, H.nranks);
+    k_gather_unpack<<<g, 256, 0, s>>>(H.gbuf_recv, cnt, H.nz, v, C.ld);
+    ++H.launches;
+}
+
+void launch_update_p(const Hierarchy& H, const DevLevel& L, double* p, const double* z, cudaStream_t s) {
+    ProfScope ps(H, kKVector, L.ref, s);
+    dim3 g(blocks(L.n, 256), H.nz);
+    k_update_p<<<g, 256, 0, s>>>(p, z, L.n, L.ld, H.scal);
+    ++H.launches;
     ++H.launches;
 }
 

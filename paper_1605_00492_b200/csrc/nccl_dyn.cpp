@@ -1,0 +1,46 @@
+#include "nccl_dyn.h"
+
+#include <dlfcn.h>
+
+#include <cstdlib>
+#include <mutex>
+
+namespace hmg {
+
+const Nccl* nccl(std::string* err) {
+    static Nccl table;
+    static bool ok = false;
+    static std::string load_err;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = nullptr;
+        if (const char* p = std::getenv("HMG_NCCL_LIB")) h = dlopen(p, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);   // the copy torch loaded
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            load_err = "cannot load libnccl.so.2 (set HMG_NCCL_LIB)";
+            return;
+        }
+        auto sym = [&](const char* name) { return dlsym(h, name); };
+        table.GetUniqueId = reinterpret_cast<decltype(table.GetUniqueId)>(sym("ncclGetUniqueId"));
+        table.CommInitRank = reinterpret_cast<decltype(table.CommInitRank)>(sym("ncclCommInitRank"));
+        table.CommDestroy = reinterpret_cast<decltype(table.CommDestroy)>(sym("ncclCommDestroy"));
+        table.AllReduce = reinterpret_cast<decltype(table.AllReduce)>(sym("ncclAllReduce"));
+        table.AllGather = reinterpret_cast<decltype(table.AllGather)>(sym("ncclAllGather"));
+        table.Send = reinterpret_cast<decltype(table.Send)>(sym("ncclSend"));
+        table.Recv = reinterpret_cast<decltype(table.Recv)>(sym("ncclRecv"));
+        table.GroupStart = reinterpret_cast<decltype(table.GroupStart)>(sym("ncclGroupStart"));
+        table.GroupEnd = reinterpret_cast<decltype(table.GroupEnd)>(sym("ncclGroupEnd"));
+        table.GetErrorString = reinterpret_cast<decltype(table.GetErrorString)>(sym("ncclGetErrorString"));
+        ok = table.GetUniqueId && table.CommInitRank && table.CommDestroy && table.AllReduce && table.AllGather &&
+             table.Send && table.Recv && table.GroupStart && table.GroupEnd && table.GetErrorString;
+        if (!ok) load_err = "libnccl.so.2 lacks a required symbol";
+    });
+    if (!ok) {
+        if (err) *err = load_err;
+        return nullptr;
+    }
+    return &table;
+}
+
+}  // namespace hmg

@@ -278,3 +278,28 @@ def test_sweep_exact_division_fallback(ref, fine):
         u = g.to_device(ref, u0)
         g.line_smooth(ref, g.to_device(ref, bb), u, 2, 0.8, zero)
         assert np.array_equal(g.to_host(ref, u), o.sweep(ref, bb, None if zero else u0, 2, 0.8))
+
+
+@pytest.mark.parametrize("gather_ref", [2, 3, 5])
+@pytest.mark.parametrize("force", ["0", "1"])
+def test_distributed_path_one_rank(monkeypatch, gather_ref, force):
+    """The multi-GPU code path with a one-rank NCCL communicator: distributed
+    levels above gather_ref (unfused prolongation, halo exchange plan, coarse
+    gather) give the oracle's V-cycle bit for bit and the same CG count;
+    HMG_FORCE_COLLECTIVES=1 runs the NCCL all-reduce / all-gather and their
+    pack kernels anyway."""
+    from paper_1605_00492_b200 import nccl_unique_id
+    monkeypatch.setenv("HMG_FORCE_COLLECTIVES", force)
+    cfg = hi.Config("dist1", 5, 0, 16, 0.01, 1e-3)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(5, 0, 16, 0.01, 1e-3, lam, dist=(0, 1, nccl_unique_id(), gather_ref))
+    o = oracle.Hierarchy(5, 0, 16, 0.01, 1e-3, lam)
+    bd = g.to_device(5, b)
+    assert np.array_equal(g.to_host(5, g.apply_helmholtz(5, bd)), o.apply(5, b))
+    for params in (MGParams(), MGParams(0, 2, 5, 0.8), MGParams(2, 0, 3, 0.8)):
+        z = g.to_host(5, g.vcycle(bd, params=params))
+        assert np.array_equal(z, o.vcycle(b, params.nu_pre, params.nu_post, params.n_coarse, params.omega))
+    _, it, rr, st = g.pcg_solve(bd)
+    assert st == "HMG_OK" and it == o.pcg(b)[1]
+    g.close()
+    o.close()
