@@ -210,6 +210,10 @@ const double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b,
 void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const double* b, double* out,
                   cudaStream_t s) {
     const DevLevel& L = H.lev[ref];
+    if (ref == H.coop_ref && coarse_coop_supported(H)) {   // levels <= coop_ref: one cooperative launch
+        launch_coarse_coop(H, p, b, out, s);
+        return;
+    }
     if (ref == H.tail_ref) {                    // levels <= tail_ref: one launch
         launch_coarse_tail(H, p, b, out, s);
         return;
@@ -375,11 +379,25 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_SMALL")) H->use_small_sweep = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     {
-        int tail = -1;   // default: per-level kernels (HMG_TAIL_REF=r enables the one-launch tail)
+        // Cooperative coarse tail (coarse_coop.cu): by default every level of at
+        // most kCoopMaxCells cells runs in one cooperative launch -- those levels
+        // are latency-bound (a sweep is a 2 x nz-step dependency chain, ~4 us,
+        // against ~3 us per dependent kernel launch).  HMG_COOP_REF=r overrides
+        // (-1: off).  It never spans distributed levels.
+        int coop = coarsest_ref;
+        while (coop < fine_ref && 20LL * (1LL << (2 * (coop + 1))) <= kCoopMaxCells) ++coop;
+        if (const char* e = std::getenv("HMG_COOP_REF")) coop = std::atoi(e);
+        H->coop_ref = coop < 0 ? -1 : std::min(std::max(coop, coarsest_ref), dist ? gather_ref : fine_ref);
+        // Diagnostic alternative (HMG_TAIL_REF=r): levels <= r in the global-memory
+        // tail kernel (coarse_tail.cu); HMG_TAIL_GRID=1 makes it cooperative.
+        int tail = -1;
         if (const char* e = std::getenv("HMG_TAIL_REF")) tail = std::atoi(e);
+        if (const char* e = std::getenv("HMG_TAIL_GRID")) H->tail_grid = std::string(e) != "0";
+        if (const char* e = std::getenv("HMG_TAIL_THREADS")) H->tail_threads = std::max(32, std::min(128, std::atoi(e)));
         if (tail < 0) {
             H->tail_ref = -1;
         } else {
+            H->coop_ref = -1;
             tail = std::max(tail, coarsest_ref);
             H->tail_ref = std::min(tail, dist ? gather_ref : fine_ref);   // the tail never spans distributed levels
         }
@@ -617,7 +635,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     // for every level too small to fill the GPU (latency-bound sweeps)
     for (int r = coarsest_ref; r <= fine_ref; ++r) {
         DevLevel& L = H->lev[r];
-        if (!(r <= H->tail_ref || L.n <= kFactMaxCells)) continue;
+        if (!(r <= H->tail_ref || r <= H->coop_ref || L.n <= kFactMaxCells)) continue;
         const size_t vb = sizeof(double) * nlayers * L.ld;
         BCUDA(cudaMalloc(&L.fden, 3 * vb));          // [3][nz][ld]: den, y, g (one TMA box)
         L.fy = L.fden + (size_t)nlayers * L.ld;

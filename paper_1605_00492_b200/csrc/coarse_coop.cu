@@ -1,0 +1,393 @@
+// Coarse levels of the V-cycle in ONE cooperative kernel launch, with the
+// operands of each 32-column tile resident in shared memory.
+//
+// Alg. 1 below the level `top` (default: ref 4, the first level
+// whose sweeps are bounded by the length of the column recurrences rather
+// than by HBM bandwidth; the paper saw the same coarse-level inefficiency on
+// CPUs): presmoothing, residual restriction, the coarsest level's
+// n_coarse sweeps (BASELINE.json: 20) and the postsmoothing with the fused
+// prolongation.  Each CTA is one warp owning 32-column tiles; per level it
+// brings the tile's bands and precomputed Thomas factors into shared memory
+// with two TMA tensor copies, and each dependent step (a sweep, a restriction)
+// ends in a grid barrier (~1.2 us on B200) instead of a kernel boundary
+// (~3 us per dependent launch plus the TMA prologue of a fresh CTA).  Between
+// steps, values cross tiles through global memory (L2): every step reloads
+// the tile's iterate and its <= 32 off-tile neighbour cells.
+//
+// Arithmetic: tile_sweep (small_tile.cuh), identical in operation order to
+// every other sweep (readings R5-R9), so the result is bitwise the oracle's.
+#include <cuda.h>
+
+#include <cooperative_groups.h>
+#include <cstring>
+#include <stdexcept>
+
+#include "hmg_internal.h"
+#include "small_tile.cuh"
+#include "sm100_ptx.cuh"
+
+namespace hmg {
+
+CUtensorMap make_tensor_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes);
+
+namespace {
+
+constexpr int kCoopLevels = 5;
+
+#ifdef HMG_TIMING
+__device__ long long g_coop_timing[512];
+__device__ int g_coop_ntiming;
+#define CSTAMP()                                                              \
+    do {                                                                      \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && nst < 512) g_coop_timing[nst++] = clock64(); \
+    } while (0)
+#else
+#define CSTAMP() do {} while (0)
+#endif   // levels top..coarsest handled (index = ref - coarsest)
+
+struct CoopLevel {
+    LevelView V;
+    SmallHalo sh;
+    double *wa, *wb, *b, *u;
+    int ntiles;
+};
+
+struct CoopParams {
+    CUtensorMap bands[kCoopLevels];   // 3-D box 32 x nzp x 5 (D, U, H0, H1, H2)
+    CUtensorMap fact[kCoopLevels];    // 3-D box 32 x nzp x 3 (den, y, g)
+    CoopLevel lev[kCoopLevels];
+    int nz, top, coarsest, nu_pre, nu_post, n_coarse;
+    double omega;
+    const double* b_top;
+    double* out_top;
+};
+
+struct CoopSmem {
+    size_t bands, fact, b, u, hu, z, uc, huc, bar, total;
+};
+
+__host__ __device__ inline CoopSmem coop_layout(int nz) {
+    CoopSmem L;
+    const size_t plane = sizeof(double) * (size_t)((nz + 7) & ~7) * kTileW;   // layers padded to 8
+    size_t off = 0;
+    L.bands = off; off += 5 * plane;
+    L.fact = off;  off += 3 * plane;
+    L.b = off;     off += plane;
+    L.u = off;     off += plane;
+    L.hu = off;    off += plane;
+    L.z = off;     off += plane;
+    L.uc = off;    off += plane / 4;      // [nz][8] parents of the tile (prolongation)
+    L.huc = off;   off += plane;          // [nz][32] parents of the halo cells
+    L.bar = off;   off += 64;
+    L.total = off;
+    return L;
+}
+
+constexpr int kCoopThreads = kTileW * kTileWarps;   // 4 warps per 32-column tile
+
+__global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_constant__ CoopParams P) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    const int nz = P.nz, nzp = (nz + 7) & ~7;
+    const int tid = threadIdx.x, j = tid & 31, warp = tid >> 5;   // j: the column of this lane
+    const CoopSmem lay = coop_layout(nz);
+    const int PL = nzp * kTileW;                       // doubles per plane
+    double* sB = reinterpret_cast<double*>(smraw + lay.bands);
+    double* sF = reinterpret_cast<double*>(smraw + lay.fact);
+    double* sb = reinterpret_cast<double*>(smraw + lay.b);
+    double* su = reinterpret_cast<double*>(smraw + lay.u);
+    double* shu = reinterpret_cast<double*>(smraw + lay.hu);
+    double* sz = reinterpret_cast<double*>(smraw + lay.z);
+    double* suc = reinterpret_cast<double*>(smraw + lay.uc);
+    double* shuc = reinterpret_cast<double*>(smraw + lay.huc);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + lay.bar);
+    const TileSmem S{sB, sB + PL, sB + 2 * PL, sB + 3 * PL, sB + 4 * PL, sF, sF + PL, sF + 2 * PL, sb, su, shu, sz};
+    if (tid == 0) {
+        ptx::mbar_init(bar, 1);
+        ptx::fence_mbar_init();
+    }
+    // padding rows (layers nz..nzp-1) of the vector planes stay zero
+    for (int q = nz * kTileW + tid; q < PL; q += kCoopThreads) sb[q] = su[q] = shu[q] = 0.0;
+    __syncthreads();
+#ifdef HMG_TIMING
+    int nst = 0;
+#endif
+    CSTAMP();
+    uint32_t phase = 0;
+    int loaded_l = -1, loaded_tile = -1;               // which tile's bands/factors are in shared memory
+
+    // bands + factors of (level l, tile t): two TMA tensor copies (the caller
+    // has synchronised the CTA since the planes were last read)
+    auto load_static = [&](int l, int t) {
+        if (loaded_l == l && loaded_tile == t) return;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads before async writes
+        if (tid == 0) {
+            ptx::mbar_arrive_expect_tx(bar, (uint32_t)(8 * sizeof(double) * PL));
+            ptx::tma_load_3d(sB, &P.bands[l - P.coarsest], t * kTileW, 0, 0, bar);
+            ptx::tma_load_3d(sF, &P.fact[l - P.coarsest], t * kTileW, 0, 0, bar);
+        }
+        ptx::mbar_wait(bar, phase);
+        phase ^= 1u;
+        loaded_l = l;
+        loaded_tile = t;
+    };
+    const CoopLevel* LV = P.lev - P.coarsest;          // LV[ref]
+    // Vector loads are asynchronous copies (one round trip for a whole tile):
+    // rows of w columns starting at col0 of v (leading dimension ld) into the
+    // plane dst [nz][w], 16 bytes per copy (w = 32 or 8).  Columns beyond n are
+    // padding and only feed lanes whose results are discarded.
+    auto cp_rows = [&](double* dst, const double* v, int64_t ld, int64_t col0, int w) {
+        const int cpr = w / 2;                          // 16-byte chunks per row
+        for (int q = tid; q < nz * cpr; q += kCoopThreads) {
+            const int k = q / cpr, ch = q - k * cpr;
+            ptx::cp_async16(dst + k * w + 2 * ch, v + k * ld + col0 + 2 * ch);
+        }
+    };
+    // off-tile neighbour values of v (cell >> shift) into the plane dst: lane h
+    // of every warp gathers halo cell h, warps split the layers
+    auto cp_halo = [&](double* dst, const double* v, const CoopLevel& L, int t, int shift, int64_t ldv) {
+        const int hcount = L.sh.count[t];
+        if (j < hcount) {
+            const int32_t hc = L.sh.cells[t * kSmallHaloMax + j] >> shift;
+            for (int k = warp; k < nz; k += kTileWarps) ptx::cp_async8(dst + k * kTileW + j, v + k * ldv + hc);
+        }
+    };
+    auto cp_wait = [&]() {
+        ptx::cp_async_wait_all();
+        __syncthreads();
+    };
+    auto store_own = [&](double* dst, const CoopLevel& L, int64_t c) {
+        if (c < L.V.n)
+            for (int k = warp; k < nz; k += kTileWarps) dst[k * L.V.ld + c] = su[k * kTileW + j];
+    };
+    auto slots = [&](const CoopLevel& L, int64_t c, int& l0, int& l1, int& l2) {
+        const uint32_t loc = L.sh.loc[c < L.V.n ? c : L.V.n - 1];
+        l0 = loc & 0xff;
+        l1 = (loc >> 8) & 0xff;
+        l2 = (loc >> 16) & 0xff;
+    };
+    // one damped sweep of level l from iterate uin (nullptr: zero guess) to uout, all tiles
+    auto sweep_step = [&](int l, const double* bl, const double* uin, double* uout) {
+        const CoopLevel& L = LV[l];
+        for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
+            const int64_t c = (int64_t)t * kTileW + j;
+            int l0, l1, l2;
+            slots(L, c, l0, l1, l2);
+            __syncthreads();                           // every thread is done with the previous tile's planes
+            cp_rows(sb, bl, L.V.ld, (int64_t)t * kTileW, kTileW);
+            if (uin) {
+                cp_rows(su, uin, L.V.ld, (int64_t)t * kTileW, kTileW);
+                cp_halo(shu, uin, L, t, 0, L.V.ld);
+            }
+            load_static(l, t);
+            cp_wait();
+            CSTAMP();
+            tile_sweep_cta(S, nz, warp, j, l0, l1, l2, uin == nullptr, P.omega, c < L.V.n);
+            CSTAMP();
+            store_own(uout, L, c);
+        }
+    };
+
+    const double* cur[kMaxRef + 1];
+    // ---- down leg: presmooth, restrict the residual ----
+    for (int l = P.top; l > P.coarsest; --l) {
+        const CoopLevel& L = LV[l];
+        const CoopLevel& C = LV[l - 1];
+        const double* bl = (l == P.top) ? P.b_top : L.b;
+        const double* c_in = nullptr;
+        for (int s = 0; s < P.nu_pre; ++s) {
+            double* dst = (c_in == L.wa) ? L.wb : L.wa;
+            sweep_step(l, bl, c_in, dst);
+            grid.sync();
+            CSTAMP();
+            c_in = dst;
+        }
+        cur[l] = c_in;
+        for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
+            const int64_t c = (int64_t)t * kTileW + j;
+            int l0, l1, l2;
+            slots(L, c, l0, l1, l2);
+            __syncthreads();
+            cp_rows(sb, bl, L.V.ld, (int64_t)t * kTileW, kTileW);
+            if (c_in) {
+                cp_rows(su, c_in, L.V.ld, (int64_t)t * kTileW, kTileW);
+                cp_halo(shu, c_in, L, t, 0, L.V.ld);
+            }
+            load_static(l, t);
+            cp_wait();
+            CSTAMP();
+            tile_residuals_cta(S, nz, warp, j, l0, l1, l2, c_in == nullptr);   // r = b - H^ u (r = b from zero)
+            __syncthreads();
+            // b_c[k][p] = ((r0 + r1) + r2) + r3 over the children 4p..4p+3: thread = (parent, layer phase)
+            const int pp = tid & 7, kph = tid >> 3;
+            const int64_t p = (int64_t)t * (kTileW / 4) + pp;
+            if (p < C.V.n)
+                for (int k = kph; k < nz; k += kCoopThreads / 8) {
+                    const double* r = sz + k * kTileW + 4 * pp;
+                    C.b[k * C.V.ld + p] = ((r[0] + r[1]) + r[2]) + r[3];
+                }
+        }
+        grid.sync();
+        CSTAMP();
+    }
+    // ---- coarsest level: n_coarse sweeps from zero ----
+    {
+        const int l = P.coarsest;
+        const CoopLevel& L = LV[l];
+        const double* bl = (l == P.top) ? P.b_top : L.b;
+        double* out = (l == P.top) ? P.out_top : L.u;
+        if (L.ntiles == 1) {
+            // one tile: every sweep stays in shared memory (no off-tile neighbours)
+            if (blockIdx.x == 0) {
+                const int64_t c = j;
+                int l0, l1, l2;
+                slots(L, c, l0, l1, l2);
+                __syncthreads();
+                cp_rows(sb, bl, L.V.ld, 0, kTileW);
+                load_static(l, 0);
+                cp_wait();
+                CSTAMP();
+                for (int s = 0; s < P.n_coarse; ++s)
+                    tile_sweep_cta(S, nz, warp, j, l0, l1, l2, s == 0, P.omega, c < L.V.n);
+                CSTAMP();
+                store_own(out, L, c);
+            }
+        } else {
+            const double* c_in = nullptr;
+            for (int s = 0; s < P.n_coarse; ++s) {
+                double* dst = (s == P.n_coarse - 1) ? out : ((c_in == L.wa) ? L.wb : L.wa);
+                sweep_step(l, bl, c_in, dst);
+                if (s < P.n_coarse - 1) grid.sync();
+                c_in = dst;
+            }
+        }
+        grid.sync();
+        CSTAMP();
+    }
+    // ---- up leg: prolongation fused into the first postsmoothing sweep ----
+    for (int l = P.coarsest + 1; l <= P.top; ++l) {
+        const CoopLevel& L = LV[l];
+        const CoopLevel& C = LV[l - 1];
+        const double* bl = (l == P.top) ? P.b_top : L.b;
+        double* out = (l == P.top) ? P.out_top : L.u;
+        const double* c_in = cur[l];                   // presmoothed iterate (nullptr: zero)
+        // first step: u = c_in + P u_c formed in shared memory for the tile and its halo
+        double* dst = (P.nu_post <= 1) ? out : ((c_in == L.wa) ? L.wb : L.wa);
+        for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
+            const int64_t c = (int64_t)t * kTileW + j;
+            const bool valid = c < L.V.n;
+            int l0, l1, l2;
+            slots(L, c, l0, l1, l2);
+            const int64_t c0 = (int64_t)t * kTileW;
+            __syncthreads();
+            cp_rows(sb, bl, L.V.ld, c0, kTileW);
+            if (c_in) {
+                cp_rows(su, c_in, L.V.ld, c0, kTileW);
+                cp_halo(shu, c_in, L, t, 0, L.V.ld);
+            }
+            cp_rows(suc, C.u, C.V.ld, c0 / 4, kTileW / 4);
+            cp_halo(shuc, C.u, L, t, 2, C.V.ld);
+            load_static(l, t);
+            cp_wait();
+            // u + P u_c, the addition of the prolongation (0 + u_c from a zero iterate)
+            const int hcount = L.sh.count[t];
+            for (int k = warp; k < nz; k += kTileWarps) {
+                const double v = c_in ? su[k * kTileW + j] : 0.0;
+                su[k * kTileW + j] = v + suc[k * (kTileW / 4) + (j >> 2)];
+                if (j < hcount) {
+                    const double h = c_in ? shu[k * kTileW + j] : 0.0;
+                    shu[k * kTileW + j] = h + shuc[k * kTileW + j];
+                }
+            }
+            __syncthreads();
+            CSTAMP();
+            if (P.nu_post > 0) tile_sweep_cta(S, nz, warp, j, l0, l1, l2, false, P.omega, valid);
+            CSTAMP();
+            store_own(dst, L, c);
+        }
+        grid.sync();
+        CSTAMP();
+        const double* prev = dst;
+        for (int s = 1; s < P.nu_post; ++s) {
+            double* d2 = (s == P.nu_post - 1) ? out : ((prev == L.wa) ? L.wb : L.wa);
+            sweep_step(l, bl, prev, d2);
+            grid.sync();
+            CSTAMP();
+            prev = d2;
+        }
+    }
+}
+
+#ifdef HMG_TIMING
+}  // namespace
+extern "C" void hmg_debug_coop_timing(long long* out) { cudaMemcpyFromSymbol(out, g_coop_timing, sizeof(long long) * 512); }
+extern "C" unsigned long long hmg_debug_tile_slow() {
+    unsigned long long v = 0;
+    cudaMemcpyFromSymbol(&v, g_tile_slow_count, sizeof(v));
+    return v;
+}
+namespace {
+#endif
+
+}  // namespace
+
+bool coarse_coop_supported(const Hierarchy& H) {
+    if (H.coop_ref < 0) return false;
+    if (H.coop_ref - H.coarsest_ref + 1 > kCoopLevels) return false;
+    if (coop_layout(H.nz).total > 227 * 1024) return false;
+    for (int r = H.coarsest_ref; r <= H.coop_ref; ++r) {
+        const DevLevel& L = H.lev[r];
+        if (!L.fden || !L.small.loc) return false;
+    }
+    return true;
+}
+
+void launch_coarse_coop(const Hierarchy& H, const hmg_mg_params& p, const double* b_top, double* out_top,
+                        cudaStream_t s) {
+    static_assert(sizeof(CoopParams) <= 4096, "kernel parameter block");
+    CoopParams P;
+    std::memset(&P, 0, sizeof(P));
+    const int nz = H.nz, nzp = (nz + 7) & ~7;
+    P.nz = nz;
+    P.top = H.coop_ref;
+    P.coarsest = H.coarsest_ref;
+    P.nu_pre = p.nu_pre;
+    P.nu_post = p.nu_post;
+    P.n_coarse = p.n_coarse;
+    P.omega = p.omega;
+    P.b_top = b_top;
+    P.out_top = out_top;
+    for (int r = H.coarsest_ref; r <= H.coop_ref; ++r) {
+        const DevLevel& L = H.lev[r];
+        const int i = r - H.coarsest_ref;
+        CoopLevel& C = P.lev[i];
+        C.V = L.view(nz);
+        C.sh = L.small;
+        C.wa = L.wa;
+        C.wb = L.wb;
+        C.b = L.b;
+        C.u = L.u;
+        C.ntiles = (int)((L.n + kTileW - 1) / kTileW);
+        P.bands[i] = make_tensor_map(C.V.D, L.ld, nz, kTileW, nzp, 5);
+        P.fact[i] = make_tensor_map(L.fden, L.ld, nz, kTileW, nzp, 3);
+    }
+    const size_t smem = coop_layout(nz).total;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_coarse_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_coop, kCoopThreads, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
+    int grid = P.lev[H.coop_ref - H.coarsest_ref].ntiles;
+    const int cap = (per_sm < 1 ? 1 : per_sm) * sms;
+    if (grid > cap) grid = cap;
+    ProfScope ps(H, kKCoarseTail, H.coop_ref, s);
+    void* args[] = {&P};
+    cudaLaunchCooperativeKernel((const void*)k_coarse_coop, dim3(grid), dim3(kCoopThreads), args, smem, s);
+    ++H.launches;
+}
+
+}  // namespace hmg

@@ -15,6 +15,8 @@
 // (<= 1 MB at tail_ref 2) stays in L1/L2.
 #include <cfloat>
 
+#include <cooperative_groups.h>
+
 #include "hmg_internal.h"
 #include "sm100_ptx.cuh"
 
@@ -148,11 +150,28 @@ __device__ void resid_restrict_cell(const TailLevel& F, int nz, const double* b,
     }
 }
 
-__global__ void __launch_bounds__(512, 1) k_coarse_tail(TailParams P) {
+// Block-wide or grid-wide barrier between the dependent steps of the tail.
+template <bool GRID>
+__device__ __forceinline__ void tail_sync() {
+    if (GRID)
+        cooperative_groups::this_grid().sync();
+    else
+        __syncthreads();
+}
+
+// GRID = false: one CTA runs every step (__syncthreads between them).
+// GRID = true: a cooperative launch of several CTAs; columns are dealt out
+// over all threads of the grid and the dependent steps are separated by grid
+// barriers (~1 us each on B200, against ~3 us per dependent kernel launch);
+// the coarsest level's sweeps run in CTA 0 alone when its columns fit there.
+template <bool GRID>
+__global__ void __launch_bounds__(GRID ? 128 : 512, 1) k_coarse_tail(TailParams P) {
     extern __shared__ double zsm[];          // [nz][blockDim]: Thomas z of each thread's current column
     const int nz = P.nz;
-    const int T = blockDim.x, t = threadIdx.x;
-    double* zs = zsm + t;
+    const int zstride = blockDim.x;
+    const int64_t t = GRID ? (int64_t)blockIdx.x * blockDim.x + threadIdx.x : threadIdx.x;
+    const int64_t T = GRID ? (int64_t)gridDim.x * blockDim.x : blockDim.x;
+    double* zs = zsm + threadIdx.x;
     const double w = P.omega;
     const double* cur[kMaxRef + 1];          // presmoothed iterate per level
     // ---- down leg: presmooth, restrict the residual ----
@@ -163,14 +182,14 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tail(TailParams P) {
         double* dst = L.wa;
         for (int s = 0; s < P.nu_pre; ++s) {
             dst = (c_in == L.wa) ? L.wb : L.wa;
-            for (int64_t c = t; c < L.V.n; c += T) sweep_col(L, nz, bl, c_in, nullptr, dst, w, c, zs, T);
-            __syncthreads();
+            for (int64_t c = t; c < L.V.n; c += T) sweep_col(L, nz, bl, c_in, nullptr, dst, w, c, zs, zstride);
+            tail_sync<GRID>();
             c_in = dst;
         }
         cur[l] = c_in;
         const TailLevel& C = P.lev[l - 1];
         for (int64_t p = t; p < C.V.n; p += T) resid_restrict_cell(L, nz, bl, c_in, C.b, C.V.ld, p);
-        __syncthreads();
+        tail_sync<GRID>();
     }
     // ---- coarsest level: n_coarse sweeps from zero, result in its u ----
     {
@@ -179,12 +198,20 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tail(TailParams P) {
         const double* bl = (l == P.top) ? P.b_top : L.b;
         double* out = (l == P.top) ? P.out_top : L.u;
         const double* c_in = nullptr;
-        for (int s = 0; s < P.n_coarse; ++s) {
-            double* dst = (s == P.n_coarse - 1) ? out : ((c_in == L.wa) ? L.wb : L.wa);
-            for (int64_t c = t; c < L.V.n; c += T) sweep_col(L, nz, bl, c_in, nullptr, dst, w, c, zs, T);
-            __syncthreads();
-            c_in = dst;
+        const bool one_cta = GRID && L.V.n <= (int64_t)blockDim.x;   // CTA 0 alone, block barriers
+        if (!one_cta || blockIdx.x == 0) {
+            const int64_t tt = one_cta ? threadIdx.x : t, TT = one_cta ? blockDim.x : T;
+            for (int s = 0; s < P.n_coarse; ++s) {
+                double* dst = (s == P.n_coarse - 1) ? out : ((c_in == L.wa) ? L.wb : L.wa);
+                for (int64_t c = tt; c < L.V.n; c += TT) sweep_col(L, nz, bl, c_in, nullptr, dst, w, c, zs, zstride);
+                if (one_cta)
+                    __syncthreads();
+                else
+                    tail_sync<GRID>();
+                c_in = dst;
+            }
         }
+        if (one_cta) tail_sync<GRID>();
     }
     // ---- up leg: prolongation fused into the first postsmoothing sweep ----
     for (int l = P.coarsest + 1; l <= P.top; ++l) {
@@ -195,14 +222,14 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tail(TailParams P) {
         const double* c_in = cur[l];
         if (!c_in) {                          // nu_pre = 0: the presmoothed iterate is zero
             for (int64_t i = t; i < (int64_t)nz * L.V.ld; i += T) L.wa[i] = 0.0;
-            __syncthreads();
+            tail_sync<GRID>();
             c_in = L.wa;
         }
         if (P.nu_post == 0) {
             for (int64_t c = t; c < L.V.n; c += T)
                 for (int k = 0; k < nz; ++k)
                     out[k * L.V.ld + c] = c_in[k * L.V.ld + c] + C.u[k * C.V.ld + (c >> 2)];
-            __syncthreads();
+            tail_sync<GRID>();
             continue;
         }
         for (int s = 0; s < P.nu_post; ++s) {
@@ -210,8 +237,8 @@ __global__ void __launch_bounds__(512, 1) k_coarse_tail(TailParams P) {
             TailLevel Lc = L;
             Lc.ldc = C.V.ld;
             for (int64_t c = t; c < L.V.n; c += T)
-                sweep_col(Lc, nz, bl, c_in, s == 0 ? C.u : nullptr, dst, w, c, zs, T);
-            __syncthreads();
+                sweep_col(Lc, nz, bl, c_in, s == 0 ? C.u : nullptr, dst, w, c, zs, zstride);
+            tail_sync<GRID>();
             c_in = dst;
         }
     }
@@ -250,6 +277,29 @@ void launch_coarse_tail(const Hierarchy& H, const hmg_mg_params& p, const double
         T.ldc = 0;
     }
     const int64_t n = H.lev[H.tail_ref].n;
+    ProfScope ps(H, kKCoarseTail, H.tail_ref, s);
+    if (H.tail_grid) {
+        // cooperative launch: blocks of tail_threads columns, as many as the
+        // top level needs, all co-resident (cooperative launch guarantees it)
+        const int threads = H.tail_threads;
+        const size_t smem = sizeof(double) * H.nz * threads;
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_coarse_tail<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        int per_sm = 0, sms = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_tail<true>, threads, smem);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
+        int64_t grid = (n + threads - 1) / threads;
+        const int64_t cap = (int64_t)(per_sm < 1 ? 1 : per_sm) * sms;
+        if (grid > cap) grid = cap;
+        void* args[] = {&P};
+        cudaLaunchCooperativeKernel((const void*)k_coarse_tail<true>, dim3((unsigned)grid), dim3(threads), args, smem,
+                                    s);
+        ++H.launches;
+        return;
+    }
     int threads = (int)((n + 31) / 32 * 32);
     if (threads > 512) threads = 512;
     const int cap = (int)((200 * 1024) / (sizeof(double) * H.nz)) / 32 * 32;   // z slots in shared memory
@@ -257,11 +307,10 @@ void launch_coarse_tail(const Hierarchy& H, const hmg_mg_params& p, const double
     const size_t smem = sizeof(double) * H.nz * threads;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_coarse_tail, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_coarse_tail<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    ProfScope ps(H, kKCoarseTail, H.tail_ref, s);
-    k_coarse_tail<<<1, threads, smem, s>>>(P);
+    k_coarse_tail<false><<<1, threads, smem, s>>>(P);
     ++H.launches;
 }
 

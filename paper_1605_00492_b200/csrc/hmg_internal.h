@@ -16,6 +16,7 @@ constexpr int kMaxRef = 10;
 constexpr int kSweepTile = 128;   // columns per CTA of the TMA/TMEM sweep (sweep_tc.cu)
 constexpr int kHaloMax = 64;
 constexpr int64_t kFactMaxCells = 148 * 128;
+constexpr int64_t kCoopMaxCells = 5120;   // default cooperative coarse tail: levels up to this size (ref 4)
 constexpr int kSmallTile = 32;    // columns per CTA of the small-level sweep (sweep_small.cu)
 constexpr int kSmallHaloMax = 32; // off-tile neighbours per 32-cell tile (24 observed)  // levels up to this size stream precomputed Thomas pivots      // max off-tile neighbour cells per tile (51 observed at ref >= 2)
 
@@ -143,6 +144,9 @@ struct Hierarchy {
     PcgScalars* scal_host = nullptr;  // pinned
     double *hb = nullptr, *hx = nullptr;  // device staging for the host entry point
     int tail_ref = -1;          // levels <= tail_ref run in one coarse-tail launch (-1: off)
+    bool tail_grid = false;     // the tail is a cooperative multi-CTA launch (false: one CTA)
+    int tail_threads = 64;      // threads per CTA of the cooperative tail
+    int coop_ref = -1;          // levels <= coop_ref run in one cooperative smem-tile launch (-1: off)
     // multi-GPU (hmg_build_hierarchy_dist): levels > gather_ref are distributed
     int rank = 0, nranks = 1, gather_ref = -1;
     ncclComm_t comm = nullptr;
@@ -191,6 +195,10 @@ void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, con
 // coarse_tail.cu
 void launch_factor(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
 void launch_coarse_tail(const Hierarchy& H, const hmg_mg_params& p, const double* b_top, double* out_top,
+                        cudaStream_t s);
+// coarse_coop.cu: levels <= H.coop_ref in one cooperative launch (32-column smem tiles)
+bool coarse_coop_supported(const Hierarchy& H);
+void launch_coarse_coop(const Hierarchy& H, const hmg_mg_params& p, const double* b_top, double* out_top,
                         cudaStream_t s);
 size_t coarsest_smem_bytes(int nz, int64_t n, int threads);
 void launch_coarsest(const Hierarchy& H, const DevLevel& L, const double* b, double* out, int n_coarse, double omega,

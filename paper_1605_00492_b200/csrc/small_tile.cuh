@@ -1,0 +1,263 @@
+// One damped line-Jacobi sweep on a 32-column tile whose whole operand set is
+// resident in shared memory (one warp, lane = column).  Shared by the
+// small-level sweep kernel (sweep_small.cu) and the cooperative coarse tail
+// (coarse_coop.cu).
+//
+// Same operation (Eq. 10 read with Eq. 13, readings R5-R7) and the same
+// operation order as every other sweep; bit-identical results.  The sweep is
+// split into passes with independent work batched into registers: all
+// residuals (independent per layer), then the z recurrence (the only serial
+// chain: 5 dependent fp64 ops per layer), then back substitution.  All passes
+// run over nzp = nz rounded up to 8 layers with no per-layer branches; rows
+// >= nz hold zeros and their results never reach a layer < nz (their 'slow'
+// flags are masked, and back substitution restarts at nz - 1).
+#pragma once
+#include "hmg_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace hmg {
+
+constexpr int kTileW = kSmallTile;   // 32 columns, one warp
+
+#ifdef HMG_TIMING
+__device__ unsigned long long g_tile_slow_count;   // diagnostics: exact-division redos
+#endif
+
+// Shared-memory planes of one tile, each [nzp][32] (nzp = nz rounded up to 8).
+struct TileSmem {
+    const double* D;
+    const double* U;
+    const double* H0;
+    const double* H1;
+    const double* H2;
+    const double* den;   // Thomas pivots den_k (precomputed at setup, same formulas)
+    const double* y;     // refined reciprocals of den_k
+    const double* g;     // multipliers g_k = U_k / den_k
+    const double* b;     // right-hand side
+    double* u;           // iterate: in on entry, out on exit
+    const double* hu;    // off-tile neighbour values [nz][32] (halo slot h at column h)
+    double* z;           // scratch
+};
+
+// neighbour value of local slot l at layer k (in-tile slot < 32, else halo)
+__device__ __forceinline__ double tile_nb(const TileSmem& S, int k, int l) {
+    return l < kTileW ? S.u[k * kTileW + l] : S.hu[k * kTileW + (l - kTileW)];
+}
+
+// pass 1: r_k = b_k - (H^ u)_k for every layer into S.z (zero guess: r = b)
+__device__ __forceinline__ void tile_residuals(const TileSmem& S, int nz, int j, int l0, int l1, int l2, bool zero) {
+    const int nzp = (nz + 7) & ~7;
+    if (zero) {
+        for (int k0 = 0; k0 < nzp; k0 += 8) {
+            double r[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = S.b[(k0 + i) * kTileW + j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = r[i];
+        }
+        return;
+    }
+    for (int k0 = 0; k0 < nzp; k0 += 8) {
+        double r[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = k0 + i;
+            const int q = k * kTileW + j;
+            const int qm = k > 0 ? q - kTileW : q;          // in-range address; term skipped at k = 0
+            const int qp = k < nzp - 1 ? q + kTileW : q;
+            double acc = S.D[q] * S.u[q];
+            const double lo = S.U[qm] * S.u[qm];
+            const double hi = S.U[q] * S.u[qp];
+            acc = (k > 0) ? acc + lo : acc;
+            acc = (k < nz - 1) ? acc + hi : acc;
+            acc = acc + S.H0[q] * tile_nb(S, k, l0);
+            acc = acc + S.H1[q] * tile_nb(S, k, l1);
+            acc = acc + S.H2[q] * tile_nb(S, k, l2);
+            r[i] = S.b[q] - acc;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = r[i];
+    }
+}
+
+// One sweep: S.u <- S.u + omega T^{-1}(b - H^ S.u)   (zero: S.u <- omega T^{-1} b).
+// Warp-synchronous; every lane of the warp must call it.
+__device__ __forceinline__ void tile_sweep(const TileSmem& S, int nz, int j, int l0, int l1, int l2, bool zero,
+                                           double omega, bool valid) {
+    const int nzp = (nz + 7) & ~7;
+    tile_residuals(S, nz, j, l0, l1, l2, zero);
+    // pass 2: z_k = (r_k - U_{k-1} z_{k-1}) / den_k, operands of 8 layers per batch
+    bool slow = false;
+    double zprev = 0.0;
+    for (int k0 = 0; k0 < nzp; k0 += 8) {
+        double rr[8], um[8], dd[8], yy[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = k0 + i;
+            const int q = k * kTileW + j;
+            rr[i] = S.z[q];
+            um[i] = S.U[k > 0 ? q - kTileW : q];
+            dd[i] = S.den[q];
+            yy[i] = S.y[q];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = k0 + i;
+            const double num = (k == 0) ? rr[i] : rr[i] - um[i] * zprev;
+            bool sl = false;
+            const double zk = div_fast(num, dd[i], yy[i], sl);
+            slow = slow || (sl && k < nz);
+            rr[i] = zk;
+            zprev = zk;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = rr[i];
+    }
+    if (__any_sync(0xffffffffu, slow && valid)) {  // rare: recompute with '/' (bitwise the same as the oracle)
+#ifdef HMG_TIMING
+        if (j == 0) atomicAdd(&g_tile_slow_count, 1ull);
+#endif
+        __syncwarp();
+        tile_residuals(S, nz, j, l0, l1, l2, zero);
+        zprev = 0.0;
+        for (int k = 0; k < nz; ++k) {
+            const int q = k * kTileW + j;
+            const double num = (k == 0) ? S.z[q] : S.z[q] - S.U[q - kTileW] * zprev;
+            const double zk = num / S.den[q];
+            S.z[q] = zk;
+            zprev = zk;
+        }
+    }
+    __syncwarp();                                   // every lane's residual pass has read S.u
+    // pass 3: back substitution, u' = u + omega delta, into S.u
+    double dl = 0.0;
+    for (int k1 = nzp - 1; k1 >= 0; k1 -= 8) {
+        double zz[8], gg[8], uo[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int q = (k1 - i) * kTileW + j;
+            zz[i] = S.z[q];
+            gg[i] = S.g[q];
+            uo[i] = S.u[q];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int k = k1 - i;
+            dl = (k >= nz - 1) ? zz[i] : zz[i] - gg[i] * dl;
+            uo[i] = zero ? omega * dl : uo[i] + omega * dl;
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) S.u[(k1 - i) * kTileW + j] = uo[i];
+    }
+    __syncwarp();
+}
+
+// The same sweep for a CTA of kTileWarps warps on one tile: the residual pass
+// (independent per layer; issue-bound for a single warp) is split over the
+// warps by 8-layer batches, then warp 0 alone runs the serial z recurrence and
+// back substitution (latency-bound: more warps cannot shorten a column's
+// chain).  Every thread of the CTA must call it; `lane` is the column.
+constexpr int kTileWarps = 4;
+__device__ __forceinline__ void tile_residuals_cta(const TileSmem& S, int nz, int warp, int j, int l0, int l1, int l2,
+                                                   bool zero) {
+    const int nzp = (nz + 7) & ~7;
+    for (int k0 = 8 * warp; k0 < nzp; k0 += 8 * kTileWarps) {
+        double r[8];
+        if (zero) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) r[i] = S.b[(k0 + i) * kTileW + j];
+        } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int k = k0 + i;
+                const int q = k * kTileW + j;
+                const int qm = k > 0 ? q - kTileW : q;          // in-range address; term skipped at k = 0
+                const int qp = k < nzp - 1 ? q + kTileW : q;
+                double acc = S.D[q] * S.u[q];
+                const double lo = S.U[qm] * S.u[qm];
+                const double hi = S.U[q] * S.u[qp];
+                acc = (k > 0) ? acc + lo : acc;
+                acc = (k < nz - 1) ? acc + hi : acc;
+                acc = acc + S.H0[q] * tile_nb(S, k, l0);
+                acc = acc + S.H1[q] * tile_nb(S, k, l1);
+                acc = acc + S.H2[q] * tile_nb(S, k, l2);
+                r[i] = S.b[q] - acc;
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = r[i];
+    }
+}
+
+__device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int warp, int j, int l0, int l1, int l2,
+                                               bool zero, double omega, bool valid) {
+    const int nzp = (nz + 7) & ~7;
+    tile_residuals_cta(S, nz, warp, j, l0, l1, l2, zero);
+    __syncthreads();
+    if (warp == 0) {
+        bool slow = false;
+        double zprev = 0.0;
+        for (int k0 = 0; k0 < nzp; k0 += 8) {
+            double rr[8], um[8], dd[8], yy[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int k = k0 + i;
+                const int q = k * kTileW + j;
+                rr[i] = S.z[q];
+                um[i] = S.U[k > 0 ? q - kTileW : q];
+                dd[i] = S.den[q];
+                yy[i] = S.y[q];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int k = k0 + i;
+                const double num = (k == 0) ? rr[i] : rr[i] - um[i] * zprev;
+                bool sl = false;
+                const double zk = div_fast(num, dd[i], yy[i], sl);
+                slow = slow || (sl && k < nz);
+                rr[i] = zk;
+                zprev = zk;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = rr[i];
+        }
+        if (__any_sync(0xffffffffu, slow && valid)) {  // rare: recompute with '/' (bitwise the same as the oracle)
+#ifdef HMG_TIMING
+            if (j == 0) atomicAdd(&g_tile_slow_count, 1ull);
+#endif
+            __syncwarp();
+            tile_residuals(S, nz, j, l0, l1, l2, zero);
+            zprev = 0.0;
+            for (int k = 0; k < nz; ++k) {
+                const int q = k * kTileW + j;
+                const double num = (k == 0) ? S.z[q] : S.z[q] - S.U[q - kTileW] * zprev;
+                const double zk = num / S.den[q];
+                S.z[q] = zk;
+                zprev = zk;
+            }
+        }
+        __syncwarp();
+        double dl = 0.0;
+        for (int k1 = nzp - 1; k1 >= 0; k1 -= 8) {
+            double zz[8], gg[8], uo[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int q = (k1 - i) * kTileW + j;
+                zz[i] = S.z[q];
+                gg[i] = S.g[q];
+                uo[i] = S.u[q];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int k = k1 - i;
+                dl = (k >= nz - 1) ? zz[i] : zz[i] - gg[i] * dl;
+                uo[i] = zero ? omega * dl : uo[i] + omega * dl;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) S.u[(k1 - i) * kTileW + j] = uo[i];
+        }
+    }
+    __syncthreads();
+}
+
+}  // namespace hmg

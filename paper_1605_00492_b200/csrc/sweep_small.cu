@@ -10,10 +10,9 @@
 //    right-hand side, precomputed pivots (den, y, g) and iterate into shared
 //    memory in one shot; the <= 32 off-tile neighbour cells ("halo") come with
 //    8-byte cp.async, one halo cell per lane;
-//  * the sweep is split into passes with independent work batched into
-//    registers: all residuals (independent per layer), then the z recurrence,
-//    then back substitution -- so shared-memory latency is paid once per
-//    batch and the only serial chain is z_k's (5 dependent fp64 ops);
+//  * the sweep itself (tile_sweep, small_tile.cuh) is split into passes with
+//    independent work batched into registers, so the only serial chain is
+//    z_k's (5 dependent fp64 ops);
 //  * the coarsest level (one tile) runs all n_coarse sweeps in one launch,
 //    iterating in shared memory.
 #include <cuda.h>
@@ -23,6 +22,7 @@
 
 #include "hmg_internal.h"
 #include "sm100_ptx.cuh"
+#include "small_tile.cuh"
 
 namespace hmg {
 
@@ -140,118 +140,9 @@ __global__ void __launch_bounds__(kTS, 1)
         __syncwarp();
     }
     SSTAMP(1);
-    // neighbour value of slot l at layer k (in-tile slot < 32, else halo)
-    auto NB = [&](int k, int l) -> double { return l < kTS ? su[k * kTS + l] : shu[k * kTS + (l - kTS)]; };
-
-    // All passes run over nzp = nz rounded up to 8 layers with no per-layer
-    // branches, so the compiler can interleave the independent work of a
-    // batch; rows >= nz hold the TMA's zero fill and their results are never
-    // used (their 'slow' flags are masked, and nothing they produce reaches a
-    // layer < nz: the back substitution restarts at nz - 1).
-    const int nzp = (nz + 7) & ~7;
-    for (int sweep = 0; sweep < nsweeps; ++sweep) {
-        const bool zero = ZERO && sweep == 0;          // later sweeps of a multi-sweep launch use u
-        // pass 1: residuals r_k (independent across layers)
-        auto residuals = [&]() {
-            if (zero) {
-                for (int k0 = 0; k0 < nzp; k0 += 8) {
-                    double r[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) r[i] = sb[(k0 + i) * kTS + j];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) sz[(k0 + i) * kTS + j] = r[i];
-                }
-                return;
-            }
-            for (int k0 = 0; k0 < nzp; k0 += 8) {
-                double r[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int k = k0 + i;
-                    const int q = k * kTS + j;
-                    const int qm = k > 0 ? q - kTS : q;          // in-range address; term skipped at k = 0
-                    const int qp = k < nzp - 1 ? q + kTS : q;
-                    double acc = D[q] * su[q];
-                    const double lo = U[qm] * su[qm];
-                    const double hi = U[q] * su[qp];
-                    acc = (k > 0) ? acc + lo : acc;
-                    acc = (k < nz - 1) ? acc + hi : acc;
-                    acc = acc + H0[q] * NB(k, l0);
-                    acc = acc + H1[q] * NB(k, l1);
-                    acc = acc + H2[q] * NB(k, l2);
-                    r[i] = sb[q] - acc;
-                }
-#pragma unroll
-                for (int i = 0; i < 8; ++i) sz[(k0 + i) * kTS + j] = r[i];
-            }
-        };
-        residuals();
-        if (sweep < 4) SSTAMP(2 + 4 * sweep);
-        // pass 2: z_k = (r_k - U_{k-1} z_{k-1}) / den_k, operands of 8 layers per batch
-        bool slow = false;
-        double zprev = 0.0;
-        for (int k0 = 0; k0 < nzp; k0 += 8) {
-            double rr[8], um[8], dd[8], yy[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int k = k0 + i;
-                const int q = k * kTS + j;
-                rr[i] = sz[q];
-                um[i] = U[k > 0 ? q - kTS : q];
-                dd[i] = den[q];
-                yy[i] = yv[q];
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int k = k0 + i;
-                const double num = (k == 0) ? rr[i] : rr[i] - um[i] * zprev;
-                bool sl = false;
-                const double zk = div_fast(num, dd[i], yy[i], sl);
-                slow = slow || (sl && k < nz);
-                rr[i] = zk;
-                zprev = zk;
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) sz[(k0 + i) * kTS + j] = rr[i];
-        }
-        if (__any_sync(0xffffffffu, slow && valid)) {  // rare: recompute with '/' (bitwise the same as the oracle)
-            __syncwarp();
-            residuals();
-            zprev = 0.0;
-            for (int k = 0; k < nz; ++k) {
-                const int q = k * kTS + j;
-                const double num = (k == 0) ? sz[q] : sz[q] - U[q - kTS] * zprev;
-                const double zk = num / den[q];
-                sz[q] = zk;
-                zprev = zk;
-            }
-        }
-        if (sweep < 4) SSTAMP(3 + 4 * sweep);
-        __syncwarp();                                   // every lane's residual pass has read su
-        // pass 3: back substitution, u' = u + omega delta, into su
-        double dl = 0.0;
-        for (int k1 = nzp - 1; k1 >= 0; k1 -= 8) {
-            double zz[8], gg[8], uo[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int q = (k1 - i) * kTS + j;
-                zz[i] = sz[q];
-                gg[i] = g[q];
-                uo[i] = su[q];
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int k = k1 - i;
-                dl = (k >= nz - 1) ? zz[i] : zz[i] - gg[i] * dl;
-                uo[i] = zero ? omega * dl : uo[i] + omega * dl;
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) su[(k1 - i) * kTS + j] = uo[i];
-        }
-        if (sweep < 4) SSTAMP(4 + 4 * sweep);
-        __syncwarp();
-        if (sweep < 4) SSTAMP(5 + 4 * sweep);
-    }
+    const TileSmem S{D, U, H0, H1, H2, den, yv, g, sb, su, shu, sz};
+    for (int sweep = 0; sweep < nsweeps; ++sweep)   // later sweeps of a multi-sweep launch use u
+        tile_sweep(S, nz, j, l0, l1, l2, ZERO && sweep == 0, omega, valid);
     if (valid)
         for (int k = 0; k < nz; ++k) uout[(int64_t)k * ld + c] = su[k * kTS + j];
 }

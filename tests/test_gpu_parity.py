@@ -242,11 +242,14 @@ def test_shared_reciprocal_division_is_bitwise_ieee():
 
 
 @pytest.mark.parametrize("tail", ["-1", "0", "1", "3", "4"])
+@pytest.mark.parametrize("grid", ["0", "1"])
 @pytest.mark.parametrize("params", [MGParams(), MGParams(0, 1, 3, 0.8), MGParams(1, 0, 2, 0.9)])
-def test_coarse_tail_settings(monkeypatch, tail, params):
-    """The single-launch coarse tail (levels <= HMG_TAIL_REF) and the per-level
-    kernels give the same bits as the oracle, for any split point."""
+def test_coarse_tail_settings(monkeypatch, tail, grid, params):
+    """The single-launch coarse tail (levels <= HMG_TAIL_REF; one CTA, or a
+    cooperative grid with grid barriers) and the per-level kernels give the
+    same bits as the oracle, for any split point."""
     monkeypatch.setenv("HMG_TAIL_REF", tail)
+    monkeypatch.setenv("HMG_TAIL_GRID", grid)
     cfg = hi.Config("tail", 4, 0, 16, 0.01, 1e-3)
     lam, b = hi.make_inputs(cfg)
     g = Hierarchy(4, 0, 16, 0.01, 1e-3, lam)
@@ -259,6 +262,45 @@ def test_coarse_tail_settings(monkeypatch, tail, params):
     _, it_o, _, _, st_o = o.pcg(b, nu_pre=params.nu_pre, nu_post=params.nu_post, n_coarse=params.n_coarse,
                                 omega=params.omega, maxit=60)
     assert it == it_o and (st == "HMG_OK") == (st_o == 0)
+
+
+@pytest.mark.parametrize("coop", ["-1", "0", "1", "2", "3", "4"])
+@pytest.mark.parametrize("params", [MGParams(), MGParams(0, 1, 3, 0.8), MGParams(1, 0, 2, 0.9),
+                                    MGParams(3, 3, 4, 1.0)])
+def test_cooperative_coarse_levels(monkeypatch, coop, params):
+    """Levels <= HMG_COOP_REF in one cooperative launch (32-column tiles in
+    shared memory, grid barriers between the dependent steps; ref 4 has more
+    tiles than SMs, so CTAs take several): the same bits as the oracle."""
+    monkeypatch.setenv("HMG_COOP_REF", coop)
+    cfg = hi.Config("coop", 5, 0, 24, 0.01, 1e-3)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(5, 0, 24, 0.01, 1e-3, lam)
+    o = oracle.Hierarchy(5, 0, 24, 0.01, 1e-3, lam)
+    z = g.to_host(5, g.vcycle(g.to_device(5, b), params=params))
+    assert np.array_equal(z, o.vcycle(b, params.nu_pre, params.nu_post, params.n_coarse, params.omega))
+    g.close()
+    o.close()
+
+
+@pytest.mark.parametrize("grid", ["0", "1"])
+@pytest.mark.parametrize("fine,coarsest,nz", [(4, 2, 64), (5, 1, 128), (3, 0, 1), (2, 2, 13)])
+def test_coarse_tail_shapes(monkeypatch, grid, fine, coarsest, nz):
+    """Coarse tails with a coarsest level wider than one tile (grid barriers
+    between its sweeps), 128 layers (the cooperative smem-tile kernel does not
+    fit; per-level kernels run), a one-layer mesh, and a layer count that is not
+    a multiple of 8: bitwise equal to the oracle -- for the default cooperative
+    tail and for the global-memory tail kernel (HMG_TAIL_REF)."""
+    if grid == "1":
+        monkeypatch.setenv("HMG_TAIL_REF", str(fine))
+        monkeypatch.setenv("HMG_TAIL_GRID", "1")
+    cfg = hi.Config("coop", fine, coarsest, nz, 0.001, 1e-5)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(fine, coarsest, nz, 0.001, 1e-5, lam)
+    o = oracle.Hierarchy(fine, coarsest, nz, 0.001, 1e-5, lam)
+    z = g.to_host(fine, g.vcycle(g.to_device(fine, b)))
+    assert np.array_equal(z, o.vcycle(b, 2, 2, 20, 0.8))
+    g.close()
+    o.close()
 
 
 @pytest.mark.parametrize("ref,fine", [(2, 2), (4, 4), (3, 5)])
