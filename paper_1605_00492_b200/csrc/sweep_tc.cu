@@ -26,6 +26,8 @@
 #include <cuda.h>
 
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -97,12 +99,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t c0 = (int64_t)blockIdx.x * kTile;
     const SweepSmem lay = sweep_layout(nz, ZERO, PROLONG, FACT, S, G);
     constexpr int kFactRow = ZERO ? 3 : 6;                            // den, y, g rows (FACT)
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
     uint64_t* empty = full + S;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + S);
+    const int ntiles = (int)((L.n + kTile - 1) / kTile);
     double* utile = reinterpret_cast<double*>(smraw + lay.off_u);     // [rows_pad][kTile]
     double* uctile = reinterpret_cast<double*>(smraw + lay.off_uc);   // [rows_pad][kTile/4]
     double* stages = reinterpret_cast<double*>(smraw + lay.off_stage);
@@ -125,18 +127,24 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     if (warp == kConsumerWarps) {
         // ======================= producer warp =======================
+        // persistent: tiles blockIdx.x, blockIdx.x + gridDim.x, ...; the ring
+        // runs on across tile boundaries, so the next tile's first stages
+        // stream while the consumers finish the current tile
+        const uint32_t ublock = (uint32_t)(sizeof(double) * G * kTile);
+        const uint32_t ucblock = (uint32_t)(sizeof(double) * G * (kTile / 4));
+        int s = 0;
+        uint32_t phase = 0;
+        uint32_t it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int64_t c0 = (int64_t)tile * kTile;
         int hcount = 0;
         int32_t h0 = 0, h1 = 0;
         if (!ZERO) {
-            hcount = th.count[blockIdx.x];
-            if (lane < hcount) h0 = th.cells[blockIdx.x * kHaloMax + lane];
-            if (lane + 32 < hcount) h1 = th.cells[blockIdx.x * kHaloMax + lane + 32];
+            hcount = th.count[tile];
+            if (lane < hcount) h0 = th.cells[tile * kHaloMax + lane];
+            if (lane + 32 < hcount) h1 = th.cells[tile * kHaloMax + lane + 32];
         }
-        const uint32_t ublock = (uint32_t)(sizeof(double) * G * kTile);
-        const uint32_t ucblock = (uint32_t)(sizeof(double) * G * (kTile / 4));
         const int x = (int)c0, xc = (int)(c0 / 4);
-        int s = 0;
-        uint32_t phase = 0;
         for (int gi = 0; gi < ngroups; ++gi, (++s == S ? (s = 0, phase ^= 1u) : 0)) {
             ptx::mbar_wait(&empty[s], phase ^ 1u);
             double* st = stages + (size_t)s * lay.stage_doubles;
@@ -182,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 ptx::tma_load_3d(st, &maps.bands, x, gi * G, 0, &full[s]);
                 ptx::tma_load_2d(st + nb * row_block, &maps.b, x, gi * G, &full[s]);
                 if (FACT) ptx::tma_load_3d(st + (nb + 1) * row_block, &maps.fact, x, gi * G, 0, &full[s]);
+                (void)it;   // only the zero-guess form (no u tile) runs persistent, see launch_tc
                 if (u0) {
                     ptx::tma_load_2d(utile, &maps.u, x, 0, &full[s]);
                     if (PROLONG) ptx::tma_load_2d(uctile, &maps.uc, xc, 0, &full[s]);
@@ -193,9 +202,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
             }
         }
+        }
     } else {
         // ======================= consumer warps: one column per thread =======================
         const int j = threadIdx.x;
+        int s = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t c0 = (int64_t)tile * kTile;
         const int64_t c = c0 + j;
         const bool valid = c < L.n;
         uint32_t loc = 0;
@@ -250,8 +264,6 @@ __global__ void __launch_bounds__(kThreads, 2)
             zprev = z;
             gprev = g;
         };
-        int s = 0;
-        uint32_t phase = 0;
 #ifdef HMG_TIMING
         long long wait_acc = 0;
 #endif
@@ -383,6 +395,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             k = k0 - 1;
         }
+        }
     }
     TSTAMP(5);
     ptx::tc_fence_before();
@@ -507,7 +520,17 @@ void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const dou
         ldc = C.ld;
         maps.uc = make_map(uc, C.ld, nz, kTile / 4, G);
     }
-    k_sweep_tc<Z, P, F, G><<<grid, kThreads, smem, s>>>(maps, V, L.halo, b, uin, uc, ldc, L.fden, L.fg, uout, omega,
+    // The zero-guess form (no resident u tile) runs persistent CTAs, two per SM,
+    // each looping over tiles: the producer streams the next tile's first
+    // stages while the consumers finish the current tile's back substitution.
+    // The other forms keep one tile per CTA (their u tile rows would have to
+    // be released before the next tile's could land; measured slower).
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
+    unsigned cap = Z ? (unsigned)((cols <= 256 && grid > (unsigned)sms) ? 2 * sms : sms) : grid;
+    if (const char* e = std::getenv("HMG_TC_PERSIST"))
+        if (std::string(e) == "0") cap = grid;
+    k_sweep_tc<Z, P, F, G><<<grid < cap ? grid : cap, kThreads, smem, s>>>(maps, V, L.halo, b, uin, uc, ldc, L.fden, L.fg, uout, omega,
                                                         L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
 }
 
