@@ -159,6 +159,7 @@ struct Hierarchy {
     // small-level kernel, HMG_L2PF sets the streamed sweep's L2 prefetch
     // distance in ring stages, HMG_TAIL_REF the one-launch coarse tail
     bool use_tc_sweep = true;
+    bool use_st_sweep = true;   // HMG_SWEEP_ST=0: non-zero-guess sweeps by k_sweep_tc instead of k_sweep_st
     bool use_small_sweep = true;
     int l2_prefetch_groups = 3;
 };
@@ -190,6 +191,11 @@ int partials_needed(int64_t n, int nz);
 // sweep_tc.cu: TMA-streamed, TMEM-state sweep (same arithmetic as launch_sweep's kernel)
 bool sweep_tc_supported(const Hierarchy& H, const DevLevel& L);
 void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
+                     double* uout, double omega, cudaStream_t s);
+
+// sweep_st.cu: streamed persistent sweep with a non-zero iterate (same arithmetic)
+bool sweep_st_supported(const Hierarchy& H, const DevLevel& L);
+void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                      double* uout, double omega, cudaStream_t s);
 
 // coarse_tail.cu

@@ -539,6 +539,10 @@ void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const 
         launch_sweep_small(H, L, b, uin, uc, uout, omega, 1, s);
         return;
     }
+    if (uin && !L.fden && H.use_tc_sweep && sweep_st_supported(H, L)) {
+        launch_sweep_st(H, L, b, uin, uc, uout, omega, s);
+        return;
+    }
     if (H.use_tc_sweep && sweep_tc_supported(H, L)) {
         launch_sweep_tc(H, L, b, uin, uc, uout, omega, s);
         return;

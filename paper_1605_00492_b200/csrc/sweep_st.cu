@@ -1,0 +1,405 @@
+// Fused line-Jacobi sweep with a non-zero iterate, fully streamed: persistent
+// CTAs, no shared-memory-resident tile of the iterate.
+//
+// Computes exactly what k_sweep (kernels.cu) and k_sweep_tc (sweep_tc.cu)
+// compute for every column -- r = b - H^ u, delta = T^{-1} r (Thomas,
+// P:741-744), u' = u + omega delta (Eq. 10 read with Eq. 13; readings R5-R7),
+// with the prolongation u <- u + P u_c optionally fused (Alg. 1 M4) -- in the
+// same operation order, so the results are bitwise identical.  What differs
+// from k_sweep_tc is the data movement:
+//
+//  * k_sweep_tc keeps the tile's u rows (64 KB at nz = 64) in shared memory
+//    for the in-tile neighbours and the back substitution's u_old; that halves
+//    its TMA ring and, with the fused prolongation, leaves two stages.  Here
+//    the u rows travel in the ring like every other operand: a forward stage
+//    carries G layers of the bands and b, G + 1 layers of u (layer k + 1 of the
+//    own column is needed at layer k) and the <= 64 off-tile neighbours; after
+//    the tile's forward stages, backward stages bring the u rows again,
+//    8 layers at a time in descending order, for u' = u_old + omega delta.
+//    That re-read is an L2 hit: the forward copies of u use an evict_last
+//    policy and the streamed-once bands an evict_first policy.
+//  * CTAs are persistent (two per SM), each looping over tiles; the producer
+//    warp streams the next tile's forward stages while the consumers finish
+//    the current tile's back substitution.
+//  * The Thomas state (z_k, g_k) of a column stays in tensor memory.
+// HBM traffic per dof: u, b, D, U, H0, H1, H2 read once, u' written once
+// (64 B/dof; + 2 B/dof of u_c with the fused prolongation).
+#include <cuda.h>
+
+#include <cfloat>
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "hmg_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace hmg {
+
+CUtensorMap make_tensor_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes);
+extern thread_local std::string g_launch_error;
+
+namespace {
+
+constexpr int kTile = kSweepTile;          // columns per tile (one consumer thread each)
+constexpr int kConsumerWarps = kTile / 32;
+constexpr int kThreads = kTile + 32;       // + one producer warp
+constexpr int kBack = 8;                   // layers per backward stage
+
+__device__ __forceinline__ bool pivot_ok(double den) { return den > 0.0 && den <= DBL_MAX; }
+
+struct StMaps {
+    CUtensorMap bands;  // 3-D box kTile x G x 5 (D, U, H0, H1, H2)
+    CUtensorMap b;      // box kTile x G
+    CUtensorMap uf;     // box kTile x (G + 1): forward u rows
+    CUtensorMap ub;     // box kTile x 8: backward u rows
+    CUtensorMap ucf;    // box kTile/4 x (G + 1)   (PROLONG)
+    CUtensorMap ucb;    // box kTile/4 x 8         (PROLONG)
+};
+
+// Doubles of one ring stage, and the offsets of its parts (forward layout;
+// a backward stage uses [0, 8 kTile) for u and [8 kTile, 8 kTile + 2 kTile) for u_c).
+struct StLayout {
+    int bands, b, u, uc, hu, huc, fwd, bwd, stage;
+};
+__host__ __device__ constexpr StLayout st_layout(bool prolong, int G) {
+    StLayout L{};
+    L.bands = 0;
+    L.b = 5 * G * kTile;
+    L.u = 6 * G * kTile;
+    L.uc = L.u + (G + 1) * kTile;
+    L.hu = L.uc + (prolong ? (G + 1) * (kTile / 4) : 0);
+    L.huc = L.hu + G * kHaloMax;
+    L.fwd = L.huc + (prolong ? G * kHaloMax : 0);
+    L.bwd = kBack * kTile + (prolong ? kBack * (kTile / 4) : 0);
+    L.stage = L.fwd > L.bwd ? L.fwd : L.bwd;
+    return L;
+}
+
+template <bool PROLONG, int G>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_sweep_st(const __grid_constant__ StMaps maps, LevelView L, TileHalo th, const double* __restrict__ bvec,
+               const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc, double* __restrict__ uout,
+               double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols, int pf_groups) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    constexpr StLayout SL = st_layout(PROLONG, G);
+    const int nz = L.nz;
+    const int64_t ld = L.ld;
+    const int ngroups = (nz + G - 1) / G;
+    const int nchunks = (nz + kBack - 1) / kBack;
+    const int ntiles = (int)((L.n + kTile - 1) / kTile);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+    uint64_t* empty = full + S;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + S);
+    double* stages = reinterpret_cast<double*>(smraw + 1024);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], kConsumerWarps);
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc(tmem_slot, tmem_cols);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tbase = *tmem_slot;
+
+    if (warp == kConsumerWarps) {
+        // ======================= producer warp =======================
+        const uint64_t pol_stream = ptx::policy_evict_first();
+        const uint64_t pol_keep = ptx::policy_evict_last();
+        const uint32_t fwd_bytes = (uint32_t)(sizeof(double) * (6 * G * kTile + (G + 1) * kTile +
+                                                                (PROLONG ? (G + 1) * (kTile / 4) : 0)));
+        const uint32_t bwd_bytes = (uint32_t)(sizeof(double) * (kBack * kTile + (PROLONG ? kBack * (kTile / 4) : 0)));
+        int s = 0;
+        uint32_t phase = 0;
+        auto advance = [&]() {
+            if (++s == S) {
+                s = 0;
+                phase ^= 1u;
+            }
+        };
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int x = tile * kTile, xc = x / 4;
+            const int hcount = th.count[tile];
+            const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
+            const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
+            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+                ptx::mbar_wait(&empty[s], phase ^ 1u);
+                double* st = stages + (size_t)s * SL.stage;
+                for (int kk = 0; kk < G; ++kk) {          // off-tile neighbours of the G layers
+                    const int k = gi * G + kk;
+                    if (k >= nz) break;
+                    const double* src = uin + (int64_t)k * ld;
+                    if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * kHaloMax + lane, src + h0);
+                    if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * kHaloMax + lane + 32, src + h1);
+                    if (PROLONG) {
+                        const double* srcc = uc + (int64_t)k * ldc;
+                        if (lane < hcount) ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane, srcc + (h0 >> 2));
+                        if (lane + 32 < hcount)
+                            ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane + 32, srcc + (h1 >> 2));
+                    }
+                }
+                ptx::cp_async_arrive(&full[s]);
+                __syncwarp();
+                if (lane == 0) {
+                    if (pf_groups > 0 && gi + pf_groups < ngroups) {   // L2 prefetch a few stages ahead
+                        const int gp = gi + pf_groups;
+                        ptx::tma_prefetch_3d(&maps.bands, x, gp * G, 0);
+                        ptx::tma_prefetch_2d(&maps.b, x, gp * G);
+                        ptx::tma_prefetch_2d(&maps.uf, x, gp * G);
+                    }
+                    ptx::mbar_arrive_expect_tx(&full[s], fwd_bytes);
+                    ptx::tma_load_3d_hint(st + SL.bands, &maps.bands, x, gi * G, 0, &full[s], pol_stream);
+                    ptx::tma_load_2d_hint(st + SL.b, &maps.b, x, gi * G, &full[s], pol_stream);
+                    ptx::tma_load_2d_hint(st + SL.u, &maps.uf, x, gi * G, &full[s], pol_keep);
+                    if (PROLONG) ptx::tma_load_2d_hint(st + SL.uc, &maps.ucf, xc, gi * G, &full[s], pol_keep);
+                }
+            }
+            for (int m = nchunks - 1; m >= 0; --m, advance()) {   // u rows again for the back substitution
+                ptx::mbar_wait(&empty[s], phase ^ 1u);
+                double* st = stages + (size_t)s * SL.stage;
+                if (lane == 0) {
+                    ptx::mbar_arrive_expect_tx(&full[s], bwd_bytes);
+                    ptx::tma_load_2d_hint(st, &maps.ub, x, m * kBack, &full[s], pol_stream);
+                    if (PROLONG) ptx::tma_load_2d_hint(st + kBack * kTile, &maps.ucb, xc, m * kBack, &full[s], pol_stream);
+                }
+            }
+        }
+    } else {
+        // ======================= consumer warps: one column per thread =======================
+        const int j = threadIdx.x;
+        const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+        const uint32_t gcol = 2u * (uint32_t)nz;   // g_k at TMEM columns 2nz + 2k, z_k at 2k
+        int s = 0;
+        uint32_t phase = 0;
+        auto advance = [&]() {
+            if (++s == S) {
+                s = 0;
+                phase ^= 1u;
+            }
+        };
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t c = (int64_t)tile * kTile + j;
+            const bool valid = c < L.n;
+            const uint32_t loc = th.loc[valid ? c : L.n - 1];
+            const int l0 = loc & 0xff, l1 = (loc >> 8) & 0xff, l2 = (loc >> 16) & 0xff;
+
+            // Thomas forward elimination, reading R6 order (as k_sweep_tc's `layer`)
+            double um = 0.0, Um = 0.0, gprev = 0.0, zprev = 0.0;
+            bool ok = true, slow = false;
+            auto layer = [&](int k, double Dk, double Uk, double r, bool exact) {
+                const double num = (k == 0) ? r : r - Um * zprev;
+                const bool has_g = k < nz - 1;
+                const double den = (k == 0) ? Dk : Dk - Um * gprev;
+                double z, g = 0.0;
+                if (exact) {
+                    z = num / den;
+                    if (has_g) g = Uk / den;
+                } else {
+                    const double y = div_recip(den);
+                    z = div_fast(num, den, y, slow);
+                    if (has_g) g = div_fast(Uk, den, y, slow);
+                }
+                ok = ok && pivot_ok(den);
+                ptx::tmem_st_f64(tl + 2u * (uint32_t)k, z);
+                if (has_g) ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, g);
+                zprev = z;
+                gprev = g;
+            };
+            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+                ptx::mbar_wait(&full[s], phase);
+                const double* st = stages + (size_t)s * SL.stage;
+                const double* su = st + SL.u;
+                const double* suc = st + SL.uc;
+                const double* hu = st + SL.hu;
+                const double* huc = st + SL.huc;
+                // u value (with the fused prolongation) of local slot l at stage row kk
+                auto UV = [&](int kk, int l) -> double {
+                    double v = su[kk * kTile + l];
+                    if (PROLONG) v = v + suc[kk * (kTile / 4) + (l >> 2)];
+                    return v;
+                };
+                auto NBR = [&](int kk, int l) -> double {
+                    if (l < kTile) return UV(kk, l);
+                    double v = hu[kk * kHaloMax + l - kTile];
+                    if (PROLONG) v = v + huc[kk * kHaloMax + l - kTile];
+                    return v;
+                };
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) {
+                    const int k = gi * G + kk;
+                    if (k >= nz) break;
+                    const double* sr = st + kk * kTile + j;
+                    const double Dk = sr[0];
+                    const double Uk = sr[G * kTile];
+                    const double uk = UV(kk, j);
+                    double up = 0.0;
+                    if (k < nz - 1) up = UV(kk + 1, j);
+                    double acc = Dk * uk;
+                    if (k > 0) acc = acc + Um * um;
+                    if (k < nz - 1) acc = acc + Uk * up;
+                    acc = acc + sr[2 * G * kTile] * NBR(kk, l0);
+                    acc = acc + sr[3 * G * kTile] * NBR(kk, l1);
+                    acc = acc + sr[4 * G * kTile] * NBR(kk, l2);
+                    const double r = sr[5 * G * kTile] - acc;
+                    layer(k, Dk, Uk, r, false);
+                    um = uk;
+                    Um = Uk;
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            }
+            // Rare: a quotient left the fast path's exact range.  The warp redoes
+            // its columns' forward pass from global memory with '/'.
+            if (__any_sync(0xffffffffu, slow && valid)) {
+                const int64_t ce = valid ? c : L.n - 1;
+                const int32_t g0 = L.nbr[ce], g1 = L.nbr[ld + ce], g2 = L.nbr[2 * ld + ce];
+                auto GU = [&](int kk, int64_t cell) -> double {
+                    double v = uin[(int64_t)kk * ld + cell];
+                    if (PROLONG) v = v + uc[(int64_t)kk * ldc + (cell >> 2)];
+                    return v;
+                };
+                um = Um = gprev = zprev = 0.0;
+                double uk = GU(0, ce);
+                for (int k = 0; k < nz; ++k) {
+                    const int64_t i = (int64_t)k * ld + ce;
+                    const double Dk = L.D[i], Uk = L.U[i];
+                    double up = 0.0;
+                    if (k < nz - 1) up = GU(k + 1, ce);
+                    double acc = Dk * uk;
+                    if (k > 0) acc = acc + Um * um;
+                    if (k < nz - 1) acc = acc + Uk * up;
+                    acc = acc + L.H0[i] * GU(k, g0);
+                    acc = acc + L.H1[i] * GU(k, g1);
+                    acc = acc + L.H2[i] * GU(k, g2);
+                    layer(k, Dk, Uk, bvec[i] - acc, true);
+                    um = uk;
+                    uk = up;
+                    Um = Uk;
+                }
+            }
+            if (valid && !ok) atomicMin(bad, ((unsigned long long)ref << 40) | (unsigned long long)c);
+            ptx::tmem_wait_st();
+
+            // back substitution from the top: delta_{nz-1} = z_{nz-1},
+            // delta_k = z_k - g_k delta_{k+1}; u' = u_old + omega delta
+            double dl = 0.0;
+            for (int m = nchunks - 1; m >= 0; --m, advance()) {
+                const int k0 = m * kBack;
+                const int kt = (k0 + kBack - 1 < nz - 1) ? k0 + kBack - 1 : nz - 1;   // top layer of the chunk
+                uint32_t zr[16], gr[16];
+                if (kt - k0 == kBack - 1) {
+                    ptx::tmem_ld_8f64(tl + 2u * (uint32_t)k0, zr);
+                    ptx::tmem_ld_8f64(tl + gcol + 2u * (uint32_t)k0, gr);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kBack; ++i) {      // partial top chunk
+                        if (i > kt - k0) break;
+                        uint32_t z2[2], g2[2];
+                        ptx::tmem_ld_1f64(tl + 2u * (uint32_t)(k0 + i), z2);
+                        ptx::tmem_ld_1f64(tl + gcol + 2u * (uint32_t)(k0 + i), g2);
+                        ptx::tmem_wait_ld();
+                        zr[2 * i] = z2[0];
+                        zr[2 * i + 1] = z2[1];
+                        gr[2 * i] = g2[0];
+                        gr[2 * i + 1] = g2[1];
+                    }
+                }
+                ptx::tmem_wait_ld();
+                ptx::mbar_wait(&full[s], phase);
+                const double* su = stages + (size_t)s * SL.stage;
+                const double* suc = su + kBack * kTile;
+#pragma unroll
+                for (int i = kBack - 1; i >= 0; --i) {
+                    const int k = k0 + i;
+                    if (k > kt) continue;
+                    const double zk = ptx::f64_from(zr[2 * i], zr[2 * i + 1]);
+                    if (k == nz - 1)
+                        dl = zk;
+                    else
+                        dl = zk - ptx::f64_from(gr[2 * i], gr[2 * i + 1]) * dl;
+                    double uo = su[i * kTile + j];
+                    if (PROLONG) uo = uo + suc[i * (kTile / 4) + (j >> 2)];
+                    if (valid) uout[(int64_t)k * ld + c] = uo + omega * dl;
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc(tbase, tmem_cols);
+}
+
+uint32_t st_tmem_cols(int nz) {
+    uint32_t need = 4u * (uint32_t)nz, c = 32;
+    while (c < need) c <<= 1;
+    return c;
+}
+
+template <bool P, int G>
+void launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
+               double* uout, double omega, cudaStream_t s) {
+    const int nz = H.nz;
+    const uint32_t cols = st_tmem_cols(nz);
+    constexpr StLayout SL = st_layout(P, G);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
+    const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
+    const bool two = cols <= 256;                  // two CTAs' Thomas state fit one SM's tensor memory
+    const size_t budget = two ? 110 * 1024 : 220 * 1024;
+    int S = (int)((budget - 1024) / (sizeof(double) * SL.stage));
+    S = S < 2 ? 2 : (S > 32 ? 32 : S);
+    size_t smem = 1024 + sizeof(double) * (size_t)S * SL.stage;
+    const size_t floor_smem = two ? 80 * 1024 : 120 * 1024;   // never a third CTA per SM (TMEM)
+    if (smem < floor_smem) smem = floor_smem;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_sweep_st<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    StMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    const LevelView V = L.view(nz);
+    maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, 5);
+    maps.b = make_tensor_map(b, L.ld, nz, kTile, G, 1);
+    maps.uf = make_tensor_map(uin, L.ld, nz, kTile, G + 1, 1);
+    maps.ub = make_tensor_map(uin, L.ld, nz, kTile, kBack, 1);
+    int64_t ldc = 0;
+    if (P) {
+        const DevLevel& C = H.lev[L.ref - 1];
+        ldc = C.ld;
+        maps.ucf = make_tensor_map(uc, C.ld, nz, kTile / 4, G + 1, 1);
+        maps.ucb = make_tensor_map(uc, C.ld, nz, kTile / 4, kBack, 1);
+    }
+    const unsigned cap = (unsigned)((two ? 2 : 1) * sms);
+    k_sweep_st<P, G><<<ntiles < cap ? ntiles : cap, kThreads, smem, s>>>(
+        maps, V, L.halo, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
+}
+
+}  // namespace
+
+bool sweep_st_supported(const Hierarchy& H, const DevLevel& L) {
+    return H.use_st_sweep && H.nz <= 128 && L.halo.loc != nullptr;
+}
+
+void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
+                     double* uout, double omega, cudaStream_t s) {
+    try {
+        if (uc)
+            launch_st<true, 2>(H, L, b, uin, uc, uout, omega, s);
+        else
+            launch_st<false, 2>(H, L, b, uin, nullptr, uout, omega, s);
+    } catch (const std::exception& e) {
+        g_launch_error = std::string("sweep launch: ") + e.what();
+    }
+    ++H.launches;
+}
+
+}  // namespace hmg
