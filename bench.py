@@ -45,7 +45,8 @@ import hmg_inputs as hi  # noqa: E402
 METRIC = "fp64 Helmholtz dofs/s per V-cycle"
 UNIT = "dof/s"
 # Algorithmic bytes per dof of each kernel class
-BYTES_PER_DOF = {"sweep": 64.0, "sweep_zero": 32.0, "sweep_prolong": 66.0, "apply": 56.0, "resid_restrict": 58.0}
+BYTES_PER_DOF = {"sweep": 64.0, "sweep_zero": 32.0, "sweep_prolong": 66.0, "apply": 56.0, "apply_pupdate": 72.0,
+                 "resid_restrict": 58.0}
 
 
 def parse():
@@ -277,11 +278,12 @@ def run_hmg(args, ws, rank, local):
     peak, peak_note = measured_peak()
     achieved = bytes_sw / (avg_sw * 1e-3) / 1e9
     shares = {}
-    for k in ("sweep", "sweep_zero", "sweep_prolong", "apply", "resid_restrict", "restrict", "prolong", "vector"):
+    for k in ("sweep", "sweep_zero", "sweep_prolong", "apply", "apply_pupdate", "resid_restrict", "restrict", "prolong",
+              "vector", "coarse_tail"):
         n_k, ms_k = h.profile_query(k, -1)
         shares[k] = round(ms_k / (ms * args.steps), 4)
     fine = {}
-    for k in ("sweep", "sweep_zero", "sweep_prolong", "apply", "resid_restrict"):
+    for k in ("sweep", "sweep_zero", "sweep_prolong", "apply", "apply_pupdate", "resid_restrict"):
         n_k, ms_k = h.profile_query(k, r)
         if n_k:
             avg = ms_k / n_k
@@ -337,9 +339,9 @@ def run_hmg(args, ws, rank, local):
             "pcg_solve_ms": ms,
             "vcycle_only": {"value": cfg.ndofs / (ms_vc * 1e-3), "unit": UNIT, "ms": ms_vc},
             "setup_s": setup_s,
-            "roofline": {"kernel": "k_sweep_tc (fused residual + Thomas line sweep, finest level)",
+            "roofline": {"kernel": "k_sweep_st (fused residual + Thomas line sweep, finest level)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic("k_sweep_tc<0, 0, 0, 2>"),
+                         "frac": achieved / peak, "traffic": ncu_traffic("k_sweep_st<0, 2>"),
                          "algorithmic_bytes_per_launch": bytes_sw, "avg_launch_us": avg_sw * 1e3,
                          "launches_timed": n_sw, "peak_source": peak_note},
             "fine_level_kernels": fine,

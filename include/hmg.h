@@ -210,7 +210,8 @@ int64_t hmg_launch_count(const hmg_hierarchy* h);
  * one kernel class on level `ref` (ref < 0: all levels).  Classes:
  * 0 apply, 1 zero-guess sweep, 2 sweep, 3 sweep with fused prolongation,
  * 4 residual+restriction, 5 restriction, 6 prolongation, 7 CG vector kernels,
- * 8 coarse-tail V-cycle (all levels <= the tail level in one launch). */
+ * 8 coarse-tail V-cycle (all levels <= the tail level in one launch),
+ * 9 operator apply with the CG direction update p = z + beta p fused. */
 hmg_status hmg_profile_begin(hmg_hierarchy* h);
 hmg_status hmg_profile_end(hmg_hierarchy* h);
 hmg_status hmg_profile_query(const hmg_hierarchy* h, int kernel_class, int ref, int64_t* count, double* total_ms);

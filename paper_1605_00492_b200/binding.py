@@ -286,7 +286,7 @@ class Hierarchy:
 
     # -- diagnostics -----------------------------------------------------------
     KERNEL_CLASSES = {"apply": 0, "sweep_zero": 1, "sweep": 2, "sweep_prolong": 3, "resid_restrict": 4,
-                      "restrict": 5, "prolong": 6, "vector": 7, "coarse_tail": 8}
+                      "restrict": 5, "prolong": 6, "vector": 7, "coarse_tail": 8, "apply_pupdate": 9}
 
     def profile_begin(self):
         _check(load_library().hmg_profile_begin(self._h))

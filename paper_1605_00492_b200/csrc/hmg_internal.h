@@ -123,7 +123,7 @@ struct PcgScalars {
 // (kernel class, level).  Off by default; the benchmark turns it on for the
 // timed region to report the dominant kernel's live duration.
 enum KernelClass { kKApply = 0, kKSweepZero, kKSweep, kKSweepProlong, kKResidRestrict, kKRestrict, kKProlong,
-                   kKVector, kKCoarseTail, kKNumClasses };
+                   kKVector, kKCoarseTail, kKApplyP, kKNumClasses };
 struct Profiler {
     bool on = false;
     std::vector<cudaEvent_t> pool;   // pairs

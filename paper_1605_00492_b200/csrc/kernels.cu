@@ -567,7 +567,7 @@ void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const 
 
 void launch_apply_pupdate_dot(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
                               double* q, cudaStream_t s) {
-    ProfScope ps(H, kKApply, L.ref, s);
+    ProfScope ps(H, kKApplyP, L.ref, s);
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
     k_apply_t<true, true><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), pold, q, H.partials, z, pnew, H.scal);
     ++H.launches;
