@@ -354,9 +354,13 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     const int64_t nfine = 20 * (int64_t(1) << (2 * fine_ref));
     const bool dist_fine = dist && gather_ref < fine_ref;
     const int64_t nlam = dist_fine ? nfine / nranks : nfine;
-    for (int64_t i = 0; i < nlam * nlayers; ++i)
+    double lam_min = HUGE_VAL, lam_max = 0.0;
+    for (int64_t i = 0; i < nlam * nlayers; ++i) {
         if (!(lam_host[i] > 0) || !std::isfinite(lam_host[i]))
             return fail(HMG_ERR_INVALID_ARG, "lam_host: entry " + std::to_string(i) + " is not finite and > 0");
+        lam_min = std::min(lam_min, lam_host[i]);
+        lam_max = std::max(lam_max, lam_host[i]);
+    }
     int ndev = 0;
     HMG_CUDA(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(HMG_ERR_INVALID_ARG, "device: no CUDA device " + std::to_string(device));
@@ -378,6 +382,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_SWEEP")) H->use_tc_sweep = std::string(e) != "simple";
     if (const char* e = std::getenv("HMG_SMALL")) H->use_small_sweep = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_SWEEP_ST")) H->use_st_sweep = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_OPERATOR")) H->matrix_free = std::string(e) == "free";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at
@@ -515,6 +520,30 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
         }
         BCUDA(cudaMemcpy(L.nbr, nbr.data(), sizeof(int32_t) * 3 * L.ld, cudaMemcpyHostToDevice));
         BCUDA(cudaMemcpy(L.geom, geom.data(), sizeof(double) * 7 * L.ld, cudaMemcpyHostToDevice));
+        if (!dist) {
+            // Matrix-free couplings without the per-quotient fast-path test
+            // (mf_ops.cuh): prove every numerator, divisor and quotient of this
+            // level within [2^-900, 2^900].  Coarse coefficients are means of
+            // fine ones, so the fine range [lam_min, lam_max] bounds every level.
+            double amin = HUGE_VAL, amax = 0, lmn = HUGE_VAL, lmx = 0, cmn = HUGE_VAL, cmx = 0;
+            for (int64_t g = 0; g < HL.n; ++g) {
+                amin = std::min(amin, HL.area[g]);
+                amax = std::max(amax, HL.area[g]);
+                for (int j = 0; j < 3; ++j) {
+                    lmn = std::min(lmn, HL.len[g * 3 + j]);
+                    lmx = std::max(lmx, HL.len[g * 3 + j]);
+                    cmn = std::min(cmn, HL.cd[g * 3 + j]);
+                    cmx = std::max(cmx, HL.cd[g * 3 + j]);
+                }
+            }
+            auto in = [](double v) { return v >= 0x1p-900 && v <= 0x1p900; };
+            const double nv0 = w2 * amin * lam_min, nv1 = w2 * amax * lam_max;
+            const double dz = H->dz;
+            const double nh0 = w2 * lmn * dz * lam_min, nh1 = w2 * lmx * dz * lam_max;
+            L.mf_safe = w2 == 0.0 ||
+                        (in(dz) && in(cmn) && in(cmx) && in(nv0) && in(nv1) && in(nh0) && in(nh1) && in(nv0 / dz) &&
+                         in(nv1 / dz) && in(nh0 / cmx) && in(nh1 / cmn));
+        }
         if (dist) {      // coefficients: owned + halo cells from the host copy
             std::vector<double> lam((size_t)nlayers * L.ld, 1.0);
             const std::vector<double>& G = lam_levels[r];

@@ -89,6 +89,7 @@ struct DevLevel {
     double* fden = nullptr;
     double* fy = nullptr;
     double* fg = nullptr;
+    bool mf_safe = false;       // matrix-free quotients provably in the fast path's exact range (build_impl)
     DistLevel dist;
     LevelView view(int nz) const {
         const int64_t s = (int64_t)nz * ld;
@@ -159,7 +160,8 @@ struct Hierarchy {
     // small-level kernel, HMG_L2PF sets the streamed sweep's L2 prefetch
     // distance in ring stages, HMG_TAIL_REF the one-launch coarse tail
     bool use_tc_sweep = true;
-    bool use_st_sweep = true;   // HMG_SWEEP_ST=0: non-zero-guess sweeps by k_sweep_tc instead of k_sweep_st
+    bool use_st_sweep = true;
+    bool matrix_free = false;   // operator applies recompute the couplings from lam + geometry (NEXT-2)   // HMG_SWEEP_ST=0: non-zero-guess sweeps by k_sweep_tc instead of k_sweep_st
     bool use_small_sweep = true;
     int l2_prefetch_groups = 3;
 };

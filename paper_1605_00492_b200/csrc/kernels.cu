@@ -7,8 +7,11 @@
 // DESIGN.md (readings R4-R10) with no FMA contraction (-fmad=false), so the
 // V-cycle path is bitwise equal to the oracle.
 #include <cfloat>
+#include <cstdlib>
 
 #include "hmg_internal.h"
+#include "sm100_ptx.cuh"
+#include "mf_ops.cuh"
 
 namespace hmg {
 namespace {
@@ -133,6 +136,97 @@ __global__ void __launch_bounds__(kApplyBlock) k_apply_t(LevelView L, const doub
             xk = xp;
             Um = Uk;
         }
+    }
+    if (DOT) {
+        const double s = block_sum(dot, red);
+        if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Matrix-free operator apply (the paper's matrix-free
+// store): the couplings of reading R4 are recomputed from the
+// coefficient lam and the column geometry instead of streamed from the band
+// store -- lam, x in and y out (24 B/dof instead of 56).  Every coupling is
+// formed with k_assemble's operations in k_assemble's order, so it is
+// bitwise the stored band; the quotients by dz and by the centroid distances
+// use one reciprocal per column (div_fast, bitwise '/', exact redo otherwise).
+// ---------------------------------------------------------------------------
+// One column's layers [k0, k1) of y = H^ x with the couplings recomputed.
+// Returns the column's contribution to x.y (DOT).
+template <bool DOT, bool PUPD, bool EXACT>
+__device__ __forceinline__ double apply_mf_column(const LevelView& L, const ColumnGeom& G, const double* __restrict__ lam,
+                                                  double dz, double ydz, int64_t c, int k0, int k1,
+                                                  const double* __restrict__ xin, double* __restrict__ y,
+                                                  const double* __restrict__ zv, double* __restrict__ pnew, double beta,
+                                                  bool& slow) {
+    const int nz = L.nz;
+    const int64_t ld = L.ld;
+    const int32_t n0 = L.nbr[c], n1 = L.nbr[ld + c], n2 = L.nbr[2 * ld + c];
+    auto X = [&](int64_t i) -> double {
+        if (PUPD) return zv[i] + beta * xin[i];
+        return xin[i];
+    };
+    // vertical coupling between layers k and k + 1 (k_assemble's vup / vdn)
+    auto vcoup = [&](double la, double lb) { return mf_vcoup<EXACT>(G, la, lb, dz, ydz, slow); };
+    double dot = 0.0;
+    double lk = lam[(int64_t)k0 * ld + c];
+    double vdn = 0.0, xm = 0.0;
+    if (k0 > 0) {
+        vdn = vcoup(lam[(int64_t)(k0 - 1) * ld + c], lk);
+        xm = X((int64_t)(k0 - 1) * ld + c);
+    }
+    double xk = X((int64_t)k0 * ld + c);
+#pragma unroll 2
+    for (int k = k0; k < k1; ++k) {
+        const int64_t row = k * ld, i = row + c;
+        double xp = 0.0, lp = 0.0, vup = 0.0;
+        if (k + 1 < nz) {
+            xp = X(i + ld);
+            lp = lam[i + ld];
+            vup = vcoup(lk, lp);
+        }
+        const double hc0 = mf_hcoup<EXACT>(G, 0, lk, lam[row + n0], slow);
+        const double hc1 = mf_hcoup<EXACT>(G, 1, lk, lam[row + n1], slow);
+        const double hc2 = mf_hcoup<EXACT>(G, 2, lk, lam[row + n2], slow);
+        const double d = mf_diag(G, k, nz, vdn, vup, hc0, hc1, hc2);
+        double acc = d * xk;
+        if (k > 0) acc = acc + (-vdn) * xm;
+        if (k < nz - 1) acc = acc + (-vup) * xp;
+        acc = acc + (-hc0) * X(row + n0);
+        acc = acc + (-hc1) * X(row + n1);
+        acc = acc + (-hc2) * X(row + n2);
+        y[i] = acc;
+        if (PUPD) pnew[i] = xk;
+        if (DOT) dot = dot + xk * acc;
+        xm = xk;
+        xk = xp;
+        vdn = vup;
+        lk = lp;
+    }
+    return dot;
+}
+
+template <bool DOT, bool PUPD>
+__global__ void __launch_bounds__(kApplyBlock) k_apply_mf(LevelView L, const double* __restrict__ geom,
+                                                          const double* __restrict__ lam, double w2, double dz,
+                                                          const double* __restrict__ xin, double* __restrict__ y,
+                                                          double* __restrict__ partial, const double* __restrict__ zv,
+                                                          double* __restrict__ pnew, const PcgScalars* __restrict__ sc) {
+    __shared__ double red[kApplyBlock / 32];
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int nz = L.nz;
+    const int kc = (nz + gridDim.y - 1) / gridDim.y;
+    const int k0 = blockIdx.y * kc, k1 = min(nz, k0 + kc);
+    double dot = 0.0;
+    const double beta = PUPD ? sc->beta : 0.0;
+    if (c < L.n && k0 < k1) {
+        const ColumnGeom G = column_geom(geom, L.ld, c, w2, dz);
+        const double ydz = div_recip(dz);
+        bool slow = false;
+        dot = apply_mf_column<DOT, PUPD, false>(L, G, lam, dz, ydz, c, k0, k1, xin, y, zv, pnew, beta, slow);
+        if (slow)   // rare: a quotient left the fast path's exact range; redo the column with '/'
+            dot = apply_mf_column<DOT, PUPD, true>(L, G, lam, dz, ydz, c, k0, k1, xin, y, zv, pnew, beta, slow);
     }
     if (DOT) {
         const double s = block_sum(dot, red);
@@ -440,6 +534,11 @@ inline unsigned blocks(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 // fill the GPU; on small (coarse) levels split the layers so that the
 // sequential per-thread loop is short (these levels are latency-bound).
 unsigned vchunks(int64_t n, int nz) {
+    static const int forced = [] {
+        const char* e = std::getenv("HMG_VCHUNK_LAYERS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (forced > 0) return (unsigned)((nz + forced - 1) / forced);
     const int64_t target = 148LL * 1024;
     int64_t c = (target + n - 1) / n;
     if (c > nz / 4) c = nz / 4;
@@ -520,14 +619,22 @@ void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
 void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
     ProfScope ps(H, kKApply, L.ref, s);
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
-    k_apply_t<false, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, nullptr, nullptr, nullptr, nullptr);
+    if (H.matrix_free)
+        k_apply_mf<false, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), L.geom, L.lam, H.w2, H.dz, x, y, nullptr,
+                                                           nullptr, nullptr, nullptr);
+    else
+        k_apply_t<false, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, nullptr, nullptr, nullptr, nullptr);
     ++H.launches;
 }
 
 void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
     ProfScope ps(H, kKApply, L.ref, s);
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
-    k_apply_t<true, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, H.partials, nullptr, nullptr, nullptr);
+    if (H.matrix_free)
+        k_apply_mf<true, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), L.geom, L.lam, H.w2, H.dz, x, y, H.partials,
+                                                          nullptr, nullptr, nullptr);
+    else
+        k_apply_t<true, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), x, y, H.partials, nullptr, nullptr, nullptr);
     ++H.launches;
     finalize_parts(H, (int)(g.x * g.y), kFinPQ, s);
 }
@@ -539,7 +646,7 @@ void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const 
         launch_sweep_small(H, L, b, uin, uc, uout, omega, 1, s);
         return;
     }
-    if (uin && !L.fden && H.use_tc_sweep && sweep_st_supported(H, L)) {
+    if ((uin || H.matrix_free) && !L.fden && H.use_tc_sweep && sweep_st_supported(H, L)) {
         launch_sweep_st(H, L, b, uin, uc, uout, omega, s);
         return;
     }
@@ -569,7 +676,11 @@ void launch_apply_pupdate_dot(const Hierarchy& H, const DevLevel& L, const doubl
                               double* q, cudaStream_t s) {
     ProfScope ps(H, kKApplyP, L.ref, s);
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
-    k_apply_t<true, true><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), pold, q, H.partials, z, pnew, H.scal);
+    if (H.matrix_free)
+        k_apply_mf<true, true><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), L.geom, L.lam, H.w2, H.dz, pold, q, H.partials,
+                                                         z, pnew, H.scal);
+    else
+        k_apply_t<true, true><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), pold, q, H.partials, z, pnew, H.scal);
     ++H.launches;
     finalize_parts(H, (int)(g.x * g.y), kFinPQ, s);
 }

@@ -34,6 +34,7 @@
 
 #include "hmg_internal.h"
 #include "sm100_ptx.cuh"
+#include "mf_ops.cuh"
 
 namespace hmg {
 
@@ -45,12 +46,15 @@ namespace {
 constexpr int kTile = kSweepTile;          // columns per tile (one consumer thread each)
 constexpr int kConsumerWarps = kTile / 32;
 constexpr int kThreads = kTile + 32;       // + one producer warp
+constexpr int kMfWarps = kTile / 32;       // matrix-free: warps forming the couplings of each stage
+constexpr int kThreadsMf = kThreads + 32 * kMfWarps;
 constexpr int kBack = 8;                   // layers per backward stage
 
 __device__ __forceinline__ bool pivot_ok(double den) { return den > 0.0 && den <= DBL_MAX; }
 
 struct StMaps {
-    CUtensorMap bands;  // 3-D box kTile x G x 5 (D, U, H0, H1, H2)
+    CUtensorMap bands;  // 3-D box kTile x G x 5 (D, U, H0, H1, H2)     (stored bands)
+    CUtensorMap lam;    // box kTile x (G + 1): coefficient rows          (matrix-free)
     CUtensorMap b;      // box kTile x G
     CUtensorMap uf;     // box kTile x (G + 1): forward u rows
     CUtensorMap ub;     // box kTile x 8: backward u rows
@@ -58,47 +62,62 @@ struct StMaps {
     CUtensorMap ucb;    // box kTile/4 x 8         (PROLONG)
 };
 
-// Doubles of one ring stage, and the offsets of its parts (forward layout;
-// a backward stage uses [0, 8 kTile) for u and [8 kTile, 8 kTile + 2 kTile) for u_c).
+// Doubles of one ring stage and the offsets of its parts.  Forward stage:
+// operator rows (5 G band rows, or G + 1 lam rows), G rows of b, G + 1 rows
+// of u (+ u_c), off-tile neighbour values (u, u_c, lam) of the G layers.
+// Backward stage: [0, 8 kTile) u rows, then 8 kTile/4 u_c rows.
 struct StLayout {
-    int bands, b, u, uc, hu, huc, fwd, bwd, stage;
+    int op, band, b, u, uc, hu, huc, hlam, fwd, bwd, stage;
 };
-__host__ __device__ constexpr StLayout st_layout(bool prolong, int G) {
+__host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool mf, int G) {
     StLayout L{};
-    L.bands = 0;
-    L.b = 5 * G * kTile;
-    L.u = 6 * G * kTile;
-    L.uc = L.u + (G + 1) * kTile;
+    L.op = 0;                                        // band rows (stored), or lam rows (matrix-free)
+    L.band = mf ? (G + 1) * kTile : 0;               // band rows as the consumers read them
+    L.b = L.band + 5 * G * kTile;
+    L.u = L.b + G * kTile;
+    L.uc = L.u + (zero ? 0 : (G + 1) * kTile);
     L.hu = L.uc + (prolong ? (G + 1) * (kTile / 4) : 0);
-    L.huc = L.hu + G * kHaloMax;
-    L.fwd = L.huc + (prolong ? G * kHaloMax : 0);
-    L.bwd = kBack * kTile + (prolong ? kBack * (kTile / 4) : 0);
+    L.huc = L.hu + (zero ? 0 : G * kHaloMax);
+    L.hlam = L.huc + (prolong ? G * kHaloMax : 0);
+    L.fwd = L.hlam + (mf ? G * kHaloMax : 0);
+    L.bwd = zero ? 0 : kBack * kTile + (prolong ? kBack * (kTile / 4) : 0);
     L.stage = L.fwd > L.bwd ? L.fwd : L.bwd;
     return L;
 }
 
-template <bool PROLONG, int G>
-__global__ void __launch_bounds__(kThreads, 2)
-    k_sweep_st(const __grid_constant__ StMaps maps, LevelView L, TileHalo th, const double* __restrict__ bvec,
+// Operator of one launch: the level's stored bands (view) or, matrix-free,
+// its coefficient and geometry.
+struct StOp {
+    const double* lam;
+    const double* geom;
+    double w2, dz;
+};
+
+template <bool ZERO, bool PROLONG, bool MF, int G, bool CHK>
+__global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
+    k_sweep_st(const __grid_constant__ StMaps maps, LevelView L, StOp op, TileHalo th, const double* __restrict__ bvec,
                const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc, double* __restrict__ uout,
                double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols, int pf_groups) {
     extern __shared__ __align__(1024) unsigned char smraw[];
-    constexpr StLayout SL = st_layout(PROLONG, G);
+    constexpr StLayout SL = st_layout(ZERO, PROLONG, MF, G);
+    constexpr bool HALO = !ZERO || MF;       // off-tile neighbour values needed
     const int nz = L.nz;
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
-    const int nchunks = (nz + kBack - 1) / kBack;
+    const int nchunks = ZERO ? 0 : (nz + kBack - 1) / kBack;
     const int ntiles = (int)((L.n + kTile - 1) / kTile);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
     uint64_t* empty = full + S;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + S);
+    uint64_t* mid = empty + S;                        // matrix-free: the stage's band rows are formed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mid + S);
     double* stages = reinterpret_cast<double*>(smraw + 1024);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
             ptx::mbar_init(&empty[s], kConsumerWarps);
+            ptx::mbar_init(&mid[s], kMfWarps);
         }
         ptx::fence_mbar_init();
     }
@@ -108,12 +127,83 @@ __global__ void __launch_bounds__(kThreads, 2)
     ptx::tc_fence_after();
     const uint32_t tbase = *tmem_slot;
 
-    if (warp == kConsumerWarps) {
+    if (MF && warp > kConsumerWarps) {
+        // ============ matrix-free warps: the couplings of each forward stage ============
+        // Thread = column.  Writes D, U, H0, H1, H2 of the stage's G layers into
+        // its band rows (k_assemble's values, bitwise) for the Thomas warps; passes
+        // backward stages through.  A quotient outside the fast path's exact range
+        // is recomputed with '/' on the spot (rare).
+        const int j = threadIdx.x - 32 * (kConsumerWarps + 1);
+        const int mlane = j & 31;
+        const double ydz = div_recip(op.dz);
+        int s = 0;
+        uint32_t phase = 0;
+        auto advance = [&]() {
+            if (++s == S) {
+                s = 0;
+                phase ^= 1u;
+            }
+        };
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t c = (int64_t)tile * kTile + j;
+            const int64_t cv = c < L.n ? c : L.n - 1;
+            const uint32_t loc = th.loc[cv];
+            const int ls[3] = {(int)(loc & 0xff), (int)((loc >> 8) & 0xff), (int)((loc >> 16) & 0xff)};
+            const ColumnGeom cg = column_geom(op.geom, ld, cv, op.w2, op.dz);
+            double vdn = 0.0;
+            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+                ptx::mbar_wait(&full[s], phase);
+                double* st = stages + (size_t)s * SL.stage;
+                const double* sl = st + SL.op;
+                const double* hl = st + SL.hlam;
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) {
+                    const int k = gi * G + kk;
+                    if (k >= nz) break;
+                    const double lk = sl[kk * kTile + j];
+                    bool slow = false;
+                    double lp = 0.0, vup = 0.0;
+                    if (k < nz - 1) {
+                        lp = sl[(kk + 1) * kTile + j];
+                        vup = mf_vcoup<false, CHK>(cg, lk, lp, op.dz, ydz, slow);
+                    }
+                    double hc[3], ln[3];
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        ln[q] = ls[q] < kTile ? sl[kk * kTile + ls[q]] : hl[kk * kHaloMax + ls[q] - kTile];
+                        hc[q] = mf_hcoup<false, CHK>(cg, q, lk, ln[q], slow);
+                    }
+                    if (CHK && slow) {                     // rare: exact quotients
+                        bool dummy = false;
+                        if (k < nz - 1) vup = mf_vcoup<true>(cg, lk, lp, op.dz, ydz, dummy);
+#pragma unroll
+                        for (int q = 0; q < 3; ++q) hc[q] = mf_hcoup<true>(cg, q, lk, ln[q], dummy);
+                    }
+                    double* br = st + SL.band + kk * kTile + j;
+                    br[0] = mf_diag(cg, k, nz, vdn, vup, hc[0], hc[1], hc[2]);
+                    br[G * kTile] = (k < nz - 1) ? -vup : 0.0;
+                    br[2 * G * kTile] = -hc[0];
+                    br[3 * G * kTile] = -hc[1];
+                    br[4 * G * kTile] = -hc[2];
+                    vdn = vup;
+                }
+                __syncwarp();
+                if (mlane == 0) ptx::mbar_arrive(&mid[s]);
+            }
+            for (int m = nchunks - 1; m >= 0; --m, advance()) {   // backward stages: pass through
+                ptx::mbar_wait(&full[s], phase);
+                __syncwarp();
+                if (mlane == 0) ptx::mbar_arrive(&mid[s]);
+            }
+        }
+    } else if (warp == kConsumerWarps) {
         // ======================= producer warp =======================
         const uint64_t pol_stream = ptx::policy_evict_first();
         const uint64_t pol_keep = ptx::policy_evict_last();
-        const uint32_t fwd_bytes = (uint32_t)(sizeof(double) * (6 * G * kTile + (G + 1) * kTile +
-                                                                (PROLONG ? (G + 1) * (kTile / 4) : 0)));
+        constexpr int op_rows = MF ? (G + 1) * kTile : 5 * G * kTile;
+        const uint32_t fwd_bytes =
+            (uint32_t)(sizeof(double) * (op_rows + G * kTile + (ZERO ? 0 : (G + 1) * kTile) +
+                                         (PROLONG ? (G + 1) * (kTile / 4) : 0)));
         const uint32_t bwd_bytes = (uint32_t)(sizeof(double) * (kBack * kTile + (PROLONG ? kBack * (kTile / 4) : 0)));
         int s = 0;
         uint32_t phase = 0;
@@ -125,38 +215,53 @@ __global__ void __launch_bounds__(kThreads, 2)
         };
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int x = tile * kTile, xc = x / 4;
-            const int hcount = th.count[tile];
+            const int hcount = HALO ? th.count[tile] : 0;
             const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
             const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
                 ptx::mbar_wait(&empty[s], phase ^ 1u);
                 double* st = stages + (size_t)s * SL.stage;
-                for (int kk = 0; kk < G; ++kk) {          // off-tile neighbours of the G layers
-                    const int k = gi * G + kk;
-                    if (k >= nz) break;
-                    const double* src = uin + (int64_t)k * ld;
-                    if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * kHaloMax + lane, src + h0);
-                    if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * kHaloMax + lane + 32, src + h1);
-                    if (PROLONG) {
-                        const double* srcc = uc + (int64_t)k * ldc;
-                        if (lane < hcount) ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane, srcc + (h0 >> 2));
-                        if (lane + 32 < hcount)
-                            ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane + 32, srcc + (h1 >> 2));
+                if (HALO) {
+                    for (int kk = 0; kk < G; ++kk) {          // off-tile neighbours of the G layers
+                        const int k = gi * G + kk;
+                        if (k >= nz) break;
+                        if (!ZERO) {
+                            const double* src = uin + (int64_t)k * ld;
+                            if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * kHaloMax + lane, src + h0);
+                            if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * kHaloMax + lane + 32, src + h1);
+                        }
+                        if (PROLONG) {
+                            const double* srcc = uc + (int64_t)k * ldc;
+                            if (lane < hcount) ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane, srcc + (h0 >> 2));
+                            if (lane + 32 < hcount)
+                                ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane + 32, srcc + (h1 >> 2));
+                        }
+                        if (MF) {
+                            const double* srcl = op.lam + (int64_t)k * ld;
+                            if (lane < hcount) ptx::cp_async8(st + SL.hlam + kk * kHaloMax + lane, srcl + h0);
+                            if (lane + 32 < hcount) ptx::cp_async8(st + SL.hlam + kk * kHaloMax + lane + 32, srcl + h1);
+                        }
                     }
+                    ptx::cp_async_arrive(&full[s]);
                 }
-                ptx::cp_async_arrive(&full[s]);
                 __syncwarp();
                 if (lane == 0) {
                     if (pf_groups > 0 && gi + pf_groups < ngroups) {   // L2 prefetch a few stages ahead
                         const int gp = gi + pf_groups;
-                        ptx::tma_prefetch_3d(&maps.bands, x, gp * G, 0);
+                        if (MF)
+                            ptx::tma_prefetch_2d(&maps.lam, x, gp * G);
+                        else
+                            ptx::tma_prefetch_3d(&maps.bands, x, gp * G, 0);
                         ptx::tma_prefetch_2d(&maps.b, x, gp * G);
-                        ptx::tma_prefetch_2d(&maps.uf, x, gp * G);
+                        if (!ZERO) ptx::tma_prefetch_2d(&maps.uf, x, gp * G);
                     }
                     ptx::mbar_arrive_expect_tx(&full[s], fwd_bytes);
-                    ptx::tma_load_3d_hint(st + SL.bands, &maps.bands, x, gi * G, 0, &full[s], pol_stream);
+                    if (MF)
+                        ptx::tma_load_2d_hint(st + SL.op, &maps.lam, x, gi * G, &full[s], pol_stream);
+                    else
+                        ptx::tma_load_3d_hint(st + SL.op, &maps.bands, x, gi * G, 0, &full[s], pol_stream);
                     ptx::tma_load_2d_hint(st + SL.b, &maps.b, x, gi * G, &full[s], pol_stream);
-                    ptx::tma_load_2d_hint(st + SL.u, &maps.uf, x, gi * G, &full[s], pol_keep);
+                    if (!ZERO) ptx::tma_load_2d_hint(st + SL.u, &maps.uf, x, gi * G, &full[s], pol_keep);
                     if (PROLONG) ptx::tma_load_2d_hint(st + SL.uc, &maps.ucf, xc, gi * G, &full[s], pol_keep);
                 }
             }
@@ -175,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int j = threadIdx.x;
         const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
         const uint32_t gcol = 2u * (uint32_t)nz;   // g_k at TMEM columns 2nz + 2k, z_k at 2k
+        const double ydz = MF ? div_recip(op.dz) : 0.0;   // exact redo only
         int s = 0;
         uint32_t phase = 0;
         auto advance = [&]() {
@@ -186,11 +292,18 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int64_t c = (int64_t)tile * kTile + j;
             const bool valid = c < L.n;
-            const uint32_t loc = th.loc[valid ? c : L.n - 1];
-            const int l0 = loc & 0xff, l1 = (loc >> 8) & 0xff, l2 = (loc >> 16) & 0xff;
+            const int64_t cv = valid ? c : L.n - 1;
+            int l0 = 0, l1 = 0, l2 = 0;
+            if (HALO) {
+                const uint32_t loc = th.loc[cv];
+                l0 = loc & 0xff;
+                l1 = (loc >> 8) & 0xff;
+                l2 = (loc >> 16) & 0xff;
+            }
+            ColumnGeom cg{};
 
             // Thomas forward elimination, reading R6 order (as k_sweep_tc's `layer`)
-            double um = 0.0, Um = 0.0, gprev = 0.0, zprev = 0.0;
+            double um = 0.0, Um = 0.0, gprev = 0.0, zprev = 0.0, vdn = 0.0;
             bool ok = true, slow = false;
             auto layer = [&](int k, double Dk, double Uk, double r, bool exact) {
                 const double num = (k == 0) ? r : r - Um * zprev;
@@ -212,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 gprev = g;
             };
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
-                ptx::mbar_wait(&full[s], phase);
+                ptx::mbar_wait(MF ? &mid[s] : &full[s], phase);
                 const double* st = stages + (size_t)s * SL.stage;
                 const double* su = st + SL.u;
                 const double* suc = st + SL.uc;
@@ -230,25 +343,37 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (PROLONG) v = v + huc[kk * kHaloMax + l - kTile];
                     return v;
                 };
-#pragma unroll
+                // u value (with the fused prolongation) of local slot l at stage row kk#pragma unroll
                 for (int kk = 0; kk < G; ++kk) {
                     const int k = gi * G + kk;
                     if (k >= nz) break;
-                    const double* sr = st + kk * kTile + j;
-                    const double Dk = sr[0];
-                    const double Uk = sr[G * kTile];
-                    const double uk = UV(kk, j);
-                    double up = 0.0;
-                    if (k < nz - 1) up = UV(kk + 1, j);
-                    double acc = Dk * uk;
-                    if (k > 0) acc = acc + Um * um;
-                    if (k < nz - 1) acc = acc + Uk * up;
-                    acc = acc + sr[2 * G * kTile] * NBR(kk, l0);
-                    acc = acc + sr[3 * G * kTile] * NBR(kk, l1);
-                    acc = acc + sr[4 * G * kTile] * NBR(kk, l2);
-                    const double r = sr[5 * G * kTile] - acc;
+                    double Dk, Uk, H0, H1, H2;
+                    {
+                        const double* sr = st + SL.band + kk * kTile + j;
+                        Dk = sr[0];
+                        Uk = sr[G * kTile];
+                        H0 = sr[2 * G * kTile];
+                        H1 = sr[3 * G * kTile];
+                        H2 = sr[4 * G * kTile];
+                    }
+                    const double bk = st[SL.b + kk * kTile + j];
+                    double r;
+                    if (ZERO) {
+                        r = bk;
+                    } else {
+                        const double uk = UV(kk, j);
+                        double up = 0.0;
+                        if (k < nz - 1) up = UV(kk + 1, j);
+                        double acc = Dk * uk;
+                        if (k > 0) acc = acc + Um * um;
+                        if (k < nz - 1) acc = acc + Uk * up;
+                        acc = acc + H0 * NBR(kk, l0);
+                        acc = acc + H1 * NBR(kk, l1);
+                        acc = acc + H2 * NBR(kk, l2);
+                        r = bk - acc;
+                        um = uk;
+                    }
                     layer(k, Dk, Uk, r, false);
-                    um = uk;
                     Um = Uk;
                 }
                 __syncwarp();
@@ -257,29 +382,56 @@ __global__ void __launch_bounds__(kThreads, 2)
             // Rare: a quotient left the fast path's exact range.  The warp redoes
             // its columns' forward pass from global memory with '/'.
             if (__any_sync(0xffffffffu, slow && valid)) {
-                const int64_t ce = valid ? c : L.n - 1;
-                const int32_t g0 = L.nbr[ce], g1 = L.nbr[ld + ce], g2 = L.nbr[2 * ld + ce];
+                const int32_t g0 = L.nbr[cv], g1 = L.nbr[ld + cv], g2 = L.nbr[2 * ld + cv];
                 auto GU = [&](int kk, int64_t cell) -> double {
                     double v = uin[(int64_t)kk * ld + cell];
                     if (PROLONG) v = v + uc[(int64_t)kk * ldc + (cell >> 2)];
                     return v;
                 };
-                um = Um = gprev = zprev = 0.0;
-                double uk = GU(0, ce);
+                um = Um = gprev = zprev = vdn = 0.0;
+                bool dummy = false;
+                if (MF) cg = column_geom(op.geom, ld, cv, op.w2, op.dz);
+                double uk = ZERO ? 0.0 : GU(0, cv);
                 for (int k = 0; k < nz; ++k) {
-                    const int64_t i = (int64_t)k * ld + ce;
-                    const double Dk = L.D[i], Uk = L.U[i];
-                    double up = 0.0;
-                    if (k < nz - 1) up = GU(k + 1, ce);
-                    double acc = Dk * uk;
-                    if (k > 0) acc = acc + Um * um;
-                    if (k < nz - 1) acc = acc + Uk * up;
-                    acc = acc + L.H0[i] * GU(k, g0);
-                    acc = acc + L.H1[i] * GU(k, g1);
-                    acc = acc + L.H2[i] * GU(k, g2);
-                    layer(k, Dk, Uk, bvec[i] - acc, true);
-                    um = uk;
-                    uk = up;
+                    const int64_t i = (int64_t)k * ld + cv;
+                    double Dk, Uk, H0, H1, H2;
+                    if (MF) {
+                        const double lk = op.lam[i];
+                        double vup = 0.0;
+                        if (k < nz - 1) vup = mf_vcoup<true>(cg, lk, op.lam[i + ld], op.dz, ydz, dummy);
+                        const double hc0 = mf_hcoup<true>(cg, 0, lk, op.lam[(int64_t)k * ld + g0], dummy);
+                        const double hc1 = mf_hcoup<true>(cg, 1, lk, op.lam[(int64_t)k * ld + g1], dummy);
+                        const double hc2 = mf_hcoup<true>(cg, 2, lk, op.lam[(int64_t)k * ld + g2], dummy);
+                        Dk = mf_diag(cg, k, nz, vdn, vup, hc0, hc1, hc2);
+                        Uk = (k < nz - 1) ? -vup : 0.0;
+                        H0 = -hc0;
+                        H1 = -hc1;
+                        H2 = -hc2;
+                        vdn = vup;
+                    } else {
+                        Dk = L.D[i];
+                        Uk = L.U[i];
+                        H0 = L.H0[i];
+                        H1 = L.H1[i];
+                        H2 = L.H2[i];
+                    }
+                    double r;
+                    if (ZERO) {
+                        r = bvec[i];
+                    } else {
+                        double up = 0.0;
+                        if (k < nz - 1) up = GU(k + 1, cv);
+                        double acc = Dk * uk;
+                        if (k > 0) acc = acc + Um * um;
+                        if (k < nz - 1) acc = acc + Uk * up;
+                        acc = acc + H0 * GU(k, g0);
+                        acc = acc + H1 * GU(k, g1);
+                        acc = acc + H2 * GU(k, g2);
+                        r = bvec[i] - acc;
+                        um = uk;
+                        uk = up;
+                    }
+                    layer(k, Dk, Uk, r, true);
                     Um = Uk;
                 }
             }
@@ -287,9 +439,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             ptx::tmem_wait_st();
 
             // back substitution from the top: delta_{nz-1} = z_{nz-1},
-            // delta_k = z_k - g_k delta_{k+1}; u' = u_old + omega delta
+            // delta_k = z_k - g_k delta_{k+1}; u' = u_old + omega delta (zero guess: omega delta)
             double dl = 0.0;
-            for (int m = nchunks - 1; m >= 0; --m, advance()) {
+            for (int m = (nz + kBack - 1) / kBack - 1; m >= 0; --m) {
                 const int k0 = m * kBack;
                 const int kt = (k0 + kBack - 1 < nz - 1) ? k0 + kBack - 1 : nz - 1;   // top layer of the chunk
                 uint32_t zr[16], gr[16];
@@ -311,9 +463,11 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                 }
                 ptx::tmem_wait_ld();
-                ptx::mbar_wait(&full[s], phase);
-                const double* su = stages + (size_t)s * SL.stage;
-                const double* suc = su + kBack * kTile;
+                const double* su = nullptr;
+                if (!ZERO) {
+                    ptx::mbar_wait(MF ? &mid[s] : &full[s], phase);
+                    su = stages + (size_t)s * SL.stage;
+                }
 #pragma unroll
                 for (int i = kBack - 1; i >= 0; --i) {
                     const int k = k0 + i;
@@ -323,12 +477,21 @@ __global__ void __launch_bounds__(kThreads, 2)
                         dl = zk;
                     else
                         dl = zk - ptx::f64_from(gr[2 * i], gr[2 * i + 1]) * dl;
-                    double uo = su[i * kTile + j];
-                    if (PROLONG) uo = uo + suc[i * (kTile / 4) + (j >> 2)];
-                    if (valid) uout[(int64_t)k * ld + c] = uo + omega * dl;
+                    double o;
+                    if (ZERO) {
+                        o = omega * dl;
+                    } else {
+                        double uo = su[i * kTile + j];
+                        if (PROLONG) uo = uo + su[kBack * kTile + i * (kTile / 4) + (j >> 2)];
+                        o = uo + omega * dl;
+                    }
+                    if (valid) uout[(int64_t)k * ld + c] = o;
                 }
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&empty[s]);
+                if (!ZERO) {
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&empty[s]);
+                    advance();
+                }
             }
         }
     }
@@ -343,12 +506,12 @@ uint32_t st_tmem_cols(int nz) {
     return c;
 }
 
-template <bool P, int G>
+template <bool Z, bool P, bool M, int G, bool CK = true>
 void launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                double* uout, double omega, cudaStream_t s) {
     const int nz = H.nz;
     const uint32_t cols = st_tmem_cols(nz);
-    constexpr StLayout SL = st_layout(P, G);
+    constexpr StLayout SL = st_layout(Z, P, M, G);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
     const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
@@ -361,16 +524,21 @@ void launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const dou
     if (smem < floor_smem) smem = floor_smem;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_sweep_st<P, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_sweep_st<Z, P, M, G, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
     StMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     const LevelView V = L.view(nz);
-    maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, 5);
+    if (M)
+        maps.lam = make_tensor_map(L.lam, L.ld, nz, kTile, G + 1, 1);
+    else
+        maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, 5);
     maps.b = make_tensor_map(b, L.ld, nz, kTile, G, 1);
-    maps.uf = make_tensor_map(uin, L.ld, nz, kTile, G + 1, 1);
-    maps.ub = make_tensor_map(uin, L.ld, nz, kTile, kBack, 1);
+    if (!Z) {
+        maps.uf = make_tensor_map(uin, L.ld, nz, kTile, G + 1, 1);
+        maps.ub = make_tensor_map(uin, L.ld, nz, kTile, kBack, 1);
+    }
     int64_t ldc = 0;
     if (P) {
         const DevLevel& C = H.lev[L.ref - 1];
@@ -378,9 +546,10 @@ void launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const dou
         maps.ucf = make_tensor_map(uc, C.ld, nz, kTile / 4, G + 1, 1);
         maps.ucb = make_tensor_map(uc, C.ld, nz, kTile / 4, kBack, 1);
     }
+    const StOp op{L.lam, L.geom, H.w2, H.dz};
     const unsigned cap = (unsigned)((two ? 2 : 1) * sms);
-    k_sweep_st<P, G><<<ntiles < cap ? ntiles : cap, kThreads, smem, s>>>(
-        maps, V, L.halo, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
+    k_sweep_st<Z, P, M, G, CK><<<ntiles < cap ? ntiles : cap, M ? kThreadsMf : kThreads, smem, s>>>(
+        maps, V, op, L.halo, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
 }
 
 }  // namespace
@@ -392,10 +561,28 @@ bool sweep_st_supported(const Hierarchy& H, const DevLevel& L) {
 void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                      double* uout, double omega, cudaStream_t s) {
     try {
-        if (uc)
-            launch_st<true, 2>(H, L, b, uin, uc, uout, omega, s);
-        else
-            launch_st<false, 2>(H, L, b, uin, nullptr, uout, omega, s);
+        if (H.matrix_free && L.mf_safe) {
+            if (!uin)
+                launch_st<true, false, true, 2, false>(H, L, b, nullptr, nullptr, uout, omega, s);
+            else if (uc)
+                launch_st<false, true, true, 2, false>(H, L, b, uin, uc, uout, omega, s);
+            else
+                launch_st<false, false, true, 2, false>(H, L, b, uin, nullptr, uout, omega, s);
+        } else if (H.matrix_free) {
+            if (!uin)
+                launch_st<true, false, true, 2>(H, L, b, nullptr, nullptr, uout, omega, s);
+            else if (uc)
+                launch_st<false, true, true, 2>(H, L, b, uin, uc, uout, omega, s);
+            else
+                launch_st<false, false, true, 2>(H, L, b, uin, nullptr, uout, omega, s);
+        } else {
+            if (!uin)
+                launch_st<true, false, false, 2>(H, L, b, nullptr, nullptr, uout, omega, s);
+            else if (uc)
+                launch_st<false, true, false, 2>(H, L, b, uin, uc, uout, omega, s);
+            else
+                launch_st<false, false, false, 2>(H, L, b, uin, nullptr, uout, omega, s);
+        }
     } catch (const std::exception& e) {
         g_launch_error = std::string("sweep launch: ") + e.what();
     }

@@ -345,3 +345,27 @@ def test_distributed_path_one_rank(monkeypatch, gather_ref, force):
     assert st == "HMG_OK" and it == o.pcg(b)[1]
     g.close()
     o.close()
+
+
+@pytest.mark.parametrize("w2", [1e-4, 1e-290])
+def test_matrix_free_operator(monkeypatch, w2):
+    """NEXT-2 matrix-free store (HMG_OPERATOR=free): couplings recomputed from
+    lam and the column geometry in k_assemble's order, so applies, sweeps (zero
+    guess, general, with the fused prolongation) and the V-cycle are bitwise the
+    oracle's.  w2 = 1e-290 makes the couplings subnormal: the build-time range
+    proof fails, the checked division runs and its exact redo path is taken."""
+    monkeypatch.setenv("HMG_OPERATOR", "free")
+    cfg = hi.Config("mf", 5, 0, 16, 0.01, w2)       # ref 5 (20,480 cells): streamed kernels, no precomputed pivots
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(5, 0, 16, 0.01, w2, lam)
+    o = oracle.Hierarchy(5, 0, 16, 0.01, w2, lam)
+    x = hi.uniform_vector(b.shape, 7)
+    assert np.array_equal(g.to_host(5, g.apply_helmholtz(5, g.to_device(5, x))), o.apply(5, x))
+    for zero in (True, False):
+        u = g.to_device(5, np.zeros_like(x) if zero else x)
+        g.line_smooth(5, g.to_device(5, b), u, 2, 0.8, zero)
+        assert np.array_equal(g.to_host(5, u), o.sweep(5, b, None if zero else x, 2, 0.8))
+    z = g.to_host(5, g.vcycle(g.to_device(5, b)))
+    assert np.array_equal(z, o.vcycle(b, 2, 2, 20, 0.8))
+    g.close()
+    o.close()
