@@ -358,11 +358,87 @@ def run_hmg(args, ws, rank, local):
         dist.destroy_process_group()
 
 
+def run_c1(args):
+    """BASELINE.json config C1: kernel microbench at ref 5 x 64 layers (1,310,720
+    dofs): 100 launches each of the operator apply, one fused line-Jacobi sweep
+    with a non-zero iterate, restriction 5 -> 4 and prolongation 4 -> 5, each
+    launch preceded by a 256 MB write that flushes the 126 MB L2 (the C1 working
+    set, ~84 MB, would otherwise stay resident).  Kernel durations are the
+    library's CUDA events around each launch, on the launching stream."""
+    import torch
+    from paper_1605_00492_b200 import Hierarchy
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA GPU (no CPU fallback exists)")
+    cfg = hi.CONFIGS["C1"]
+    lam, b = hi.make_inputs(cfg)
+    r = cfg.fine_ref
+    x = hi.uniform_vector(b.shape, 101)
+    u = hi.uniform_vector(b.shape, 102)
+    h = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    xd, bd, ud, yd = h.to_device(r, x), h.to_device(r, b), h.to_device(r, u), h.empty(r)
+    cd = h.empty(r - 1)
+    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    ops = {
+        "apply": (lambda: h.apply_helmholtz(r, xd, yd), "apply", r, 56.0),
+        "sweep": (lambda: h.line_smooth(r, bd, ud, 1, 0.8, False), "sweep", r, 64.0),
+        "restrict": (lambda: h.restrict(r, xd, cd), "restrict", r, 10.0),
+        "prolong": (lambda: h.prolong_add(r, cd, yd), "prolong", r, 18.0),
+    }
+    peak, peak_note = measured_peak()
+    reps = max(args.steps, 100)
+    # warm: 100 launches back to back (the sweep as one 100-sweep line_smooth call)
+    warm_ops = {
+        "apply": lambda: [h.apply_helmholtz(r, xd, yd) for _ in range(reps)],
+        "sweep": lambda: h.line_smooth(r, bd, ud, reps, 0.8, False),
+        "restrict": lambda: [h.restrict(r, xd, cd) for _ in range(reps)],
+        "prolong": lambda: [h.prolong_add(r, cd, yd) for _ in range(reps)],
+    }
+    out = {}
+    for name, (fn, cls, ref, bpd) in ops.items():
+        for _ in range(max(args.warmup, 3)):
+            fn()
+        torch.cuda.synchronize()
+        h.profile_begin()
+        for _ in range(reps):
+            flush.zero_()
+            fn()
+        torch.cuda.synchronize()
+        h.profile_end()
+        n, ms = h.profile_query(cls, ref)
+        us = ms * 1e3 / max(n, 1)
+        h.profile_begin()
+        warm_ops[name]()
+        torch.cuda.synchronize()
+        h.profile_end()
+        nw, msw = h.profile_query(cls, ref)
+        usw = msw * 1e3 / max(nw, 1)
+        gbs = bpd * cfg.ndofs / (us * 1e-6) / 1e9
+        gbw = bpd * cfg.ndofs / (usw * 1e-6) / 1e9
+        out[name] = {"us": round(us, 2), "launches": n, "bytes_per_dof": bpd, "GB/s": round(gbs, 1),
+                     "frac": round(gbs / peak, 3),
+                     "warm": {"us": round(usw, 2), "launches": nw, "GB/s": round(gbw, 1), "frac": round(gbw / peak, 3)}}
+    a = out["apply"]
+    print(json.dumps({
+        "metric": "C1 operator apply dofs/s (kernel microbench)", "value": cfg.ndofs / (a["us"] * 1e-6),
+        "unit": "dof/s", "n_gpus": 1, "steps": reps, "warmup": args.warmup, "higher_is_better": True,
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C1: ref 5 x 64 layers, 1,310,720 dofs; t 0.01, w2 1e-4",
+                   "cache": "L2 flushed (256 MB write) before every launch; 'warm': 100 launches back to back, "
+                            "working set (84 MB) L2-resident"},
+        "roofline": {"kernel": "k_apply_t (operator apply, ref 5)", "bound": "hbm", "achieved": a["GB/s"],
+                     "peak": peak, "unit": "GB/s", "frac": a["frac"], "peak_source": peak_note},
+        "kernels": out}))
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
     if args.impl == "reference":
         run_reference(args, ws, rank)
+    elif args.config == "C1":
+        if rank == 0:
+            run_c1(args)
     else:
         run_hmg(args, ws, rank, local)
 

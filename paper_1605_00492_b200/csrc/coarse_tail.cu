@@ -105,7 +105,7 @@ __device__ void sweep_col(const TailLevel& T, int nz, const double* __restrict__
         const double den = den_p[i];
         const double num = (k == 0) ? r : r - Um * zprev;
         bool slow = false;
-        double z = div_fast(num, den, y_p[i], slow);
+        double z = div_fast_z(num, den, y_p[i], slow);
         if (slow) z = num / den;
         zs[k * stride] = z;
         zprev = z;
@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(128, 1)
                 const int i = k * n + c;
                 const double r = z[k * T];
                 const double num = (k == 0) ? r : r - U[i - n] * zprev;
-                const double zk = div_fast(num, den[i], y[i], slow);
+                const double zk = div_fast_z(num, den[i], y[i], slow);
                 z[k * T] = zk;
                 zprev = zk;
             }

@@ -105,7 +105,7 @@ __device__ __forceinline__ void tile_sweep(const TileSmem& S, int nz, int j, int
             const int k = k0 + i;
             const double num = (k == 0) ? rr[i] : rr[i] - um[i] * zprev;
             bool sl = false;
-            const double zk = div_fast(num, dd[i], yy[i], sl);
+            const double zk = div_fast_z(num, dd[i], yy[i], sl);
             slow = slow || (sl && k < nz);
             rr[i] = zk;
             zprev = zk;
@@ -213,7 +213,7 @@ __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int wa
                 const int k = k0 + i;
                 const double num = (k == 0) ? rr[i] : rr[i] - um[i] * zprev;
                 bool sl = false;
-                const double zk = div_fast(num, dd[i], yy[i], sl);
+                const double zk = div_fast_z(num, dd[i], yy[i], sl);
                 slow = slow || (sl && k < nz);
                 rr[i] = zk;
                 zprev = zk;

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     if (has_g) g = Uk / den;
                 } else {
                     const double y = div_recip(den);
-                    z = div_fast(num, den, y, slow);
+                    z = div_fast_z(num, den, y, slow);
                     if (has_g) g = div_fast(Uk, den, y, slow);
                 }
                 ok = ok && pivot_ok(den);

@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (FACT) {                           // pivots precomputed at setup (matrix-only)
                 den = fden;
                 g = fg;
-                z = exact ? num / den : div_fast(num, den, fy, slow);
+                z = exact ? num / den : div_fast_z(num, den, fy, slow);
             } else {
                 den = (k == 0) ? Dk : Dk - Um * gprev;
                 if (exact) {
@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (has_g) g = Uk / den;
                 } else {
                     const double y = div_recip(den);
-                    z = div_fast(num, den, y, slow);
+                    z = div_fast_z(num, den, y, slow);
                     if (has_g) g = div_fast(Uk, den, y, slow);
                 }
                 ok = ok && pivot_ok(den);
