@@ -362,7 +362,7 @@ def run_c1(args):
     """BASELINE.json config C1: kernel microbench at ref 5 x 64 layers (1,310,720
     dofs): 100 launches each of the operator apply, one fused line-Jacobi sweep
     with a non-zero iterate, restriction 5 -> 4 and prolongation 4 -> 5, each
-    launch preceded by a 256 MB write that flushes the 126 MB L2 (the C1 working
+    launch preceded by a 256 MB read that evicts the 126 MB L2 (the C1 working
     set, ~84 MB, would otherwise stay resident).  Kernel durations are the
     library's CUDA events around each launch, on the launching stream."""
     import torch
@@ -378,7 +378,17 @@ def run_c1(args):
     h = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
     xd, bd, ud, yd = h.to_device(r, x), h.to_device(r, b), h.to_device(r, u), h.empty(r)
     cd = h.empty(r - 1)
-    flush = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    # L2 eviction by READING 256 MB (a write would leave ~126 MB of dirty lines whose
+    # write-back then competes with the timed kernel)
+    flush_buf = torch.ones(256 * 2 ** 20 // 4, dtype=torch.float32, device="cuda")
+    flush_out = torch.empty((), dtype=torch.float32, device="cuda")
+
+    class _Flush:
+        @staticmethod
+        def zero_():
+            torch.sum(flush_buf, dim=0, out=flush_out)
+
+    flush = _Flush()
     ops = {
         "apply": (lambda: h.apply_helmholtz(r, xd, yd), "apply", r, 56.0),
         "sweep": (lambda: h.line_smooth(r, bd, ud, 1, 0.8, False), "sweep", r, 64.0),
@@ -424,7 +434,7 @@ def run_c1(args):
         "unit": "dof/s", "n_gpus": 1, "steps": reps, "warmup": args.warmup, "higher_is_better": True,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "C1: ref 5 x 64 layers, 1,310,720 dofs; t 0.01, w2 1e-4",
-                   "cache": "L2 flushed (256 MB write) before every launch; 'warm': 100 launches back to back, "
+                   "cache": "L2 evicted (256 MB read) before every launch; 'warm': 100 launches back to back, "
                             "working set (84 MB) L2-resident"},
         "roofline": {"kernel": "k_apply_t (operator apply, ref 5)", "bound": "hbm", "achieved": a["GB/s"],
                      "peak": peak, "unit": "GB/s", "frac": a["frac"], "peak_source": peak_note},

@@ -27,7 +27,9 @@ struct Nccl {
     const char* (*GetErrorString)(int) = nullptr;
 };
 
-// Loaded table, or nullptr with `err` set.
+// Loaded table, or nullptr with `err` set.  HMG_TRANSPORT=local selects the
+// in-process transport of local_transport.cu (all ranks threads of one
+// process on one GPU; for testing the multi-GPU path on a single device).
 const Nccl* nccl(std::string* err);
 
 }  // namespace hmg
