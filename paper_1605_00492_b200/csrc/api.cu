@@ -383,6 +383,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_SMALL")) H->use_small_sweep = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_SWEEP_ST")) H->use_st_sweep = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_OPERATOR")) H->matrix_free = std::string(e) == "free";
+    if (const char* e = std::getenv("HMG_APPLY_ST")) H->use_st_apply = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at

@@ -1,0 +1,256 @@
+// Operator apply y = H^ x (reading R5) streamed through a TMA ring:
+// persistent CTAs, 128-column tiles, one producer warp, four consumer warps.
+//
+// Same operation order as k_apply_t (kernels.cu), so bitwise the same result:
+//   y = ((((D x_k + U_{k-1} x_{k-1}) + U_k x_{k+1}) + H0 x_N0) + H1 x_N1) + H2 x_N2.
+// What differs is the data movement.  The thread-per-column k_apply_t keeps
+// only a few layers' loads in flight per thread and gathers the face
+// neighbours from L2 (ncu: ~50 cycles per issued instruction, long-scoreboard
+// bound, 0.64-0.71 of the HBM peak).  Here a producer warp streams, per stage
+// of G layers, one 3-D TMA box with the five bands, G + 1 rows of x (row k + 1
+// of the own column is needed at layer k) and the tile's <= 64 off-tile
+// neighbours (8-byte cp.async); in-tile neighbours come from shared memory.
+//  * PUPD (CG): the operand is p = z + beta p_old formed on the fly for the
+//    cell and its neighbours (the same addition as a separate update) and
+//    written back -- the p update fused into q = H^ p; rows of both z and
+//    p_old travel in the stage.
+//  * DOT: <x, H^ x> accumulated per thread, reduced per CTA in a fixed order.
+// HBM traffic per dof: 56 B (x, bands in; y out), 72 B with the p update.
+#include <cuda.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "hmg_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace hmg {
+
+CUtensorMap make_tensor_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes);
+extern thread_local std::string g_launch_error;
+void finalize_parts(const Hierarchy& H, int nparts, int op, cudaStream_t s);
+
+namespace {
+
+constexpr int kTile = kSweepTile;
+constexpr int kConsumerWarps = kTile / 32;
+constexpr int kThreads = kTile + 32;
+
+struct ApMaps {
+    CUtensorMap bands;  // 3-D box kTile x G x 5
+    CUtensorMap x;      // box kTile x (G + 1): x, or p_old (PUPD)
+    CUtensorMap z;      // box kTile x (G + 1): z (PUPD)
+};
+
+struct ApLayout {
+    int x, z, hx, hz, stage;
+};
+__host__ __device__ constexpr ApLayout ap_layout(bool pupd, int G) {
+    ApLayout L{};
+    L.x = 5 * G * kTile;
+    L.z = L.x + (G + 1) * kTile;
+    L.hx = L.z + (pupd ? (G + 1) * kTile : 0);
+    L.hz = L.hx + G * kHaloMax;
+    L.stage = L.hz + (pupd ? G * kHaloMax : 0);
+    return L;
+}
+
+template <bool DOT, bool PUPD, int G>
+__global__ void __launch_bounds__(kThreads, 2)
+    k_apply_st(const __grid_constant__ ApMaps maps, LevelView L, TileHalo th, const double* __restrict__ xin,
+               const double* __restrict__ zv, double* __restrict__ y, double* __restrict__ pnew,
+               double* __restrict__ partial, const PcgScalars* __restrict__ sc, int S) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    __shared__ double red[kThreads / 32];
+    constexpr ApLayout AL = ap_layout(PUPD, G);
+    const int nz = L.nz;
+    const int64_t ld = L.ld;
+    const int ngroups = (nz + G - 1) / G;
+    const int ntiles = (int)((L.n + kTile - 1) / kTile);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
+    uint64_t* empty = full + S;
+    double* stages = reinterpret_cast<double*>(smraw + 1024);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], kConsumerWarps);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    double dot = 0.0;
+    int s = 0;
+    uint32_t phase = 0;
+    auto advance = [&]() {
+        if (++s == S) {
+            s = 0;
+            phase ^= 1u;
+        }
+    };
+    if (warp == kConsumerWarps) {
+        // ======================= producer warp =======================
+        const uint64_t pol = ptx::policy_evict_first();
+        const uint32_t bytes = (uint32_t)(sizeof(double) * (5 * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile));
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int x = tile * kTile;
+            const int hcount = th.count[tile];
+            const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
+            const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
+            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+                ptx::mbar_wait(&empty[s], phase ^ 1u);
+                double* st = stages + (size_t)s * AL.stage;
+                for (int kk = 0; kk < G; ++kk) {
+                    const int k = gi * G + kk;
+                    if (k >= nz) break;
+                    const double* src = xin + (int64_t)k * ld;
+                    if (lane < hcount) ptx::cp_async8(st + AL.hx + kk * kHaloMax + lane, src + h0);
+                    if (lane + 32 < hcount) ptx::cp_async8(st + AL.hx + kk * kHaloMax + lane + 32, src + h1);
+                    if (PUPD) {
+                        const double* srz = zv + (int64_t)k * ld;
+                        if (lane < hcount) ptx::cp_async8(st + AL.hz + kk * kHaloMax + lane, srz + h0);
+                        if (lane + 32 < hcount) ptx::cp_async8(st + AL.hz + kk * kHaloMax + lane + 32, srz + h1);
+                    }
+                }
+                ptx::cp_async_arrive(&full[s]);
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive_expect_tx(&full[s], bytes);
+                    ptx::tma_load_3d_hint(st, &maps.bands, x, gi * G, 0, &full[s], pol);
+                    ptx::tma_load_2d(st + AL.x, &maps.x, x, gi * G, &full[s]);
+                    if (PUPD) ptx::tma_load_2d(st + AL.z, &maps.z, x, gi * G, &full[s]);
+                }
+            }
+        }
+    } else {
+        // ======================= consumers: one column per thread =======================
+        const int j = threadIdx.x;
+        const double beta = PUPD ? sc->beta : 0.0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int64_t c = (int64_t)tile * kTile + j;
+            const bool valid = c < L.n;
+            const uint32_t loc = th.loc[valid ? c : L.n - 1];
+            const int l0 = loc & 0xff, l1 = (loc >> 8) & 0xff, l2 = (loc >> 16) & 0xff;
+            double xm = 0.0, Um = 0.0;
+            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+                ptx::mbar_wait(&full[s], phase);
+                const double* st = stages + (size_t)s * AL.stage;
+                const double* sx = st + AL.x;
+                const double* sz = st + AL.z;
+                const double* hx = st + AL.hx;
+                const double* hz = st + AL.hz;
+                auto XV = [&](int kk, int l) -> double {   // operand of local slot l at stage row kk
+                    if (l < kTile) {
+                        if (PUPD) return sz[kk * kTile + l] + beta * sx[kk * kTile + l];
+                        return sx[kk * kTile + l];
+                    }
+                    if (PUPD) return hz[kk * kHaloMax + l - kTile] + beta * hx[kk * kHaloMax + l - kTile];
+                    return hx[kk * kHaloMax + l - kTile];
+                };
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) {
+                    const int k = gi * G + kk;
+                    if (k >= nz) break;
+                    const double* sr = st + kk * kTile + j;
+                    const double Dk = sr[0];
+                    const double Uk = sr[G * kTile];
+                    const double xk = XV(kk, j);
+                    double xp = 0.0;
+                    if (k < nz - 1) xp = XV(kk + 1, j);
+                    double acc = Dk * xk;
+                    if (k > 0) acc = acc + Um * xm;
+                    if (k < nz - 1) acc = acc + Uk * xp;
+                    acc = acc + sr[2 * G * kTile] * XV(kk, l0);
+                    acc = acc + sr[3 * G * kTile] * XV(kk, l1);
+                    acc = acc + sr[4 * G * kTile] * XV(kk, l2);
+                    if (valid) {
+                        const int64_t i = (int64_t)k * ld + c;
+                        y[i] = acc;
+                        if (PUPD) pnew[i] = xk;
+                        if (DOT) dot = dot + xk * acc;
+                    }
+                    xm = xk;
+                    Um = Uk;
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            }
+        }
+    }
+    if (DOT) {   // fixed-order CTA reduction (the producer warp contributes 0)
+        for (int off = 16; off > 0; off >>= 1) dot = dot + __shfl_down_sync(0xffffffffu, dot, off);
+        if (lane == 0) red[warp] = dot;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < kThreads / 32; ++w) t = t + red[w];
+            partial[blockIdx.x] = t;
+        }
+    }
+}
+
+template <bool DOT, bool PUPD, int G>
+int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const double* z, double* y, double* pnew,
+              cudaStream_t s) {
+    const int nz = H.nz;
+    constexpr ApLayout AL = ap_layout(PUPD, G);
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
+    const size_t budget = 110 * 1024;
+    int S = (int)((budget - 1024) / (sizeof(double) * AL.stage));
+    S = S < 2 ? 2 : (S > 32 ? 32 : S);
+    const size_t smem = 1024 + sizeof(double) * (size_t)S * AL.stage;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_apply_st<DOT, PUPD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    ApMaps maps;
+    std::memset(&maps, 0, sizeof(maps));
+    const LevelView V = L.view(nz);
+    maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, 5);
+    maps.x = make_tensor_map(x, L.ld, nz, kTile, G + 1, 1);
+    if (PUPD) maps.z = make_tensor_map(z, L.ld, nz, kTile, G + 1, 1);
+    const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
+    const unsigned cap = (unsigned)(2 * sms);
+    const unsigned grid = ntiles < cap ? ntiles : cap;
+    k_apply_st<DOT, PUPD, G><<<grid, kThreads, smem, s>>>(maps, V, L.halo, x, z, y, pnew, H.partials, H.scal, S);
+    return (int)grid;
+}
+
+}  // namespace
+
+bool apply_st_supported(const Hierarchy& H, const DevLevel& L) {
+    return H.use_st_apply && L.halo.loc != nullptr && H.nz >= 2;
+}
+
+// y = H^ x (dot: partial <x, H^ x> per CTA into H.partials, returns the count; 0 otherwise)
+int launch_apply_st(const Hierarchy& H, const DevLevel& L, const double* x, double* y, bool dot, cudaStream_t s) {
+    int n = 0;
+    try {
+        if (dot)
+            n = launch_ap<true, false, 2>(H, L, x, nullptr, y, nullptr, s);
+        else
+            launch_ap<false, false, 2>(H, L, x, nullptr, y, nullptr, s);
+    } catch (const std::exception& e) {
+        g_launch_error = std::string("apply launch: ") + e.what();
+    }
+    ++H.launches;
+    return n;
+}
+
+// q = H^ p with p = z + beta p_old formed on the fly and stored in pnew; partial <p, q>
+int launch_apply_pupdate_st(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
+                            double* q, cudaStream_t s) {
+    int n = 0;
+    try {
+        n = launch_ap<true, true, 2>(H, L, pold, z, q, pnew, s);
+    } catch (const std::exception& e) {
+        g_launch_error = std::string("apply launch: ") + e.what();
+    }
+    ++H.launches;
+    return n;
+}
+
+}  // namespace hmg

@@ -161,6 +161,7 @@ struct Hierarchy {
     // distance in ring stages, HMG_TAIL_REF the one-launch coarse tail
     bool use_tc_sweep = true;
     bool use_st_sweep = true;
+    bool use_st_apply = true;   // HMG_APPLY_ST=0: thread-per-column k_apply_t instead of k_apply_st
     bool matrix_free = false;   // operator applies recompute the couplings from lam + geometry (NEXT-2)   // HMG_SWEEP_ST=0: non-zero-guess sweeps by k_sweep_tc instead of k_sweep_st
     bool use_small_sweep = true;
     int l2_prefetch_groups = 3;
@@ -199,6 +200,14 @@ void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, con
 bool sweep_st_supported(const Hierarchy& H, const DevLevel& L);
 void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                      double* uout, double omega, cudaStream_t s);
+
+// apply_st.cu: TMA-streamed persistent operator apply (same arithmetic as k_apply_t);
+// the dot forms return the number of per-CTA partial sums written to H.partials
+bool apply_st_supported(const Hierarchy& H, const DevLevel& L);
+int launch_apply_st(const Hierarchy& H, const DevLevel& L, const double* x, double* y, bool dot, cudaStream_t s);
+int launch_apply_pupdate_st(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
+                            double* q, cudaStream_t s);
+void finalize_parts(const Hierarchy& H, int nparts, int op, cudaStream_t s);
 
 // coarse_tail.cu
 void launch_factor(const Hierarchy& H, const DevLevel& L, cudaStream_t s);

@@ -618,6 +618,10 @@ void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
 
 void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
     ProfScope ps(H, kKApply, L.ref, s);
+    if (!H.matrix_free && apply_st_supported(H, L)) {
+        launch_apply_st(H, L, x, y, false, s);
+        return;
+    }
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
     if (H.matrix_free)
         k_apply_mf<false, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), L.geom, L.lam, H.w2, H.dz, x, y, nullptr,
@@ -629,6 +633,11 @@ void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double
 
 void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
     ProfScope ps(H, kKApply, L.ref, s);
+    if (!H.matrix_free && apply_st_supported(H, L)) {
+        const int n = launch_apply_st(H, L, x, y, true, s);
+        finalize_parts(H, n, kFinPQ, s);
+        return;
+    }
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
     if (H.matrix_free)
         k_apply_mf<true, false><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), L.geom, L.lam, H.w2, H.dz, x, y, H.partials,
@@ -675,6 +684,11 @@ void launch_sweep(const Hierarchy& H, const DevLevel& L, const double* b, const 
 void launch_apply_pupdate_dot(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
                               double* q, cudaStream_t s) {
     ProfScope ps(H, kKApplyP, L.ref, s);
+    if (!H.matrix_free && apply_st_supported(H, L)) {
+        const int n = launch_apply_pupdate_st(H, L, z, pold, pnew, q, s);
+        finalize_parts(H, n, kFinPQ, s);
+        return;
+    }
     dim3 g(blocks(L.n, kApplyBlock), vchunks(L.n, H.nz));
     if (H.matrix_free)
         k_apply_mf<true, true><<<g, kApplyBlock, 0, s>>>(L.view(H.nz), L.geom, L.lam, H.w2, H.dz, pold, q, H.partials,
