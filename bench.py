@@ -55,7 +55,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="hmg", choices=["hmg", "reference"])
-    ap.add_argument("--config", default="C2b", choices=["C2a", "C2b", "C2c", "C0", "C1"])
+    ap.add_argument("--config", default="C2b", choices=["C2a", "C2b", "C2c", "C0", "C1", "C4"])
     ap.add_argument("--gather-ref", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -77,12 +77,13 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel: str):
-    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture."""
+def ncu_traffic(config: str, kernel: str):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu capture
+    of the same configuration (null when no capture of this config exists)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as fh:
-            return json.load(fh).get(kernel)
+            return json.load(fh).get(config, {}).get(kernel)
     except Exception:
         return None
 
@@ -337,13 +338,14 @@ def run_hmg(args, ws, rank, local):
                        "pcg_iterations": iters, "vcycles_per_step": nv, "final_relres": relres,
                        "parallelism": (f"domain decomposition x{ws} (NCCL halos, all-reduce, coarse gather at ref "
                                        f"{min(args.gather_ref, cfg.fine_ref)})") if ws > 1 else "single GPU",
-                       "cache": "inputs larger than L2 (bands 840 MB + vectors per level)"},
+                       "cache": f"inputs larger than L2 (fine bands {5 * 8 * cfg.ndofs // ws / 1e6:.0f} MB + vectors "
+                                f"per level)"},
             "pcg_solve_ms": ms,
             "vcycle_only": {"value": cfg.ndofs / (ms_vc * 1e-3), "unit": UNIT, "ms": ms_vc},
             "setup_s": setup_s,
             "roofline": {"kernel": "k_sweep_st (fused residual + Thomas line sweep, finest level)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic("k_sweep_st<0, 0, 0, 2, 1>"),
+                         "frac": achieved / peak, "traffic": ncu_traffic(cfg.name, "k_sweep_st<0, 0, 0, 2, 1>"),
                          "algorithmic_bytes_per_launch": bytes_sw, "avg_launch_us": avg_sw * 1e3,
                          "launches_timed": n_sw, "peak_source": peak_note},
             "fine_level_kernels": fine,
