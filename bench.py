@@ -306,6 +306,21 @@ def run_hmg(args, ws, rank, local):
     ms_vc = max_over_ranks(e0.elapsed_time(e1) / nvc)
     n = cfg.n // ws
 
+    # ---- NEXT-1: the paper's single-level preconditioner (2 damped line sweeps,
+    # P:815-817) in the same PCG, against the multigrid V-cycle ----
+    sl = None
+    if ws == 1:
+        xs = h.empty(r)
+        h.pcg_solve_single_level(bd, xs, nsweeps=2, omega=0.8, rtol=1e-8, maxit=2000)
+        barrier()
+        e0.record(stream)
+        _, it_sl, rr_sl, st_sl = h.pcg_solve_single_level(bd, xs, nsweeps=2, omega=0.8, rtol=1e-8, maxit=2000)
+        e1.record(stream)
+        barrier()
+        sl = {"preconditioner": "2 damped line-Jacobi sweeps (single level)", "pcg_iterations": it_sl,
+              "status": st_sl, "solve_ms": e0.elapsed_time(e1), "final_relres": rr_sl,
+              "multigrid_pcg_iterations": iters, "multigrid_solve_ms": ms}
+
     # ---- end to end: host buffers through hmg_pcg_solve_host ----------------
     hb = torch.from_numpy(b).pin_memory()
     hx = torch.empty_like(hb).pin_memory()
@@ -351,6 +366,7 @@ def run_hmg(args, ws, rank, local):
             "fine_level_kernels": fine,
             "time_share": shares,
             "cpu_baseline": cpu,
+            "single_level_comparison": sl,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * cfg.nz * n * ws),
                     "d2h_bytes_per_step": int(8 * cfg.nz * n * ws), "ms_per_step": ms_e2e},
             "gpu_launches": launches,
