@@ -274,21 +274,34 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         else
             run_sweeps(H, F, r, nullptr, nullptr, single_sweeps, z, single_omega, s);
     };
-    // r = b (internal r keeps zero padding), x = 0
-    launch_copy_pad(H, F, b, F.ld, H.r, F.ld, s);
-    HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
-    launch_dot(H, F, H.r, H.r, s);
+    if (F.dist.on) {
+        // multi-GPU: r = b (internal r keeps zero padding), x = 0, p = z copied
+        launch_copy_pad(H, F, b, F.ld, H.r, F.ld, s);
+        HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
+    }
+    const double* r0 = F.dist.on ? H.r : b;        // single GPU: the first residual is b itself
+    launch_dot(H, F, r0, r0, s);
     launch_finalize(H, kFinBB, s);
     HMG_TRY(check_launch());
     HMG_CUDA(cudaMemcpyAsync(H.scal_host, H.scal, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
     HMG_CUDA(cudaStreamSynchronize(s));
     const double bn = std::sqrt(H.scal_host->bb);
-    if (bn == 0.0) return HMG_OK;
-    precond(H.r, H.z);
-    launch_dot(H, F, H.r, H.z, s);
+    if (bn == 0.0) {
+        if (!F.dist.on) HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
+        return HMG_OK;
+    }
+    precond(r0, H.z);
+    launch_dot(H, F, r0, H.z, s);
     launch_finalize(H, kFinRhoInit, s);
-    HMG_CUDA(cudaMemcpyAsync(H.p, H.z, bytes, cudaMemcpyDeviceToDevice, s));
-    double* pc = H.p;                              // current search direction (ping-pong with p2)
+    // Single GPU: z, p_old and p_new rotate through {z, p, p2} so that p_1 = z_1
+    // needs no copy; the first x/r update reads b and writes x = 0 + alpha p,
+    // r = b - alpha q (the same arithmetic as from x = 0, r = b).
+    double* pc = H.z;                              // current search direction
+    if (F.dist.on) {
+        HMG_CUDA(cudaMemcpyAsync(H.p, H.z, bytes, cudaMemcpyDeviceToDevice, s));
+        pc = H.p;
+    }
+    double* zb = H.z;                              // buffer holding the current z
     for (int it = 1; it <= maxit; ++it) {
         if (F.dist.on) {                           // multi-GPU: p update, halo exchange, apply
             if (it > 1) launch_update_p(H, F, pc, H.z, s);
@@ -297,11 +310,14 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         } else if (it == 1) {
             launch_apply_dot(H, F, pc, H.q, s);    // q = H^ p, alpha = rho / <p, q>
         } else {                                   // p = z + beta p fused into q = H^ p
-            double* pn = (pc == H.p) ? H.p2 : H.p;
-            launch_apply_pupdate_dot(H, F, H.z, pc, pn, H.q, s);
+            double* pn = (pc != H.p2 && zb != H.p2) ? H.p2 : ((pc != H.p && zb != H.p) ? H.p : H.z);
+            launch_apply_pupdate_dot(H, F, zb, pc, pn, H.q, s);
             pc = pn;
         }
-        launch_update_xr(H, F, x, pc, s);          // x += alpha p, r -= alpha q, partial <r, r>
+        if (it == 1 && !F.dist.on)
+            launch_update_xr_first(H, F, x, pc, b, s);   // x = 0 + alpha p, r = b - alpha q, partial <r, r>
+        else
+            launch_update_xr(H, F, x, pc, s);      // x += alpha p, r -= alpha q, partial <r, r>
         launch_finalize(H, kFinRR, s);
         HMG_TRY(check_launch());
         HMG_CUDA(cudaMemcpyAsync(H.scal_host, H.scal, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
@@ -311,8 +327,9 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         *iters = it;
         *relres = rn / bn;
         if (rn <= rtol * bn) return HMG_OK;
-        precond(H.r, H.z);
-        launch_dot(H, F, H.r, H.z, s);
+        if (!F.dist.on) zb = (pc != H.z) ? H.z : H.p;   // a buffer that is not p
+        precond(H.r, zb);
+        launch_dot(H, F, H.r, zb, s);
         launch_finalize(H, kFinRZ, s);             // beta = rho' / rho, rho = rho' (p updated in the next apply)
     }
     return fail(HMG_ERR_NOT_CONVERGED, "not converged after " + std::to_string(maxit) +

@@ -185,6 +185,9 @@ void launch_prolong_add(const Hierarchy& H, const DevLevel& F, const double* uin
 void launch_dot(const Hierarchy& H, const DevLevel& L, const double* a, const double* b, cudaStream_t s);
 void launch_finalize(const Hierarchy& H, int op, cudaStream_t s);
 void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, const double* p, cudaStream_t s);
+// first iteration from x = 0, r = b: x = 0 + alpha p, r = b - alpha q (reads b, not x or r)
+void launch_update_xr_first(const Hierarchy& H, const DevLevel& L, double* x, const double* p, const double* b,
+                            cudaStream_t s);
 // q = H^ p_new with p_new = z + beta p_old formed on the fly and stored; partial <p_new, q> -> alpha
 void launch_apply_pupdate_dot(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
                               double* q, cudaStream_t s);

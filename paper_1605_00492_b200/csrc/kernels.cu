@@ -463,9 +463,13 @@ __global__ void __launch_bounds__(kVecBlock) k_dot(const double* __restrict__ a,
     if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = tot;
 }
 
+// FIRST: the first iteration from x = 0, r = b -- reads b instead of r and does
+// not read x; x = 0 + alpha p and r = b - alpha q are the same operations.
+template <bool FIRST>
 __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x, double* __restrict__ r,
                                                          const double* __restrict__ p, const double* __restrict__ q,
-                                                         int64_t n, int64_t ld, int nz, const PcgScalars* __restrict__ sc,
+                                                         const double* __restrict__ rin, int64_t n, int64_t ld, int nz,
+                                                         const PcgScalars* __restrict__ sc,
                                                          double* __restrict__ partial) {
     __shared__ double red[kVecBlock / 32];
     const double alpha = sc->alpha;
@@ -477,8 +481,8 @@ __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x,
             const int64_t c = v.c0 + h * 2 * kVecBlock;
             if (c < n) {
                 const int64_t i = k * ld + c;
-                double2 xx = *reinterpret_cast<const double2*>(x + i);
-                double2 rr = *reinterpret_cast<const double2*>(r + i);
+                double2 xx = FIRST ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(x + i);
+                double2 rr = *reinterpret_cast<const double2*>((FIRST ? rin : r) + i);
                 const double2 pp = *reinterpret_cast<const double2*>(p + i);
                 const double2 qq = *reinterpret_cast<const double2*>(q + i);
                 xx.x = xx.x + alpha * pp.x;
@@ -792,7 +796,16 @@ void launch_update_p(const Hierarchy& H, const DevLevel& L, double* p, const dou
 
 void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, const double* p, cudaStream_t s) {
     ProfScope ps(H, kKVector, H.fine_ref, s);
-    k_update_xr<<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(x, H.r, p, H.q, L.n, L.ld, H.nz, H.scal, H.partials);
+    k_update_xr<false><<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(x, H.r, p, H.q, nullptr, L.n, L.ld, H.nz, H.scal,
+                                                                 H.partials);
+    ++H.launches;
+}
+
+void launch_update_xr_first(const Hierarchy& H, const DevLevel& L, double* x, const double* p, const double* b,
+                            cudaStream_t s) {
+    ProfScope ps(H, kKVector, H.fine_ref, s);
+    k_update_xr<true><<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal,
+                                                                H.partials);
     ++H.launches;
 }
 
