@@ -214,6 +214,11 @@ int64_t hmg_launch_count(const hmg_hierarchy* h);
  * 9 operator apply with the CG direction update p = z + beta p fused. */
 hmg_status hmg_profile_begin(hmg_hierarchy* h);
 hmg_status hmg_profile_end(hmg_hierarchy* h);
+/* Restrict recording to one kernel class on one level (-1: any); an event pair
+ * separates two kernels in the stream, so recording only the kernel being
+ * measured leaves the other launches free to overlap (programmatic dependent
+ * launch).  Persists until changed; hmg_profile_select(h, -1, -1) records all. */
+hmg_status hmg_profile_select(hmg_hierarchy* h, int kernel_class, int ref);
 hmg_status hmg_profile_query(const hmg_hierarchy* h, int kernel_class, int ref, int64_t* count, double* total_ms);
 
 /* Diagnostic: for device arrays a, b of length n, writes fast[i] = the

@@ -82,6 +82,7 @@ def load_library():
         "hmg_selftest_div": [P, P, P, P, I64, P],
         "hmg_profile_begin": [P],
         "hmg_profile_end": [P],
+        "hmg_profile_select": [P, I, I],
         "hmg_profile_query": [P, I, I, pI64, pD],
         "hmg_build_hierarchy_dist": [I, I, I, D, D, P, I, P, ctypes.POINTER(P)],
         "hmg_nccl_unique_id": [P],
@@ -290,6 +291,11 @@ class Hierarchy:
 
     def profile_begin(self):
         _check(load_library().hmg_profile_begin(self._h))
+
+    def profile_select(self, kernel_class: str | None = None, ref: int = -1):
+        """Record only one kernel class on one level (None: all)."""
+        cls = -1 if kernel_class is None else self.KERNEL_CLASSES[kernel_class]
+        _check(load_library().hmg_profile_select(self._h, cls, ref))
 
     def profile_end(self):
         _check(load_library().hmg_profile_end(self._h))

@@ -401,6 +401,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_SWEEP_ST")) H->use_st_sweep = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_OPERATOR")) H->matrix_free = std::string(e) == "free";
     if (const char* e = std::getenv("HMG_APPLY_ST")) H->use_st_apply = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_PDL")) H->use_pdl = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at
@@ -963,6 +964,15 @@ hmg_status hmg_profile_begin(hmg_hierarchy* h) {
     P.used = 0;
     P.cls.clear();
     P.ref.clear();
+    return HMG_OK;
+}
+
+hmg_status hmg_profile_select(hmg_hierarchy* h, int kernel_class, int ref) {
+    HMG_TRY(check_h(h));
+    if (kernel_class >= kKNumClasses) return fail(HMG_ERR_INVALID_ARG, "kernel_class: unknown");
+    Profiler& P = HH(h).prof;
+    P.only_cls = kernel_class < 0 ? -1 : kernel_class;
+    P.only_ref = ref < 0 ? -1 : ref;
     return HMG_OK;
 }
 

@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
     uint64_t* empty = full + S;
     double* stages = reinterpret_cast<double*>(smraw + 1024);
+    ptx::pdl_trigger();
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -80,6 +81,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         ptx::fence_mbar_init();
     }
     __syncthreads();
+    ptx::pdl_wait();
     double dot = 0.0;
     int s = 0;
     uint32_t phase = 0;
@@ -215,7 +217,8 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
     const unsigned cap = (unsigned)(2 * sms);
     const unsigned grid = ntiles < cap ? ntiles : cap;
-    k_apply_st<DOT, PUPD, G><<<grid, kThreads, smem, s>>>(maps, V, L.halo, x, z, y, pnew, H.partials, H.scal, S);
+    launch_pdl(H, k_apply_st<DOT, PUPD, G>, dim3(grid), dim3(kThreads), smem, s, maps, V, L.halo, x, z, y, pnew,
+               H.partials, H.scal, S);
     return (int)grid;
 }
 

@@ -4,6 +4,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/hmg.h"
@@ -127,6 +128,7 @@ enum KernelClass { kKApply = 0, kKSweepZero, kKSweep, kKSweepProlong, kKResidRes
                    kKVector, kKCoarseTail, kKApplyP, kKNumClasses };
 struct Profiler {
     bool on = false;
+    int only_cls = -1, only_ref = -1;   // hmg_profile_select: record only this class / level (-1: all)
     std::vector<cudaEvent_t> pool;   // pairs
     size_t used = 0;                 // events in use
     std::vector<int> cls, ref;       // per pair
@@ -161,6 +163,7 @@ struct Hierarchy {
     // distance in ring stages, HMG_TAIL_REF the one-launch coarse tail
     bool use_tc_sweep = true;
     bool use_st_sweep = true;
+    bool use_pdl = true;        // HMG_PDL=0: plain stream-ordered launches instead of programmatic dependent launch
     bool use_st_apply = true;   // HMG_APPLY_ST=0: thread-per-column k_apply_t instead of k_apply_st
     bool matrix_free = false;   // operator applies recompute the couplings from lam + geometry (NEXT-2)   // HMG_SWEEP_ST=0: non-zero-guess sweeps by k_sweep_tc instead of k_sweep_st
     bool use_small_sweep = true;
@@ -231,6 +234,26 @@ void launch_sweep_small(const Hierarchy& H, const DevLevel& L, const double* b, 
 const char* take_launch_error();
 bool tensor_maps_available();
 void launch_selftest_div(int64_t n, const double* a, const double* b, double* fast, double* ref, cudaStream_t s);
+
+// Stream-ordered launch with programmatic dependent launch (PDL) allowed: the
+// kernel may begin (prologue, SM placement) while its predecessor finishes;
+// every kernel launched this way calls ptx::pdl_wait() before touching data a
+// predecessor produced or consumes.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(const Hierarchy& H, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = H.use_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // RAII event pair around one launch when profiling is on.
 struct ProfScope {

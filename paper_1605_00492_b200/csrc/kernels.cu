@@ -569,6 +569,7 @@ void set_smem_attr() {
 ProfScope::ProfScope(const Hierarchy& h, int cls, int ref, cudaStream_t st) : H(h), s(st) {
     Profiler& P = H.prof;
     if (!P.on) return;
+    if ((P.only_cls >= 0 && cls != P.only_cls) || (P.only_ref >= 0 && ref != P.only_ref)) return;
     if (P.used + 2 > P.pool.size()) {
         for (int i = 0; i < 256; ++i) {
             cudaEvent_t e;

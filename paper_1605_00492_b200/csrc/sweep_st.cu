@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mid + S);
     double* stages = reinterpret_cast<double*>(smraw + 1024);
 
+    ptx::pdl_trigger();                                // the next kernel may start its prologue
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    ptx::pdl_wait();                                   // the predecessor's results (b, u, u_c) are complete
 
     if (MF && warp > kConsumerWarps) {
         // ============ matrix-free warps: the couplings of each forward stage ============
@@ -553,8 +555,8 @@ void launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const dou
     const unsigned cap = (unsigned)((two ? 2 : 1) * sms);
     const unsigned rounds = (ntiles + cap - 1) / cap;
     const unsigned grid = (ntiles + rounds - 1) / rounds;
-    k_sweep_st<Z, P, M, G, CK><<<grid, M ? kThreadsMf : kThreads, smem, s>>>(
-        maps, V, op, L.halo, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
+    launch_pdl(H, k_sweep_st<Z, P, M, G, CK>, dim3(grid), dim3(M ? kThreadsMf : kThreads), smem, s, maps, V, op,
+               L.halo, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
 }
 
 }  // namespace

@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int row_block = G * kTile;                                  // doubles per array per stage
 
     TSTAMP(0);
+    ptx::pdl_trigger();
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -123,6 +124,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    ptx::pdl_wait();
     TSTAMP(1);
 
     if (warp == kConsumerWarps) {
@@ -530,8 +532,8 @@ void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const dou
     unsigned cap = Z ? (unsigned)((cols <= 256 && grid > (unsigned)sms) ? 2 * sms : sms) : grid;
     if (const char* e = std::getenv("HMG_TC_PERSIST"))
         if (std::string(e) == "0") cap = grid;
-    k_sweep_tc<Z, P, F, G><<<grid < cap ? grid : cap, kThreads, smem, s>>>(maps, V, L.halo, b, uin, uc, ldc, L.fden, L.fg, uout, omega,
-                                                        L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
+    launch_pdl(H, k_sweep_tc<Z, P, F, G>, dim3(grid < cap ? grid : cap), dim3(kThreads), smem, s, maps, V, L.halo, b,
+               uin, uc, ldc, L.fden, L.fg, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
 }
 
 }  // namespace
