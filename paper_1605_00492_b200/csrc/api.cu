@@ -199,7 +199,16 @@ const double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b,
     for (int i = 0; i < count; ++i) {
         double* dst = (i == count - 1 && out) ? out : (cur == L.wa ? L.wb : L.wa);
         if (cur) halo_exchange(H, L, cur, s);      // neighbours' old values (Jacobi)
-        launch_sweep(H, L, b, cur, i == 0 ? uc : nullptr, dst, omega, s);
+        const bool last_into_out = i == count - 1 && out;
+        if (last_into_out && H.rz_req && L.ref == H.fine_ref && cur && !(i == 0 && uc) && !L.fden && !L.dist.on &&
+            !H.matrix_free && H.use_tc_sweep && sweep_st_supported(H, L)) {
+            // the preconditioner's last sweep: <r, z> = <b, u'> accumulated on the fly
+            ProfScope ps(H, kKSweep, L.ref, s);
+            H.rz_parts = launch_sweep_st_dot(H, L, b, cur, dst, omega, s);
+            H.rz_req = false;
+        } else {
+            launch_sweep(H, L, b, cur, i == 0 ? uc : nullptr, dst, omega, s);
+        }
         cur = dst;
     }
     return cur;
@@ -290,9 +299,22 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         if (!F.dist.on) HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
         return HMG_OK;
     }
-    precond(r0, H.z);
-    launch_dot(H, F, r0, H.z, s);
-    launch_finalize(H, kFinRhoInit, s);
+    // <r, z> after each preconditioner application: fused into its last sweep
+    // when that is a streamed fine-level sweep (a fixed-order per-CTA sum, like
+    // the separate dot kernel's -- PCG parity is the iteration count)
+    auto precond_dot = [&](const double* r, double* z, int op) {
+        H.rz_req = H.fuse_rz;
+        H.rz_parts = 0;
+        precond(r, z);
+        H.rz_req = false;
+        if (H.rz_parts > 0) {
+            finalize_parts(H, H.rz_parts, op, s);
+        } else {
+            launch_dot(H, F, r, z, s);
+            launch_finalize(H, op, s);
+        }
+    };
+    precond_dot(r0, H.z, kFinRhoInit);
     // Single GPU: z, p_old and p_new rotate through {z, p, p2} so that p_1 = z_1
     // needs no copy; the first x/r update reads b and writes x = 0 + alpha p,
     // r = b - alpha q (the same arithmetic as from x = 0, r = b).
@@ -328,9 +350,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         *relres = rn / bn;
         if (rn <= rtol * bn) return HMG_OK;
         if (!F.dist.on) zb = (pc != H.z) ? H.z : H.p;   // a buffer that is not p
-        precond(H.r, zb);
-        launch_dot(H, F, H.r, zb, s);
-        launch_finalize(H, kFinRZ, s);             // beta = rho' / rho, rho = rho' (p updated in the next apply)
+        precond_dot(H.r, zb, kFinRZ);              // beta = rho' / rho, rho = rho' (p updated in the next apply)
     }
     return fail(HMG_ERR_NOT_CONVERGED, "not converged after " + std::to_string(maxit) +
                                            " iterations (relres " + std::to_string(*relres) + ")");
@@ -402,6 +422,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_OPERATOR")) H->matrix_free = std::string(e) == "free";
     if (const char* e = std::getenv("HMG_APPLY_ST")) H->use_st_apply = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_PDL")) H->use_pdl = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_FUSE_RZ")) H->fuse_rz = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at

@@ -156,6 +156,12 @@ struct Hierarchy {
     bool force_coll = false;   // HMG_FORCE_COLLECTIVES=1: run the collectives even with one rank (tests)
     double *gbuf_send = nullptr, *gbuf_recv = nullptr;   // coarse-gather staging
     mutable int64_t launches = 0;
+    // PCG: <r, z> fused into the preconditioner's last fine-level sweep (which
+    // writes z and streams r as its right-hand side): pcg_impl sets rz_req, the
+    // sweep launch that takes it writes per-CTA partial sums and sets rz_parts
+    mutable bool rz_req = false;
+    mutable int rz_parts = 0;
+    bool fuse_rz = true;        // HMG_FUSE_RZ=0: separate dot kernel
     mutable Profiler prof;
     // diagnostics switches (environment, read at build time): HMG_SWEEP=simple
     // selects the reference-layout sweep kernel, HMG_SMALL=0 disables the
@@ -206,6 +212,10 @@ void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, con
 bool sweep_st_supported(const Hierarchy& H, const DevLevel& L);
 void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                      double* uout, double omega, cudaStream_t s);
+// the same general sweep (non-zero iterate, no prolongation, stored bands) also
+// accumulating <b, u'> per CTA into H.partials; returns the number of partials
+int launch_sweep_st_dot(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, double* uout,
+                        double omega, cudaStream_t s);
 
 // apply_st.cu: TMA-streamed persistent operator apply (same arithmetic as k_apply_t);
 // the dot forms return the number of per-CTA partial sums written to H.partials

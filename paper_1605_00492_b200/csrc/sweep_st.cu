@@ -60,6 +60,7 @@ struct StMaps {
     CUtensorMap ub;     // box kTile x 8: backward u rows
     CUtensorMap ucf;    // box kTile/4 x (G + 1)   (PROLONG)
     CUtensorMap ucb;    // box kTile/4 x 8         (PROLONG)
+    CUtensorMap bb;     // box kTile x 8: backward b rows (DOT)
 };
 
 // Doubles of one ring stage and the offsets of its parts.  Forward stage:
@@ -69,7 +70,7 @@ struct StMaps {
 struct StLayout {
     int op, band, b, u, uc, hu, huc, hlam, fwd, bwd, stage;
 };
-__host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool mf, int G) {
+__host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool mf, int G, bool dot = false) {
     StLayout L{};
     L.op = 0;                                        // band rows (stored), or lam rows (matrix-free)
     L.band = mf ? (G + 1) * kTile : 0;               // band rows as the consumers read them
@@ -80,7 +81,7 @@ __host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool m
     L.huc = L.hu + (zero ? 0 : G * kHaloMax);
     L.hlam = L.huc + (prolong ? G * kHaloMax : 0);
     L.fwd = L.hlam + (mf ? G * kHaloMax : 0);
-    L.bwd = zero ? 0 : kBack * kTile + (prolong ? kBack * (kTile / 4) : 0);
+    L.bwd = zero ? 0 : kBack * kTile + (prolong ? kBack * (kTile / 4) : 0) + (dot ? kBack * kTile : 0);
     L.stage = L.fwd > L.bwd ? L.fwd : L.bwd;
     return L;
 }
@@ -93,13 +94,16 @@ struct StOp {
     double w2, dz;
 };
 
-template <bool ZERO, bool PROLONG, bool MF, int G, bool CHK>
+template <bool ZERO, bool PROLONG, bool MF, int G, bool CHK, bool DOT = false>
 __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
     k_sweep_st(const __grid_constant__ StMaps maps, LevelView L, StOp op, TileHalo th, const double* __restrict__ bvec,
                const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc, double* __restrict__ uout,
-               double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols, int pf_groups) {
+               double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols, int pf_groups,
+               double* __restrict__ partial) {
     extern __shared__ __align__(1024) unsigned char smraw[];
-    constexpr StLayout SL = st_layout(ZERO, PROLONG, MF, G);
+    __shared__ double dred[kThreads / 32];
+    constexpr StLayout SL = st_layout(ZERO, PROLONG, MF, G, DOT);
+    double dotacc = 0.0;                               // DOT: this thread's sum of b_k u'_k
     constexpr bool HALO = !ZERO || MF;       // off-tile neighbour values needed
     const int nz = L.nz;
     const int64_t ld = L.ld;
@@ -206,7 +210,8 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
         const uint32_t fwd_bytes =
             (uint32_t)(sizeof(double) * (op_rows + G * kTile + (ZERO ? 0 : (G + 1) * kTile) +
                                          (PROLONG ? (G + 1) * (kTile / 4) : 0)));
-        const uint32_t bwd_bytes = (uint32_t)(sizeof(double) * (kBack * kTile + (PROLONG ? kBack * (kTile / 4) : 0)));
+        const uint32_t bwd_bytes = (uint32_t)(sizeof(double) * (kBack * kTile + (PROLONG ? kBack * (kTile / 4) : 0) +
+                                                                (DOT ? kBack * kTile : 0)));
         int s = 0;
         uint32_t phase = 0;
         auto advance = [&]() {
@@ -262,7 +267,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         ptx::tma_load_2d_hint(st + SL.op, &maps.lam, x, gi * G, &full[s], pol_stream);
                     else
                         ptx::tma_load_3d_hint(st + SL.op, &maps.bands, x, gi * G, 0, &full[s], pol_stream);
-                    ptx::tma_load_2d_hint(st + SL.b, &maps.b, x, gi * G, &full[s], pol_stream);
+                    ptx::tma_load_2d_hint(st + SL.b, &maps.b, x, gi * G, &full[s], DOT ? pol_keep : pol_stream);
                     if (!ZERO) ptx::tma_load_2d_hint(st + SL.u, &maps.uf, x, gi * G, &full[s], pol_keep);
                     if (PROLONG) ptx::tma_load_2d_hint(st + SL.uc, &maps.ucf, xc, gi * G, &full[s], pol_keep);
                 }
@@ -274,6 +279,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     ptx::mbar_arrive_expect_tx(&full[s], bwd_bytes);
                     ptx::tma_load_2d_hint(st, &maps.ub, x, m * kBack, &full[s], pol_stream);
                     if (PROLONG) ptx::tma_load_2d_hint(st + kBack * kTile, &maps.ucb, xc, m * kBack, &full[s], pol_stream);
+                    if (DOT) ptx::tma_load_2d_hint(st + kBack * kTile, &maps.bb, x, m * kBack, &full[s], pol_stream);
                 }
             }
         }
@@ -487,7 +493,10 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         if (PROLONG) uo = uo + su[kBack * kTile + i * (kTile / 4) + (j >> 2)];
                         o = uo + omega * dl;
                     }
-                    if (valid) uout[(int64_t)k * ld + c] = o;
+                    if (valid) {
+                        uout[(int64_t)k * ld + c] = o;
+                        if (DOT) dotacc = dotacc + su[kBack * kTile + i * kTile + j] * o;
+                    }
                 }
                 if (!ZERO) {
                     __syncwarp();
@@ -497,8 +506,17 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
             }
         }
     }
+    if (DOT) {   // fixed-order CTA reduction of <b, u'> (producer / coupling warps contribute 0)
+        for (int off = 16; off > 0; off >>= 1) dotacc = dotacc + __shfl_down_sync(0xffffffffu, dotacc, off);
+        if (lane == 0 && warp < kThreads / 32) dred[warp] = dotacc;
+    }
     ptx::tc_fence_before();
     __syncthreads();
+    if (DOT && threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kThreads / 32; ++w) t = t + dred[w];
+        partial[blockIdx.x] = t;
+    }
     if (warp == 0) ptx::tmem_dealloc(tbase, tmem_cols);
 }
 
@@ -508,12 +526,12 @@ uint32_t st_tmem_cols(int nz) {
     return c;
 }
 
-template <bool Z, bool P, bool M, int G, bool CK = true>
-void launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
-               double* uout, double omega, cudaStream_t s) {
+template <bool Z, bool P, bool M, int G, bool CK = true, bool DOT = false>
+int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
+              double* uout, double omega, cudaStream_t s) {
     const int nz = H.nz;
     const uint32_t cols = st_tmem_cols(nz);
-    constexpr StLayout SL = st_layout(Z, P, M, G);
+    constexpr StLayout SL = st_layout(Z, P, M, G, DOT);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
     const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
@@ -526,7 +544,7 @@ void launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const dou
     if (smem < floor_smem) smem = floor_smem;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_sweep_st<Z, P, M, G, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_sweep_st<Z, P, M, G, CK, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
         attr = true;
     }
     StMaps maps;
@@ -548,6 +566,7 @@ void launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const dou
         maps.ucf = make_tensor_map(uc, C.ld, nz, kTile / 4, G + 1, 1);
         maps.ucb = make_tensor_map(uc, C.ld, nz, kTile / 4, kBack, 1);
     }
+    if (DOT) maps.bb = make_tensor_map(b, L.ld, nz, kTile, kBack, 1);
     const StOp op{L.lam, L.geom, H.w2, H.dz};
     // persistent grid: as many rounds of tiles as the resident CTAs need, with the
     // tiles dealt evenly (ref 6: 640 tiles -> 214 CTAs x 3 instead of 296 CTAs
@@ -555,14 +574,27 @@ void launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const dou
     const unsigned cap = (unsigned)((two ? 2 : 1) * sms);
     const unsigned rounds = (ntiles + cap - 1) / cap;
     const unsigned grid = (ntiles + rounds - 1) / rounds;
-    launch_pdl(H, k_sweep_st<Z, P, M, G, CK>, dim3(grid), dim3(M ? kThreadsMf : kThreads), smem, s, maps, V, op,
-               L.halo, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
+    launch_pdl(H, k_sweep_st<Z, P, M, G, CK, DOT>, dim3(grid), dim3(M ? kThreadsMf : kThreads), smem, s, maps, V, op,
+               L.halo, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups, H.partials);
+    return (int)grid;
 }
 
 }  // namespace
 
 bool sweep_st_supported(const Hierarchy& H, const DevLevel& L) {
     return H.use_st_sweep && H.nz <= 128 && L.halo.loc != nullptr;
+}
+
+int launch_sweep_st_dot(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, double* uout,
+                        double omega, cudaStream_t s) {
+    int n = 0;
+    try {
+        n = launch_st<false, false, false, 2, true, true>(H, L, b, uin, nullptr, uout, omega, s);
+    } catch (const std::exception& e) {
+        g_launch_error = std::string("sweep launch: ") + e.what();
+    }
+    ++H.launches;
+    return n;
 }
 
 void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
