@@ -173,7 +173,7 @@ struct Hierarchy {
     bool use_st_apply = true;   // HMG_APPLY_ST=0: thread-per-column k_apply_t instead of k_apply_st
     bool matrix_free = false;   // operator applies recompute the couplings from lam + geometry (NEXT-2)   // HMG_SWEEP_ST=0: non-zero-guess sweeps by k_sweep_tc instead of k_sweep_st
     bool use_small_sweep = true;
-    int l2_prefetch_groups = 3;
+    int l2_prefetch_groups = 0;   // measured: the ring alone is as fast at ref 7 and faster at ref 6
 };
 
 // kernels.cu
