@@ -218,6 +218,25 @@ def test_full_size_c2(name):
     o.close()
 
 
+@pytest.mark.slow
+def test_full_size_c4():
+    """BASELINE.json config C4 whole on one GPU (ref 8 x 128 = 167.8M dofs, the
+    8-GPU weak-scaling problem; 128 layers: one sweep CTA per SM, no cooperative
+    tail): the operator apply and the V-cycle bitwise equal to the oracle."""
+    cfg = hi.CONFIGS["C4"]
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    o = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    r = cfg.fine_ref
+    bd = g.to_device(r, b)
+    assert np.array_equal(g.to_host(r, g.apply_helmholtz(r, bd)), o.apply(r, b))
+    z = g.to_host(r, g.vcycle(bd))
+    zo = o.vcycle(b)
+    assert rel(z, zo) <= 1e-10 and np.array_equal(z, zo)
+    g.close()
+    o.close()
+
+
 def test_shared_reciprocal_division_is_bitwise_ieee():
     """The sweep's shared-reciprocal division equals the compiler's a / b bit
     for bit: 2^24 random pairs over a wide exponent range plus special values."""
