@@ -423,6 +423,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_APPLY_ST")) H->use_st_apply = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_PDL")) H->use_pdl = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_FUSE_RZ")) H->fuse_rz = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_FACT_MAX")) H->fact_max_cells = std::atoll(e);
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at
@@ -705,7 +706,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     // for every level too small to fill the GPU (latency-bound sweeps)
     for (int r = coarsest_ref; r <= fine_ref; ++r) {
         DevLevel& L = H->lev[r];
-        if (!(r <= H->tail_ref || r <= H->coop_ref || L.n <= kFactMaxCells)) continue;
+        if (!(r <= H->tail_ref || r <= H->coop_ref || L.n <= H->fact_max_cells)) continue;
         const size_t vb = sizeof(double) * nlayers * L.ld;
         BCUDA(cudaMalloc(&L.fden, 3 * vb));          // [3][nz][ld]: den, y, g (one TMA box)
         L.fy = L.fden + (size_t)nlayers * L.ld;

@@ -162,6 +162,7 @@ struct Hierarchy {
     mutable bool rz_req = false;
     mutable int rz_parts = 0;
     bool fuse_rz = true;        // HMG_FUSE_RZ=0: separate dot kernel
+    int64_t fact_max_cells = kFactMaxCells;   // levels up to this size carry precomputed Thomas factors
     mutable Profiler prof;
     // diagnostics switches (environment, read at build time): HMG_SWEEP=simple
     // selects the reference-layout sweep kernel, HMG_SMALL=0 disables the

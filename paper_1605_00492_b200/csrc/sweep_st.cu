@@ -31,6 +31,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "hmg_internal.h"
 #include "sm100_ptx.cuh"
@@ -49,6 +50,10 @@ constexpr int kThreads = kTile + 32;       // + one producer warp
 constexpr int kMfWarps = kTile / 32;       // matrix-free: warps forming the couplings of each stage
 constexpr int kThreadsMf = kThreads + 32 * kMfWarps;
 constexpr int kBack = 8;                   // layers per backward stage
+
+#ifdef HMG_TIMING
+__device__ long long g_st_timing[8];   // CTA 0, thread 0: [0] total, [1] forward wait, [2] backward wait, [3] tiles
+#endif
 
 __device__ __forceinline__ bool pivot_ok(double den) { return den > 0.0 && den <= DBL_MAX; }
 
@@ -104,6 +109,9 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
     __shared__ double dred[kThreads / 32];
     constexpr StLayout SL = st_layout(ZERO, PROLONG, MF, G, DOT);
     double dotacc = 0.0;                               // DOT: this thread's sum of b_k u'_k
+#ifdef HMG_TIMING
+    long long tt0 = 0, wf = 0, wb = 0, ntl = 0, tfw = 0, tbk = 0, tfw0 = 0, tws = 0;
+#endif
     constexpr bool HALO = !ZERO || MF;       // off-tile neighbour values needed
     const int nz = L.nz;
     const int64_t ld = L.ld;
@@ -297,7 +305,14 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 phase ^= 1u;
             }
         };
+#ifdef HMG_TIMING
+        tt0 = clock64();
+#endif
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+#ifdef HMG_TIMING
+            ++ntl;
+            tfw0 = clock64();
+#endif
             const int64_t c = (int64_t)tile * kTile + j;
             const bool valid = c < L.n;
             const int64_t cv = valid ? c : L.n - 1;
@@ -333,7 +348,13 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 gprev = g;
             };
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
+#ifdef HMG_TIMING
+                long long w0 = clock64();
+#endif
                 ptx::mbar_wait(MF ? &mid[s] : &full[s], phase);
+#ifdef HMG_TIMING
+                wf += clock64() - w0;
+#endif
                 const double* st = stages + (size_t)s * SL.stage;
                 const double* su = st + SL.u;
                 const double* suc = st + SL.uc;
@@ -351,19 +372,17 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     if (PROLONG) v = v + huc[kk * kHaloMax + l - kTile];
                     return v;
                 };
-                // u value (with the fused prolongation) of local slot l at stage row kk#pragma unroll
-                for (int kk = 0; kk < G; ++kk) {
+                // One layer: residual row (reading R5 order) and Thomas step.  IN
+                // (interior: 0 < k < nz - 1) drops every boundary test.
+                auto step = [&](int kk, auto interior) {
+                    constexpr bool IN = decltype(interior)::value;
                     const int k = gi * G + kk;
-                    if (k >= nz) break;
-                    double Dk, Uk, H0, H1, H2;
-                    {
-                        const double* sr = st + SL.band + kk * kTile + j;
-                        Dk = sr[0];
-                        Uk = sr[G * kTile];
-                        H0 = sr[2 * G * kTile];
-                        H1 = sr[3 * G * kTile];
-                        H2 = sr[4 * G * kTile];
-                    }
+                    const double* sr = st + SL.band + kk * kTile + j;
+                    const double Dk = sr[0];
+                    const double Uk = sr[G * kTile];
+                    const double H0 = sr[2 * G * kTile];
+                    const double H1 = sr[3 * G * kTile];
+                    const double H2 = sr[4 * G * kTile];
                     const double bk = st[SL.b + kk * kTile + j];
                     double r;
                     if (ZERO) {
@@ -371,22 +390,49 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     } else {
                         const double uk = UV(kk, j);
                         double up = 0.0;
-                        if (k < nz - 1) up = UV(kk + 1, j);
+                        if (IN || k < nz - 1) up = UV(kk + 1, j);
                         double acc = Dk * uk;
-                        if (k > 0) acc = acc + Um * um;
-                        if (k < nz - 1) acc = acc + Uk * up;
+                        if (IN || k > 0) acc = acc + Um * um;
+                        if (IN || k < nz - 1) acc = acc + Uk * up;
                         acc = acc + H0 * NBR(kk, l0);
                         acc = acc + H1 * NBR(kk, l1);
                         acc = acc + H2 * NBR(kk, l2);
                         r = bk - acc;
                         um = uk;
                     }
-                    layer(k, Dk, Uk, r, false);
+                    if (IN) {
+                        const double num = r - Um * zprev;
+                        const double den = Dk - Um * gprev;
+                        const double y = div_recip(den);
+                        const double z = div_fast_z(num, den, y, slow);
+                        const double g = div_fast(Uk, den, y, slow);
+                        ok = ok && pivot_ok(den);
+                        ptx::tmem_st_f64(tl + 2u * (uint32_t)k, z);
+                        ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, g);
+                        zprev = z;
+                        gprev = g;
+                    } else {
+                        layer(k, Dk, Uk, r, false);
+                    }
                     Um = Uk;
+                };
+                if (gi > 0 && (gi + 1) * G < nz) {     // interior stage: no layer touches a boundary
+#pragma unroll
+                    for (int kk = 0; kk < G; ++kk) step(kk, std::true_type{});
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < G; ++kk) {
+                        if (gi * G + kk >= nz) break;
+                        step(kk, std::false_type{});
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&empty[s]);
             }
+#ifdef HMG_TIMING
+            tfw += clock64() - tfw0;
+            tfw0 = clock64();
+#endif
             // Rare: a quotient left the fast path's exact range.  The warp redoes
             // its columns' forward pass from global memory with '/'.
             if (__any_sync(0xffffffffu, slow && valid)) {
@@ -445,14 +491,21 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
             }
             if (valid && !ok) atomicMin(bad, ((unsigned long long)ref << 40) | (unsigned long long)c);
             ptx::tmem_wait_st();
+#ifdef HMG_TIMING
+            tws += clock64() - tfw0;
+#endif
 
             // back substitution from the top: delta_{nz-1} = z_{nz-1},
             // delta_k = z_k - g_k delta_{k+1}; u' = u_old + omega delta (zero guess: omega delta)
+            // The (z, g) of the next chunk down are loaded from TMEM while the
+            // current chunk is computed (tcgen05.ld is asynchronous; only the top
+            // chunk, possibly partial, is loaded synchronously).
             double dl = 0.0;
-            for (int m = (nz + kBack - 1) / kBack - 1; m >= 0; --m) {
-                const int k0 = m * kBack;
-                const int kt = (k0 + kBack - 1 < nz - 1) ? k0 + kBack - 1 : nz - 1;   // top layer of the chunk
-                uint32_t zr[16], gr[16];
+            const int mtop = (nz + kBack - 1) / kBack - 1;
+            uint32_t zr[16], gr[16], zn[16], gn[16];
+            {
+                const int k0 = mtop * kBack;
+                const int kt = nz - 1;
                 if (kt - k0 == kBack - 1) {
                     ptx::tmem_ld_8f64(tl + 2u * (uint32_t)k0, zr);
                     ptx::tmem_ld_8f64(tl + gcol + 2u * (uint32_t)k0, gr);
@@ -471,20 +524,29 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     }
                 }
                 ptx::tmem_wait_ld();
+            }
+            double* const uo_row = uout + c;               // column c of row 0 (rows at stride ld)
+            for (int m = mtop; m >= 0; --m) {
+                const int k0 = m * kBack;
+                const int kt = (k0 + kBack - 1 < nz - 1) ? k0 + kBack - 1 : nz - 1;   // top layer of the chunk
+                if (m > 0) {                               // chunks below the top are full
+                    ptx::tmem_ld_8f64(tl + 2u * (uint32_t)(k0 - kBack), zn);
+                    ptx::tmem_ld_8f64(tl + gcol + 2u * (uint32_t)(k0 - kBack), gn);
+                }
                 const double* su = nullptr;
                 if (!ZERO) {
+#ifdef HMG_TIMING
+                    long long w0 = clock64();
+#endif
                     ptx::mbar_wait(MF ? &mid[s] : &full[s], phase);
+#ifdef HMG_TIMING
+                    wb += clock64() - w0;
+#endif
                     su = stages + (size_t)s * SL.stage;
                 }
-#pragma unroll
-                for (int i = kBack - 1; i >= 0; --i) {
-                    const int k = k0 + i;
-                    if (k > kt) continue;
-                    const double zk = ptx::f64_from(zr[2 * i], zr[2 * i + 1]);
-                    if (k == nz - 1)
-                        dl = zk;
-                    else
-                        dl = zk - ptx::f64_from(gr[2 * i], gr[2 * i + 1]) * dl;
+                // the chunk's results: delta chain first (branch-free below the top
+                // chunk), then u' = u_old + omega delta, the store and the fused dot
+                auto finish = [&](int i, int k) {
                     double o;
                     if (ZERO) {
                         o = omega * dl;
@@ -494,8 +556,27 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         o = uo + omega * dl;
                     }
                     if (valid) {
-                        uout[(int64_t)k * ld + c] = o;
+                        uo_row[(int64_t)k * ld] = o;
                         if (DOT) dotacc = dotacc + su[kBack * kTile + i * kTile + j] * o;
+                    }
+                };
+                if (m < mtop) {                            // full chunk, every layer below nz - 1
+#pragma unroll
+                    for (int i = kBack - 1; i >= 0; --i) {
+                        dl = ptx::f64_from(zr[2 * i], zr[2 * i + 1]) - ptx::f64_from(gr[2 * i], gr[2 * i + 1]) * dl;
+                        finish(i, k0 + i);
+                    }
+                } else {
+#pragma unroll
+                    for (int i = kBack - 1; i >= 0; --i) {
+                        const int k = k0 + i;
+                        if (k > kt) continue;
+                        const double zk = ptx::f64_from(zr[2 * i], zr[2 * i + 1]);
+                        if (k == nz - 1)
+                            dl = zk;
+                        else
+                            dl = zk - ptx::f64_from(gr[2 * i], gr[2 * i + 1]) * dl;
+                        finish(i, k);
                     }
                 }
                 if (!ZERO) {
@@ -503,9 +584,31 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     if (lane == 0) ptx::mbar_arrive(&empty[s]);
                     advance();
                 }
+                if (m > 0) {
+                    ptx::tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        zr[i] = zn[i];
+                        gr[i] = gn[i];
+                    }
+                }
             }
+#ifdef HMG_TIMING
+            tbk += clock64() - tfw0;
+#endif
         }
     }
+#ifdef HMG_TIMING
+    if (warp < kConsumerWarps && blockIdx.x == 0 && threadIdx.x == 0) {
+        g_st_timing[0] = clock64() - tt0;
+        g_st_timing[1] = wf;
+        g_st_timing[2] = wb;
+        g_st_timing[3] = ntl;
+        g_st_timing[4] = tfw;
+        g_st_timing[5] = tbk;
+        g_st_timing[6] = tws;
+    }
+#endif
     if (DOT) {   // fixed-order CTA reduction of <b, u'> (producer / coupling warps contribute 0)
         for (int off = 16; off > 0; off >>= 1) dotacc = dotacc + __shfl_down_sync(0xffffffffu, dotacc, off);
         if (lane == 0 && warp < kThreads / 32) dred[warp] = dotacc;
@@ -578,6 +681,12 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
                L.halo, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups, H.partials);
     return (int)grid;
 }
+
+#ifdef HMG_TIMING
+}  // namespace
+extern "C" void hmg_debug_st_timing(long long* out) { cudaMemcpyFromSymbol(out, g_st_timing, sizeof(long long) * 8); }
+namespace {
+#endif
 
 }  // namespace
 

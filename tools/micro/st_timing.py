@@ -1,0 +1,32 @@
+"""Where a streamed sweep CTA spends its time (CTA 0, consumer thread 0), from a
+-DHMG_TIMING build: total cycles, cycles waiting for forward / backward stages."""
+import ctypes, os, subprocess, sys
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+import paper_1605_00492_b200.binding as B
+from paper_1605_00492_b200 import build as pb
+lib = os.path.join(HERE, "libhmg_timing.so")
+cmd = [pb.NVCC, *pb.ARCH, *[f for f in pb.FLAGS if f not in ("-Xptxas", "-v")], "-DHMG_TIMING", "-shared",
+       *[os.path.join(pb.CSRC, s) for s in pb.SOURCES], "-o", lib, "-ldl"]
+subprocess.check_call(cmd)
+B._LIB_PATH = lib
+import torch
+import hmg_inputs as hi
+from paper_1605_00492_b200 import Hierarchy
+for ref in (7, 6, 5):
+    cfg = hi.Config("t", ref, ref - 1 if ref > 5 else 4, 64, 0.001, 1e-5)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(ref, cfg.coarsest_ref, 64, 0.001, 1e-5, lam)
+    bd = g.to_device(ref, b)
+    u = g.to_device(ref, hi.uniform_vector(b.shape, 3))
+    om = float(os.environ.get("OMEGA", "0.8"))
+    for _ in range(3):
+        g.line_smooth(ref, bd, u, 1, om, False)
+    torch.cuda.synchronize()
+    t = (ctypes.c_longlong * 8)()
+    B.load_library().hmg_debug_st_timing(t)
+    tot, wf, wb, nt, tf, tb, tws = t[0], t[1], t[2], t[3], t[4], t[5], t[6]
+    print(f"ref {ref}: tiles/CTA {nt}, total {tot} cyc = {tot/1965:.1f} us, per tile {tot/max(nt,1)/1965:.1f} us; "
+          f"waiting fwd {wf/tot:.0%} bwd {wb/tot:.0%}; forward phase {tf/max(nt,1)/64:.0f} cyc/layer "
+          f"(of which waiting {wf/max(nt,1)/64:.0f}), back phase incl. redo check {tb/max(nt,1)/64:.0f} cyc/layer, of which slow check + TMEM store wait {tws/max(nt,1)/64:.0f}")
+    g.close()
