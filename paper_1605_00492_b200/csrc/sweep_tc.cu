@@ -279,6 +279,31 @@ __global__ void __launch_bounds__(kThreads, 2)
 #endif
             if (gi == 0) TSTAMP(2);
             const double* st = stages + (size_t)s * lay.stage_doubles;
+            if (ZERO && !FACT && gi > 0 && (gi + 1) * G < nz) {
+                // interior stage of the zero-guess form: 0 < k < nz - 1 for every
+                // layer, so the Thomas step runs without boundary tests
+#pragma unroll
+                for (int kk = 0; kk < G; ++kk) {
+                    const int k = gi * G + kk;
+                    const double* sr = st + kk * kTile + j;
+                    const double Dk = sr[0];
+                    const double Uk = sr[row_block];
+                    const double num = sr[2 * row_block] - Um * zprev;
+                    const double den = Dk - Um * gprev;
+                    const double y = div_recip(den);
+                    const double z = div_fast_z(num, den, y, slow);
+                    const double g = div_fast(Uk, den, y, slow);
+                    ok = ok && pivot_ok(den);
+                    ptx::tmem_st_f64(tl + 2u * (uint32_t)k, z);
+                    ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, g);
+                    zprev = z;
+                    gprev = g;
+                    Um = Uk;
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&empty[s]);
+                continue;
+            }
 #pragma unroll
             for (int kk = 0; kk < G; ++kk) {
                 const int k = gi * G + kk;
@@ -369,16 +394,26 @@ __global__ void __launch_bounds__(kThreads, 2)
                 ptx::tmem_ld_8f64(tl + 2u * (uint32_t)k0, zr);
                 ptx::tmem_ld_8f64(tl + gcol + 2u * (uint32_t)k0, gr);
                 ptx::tmem_wait_ld();
+                if (k0 + 7 < nz - 1) {                  // below the top layer: no boundary test
 #pragma unroll
-                for (int i = 7; i >= 0; --i) {
-                    const int kk = k0 + i;
-                    const double zk = ptx::f64_from(zr[2 * i], zr[2 * i + 1]);
-                    if (kk == nz - 1)
-                        dl = zk;
-                    else
-                        dl = zk - ptx::f64_from(gr[2 * i], gr[2 * i + 1]) * dl;
-                    const double o = ZERO ? omega * dl : UV(kk, j) + omega * dl;
-                    if (valid) uout[(int64_t)kk * ld + c] = o;
+                    for (int i = 7; i >= 0; --i) {
+                        const int kk = k0 + i;
+                        dl = ptx::f64_from(zr[2 * i], zr[2 * i + 1]) - ptx::f64_from(gr[2 * i], gr[2 * i + 1]) * dl;
+                        const double o = ZERO ? omega * dl : UV(kk, j) + omega * dl;
+                        if (valid) uout[(int64_t)kk * ld + c] = o;
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 7; i >= 0; --i) {
+                        const int kk = k0 + i;
+                        const double zk = ptx::f64_from(zr[2 * i], zr[2 * i + 1]);
+                        if (kk == nz - 1)
+                            dl = zk;
+                        else
+                            dl = zk - ptx::f64_from(gr[2 * i], gr[2 * i + 1]) * dl;
+                        const double o = ZERO ? omega * dl : UV(kk, j) + omega * dl;
+                        if (valid) uout[(int64_t)kk * ld + c] = o;
+                    }
                 }
             } else {
                 for (int kk = k; kk >= k0; --kk) {
