@@ -21,6 +21,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 
 #include "hmg_internal.h"
 #include "sm100_ptx.cuh"
@@ -150,19 +151,19 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (PUPD) return hz[kk * kHaloMax + l - kTile] + beta * hx[kk * kHaloMax + l - kTile];
                     return hx[kk * kHaloMax + l - kTile];
                 };
-#pragma unroll
-                for (int kk = 0; kk < G; ++kk) {
+                // one layer; IN (interior, 0 < k < nz - 1) drops the boundary tests
+                auto step = [&](int kk, auto interior) {
+                    constexpr bool IN = decltype(interior)::value;
                     const int k = gi * G + kk;
-                    if (k >= nz) break;
                     const double* sr = st + kk * kTile + j;
                     const double Dk = sr[0];
                     const double Uk = sr[G * kTile];
                     const double xk = XV(kk, j);
                     double xp = 0.0;
-                    if (k < nz - 1) xp = XV(kk + 1, j);
+                    if (IN || k < nz - 1) xp = XV(kk + 1, j);
                     double acc = Dk * xk;
-                    if (k > 0) acc = acc + Um * xm;
-                    if (k < nz - 1) acc = acc + Uk * xp;
+                    if (IN || k > 0) acc = acc + Um * xm;
+                    if (IN || k < nz - 1) acc = acc + Uk * xp;
                     acc = acc + sr[2 * G * kTile] * XV(kk, l0);
                     acc = acc + sr[3 * G * kTile] * XV(kk, l1);
                     acc = acc + sr[4 * G * kTile] * XV(kk, l2);
@@ -174,6 +175,16 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                     xm = xk;
                     Um = Uk;
+                };
+                if (gi > 0 && (gi + 1) * G < nz) {
+#pragma unroll
+                    for (int kk = 0; kk < G; ++kk) step(kk, std::true_type{});
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < G; ++kk) {
+                        if (gi * G + kk >= nz) break;
+                        step(kk, std::false_type{});
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&empty[s]);
