@@ -371,7 +371,7 @@ def run_hmg(args, ws, rank, local):
             "setup_s": setup_s,
             "roofline": {"kernel": "k_sweep_st (fused residual + Thomas line sweep, finest level)",
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(cfg.name, "k_sweep_st<0, 0, 0, 2, 1>"),
+                         "frac": achieved / peak, "traffic": ncu_traffic(cfg.name, "k_sweep_st<0, 0, 0, 2, 1, 0>"),
                          "algorithmic_bytes_per_launch": bytes_sw, "avg_launch_us": avg_sw * 1e3,
                          "launches_timed": n_sw, "peak_source": peak_note},
             "fine_level_kernels": fine,
