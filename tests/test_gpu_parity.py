@@ -388,3 +388,28 @@ def test_matrix_free_operator(monkeypatch, w2):
     assert np.array_equal(z, o.vcycle(b, 2, 2, 20, 0.8))
     g.close()
     o.close()
+
+
+@pytest.mark.parametrize("nz", [1, 2, 3, 7, 9, 65, 128, 130])
+def test_streamed_kernels_layer_counts(nz):
+    """The streamed persistent kernels (k_sweep_st, k_apply_st, k_sweep_tc zero
+    guess) on a level without precomputed pivots (ref 5: 20,480 cells) for layer
+    counts that leave partial stages and a partial top back-substitution chunk,
+    the 128-layer TMEM limit and the fallback beyond it: apply, sweeps, V-cycle
+    and the fused <r, z> PCG bitwise / iteration-count equal to the oracle."""
+    cfg = hi.Config("nz", 5, 3, nz, 0.001, 1e-5)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(5, 3, nz, 0.001, 1e-5, lam)
+    o = oracle.Hierarchy(5, 3, nz, 0.001, 1e-5, lam)
+    x = hi.uniform_vector(b.shape, 21)
+    assert np.array_equal(g.to_host(5, g.apply_helmholtz(5, g.to_device(5, x))), o.apply(5, x))
+    for zero in (True, False):
+        u = g.to_device(5, np.zeros_like(x) if zero else x)
+        g.line_smooth(5, g.to_device(5, b), u, 3, 0.8, zero)
+        assert np.array_equal(g.to_host(5, u), o.sweep(5, b, None if zero else x, 3, 0.8))
+    z = g.to_host(5, g.vcycle(g.to_device(5, b)))
+    assert np.array_equal(z, o.vcycle(b, 2, 2, 20, 0.8))
+    _, it, _, st = g.pcg_solve(g.to_device(5, b))
+    assert st == "HMG_OK" and it == o.pcg(b)[1]
+    g.close()
+    o.close()
