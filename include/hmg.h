@@ -80,7 +80,9 @@ typedef struct {
  *  device        CUDA device ordinal
  *  out           receives the hierarchy; *out = NULL on failure
  * Coarse coefficients are the 4-child means (reading R3); every level is
- * rediscretised, not Galerkin. */
+ * rediscretised, not Galerkin.  The Thomas pivots of every column
+ * of every level are checked here (they depend on the operator only): a
+ * non-positive or non-finite pivot -> HMG_ERR_SINGULAR_COLUMN "ref r column c". */
 hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, double thickness,
                                double w2, const double* lam_host, int device, hmg_hierarchy** out);
 
@@ -145,7 +147,9 @@ hmg_status hmg_apply_helmholtz(const hmg_hierarchy* h, int ref, const double* x,
  * and the first sweep is u = omega * T^{-1} b (its content is ignored).
  * b, u: device [nlayers][ld]; u is updated in place (ping-pong is internal).
  * A non-positive or non-finite pivot -> HMG_ERR_SINGULAR_COLUMN (this call
- * synchronises `stream` to report it). */
+ * synchronises `stream` to report it).  The pivots depend on the operator only
+ * and hmg_build_hierarchy checks every column of every level once, so a
+ * hierarchy that was built without error cannot produce this status here. */
 hmg_status hmg_line_smooth(const hmg_hierarchy* h, int ref, const double* b, double* u,
                            int nsweeps, double omega, int u_is_zero, void* stream);
 

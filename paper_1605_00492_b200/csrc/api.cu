@@ -424,6 +424,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_PDL")) H->use_pdl = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_FUSE_RZ")) H->fuse_rz = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_FACT_MAX")) H->fact_max_cells = std::atoll(e);
+    if (const char* e = std::getenv("HMG_CHECK_SKIP")) H->check_skip = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at
@@ -712,6 +713,19 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
         L.fy = L.fden + (size_t)nlayers * L.ld;
         L.fg = L.fy + (size_t)nlayers * L.ld;
         launch_factor(*H, L, s);
+    }
+    {
+        // every other level: pivots checked once, g_k fast-path exactness recorded
+        unsigned int* gslow = nullptr;
+        BCUDA(cudaMalloc(&gslow, sizeof(unsigned int) * (fine_ref + 1)));
+        BCUDA(cudaMemset(gslow, 0, sizeof(unsigned int) * (fine_ref + 1)));
+        for (int r = coarsest_ref; r <= fine_ref; ++r)
+            if (!H->lev[r].fden) launch_pivot_check(*H, H->lev[r], gslow + r, s);
+        std::vector<unsigned int> gs(fine_ref + 1, 1u);
+        BCUDA(cudaMemcpy(gs.data(), gslow, sizeof(unsigned int) * (fine_ref + 1), cudaMemcpyDeviceToHost));
+        cudaFree(gslow);
+        for (int r = coarsest_ref; r <= fine_ref; ++r)
+            H->lev[r].g_safe = !H->lev[r].fden && gs[r] == 0 && H->check_skip;
     }
     BCUDA(cudaGetLastError());
     BCUDA(cudaDeviceSynchronize());

@@ -56,6 +56,35 @@ __global__ void k_factor(LevelView L, double* __restrict__ den_out, double* __re
     if (!ok) atomicMin(bad, ((unsigned long long)ref << 40) | (unsigned long long)c);
 }
 
+// Setup, levels without stored factors: the Thomas pivots of every column
+// (the sweeps' own operations: den_k, div_recip, g_k by the fast path) are
+// checked once -- they depend on the matrix only -- and it is recorded whether
+// any multiplier g_k = U_k / den_k left the fast path's exact range.  If none
+// did, the sweeps on this level skip both per-layer tests (DevLevel::g_safe).
+__global__ void k_pivot_check(LevelView L, int ref, unsigned long long* __restrict__ bad,
+                              unsigned int* __restrict__ gslow) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= L.n) return;
+    const int64_t ld = L.ld;
+    const int nz = L.nz;
+    double den = L.D[c];
+    bool ok = true, slow = false;
+    for (int k = 0; k < nz; ++k) {
+        ok = ok && pivot_ok(den);
+        if (k == nz - 1) break;
+        const int64_t i = k * ld + c;
+        const double Uk = L.U[i];
+        const double y = div_recip(den);
+        bool sl = false;
+        double g = div_fast(Uk, den, y, sl);
+        if (sl) g = Uk / den;
+        slow = slow || sl;
+        den = L.D[i + ld] - Uk * g;
+    }
+    if (!ok) atomicMin(bad, ((unsigned long long)ref << 40) | (unsigned long long)c);
+    if (slow) atomicOr(gslow, 1u);
+}
+
 // u value of cell `cell` at row offset `row` (with the fused prolongation)
 __device__ __forceinline__ double uval(const double* __restrict__ u, const double* __restrict__ uc, int64_t row,
                                        int64_t rowc, int64_t cell) {
@@ -245,6 +274,11 @@ __global__ void __launch_bounds__(GRID ? 128 : 512, 1) k_coarse_tail(TailParams 
 }
 
 }  // namespace
+
+void launch_pivot_check(const Hierarchy& H, const DevLevel& L, unsigned int* gslow, cudaStream_t s) {
+    k_pivot_check<<<(unsigned)((L.n + 127) / 128), 128, 0, s>>>(L.view(H.nz), L.ref, &H.scal->bad, gslow);
+    ++H.launches;
+}
 
 void launch_factor(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
     k_factor<<<(unsigned)((L.n + 127) / 128), 128, 0, s>>>(L.view(H.nz), L.fden, L.fy, L.fg, L.ref, &H.scal->bad);

@@ -91,6 +91,7 @@ struct DevLevel {
     double* fy = nullptr;
     double* fg = nullptr;
     bool mf_safe = false;       // matrix-free quotients provably in the fast path's exact range (build_impl)
+    bool g_safe = false;        // every Thomas pivot valid and every g_k exact by the fast path (k_pivot_check)
     DistLevel dist;
     LevelView view(int nz) const {
         const int64_t s = (int64_t)nz * ld;
@@ -163,6 +164,7 @@ struct Hierarchy {
     mutable int rz_parts = 0;
     bool fuse_rz = true;        // HMG_FUSE_RZ=0: separate dot kernel
     int64_t fact_max_cells = kFactMaxCells;   // levels up to this size carry precomputed Thomas factors
+    bool check_skip = true;     // HMG_CHECK_SKIP=0: keep the per-layer pivot / g tests even where proven at build
     mutable Profiler prof;
     // diagnostics switches (environment, read at build time): HMG_SWEEP=simple
     // selects the reference-layout sweep kernel, HMG_SMALL=0 disables the
@@ -228,6 +230,7 @@ void finalize_parts(const Hierarchy& H, int nparts, int op, cudaStream_t s);
 
 // coarse_tail.cu
 void launch_factor(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
+void launch_pivot_check(const Hierarchy& H, const DevLevel& L, unsigned int* gslow, cudaStream_t s);
 void launch_coarse_tail(const Hierarchy& H, const hmg_mg_params& p, const double* b_top, double* out_top,
                         cudaStream_t s);
 // coarse_coop.cu: levels <= H.coop_ref in one cooperative launch (32-column smem tiles)

@@ -405,8 +405,10 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         const double den = Dk - Um * gprev;
                         const double y = div_recip(den);
                         const double z = div_fast_z(num, den, y, slow);
-                        const double g = div_fast(Uk, den, y, slow);
-                        ok = ok && pivot_ok(den);
+                        // CHK = false: pivots and the fast-path exactness of every
+                        // g_k were established at build time (k_pivot_check)
+                        const double g = CHK ? div_fast(Uk, den, y, slow) : div_fast_unchecked(Uk, den, y);
+                        if (CHK) ok = ok && pivot_ok(den);
                         ptx::tmem_st_f64(tl + 2u * (uint32_t)k, z);
                         ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, g);
                         zprev = z;
@@ -698,7 +700,10 @@ int launch_sweep_st_dot(const Hierarchy& H, const DevLevel& L, const double* b, 
                         double omega, cudaStream_t s) {
     int n = 0;
     try {
-        n = launch_st<false, false, false, 2, true, true>(H, L, b, uin, nullptr, uout, omega, s);
+        if (L.g_safe)
+            n = launch_st<false, false, false, 2, false, true>(H, L, b, uin, nullptr, uout, omega, s);
+        else
+            n = launch_st<false, false, false, 2, true, true>(H, L, b, uin, nullptr, uout, omega, s);
     } catch (const std::exception& e) {
         g_launch_error = std::string("sweep launch: ") + e.what();
     }
@@ -709,7 +714,7 @@ int launch_sweep_st_dot(const Hierarchy& H, const DevLevel& L, const double* b, 
 void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                      double* uout, double omega, cudaStream_t s) {
     try {
-        if (H.matrix_free && L.mf_safe) {
+        if (H.matrix_free && L.mf_safe && L.g_safe) {
             if (!uin)
                 launch_st<true, false, true, 2, false>(H, L, b, nullptr, nullptr, uout, omega, s);
             else if (uc)
@@ -723,6 +728,13 @@ void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, con
                 launch_st<false, true, true, 2>(H, L, b, uin, uc, uout, omega, s);
             else
                 launch_st<false, false, true, 2>(H, L, b, uin, nullptr, uout, omega, s);
+        } else if (L.g_safe) {
+            if (!uin)
+                launch_st<true, false, false, 2, false>(H, L, b, nullptr, nullptr, uout, omega, s);
+            else if (uc)
+                launch_st<false, true, false, 2, false>(H, L, b, uin, uc, uout, omega, s);
+            else
+                launch_st<false, false, false, 2, false>(H, L, b, uin, nullptr, uout, omega, s);
         } else {
             if (!uin)
                 launch_st<true, false, false, 2>(H, L, b, nullptr, nullptr, uout, omega, s);

@@ -87,7 +87,7 @@ __device__ long long g_tc_timing[16];
 #define TSTAMP(i) do {} while (0)
 #endif
 
-template <bool ZERO, bool PROLONG, bool FACT, int G>
+template <bool ZERO, bool PROLONG, bool FACT, int G, bool CHK = true>
 __global__ void __launch_bounds__(kThreads, 2)
     k_sweep_tc(const __grid_constant__ SweepMaps maps, LevelView L, TileHalo th, const double* __restrict__ bvec,
                const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc,
@@ -292,8 +292,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                     const double den = Dk - Um * gprev;
                     const double y = div_recip(den);
                     const double z = div_fast_z(num, den, y, slow);
-                    const double g = div_fast(Uk, den, y, slow);
-                    ok = ok && pivot_ok(den);
+                    // CHK = false: pivots and every g_k's fast path verified at build (k_pivot_check)
+                    const double g = CHK ? div_fast(Uk, den, y, slow) : div_fast_unchecked(Uk, den, y);
+                    if (CHK) ok = ok && pivot_ok(den);
                     ptx::tmem_st_f64(tl + 2u * (uint32_t)k, z);
                     ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, g);
                     zprev = z;
@@ -519,7 +520,7 @@ uint32_t tmem_cols_for(int nz) {
     return c;
 }
 
-template <bool Z, bool P, bool F, int G>
+template <bool Z, bool P, bool F, int G, bool CK = true>
 void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                double* uout, double omega, cudaStream_t s) {
     const int nz = H.nz;
@@ -541,7 +542,7 @@ void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const dou
     if (smem < floor_smem) smem = floor_smem;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k_sweep_tc<Z, P, F, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        cudaFuncSetAttribute(k_sweep_tc<Z, P, F, G, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr_done = true;
     }
     SweepMaps maps;
@@ -567,7 +568,7 @@ void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const dou
     unsigned cap = Z ? (unsigned)((cols <= 256 && grid > (unsigned)sms) ? 2 * sms : sms) : grid;
     if (const char* e = std::getenv("HMG_TC_PERSIST"))
         if (std::string(e) == "0") cap = grid;
-    launch_pdl(H, k_sweep_tc<Z, P, F, G>, dim3(grid < cap ? grid : cap), dim3(kThreads), smem, s, maps, V, L.halo, b,
+    launch_pdl(H, k_sweep_tc<Z, P, F, G, CK>, dim3(grid < cap ? grid : cap), dim3(kThreads), smem, s, maps, V, L.halo, b,
                uin, uc, ldc, L.fden, L.fg, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
 }
 
@@ -619,7 +620,9 @@ void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, con
             else
                 launch_tc<false, false, true, 2>(H, L, b, uin, nullptr, uout, omega, s);
         } else {
-            if (!uin)
+            if (!uin && L.g_safe)
+                launch_tc<true, false, false, 4, false>(H, L, b, nullptr, nullptr, uout, omega, s);
+            else if (!uin)
                 launch_tc<true, false, false, 4>(H, L, b, nullptr, nullptr, uout, omega, s);
             else if (uc)
                 launch_tc<false, true, false, 2>(H, L, b, uin, uc, uout, omega, s);
