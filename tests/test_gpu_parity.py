@@ -195,6 +195,17 @@ def test_errors_name_arguments():
     assert st == "HMG_OK" and it == 0 and float(x.abs().max()) == 0.0
 
 
+def test_singular_column_reported_at_build():
+    """An overflowing vertical coupling (two adjacent coefficients of 1.7e308)
+    makes column 5's Thomas pivot non-finite: hmg_build_hierarchy fails with
+    HMG_ERR_SINGULAR_COLUMN naming the level and the column."""
+    lam, _ = hi.make_inputs(hi.CONFIGS["C0"])
+    lam = lam.copy()
+    lam[3, 5] = lam[4, 5] = 1.7e308
+    with pytest.raises(HmgError, match="singular column: ref 2 column 5"):
+        Hierarchy(2, 0, 8, 0.01, 1e-4, lam)
+
+
 @pytest.mark.slow
 @pytest.mark.parametrize("name", ["C2a", "C2b", "C2c"])
 def test_full_size_c2(name):
