@@ -200,7 +200,7 @@ const double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b,
         double* dst = (i == count - 1 && out) ? out : (cur == L.wa ? L.wb : L.wa);
         if (cur) halo_exchange(H, L, cur, s);      // neighbours' old values (Jacobi)
         const bool last_into_out = i == count - 1 && out;
-        if (last_into_out && H.rz_req && L.ref == H.fine_ref && cur && !(i == 0 && uc) && !L.fden && !L.dist.on &&
+        if (last_into_out && H.rz_req && L.ref == H.fine_ref && cur && !(i == 0 && uc) && !L.fden &&
             !H.matrix_free && H.use_tc_sweep && sweep_st_supported(H, L)) {
             // the preconditioner's last sweep: <r, z> = <b, u'> accumulated on the fly
             ProfScope ps(H, kKSweep, L.ref, s);
@@ -274,7 +274,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
                     const double* b, double* x, double rtol, int maxit, int* iters, double* relres,
                     cudaStream_t s) {
     const DevLevel& F = H.lev[H.fine_ref];
-    const size_t bytes = sizeof(double) * H.nz * F.ld;
+    const bool dist = F.dist.on;
     *iters = 0;
     *relres = 0.0;
     auto precond = [&](const double* r, double* z) {
@@ -283,12 +283,10 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         else
             run_sweeps(H, F, r, nullptr, nullptr, single_sweeps, z, single_omega, s);
     };
-    if (F.dist.on) {
-        // multi-GPU: r = b (internal r keeps zero padding), x = 0, p = z copied
-        launch_copy_pad(H, F, b, F.ld, H.r, F.ld, s);
-        HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
-    }
-    const double* r0 = F.dist.on ? H.r : b;        // single GPU: the first residual is b itself
+    // x0 = 0, r0 = b: no copies -- the first residual is b itself, and the first
+    // x/r update reads b and writes x = 0 + alpha p, r = b - alpha q (the same
+    // arithmetic as from x = 0, r = b)
+    const double* r0 = b;
     launch_dot(H, F, r0, r0, s);
     launch_finalize(H, kFinBB, s);
     HMG_TRY(check_launch());
@@ -296,7 +294,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     HMG_CUDA(cudaStreamSynchronize(s));
     const double bn = std::sqrt(H.scal_host->bb);
     if (bn == 0.0) {
-        if (!F.dist.on) HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
+        HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
         return HMG_OK;
     }
     // <r, z> after each preconditioner application: fused into its last sweep
@@ -315,28 +313,26 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         }
     };
     precond_dot(r0, H.z, kFinRhoInit);
-    // Single GPU: z, p_old and p_new rotate through {z, p, p2} so that p_1 = z_1
-    // needs no copy; the first x/r update reads b and writes x = 0 + alpha p,
-    // r = b - alpha q (the same arithmetic as from x = 0, r = b).
+    // z, p_old and p_new rotate through {z, p, p2}, so that p_1 = z_1 needs no
+    // copy and p = z + beta p_old is formed inside q = H^ p.  Multi-GPU: the halo
+    // of z is exchanged, and the halo slots of p_new are formed by the same
+    // addition from the halos of z and p_old (k_halo_pupdate).
     double* pc = H.z;                              // current search direction
-    if (F.dist.on) {
-        HMG_CUDA(cudaMemcpyAsync(H.p, H.z, bytes, cudaMemcpyDeviceToDevice, s));
-        pc = H.p;
-    }
     double* zb = H.z;                              // buffer holding the current z
     for (int it = 1; it <= maxit; ++it) {
-        if (F.dist.on) {                           // multi-GPU: p update, halo exchange, apply
-            if (it > 1) launch_update_p(H, F, pc, H.z, s);
-            halo_exchange(H, F, pc, s);
-            launch_apply_dot(H, F, pc, H.q, s);
-        } else if (it == 1) {
+        if (it == 1) {
+            if (dist) halo_exchange(H, F, pc, s);
             launch_apply_dot(H, F, pc, H.q, s);    // q = H^ p, alpha = rho / <p, q>
         } else {                                   // p = z + beta p fused into q = H^ p
             double* pn = (pc != H.p2 && zb != H.p2) ? H.p2 : ((pc != H.p && zb != H.p) ? H.p : H.z);
+            if (dist) {
+                halo_exchange(H, F, zb, s);
+                launch_halo_pupdate(H, F, zb, pc, pn, s);
+            }
             launch_apply_pupdate_dot(H, F, zb, pc, pn, H.q, s);
             pc = pn;
         }
-        if (it == 1 && !F.dist.on)
+        if (it == 1)
             launch_update_xr_first(H, F, x, pc, b, s);   // x = 0 + alpha p, r = b - alpha q, partial <r, r>
         else
             launch_update_xr(H, F, x, pc, s);      // x += alpha p, r -= alpha q, partial <r, r>
@@ -349,7 +345,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         *iters = it;
         *relres = rn / bn;
         if (rn <= rtol * bn) return HMG_OK;
-        if (!F.dist.on) zb = (pc != H.z) ? H.z : H.p;   // a buffer that is not p
+        zb = (pc != H.z) ? H.z : H.p;              // a buffer that is not p
         precond_dot(H.r, zb, kFinRZ);              // beta = rho' / rho, rho = rho' (p updated in the next apply)
     }
     return fail(HMG_ERR_NOT_CONVERGED, "not converged after " + std::to_string(maxit) +

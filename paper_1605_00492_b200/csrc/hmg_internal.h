@@ -286,6 +286,9 @@ void launch_halo_unpack(const Hierarchy& H, const DevLevel& L, double* v, cudaSt
 void launch_gather_pack(const Hierarchy& H, const DevLevel& C, const double* v, int64_t off, int64_t cnt, cudaStream_t s);
 void launch_gather_unpack(const Hierarchy& H, const DevLevel& C, double* v, int64_t cnt, cudaStream_t s);
 void launch_update_p(const Hierarchy& H, const DevLevel& L, double* p, const double* z, cudaStream_t s);
+// halo slots of p_new = z + beta p_old (multi-GPU fused CG direction update)
+void launch_halo_pupdate(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
+                         cudaStream_t s);
 // finalize of a dot when its partial sums are rank-local: local total into scal->tmp
 void launch_finalize_local(const Hierarchy& H, int nparts, cudaStream_t s);
 void launch_scalar_op(const Hierarchy& H, int op, cudaStream_t s);   // op on scal->tmp as the (global) sum

@@ -414,6 +414,18 @@ __global__ void k_gather_unpack(const double* __restrict__ buf, int64_t cnt, int
     if (i < cnt) v[k * ld + q * cnt + i] = buf[((int64_t)q * nz + k) * cnt + i];
 }
 
+// Multi-GPU: the halo slots [n_own, n_own + n_halo) of p_new = z + beta p_old,
+// from the (exchanged) halo slots of z and p_old -- the addition the fused
+// apply forms for the owned cells.
+__global__ void k_halo_pupdate(const double* __restrict__ z, const double* __restrict__ pold, double* __restrict__ pnew,
+                               int64_t n_own, int64_t n_halo, int64_t ld, int nz, const PcgScalars* __restrict__ sc) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_halo * nz) return;
+    const int k = (int)(t / n_halo);
+    const int64_t i = k * ld + n_own + (t - (int64_t)k * n_halo);
+    pnew[i] = z[i] + sc->beta * pold[i];
+}
+
 __global__ void k_update_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, int64_t ld,
                            const PcgScalars* __restrict__ sc) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -784,6 +796,14 @@ void launch_gather_pack(const Hierarchy& H, const DevLevel& C, const double* v, 
 void launch_gather_unpack(const Hierarchy& H, const DevLevel& C, double* v, int64_t cnt, cudaStream_t s) {
     dim3 g(blocks(cnt, 256), H.nz, H.nranks);
     k_gather_unpack<<<g, 256, 0, s>>>(H.gbuf_recv, cnt, H.nz, v, C.ld);
+    ++H.launches;
+}
+
+void launch_halo_pupdate(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
+                         cudaStream_t s) {
+    const int64_t tot = L.dist.n_halo * H.nz;
+    if (tot == 0) return;
+    k_halo_pupdate<<<blocks(tot, 256), 256, 0, s>>>(z, pold, pnew, L.n, L.dist.n_halo, L.ld, H.nz, H.scal);
     ++H.launches;
 }
 
