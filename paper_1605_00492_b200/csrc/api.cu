@@ -114,6 +114,7 @@ void free_hierarchy(Hierarchy* H) {
         cudaFree(L.halo_cells); cudaFree(L.halo_count); cudaFree(L.halo_loc);
         cudaFree(L.fden);
         cudaFree(L.small_cells); cudaFree(L.small_count); cudaFree(L.small_loc);
+        cudaFree(L.coop_cells); cudaFree(L.coop_count); cudaFree(L.coop_loc);
         cudaFree(L.dist.send_idx); cudaFree(L.dist.sendbuf); cudaFree(L.dist.recvbuf);
     }
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q); cudaFree(H->p2);
@@ -429,7 +430,9 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
         // against ~3 us per dependent kernel launch).  HMG_COOP_REF=r overrides
         // (-1: off).  It never spans distributed levels.
         int coop = coarsest_ref;
-        while (coop < fine_ref && 20LL * (1LL << (2 * (coop + 1))) <= kCoopMaxCells) ++coop;
+        const int ctw = coarse_coop_tile_width(nlayers);   // narrower tiles for deep columns
+        const int64_t coop_max = kCoopMaxCells * (ctw > 0 ? ctw : kSmallTile) / kSmallTile;
+        while (coop < fine_ref && 20LL * (1LL << (2 * (coop + 1))) <= coop_max) ++coop;
         if (const char* e = std::getenv("HMG_COOP_REF")) coop = std::atoi(e);
         H->coop_ref = coop < 0 ? -1 : std::min(std::max(coop, coarsest_ref), dist ? gather_ref : fine_ref);
         // Diagnostic alternative (HMG_TAIL_REF=r): levels <= r in the global-memory
@@ -668,6 +671,16 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
                 L.small.cells = L.small_cells;
                 L.small.count = L.small_count;
                 L.small.loc = L.small_loc;
+            }
+            const int ctw = coarse_coop_tile_width(nlayers);
+            if (r <= H->coop_ref && ctw == kSmallTile) {
+                L.coop_halo = L.small;
+            } else if (r <= H->coop_ref && ctw > 0) {
+                hs = build_halo(ctw, kSmallHaloMax, &L.coop_cells, &L.coop_count, &L.coop_loc);
+                if (hs != HMG_OK) return cleanup(hs);
+                L.coop_halo.cells = L.coop_cells;
+                L.coop_halo.count = L.coop_count;
+                L.coop_halo.loc = L.coop_loc;
             }
         }
     }

@@ -66,33 +66,43 @@ struct CoopSmem {
     size_t bands, fact, b, u, hu, z, uc, huc, bar, total;
 };
 
-__host__ __device__ inline CoopSmem coop_layout(int nz) {
+// TW-column tiles: TW = 32 while the tile's operands fit in shared memory
+// (nz <= 64), 16 up to nz = 128, 8 up to nz = 256; lanes >= TW idle.
+__host__ __device__ inline CoopSmem coop_layout(int nz, int TW) {
     CoopSmem L;
-    const size_t plane = sizeof(double) * (size_t)((nz + 7) & ~7) * kTileW;   // layers padded to 8
+    const size_t rows = (size_t)((nz + 7) & ~7);            // layers padded to 8
+    const size_t plane = sizeof(double) * rows * TW;
+    const size_t hplane = sizeof(double) * rows * kHaloW;   // halo planes: <= 32 off-tile cells
     size_t off = 0;
     L.bands = off; off += 5 * plane;
     L.fact = off;  off += 3 * plane;
     L.b = off;     off += plane;
     L.u = off;     off += plane;
-    L.hu = off;    off += plane;
+    L.hu = off;    off += hplane;
     L.z = off;     off += plane;
-    L.uc = off;    off += plane / 4;      // [nz][8] parents of the tile (prolongation)
-    L.huc = off;   off += plane;          // [nz][32] parents of the halo cells
+    L.uc = off;    off += plane / 4;      // [nz][TW/4] parents of the tile (prolongation)
+    L.huc = off;   off += hplane;         // [nz][kHaloW] parents of the halo cells
     L.bar = off;   off += 64;
     L.total = off;
     return L;
 }
 
-constexpr int kCoopThreads = kTileW * kTileWarps;   // 4 warps per 32-column tile
+constexpr int kCoopThreads = 32 * kTileWarps;   // 4 warps per tile
 
+template <int TW>
 __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_constant__ CoopParams P) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     const int nz = P.nz, nzp = (nz + 7) & ~7;
-    const int tid = threadIdx.x, j = tid & 31, warp = tid >> 5;   // j: the column of this lane
-    const CoopSmem lay = coop_layout(nz);
-    const int PL = nzp * kTileW;                       // doubles per plane
+    const int tid = threadIdx.x, warp = tid >> 5;
+    // j: the column of this lane; lanes >= TW repeat column TW - 1 (identical
+    // values written to identical addresses) and never store to global memory
+    const int lane = tid & 31;
+    const int j = lane < TW ? lane : TW - 1;
+    const bool jlane = lane < TW;
+    const CoopSmem lay = coop_layout(nz, TW);
+    const int PL = nzp * TW;                           // doubles per plane
     double* sB = reinterpret_cast<double*>(smraw + lay.bands);
     double* sF = reinterpret_cast<double*>(smraw + lay.fact);
     double* sb = reinterpret_cast<double*>(smraw + lay.b);
@@ -108,7 +118,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         ptx::fence_mbar_init();
     }
     // padding rows (layers nz..nzp-1) of the vector planes stay zero
-    for (int q = nz * kTileW + tid; q < PL; q += kCoopThreads) sb[q] = su[q] = shu[q] = 0.0;
+    for (int q = nz * TW + tid; q < PL; q += kCoopThreads) sb[q] = su[q] = 0.0;
+    for (int q = nz * kHaloW + tid; q < nzp * kHaloW; q += kCoopThreads) shu[q] = 0.0;
     __syncthreads();
 #ifdef HMG_TIMING
     int nst = 0;
@@ -124,8 +135,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // prior generic reads before async writes
         if (tid == 0) {
             ptx::mbar_arrive_expect_tx(bar, (uint32_t)(8 * sizeof(double) * PL));
-            ptx::tma_load_3d(sB, &P.bands[l - P.coarsest], t * kTileW, 0, 0, bar);
-            ptx::tma_load_3d(sF, &P.fact[l - P.coarsest], t * kTileW, 0, 0, bar);
+            ptx::tma_load_3d(sB, &P.bands[l - P.coarsest], t * TW, 0, 0, bar);
+            ptx::tma_load_3d(sF, &P.fact[l - P.coarsest], t * TW, 0, 0, bar);
         }
         ptx::mbar_wait(bar, phase);
         phase ^= 1u;
@@ -148,9 +159,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
     // of every warp gathers halo cell h, warps split the layers
     auto cp_halo = [&](double* dst, const double* v, const CoopLevel& L, int t, int shift, int64_t ldv) {
         const int hcount = L.sh.count[t];
-        if (j < hcount) {
-            const int32_t hc = L.sh.cells[t * kSmallHaloMax + j] >> shift;
-            for (int k = warp; k < nz; k += kTileWarps) ptx::cp_async8(dst + k * kTileW + j, v + k * ldv + hc);
+        if (lane < hcount) {
+            const int32_t hc = L.sh.cells[t * kSmallHaloMax + lane] >> shift;
+            for (int k = warp; k < nz; k += kTileWarps) ptx::cp_async8(dst + k * kHaloW + lane, v + k * ldv + hc);
         }
     };
     auto cp_wait = [&]() {
@@ -158,8 +169,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         __syncthreads();
     };
     auto store_own = [&](double* dst, const CoopLevel& L, int64_t c) {
-        if (c < L.V.n)
-            for (int k = warp; k < nz; k += kTileWarps) dst[k * L.V.ld + c] = su[k * kTileW + j];
+        if (jlane && c < L.V.n)
+            for (int k = warp; k < nz; k += kTileWarps) dst[k * L.V.ld + c] = su[k * TW + j];
     };
     auto slots = [&](const CoopLevel& L, int64_t c, int& l0, int& l1, int& l2) {
         const uint32_t loc = L.sh.loc[c < L.V.n ? c : L.V.n - 1];
@@ -171,19 +182,19 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
     auto sweep_step = [&](int l, const double* bl, const double* uin, double* uout) {
         const CoopLevel& L = LV[l];
         for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
-            const int64_t c = (int64_t)t * kTileW + j;
+            const int64_t c = (int64_t)t * TW + j;
             int l0, l1, l2;
             slots(L, c, l0, l1, l2);
             __syncthreads();                           // every thread is done with the previous tile's planes
-            cp_rows(sb, bl, L.V.ld, (int64_t)t * kTileW, kTileW);
+            cp_rows(sb, bl, L.V.ld, (int64_t)t * TW, TW);
             if (uin) {
-                cp_rows(su, uin, L.V.ld, (int64_t)t * kTileW, kTileW);
+                cp_rows(su, uin, L.V.ld, (int64_t)t * TW, TW);
                 cp_halo(shu, uin, L, t, 0, L.V.ld);
             }
             load_static(l, t);
             cp_wait();
             CSTAMP();
-            tile_sweep_cta(S, nz, warp, j, l0, l1, l2, uin == nullptr, P.omega, c < L.V.n);
+            tile_sweep_cta<TW>(S, nz, warp, j, l0, l1, l2, uin == nullptr, P.omega, jlane && c < L.V.n);
             CSTAMP();
             store_own(uout, L, c);
         }
@@ -205,26 +216,27 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         }
         cur[l] = c_in;
         for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
-            const int64_t c = (int64_t)t * kTileW + j;
+            const int64_t c = (int64_t)t * TW + j;
             int l0, l1, l2;
             slots(L, c, l0, l1, l2);
             __syncthreads();
-            cp_rows(sb, bl, L.V.ld, (int64_t)t * kTileW, kTileW);
+            cp_rows(sb, bl, L.V.ld, (int64_t)t * TW, TW);
             if (c_in) {
-                cp_rows(su, c_in, L.V.ld, (int64_t)t * kTileW, kTileW);
+                cp_rows(su, c_in, L.V.ld, (int64_t)t * TW, TW);
                 cp_halo(shu, c_in, L, t, 0, L.V.ld);
             }
             load_static(l, t);
             cp_wait();
             CSTAMP();
-            tile_residuals_cta(S, nz, warp, j, l0, l1, l2, c_in == nullptr);   // r = b - H^ u (r = b from zero)
+            tile_residuals_cta<TW>(S, nz, warp, j, l0, l1, l2, c_in == nullptr);   // r = b - H^ u (r = b from zero)
             __syncthreads();
             // b_c[k][p] = ((r0 + r1) + r2) + r3 over the children 4p..4p+3: thread = (parent, layer phase)
-            const int pp = tid & 7, kph = tid >> 3;
-            const int64_t p = (int64_t)t * (kTileW / 4) + pp;
+            constexpr int PT = TW / 4;                 // parents per tile
+            const int pp = tid % PT, kph = tid / PT;
+            const int64_t p = (int64_t)t * PT + pp;
             if (p < C.V.n)
-                for (int k = kph; k < nz; k += kCoopThreads / 8) {
-                    const double* r = sz + k * kTileW + 4 * pp;
+                for (int k = kph; k < nz; k += kCoopThreads / PT) {
+                    const double* r = sz + k * TW + 4 * pp;
                     C.b[k * C.V.ld + p] = ((r[0] + r[1]) + r[2]) + r[3];
                 }
         }
@@ -244,12 +256,12 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
                 int l0, l1, l2;
                 slots(L, c, l0, l1, l2);
                 __syncthreads();
-                cp_rows(sb, bl, L.V.ld, 0, kTileW);
+                cp_rows(sb, bl, L.V.ld, 0, TW);
                 load_static(l, 0);
                 cp_wait();
                 CSTAMP();
                 for (int s = 0; s < P.n_coarse; ++s)
-                    tile_sweep_cta(S, nz, warp, j, l0, l1, l2, s == 0, P.omega, c < L.V.n);
+                    tile_sweep_cta<TW>(S, nz, warp, j, l0, l1, l2, s == 0, P.omega, jlane && c < L.V.n);
                 CSTAMP();
                 store_own(out, L, c);
             }
@@ -275,34 +287,36 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         // first step: u = c_in + P u_c formed in shared memory for the tile and its halo
         double* dst = (P.nu_post <= 1) ? out : ((c_in == L.wa) ? L.wb : L.wa);
         for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
-            const int64_t c = (int64_t)t * kTileW + j;
+            const int64_t c = (int64_t)t * TW + j;
             const bool valid = c < L.V.n;
             int l0, l1, l2;
             slots(L, c, l0, l1, l2);
-            const int64_t c0 = (int64_t)t * kTileW;
+            const int64_t c0 = (int64_t)t * TW;
             __syncthreads();
-            cp_rows(sb, bl, L.V.ld, c0, kTileW);
+            cp_rows(sb, bl, L.V.ld, c0, TW);
             if (c_in) {
-                cp_rows(su, c_in, L.V.ld, c0, kTileW);
+                cp_rows(su, c_in, L.V.ld, c0, TW);
                 cp_halo(shu, c_in, L, t, 0, L.V.ld);
             }
-            cp_rows(suc, C.u, C.V.ld, c0 / 4, kTileW / 4);
+            cp_rows(suc, C.u, C.V.ld, c0 / 4, TW / 4);
             cp_halo(shuc, C.u, L, t, 2, C.V.ld);
             load_static(l, t);
             cp_wait();
             // u + P u_c, the addition of the prolongation (0 + u_c from a zero iterate)
             const int hcount = L.sh.count[t];
             for (int k = warp; k < nz; k += kTileWarps) {
-                const double v = c_in ? su[k * kTileW + j] : 0.0;
-                su[k * kTileW + j] = v + suc[k * (kTileW / 4) + (j >> 2)];
-                if (j < hcount) {
-                    const double h = c_in ? shu[k * kTileW + j] : 0.0;
-                    shu[k * kTileW + j] = h + shuc[k * kTileW + j];
+                if (jlane) {
+                    const double v = c_in ? su[k * TW + j] : 0.0;
+                    su[k * TW + j] = v + suc[k * (TW / 4) + (j >> 2)];
+                }
+                if (lane < hcount) {
+                    const double h = c_in ? shu[k * kHaloW + lane] : 0.0;
+                    shu[k * kHaloW + lane] = h + shuc[k * kHaloW + lane];
                 }
             }
             __syncthreads();
             CSTAMP();
-            if (P.nu_post > 0) tile_sweep_cta(S, nz, warp, j, l0, l1, l2, false, P.omega, valid);
+            if (P.nu_post > 0) tile_sweep_cta<TW>(S, nz, warp, j, l0, l1, l2, false, P.omega, jlane && valid);
             CSTAMP();
             store_own(dst, L, c);
         }
@@ -330,15 +344,52 @@ extern "C" unsigned long long hmg_debug_tile_slow() {
 namespace {
 #endif
 
+int coop_tile_width(int nz) {
+    for (int tw : {32, 16, 8})
+        if (coop_layout(nz, tw).total <= 227 * 1024) return tw;
+    return 0;
+}
+
+template <int TW>
+void launch_coop_tw(const Hierarchy& H, CoopParams& P, cudaStream_t s) {
+    const int nz = H.nz, nzp = (nz + 7) & ~7;
+    for (int r = H.coarsest_ref; r <= H.coop_ref; ++r) {
+        const DevLevel& L = H.lev[r];
+        const int i = r - H.coarsest_ref;
+        CoopLevel& C = P.lev[i];
+        C.ntiles = (int)((L.n + TW - 1) / TW);
+        P.bands[i] = make_tensor_map(C.V.D, L.ld, nz, TW, nzp, 5);
+        P.fact[i] = make_tensor_map(L.fden, L.ld, nz, TW, nzp, 3);
+    }
+    const size_t smem = coop_layout(nz, TW).total;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_coarse_coop<TW>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+        attr = true;
+    }
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_coop<TW>, kCoopThreads, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
+    int grid = P.lev[H.coop_ref - H.coarsest_ref].ntiles;
+    const int cap = (per_sm < 1 ? 1 : per_sm) * sms;
+    if (grid > cap) grid = cap;
+    ProfScope ps(H, kKCoarseTail, H.coop_ref, s);
+    void* args[] = {&P};
+    cudaLaunchCooperativeKernel((const void*)k_coarse_coop<TW>, dim3(grid), dim3(kCoopThreads), args, smem, s);
+    ++H.launches;
+}
+
 }  // namespace
+
+int coarse_coop_tile_width(int nz) { return coop_tile_width(nz); }
 
 bool coarse_coop_supported(const Hierarchy& H) {
     if (H.coop_ref < 0) return false;
     if (H.coop_ref - H.coarsest_ref + 1 > kCoopLevels) return false;
-    if (coop_layout(H.nz).total > 227 * 1024) return false;
+    if (coop_tile_width(H.nz) == 0) return false;
     for (int r = H.coarsest_ref; r <= H.coop_ref; ++r) {
         const DevLevel& L = H.lev[r];
-        if (!L.fden || !L.small.loc) return false;
+        if (!L.fden || !L.coop_halo.loc) return false;
     }
     return true;
 }
@@ -348,8 +399,7 @@ void launch_coarse_coop(const Hierarchy& H, const hmg_mg_params& p, const double
     static_assert(sizeof(CoopParams) <= 4096, "kernel parameter block");
     CoopParams P;
     std::memset(&P, 0, sizeof(P));
-    const int nz = H.nz, nzp = (nz + 7) & ~7;
-    P.nz = nz;
+    P.nz = H.nz;
     P.top = H.coop_ref;
     P.coarsest = H.coarsest_ref;
     P.nu_pre = p.nu_pre;
@@ -360,34 +410,19 @@ void launch_coarse_coop(const Hierarchy& H, const hmg_mg_params& p, const double
     P.out_top = out_top;
     for (int r = H.coarsest_ref; r <= H.coop_ref; ++r) {
         const DevLevel& L = H.lev[r];
-        const int i = r - H.coarsest_ref;
-        CoopLevel& C = P.lev[i];
-        C.V = L.view(nz);
-        C.sh = L.small;
+        CoopLevel& C = P.lev[r - H.coarsest_ref];
+        C.V = L.view(H.nz);
+        C.sh = L.coop_halo;
         C.wa = L.wa;
         C.wb = L.wb;
         C.b = L.b;
         C.u = L.u;
-        C.ntiles = (int)((L.n + kTileW - 1) / kTileW);
-        P.bands[i] = make_tensor_map(C.V.D, L.ld, nz, kTileW, nzp, 5);
-        P.fact[i] = make_tensor_map(L.fden, L.ld, nz, kTileW, nzp, 3);
     }
-    const size_t smem = coop_layout(nz).total;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_coarse_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
+    switch (coop_tile_width(H.nz)) {
+        case 32: launch_coop_tw<32>(H, P, s); break;
+        case 16: launch_coop_tw<16>(H, P, s); break;
+        default: launch_coop_tw<8>(H, P, s); break;
     }
-    int per_sm = 0, sms = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_coop, kCoopThreads, smem);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
-    int grid = P.lev[H.coop_ref - H.coarsest_ref].ntiles;
-    const int cap = (per_sm < 1 ? 1 : per_sm) * sms;
-    if (grid > cap) grid = cap;
-    ProfScope ps(H, kKCoarseTail, H.coop_ref, s);
-    void* args[] = {&P};
-    cudaLaunchCooperativeKernel((const void*)k_coarse_coop, dim3(grid), dim3(kCoopThreads), args, smem, s);
-    ++H.launches;
 }
 
 }  // namespace hmg

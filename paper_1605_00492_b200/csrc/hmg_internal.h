@@ -86,6 +86,12 @@ struct DevLevel {
     int32_t* small_count = nullptr;
     uint32_t* small_loc = nullptr;
     SmallHalo small;
+    // tiles of the cooperative coarse tail (width coarse_coop_tile_width(nz):
+    // the 32-cell tables above when that is 32, else their own)
+    int32_t* coop_cells = nullptr;
+    int32_t* coop_count = nullptr;
+    uint32_t* coop_loc = nullptr;
+    SmallHalo coop_halo;
     // Thomas factors (coarse-tail levels only): pivots, refined reciprocals, multipliers
     double* fden = nullptr;
     double* fy = nullptr;
@@ -235,6 +241,7 @@ void launch_coarse_tail(const Hierarchy& H, const hmg_mg_params& p, const double
                         cudaStream_t s);
 // coarse_coop.cu: levels <= H.coop_ref in one cooperative launch (32-column smem tiles)
 bool coarse_coop_supported(const Hierarchy& H);
+int coarse_coop_tile_width(int nz);   // 32, 16 or 8 columns per tile (0: no fit)
 void launch_coarse_coop(const Hierarchy& H, const hmg_mg_params& p, const double* b_top, double* out_top,
                         cudaStream_t s);
 size_t coarsest_smem_bytes(int nz, int64_t n, int threads);

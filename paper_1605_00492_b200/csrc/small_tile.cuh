@@ -1,5 +1,6 @@
-// One damped line-Jacobi sweep on a 32-column tile whose whole operand set is
-// resident in shared memory (one warp, lane = column).  Shared by the
+// One damped line-Jacobi sweep on a TW-column tile (TW = 32, or 16 / 8 for
+// deep columns) whose whole operand set is resident in shared memory (lane =
+// column; lanes >= TW idle).  Shared by the
 // small-level sweep kernel (sweep_small.cu) and the cooperative coarse tail
 // (coarse_coop.cu).
 //
@@ -17,13 +18,15 @@
 
 namespace hmg {
 
-constexpr int kTileW = kSmallTile;   // 32 columns, one warp
+constexpr int kTileW = kSmallTile;   // widest tile: 32 columns, one warp
+constexpr int kHaloW = kSmallHaloMax;  // width of the halo plane (<= 32 off-tile neighbours per tile)
 
 #ifdef HMG_TIMING
 __device__ unsigned long long g_tile_slow_count;   // diagnostics: exact-division redos
 #endif
 
-// Shared-memory planes of one tile, each [nzp][32] (nzp = nz rounded up to 8).
+// Shared-memory planes of one tile, each [nzp][TW] (nzp = nz rounded up to 8);
+// the halo plane is [nzp][kHaloW].
 struct TileSmem {
     const double* D;
     const double* U;
@@ -35,25 +38,27 @@ struct TileSmem {
     const double* g;     // multipliers g_k = U_k / den_k
     const double* b;     // right-hand side
     double* u;           // iterate: in on entry, out on exit
-    const double* hu;    // off-tile neighbour values [nz][32] (halo slot h at column h)
+    const double* hu;    // off-tile neighbour values [nz][kHaloW] (halo slot h at column h)
     double* z;           // scratch
 };
 
-// neighbour value of local slot l at layer k (in-tile slot < 32, else halo)
+// neighbour value of local slot l at layer k (in-tile slot < TW, else halo)
+template <int TW>
 __device__ __forceinline__ double tile_nb(const TileSmem& S, int k, int l) {
-    return l < kTileW ? S.u[k * kTileW + l] : S.hu[k * kTileW + (l - kTileW)];
+    return l < TW ? S.u[k * TW + l] : S.hu[k * kHaloW + (l - TW)];
 }
 
 // pass 1: r_k = b_k - (H^ u)_k for every layer into S.z (zero guess: r = b)
+template <int TW = kTileW>
 __device__ __forceinline__ void tile_residuals(const TileSmem& S, int nz, int j, int l0, int l1, int l2, bool zero) {
     const int nzp = (nz + 7) & ~7;
     if (zero) {
         for (int k0 = 0; k0 < nzp; k0 += 8) {
             double r[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) r[i] = S.b[(k0 + i) * kTileW + j];
+            for (int i = 0; i < 8; ++i) r[i] = S.b[(k0 + i) * TW + j];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = r[i];
+            for (int i = 0; i < 8; ++i) S.z[(k0 + i) * TW + j] = r[i];
         }
         return;
     }
@@ -62,30 +67,31 @@ __device__ __forceinline__ void tile_residuals(const TileSmem& S, int nz, int j,
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int k = k0 + i;
-            const int q = k * kTileW + j;
-            const int qm = k > 0 ? q - kTileW : q;          // in-range address; term skipped at k = 0
-            const int qp = k < nzp - 1 ? q + kTileW : q;
+            const int q = k * TW + j;
+            const int qm = k > 0 ? q - TW : q;          // in-range address; term skipped at k = 0
+            const int qp = k < nzp - 1 ? q + TW : q;
             double acc = S.D[q] * S.u[q];
             const double lo = S.U[qm] * S.u[qm];
             const double hi = S.U[q] * S.u[qp];
             acc = (k > 0) ? acc + lo : acc;
             acc = (k < nz - 1) ? acc + hi : acc;
-            acc = acc + S.H0[q] * tile_nb(S, k, l0);
-            acc = acc + S.H1[q] * tile_nb(S, k, l1);
-            acc = acc + S.H2[q] * tile_nb(S, k, l2);
+            acc = acc + S.H0[q] * tile_nb<TW>(S, k, l0);
+            acc = acc + S.H1[q] * tile_nb<TW>(S, k, l1);
+            acc = acc + S.H2[q] * tile_nb<TW>(S, k, l2);
             r[i] = S.b[q] - acc;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = r[i];
+        for (int i = 0; i < 8; ++i) S.z[(k0 + i) * TW + j] = r[i];
     }
 }
 
 // One sweep: S.u <- S.u + omega T^{-1}(b - H^ S.u)   (zero: S.u <- omega T^{-1} b).
 // Warp-synchronous; every lane of the warp must call it.
+template <int TW = kTileW>
 __device__ __forceinline__ void tile_sweep(const TileSmem& S, int nz, int j, int l0, int l1, int l2, bool zero,
                                            double omega, bool valid) {
     const int nzp = (nz + 7) & ~7;
-    tile_residuals(S, nz, j, l0, l1, l2, zero);
+    tile_residuals<TW>(S, nz, j, l0, l1, l2, zero);
     // pass 2: z_k = (r_k - U_{k-1} z_{k-1}) / den_k, operands of 8 layers per batch
     bool slow = false;
     double zprev = 0.0;
@@ -94,9 +100,9 @@ __device__ __forceinline__ void tile_sweep(const TileSmem& S, int nz, int j, int
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int k = k0 + i;
-            const int q = k * kTileW + j;
+            const int q = k * TW + j;
             rr[i] = S.z[q];
-            um[i] = S.U[k > 0 ? q - kTileW : q];
+            um[i] = S.U[k > 0 ? q - TW : q];
             dd[i] = S.den[q];
             yy[i] = S.y[q];
         }
@@ -111,18 +117,18 @@ __device__ __forceinline__ void tile_sweep(const TileSmem& S, int nz, int j, int
             zprev = zk;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = rr[i];
+        for (int i = 0; i < 8; ++i) S.z[(k0 + i) * TW + j] = rr[i];
     }
     if (__any_sync(0xffffffffu, slow && valid)) {  // rare: recompute with '/' (bitwise the same as the oracle)
 #ifdef HMG_TIMING
         if (j == 0) atomicAdd(&g_tile_slow_count, 1ull);
 #endif
         __syncwarp();
-        tile_residuals(S, nz, j, l0, l1, l2, zero);
+        tile_residuals<TW>(S, nz, j, l0, l1, l2, zero);
         zprev = 0.0;
         for (int k = 0; k < nz; ++k) {
-            const int q = k * kTileW + j;
-            const double num = (k == 0) ? S.z[q] : S.z[q] - S.U[q - kTileW] * zprev;
+            const int q = k * TW + j;
+            const double num = (k == 0) ? S.z[q] : S.z[q] - S.U[q - TW] * zprev;
             const double zk = num / S.den[q];
             S.z[q] = zk;
             zprev = zk;
@@ -135,7 +141,7 @@ __device__ __forceinline__ void tile_sweep(const TileSmem& S, int nz, int j, int
         double zz[8], gg[8], uo[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const int q = (k1 - i) * kTileW + j;
+            const int q = (k1 - i) * TW + j;
             zz[i] = S.z[q];
             gg[i] = S.g[q];
             uo[i] = S.u[q];
@@ -147,7 +153,7 @@ __device__ __forceinline__ void tile_sweep(const TileSmem& S, int nz, int j, int
             uo[i] = zero ? omega * dl : uo[i] + omega * dl;
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) S.u[(k1 - i) * kTileW + j] = uo[i];
+        for (int i = 0; i < 8; ++i) S.u[(k1 - i) * TW + j] = uo[i];
     }
     __syncwarp();
 }
@@ -158,6 +164,7 @@ __device__ __forceinline__ void tile_sweep(const TileSmem& S, int nz, int j, int
 // back substitution (latency-bound: more warps cannot shorten a column's
 // chain).  Every thread of the CTA must call it; `lane` is the column.
 constexpr int kTileWarps = 4;
+template <int TW = kTileW>
 __device__ __forceinline__ void tile_residuals_cta(const TileSmem& S, int nz, int warp, int j, int l0, int l1, int l2,
                                                    bool zero) {
     const int nzp = (nz + 7) & ~7;
@@ -165,34 +172,35 @@ __device__ __forceinline__ void tile_residuals_cta(const TileSmem& S, int nz, in
         double r[8];
         if (zero) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) r[i] = S.b[(k0 + i) * kTileW + j];
+            for (int i = 0; i < 8; ++i) r[i] = S.b[(k0 + i) * TW + j];
         } else {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const int k = k0 + i;
-                const int q = k * kTileW + j;
-                const int qm = k > 0 ? q - kTileW : q;          // in-range address; term skipped at k = 0
-                const int qp = k < nzp - 1 ? q + kTileW : q;
+                const int q = k * TW + j;
+                const int qm = k > 0 ? q - TW : q;          // in-range address; term skipped at k = 0
+                const int qp = k < nzp - 1 ? q + TW : q;
                 double acc = S.D[q] * S.u[q];
                 const double lo = S.U[qm] * S.u[qm];
                 const double hi = S.U[q] * S.u[qp];
                 acc = (k > 0) ? acc + lo : acc;
                 acc = (k < nz - 1) ? acc + hi : acc;
-                acc = acc + S.H0[q] * tile_nb(S, k, l0);
-                acc = acc + S.H1[q] * tile_nb(S, k, l1);
-                acc = acc + S.H2[q] * tile_nb(S, k, l2);
+                acc = acc + S.H0[q] * tile_nb<TW>(S, k, l0);
+                acc = acc + S.H1[q] * tile_nb<TW>(S, k, l1);
+                acc = acc + S.H2[q] * tile_nb<TW>(S, k, l2);
                 r[i] = S.b[q] - acc;
             }
         }
 #pragma unroll
-        for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = r[i];
+        for (int i = 0; i < 8; ++i) S.z[(k0 + i) * TW + j] = r[i];
     }
 }
 
+template <int TW = kTileW>
 __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int warp, int j, int l0, int l1, int l2,
                                                bool zero, double omega, bool valid) {
     const int nzp = (nz + 7) & ~7;
-    tile_residuals_cta(S, nz, warp, j, l0, l1, l2, zero);
+    tile_residuals_cta<TW>(S, nz, warp, j, l0, l1, l2, zero);
     __syncthreads();
     if (warp == 0) {
         bool slow = false;
@@ -202,9 +210,9 @@ __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int wa
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const int k = k0 + i;
-                const int q = k * kTileW + j;
+                const int q = k * TW + j;
                 rr[i] = S.z[q];
-                um[i] = S.U[k > 0 ? q - kTileW : q];
+                um[i] = S.U[k > 0 ? q - TW : q];
                 dd[i] = S.den[q];
                 yy[i] = S.y[q];
             }
@@ -219,18 +227,18 @@ __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int wa
                 zprev = zk;
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) S.z[(k0 + i) * kTileW + j] = rr[i];
+            for (int i = 0; i < 8; ++i) S.z[(k0 + i) * TW + j] = rr[i];
         }
         if (__any_sync(0xffffffffu, slow && valid)) {  // rare: recompute with '/' (bitwise the same as the oracle)
 #ifdef HMG_TIMING
             if (j == 0) atomicAdd(&g_tile_slow_count, 1ull);
 #endif
             __syncwarp();
-            tile_residuals(S, nz, j, l0, l1, l2, zero);
+            tile_residuals<TW>(S, nz, j, l0, l1, l2, zero);
             zprev = 0.0;
             for (int k = 0; k < nz; ++k) {
-                const int q = k * kTileW + j;
-                const double num = (k == 0) ? S.z[q] : S.z[q] - S.U[q - kTileW] * zprev;
+                const int q = k * TW + j;
+                const double num = (k == 0) ? S.z[q] : S.z[q] - S.U[q - TW] * zprev;
                 const double zk = num / S.den[q];
                 S.z[q] = zk;
                 zprev = zk;
@@ -242,7 +250,7 @@ __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int wa
             double zz[8], gg[8], uo[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const int q = (k1 - i) * kTileW + j;
+                const int q = (k1 - i) * TW + j;
                 zz[i] = S.z[q];
                 gg[i] = S.g[q];
                 uo[i] = S.u[q];
@@ -254,7 +262,7 @@ __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int wa
                 uo[i] = zero ? omega * dl : uo[i] + omega * dl;
             }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) S.u[(k1 - i) * kTileW + j] = uo[i];
+            for (int i = 0; i < 8; ++i) S.u[(k1 - i) * TW + j] = uo[i];
         }
     }
     __syncthreads();
