@@ -188,6 +188,22 @@ hmg_status hmg_pcg_solve_host(const hmg_hierarchy* h, const hmg_mg_params* p, co
                               double* x_host, double rtol, int maxit, int* iters, double* relres,
                               void* stream);
 
+/* Pipelined end-to-end entry point for a stream of right-hand sides: solves
+ * H^ x_i = b_i for i = 0 .. nrhs-1 (HOST buffers b_host[i], x_host[i], each
+ * [nlayers][ncells_fine] dense, as hmg_pcg_solve_host), one solve after the
+ * other on `stream`, with the host->device copy of b_{i+1} and the
+ * device->host copy of x_{i-1} on two internal copy streams overlapping solve
+ * i (two device staging pairs, ordered by events).  Each solve is exactly
+ * hmg_pcg_solve (same arithmetic, same results).  For the copies to overlap,
+ * the host buffers must be page-locked (cudaHostAlloc / cudaHostRegister);
+ * pageable buffers give correct results without overlap.  iters[i],
+ * relres[i]: per right-hand side.  Synchronous: returns after x_host[nrhs-1]
+ * has landed.  Returns HMG_ERR_NOT_CONVERGED if any solve hit maxit (all
+ * outputs filled); any other error stops the batch at that solve. */
+hmg_status hmg_pcg_solve_host_batch(const hmg_hierarchy* h, const hmg_mg_params* p, int nrhs,
+                                    const double* const* b_host, double* const* x_host, double rtol,
+                                    int maxit, int* iters, double* relres, void* stream);
+
 /* Same as hmg_pcg_solve but preconditioned by `nsweeps` line-Jacobi sweeps
  * from zero on the finest level: the paper's single-level method
  * ("two iterations of Block-Jacobi vertical line relaxation"). */

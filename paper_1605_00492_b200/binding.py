@@ -77,6 +77,7 @@ def load_library():
         "hmg_vcycle": [P, pP, P, P, P],
         "hmg_pcg_solve": [P, pP, P, P, D, I, pI, pD, P],
         "hmg_pcg_solve_host": [P, pP, P, P, D, I, pI, pD, P],
+        "hmg_pcg_solve_host_batch": [P, pP, I, P, P, D, I, pI, pD, P],
         "hmg_pcg_solve_single_level": [P, I, D, P, P, D, I, pI, pD, P],
         "hmg_export_level": [P, I, P, P, P, P],
         "hmg_selftest_div": [P, P, P, P, I64, P],
@@ -284,6 +285,26 @@ class Hierarchy:
                                                         x.ctypes.data_as(ctypes.c_void_p), rtol, maxit,
                                                         ctypes.byref(it), ctypes.byref(rr), _stream()), allow=(5,))
         return x, it.value, rr.value, STATUS[code]
+
+    def pcg_solve_host_batch(self, bs, xs, rtol: float = 1e-8, maxit: int = 200,
+                             params: MGParams = MGParams()):
+        """Pipelined end-to-end solves of several right-hand sides: host arrays
+        bs[i] -> xs[i], each [nz][n] float64 C-contiguous (page-locked for the
+        copy/compute overlap).  Returns (iters list, relres list, status)."""
+        k = len(bs)
+        if len(xs) != k:
+            raise ValueError("bs and xs must have the same length")
+        for a in list(bs) + list(xs):
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError("host buffers must be C-contiguous float64")
+        bp = (ctypes.c_void_p * max(k, 1))(*[a.ctypes.data for a in bs])
+        xp = (ctypes.c_void_p * max(k, 1))(*[a.ctypes.data for a in xs])
+        it = (ctypes.c_int * max(k, 1))()
+        rr = (ctypes.c_double * max(k, 1))()
+        p = params.c()
+        code = _check(load_library().hmg_pcg_solve_host_batch(self._h, ctypes.byref(p), k, bp, xp, rtol, maxit,
+                                                              it, rr, _stream()), allow=(5,))
+        return list(it)[:k], list(rr)[:k], STATUS[code]
 
     # -- diagnostics -----------------------------------------------------------
     KERNEL_CLASSES = {"apply": 0, "sweep_zero": 1, "sweep": 2, "sweep_prolong": 3, "resid_restrict": 4,

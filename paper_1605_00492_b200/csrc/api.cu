@@ -82,6 +82,12 @@ hmg_status check_ptr(const void* p, const char* name) {
     return HMG_OK;
 }
 
+// host scalar / pointer-array arguments: non-null only
+hmg_status check_out(const void* p, const char* name) {
+    if (!p) return fail(HMG_ERR_INVALID_ARG, std::string(name) + ": null pointer");
+    return HMG_OK;
+}
+
 hmg_status check_params(const hmg_mg_params* p) {
     if (!p) return fail(HMG_ERR_INVALID_ARG, "p: null parameters");
     if (p->nu_pre < 0) return fail(HMG_ERR_INVALID_ARG, "p->nu_pre: must be >= 0");
@@ -119,6 +125,12 @@ void free_hierarchy(Hierarchy* H) {
     }
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q); cudaFree(H->p2);
     cudaFree(H->partials); cudaFree(H->scal); cudaFree(H->hb); cudaFree(H->hx);
+    cudaFree(H->hb1); cudaFree(H->hx1);
+    if (H->cs_in) cudaStreamDestroy(H->cs_in);
+    if (H->cs_out) cudaStreamDestroy(H->cs_out);
+    for (int i = 0; i < 2; ++i)
+        for (cudaEvent_t e : {H->ev_in[i], H->ev_solved[i], H->ev_out[i]})
+            if (e) cudaEventDestroy(e);
     if (H->scal_host) cudaFreeHost(H->scal_host);
     for (cudaEvent_t e : H->prof.pool) cudaEventDestroy(e);
     cudaFree(H->gbuf_send); cudaFree(H->gbuf_recv);
@@ -291,7 +303,6 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     launch_dot(H, F, r0, r0, s);
     launch_finalize(H, kFinBB, s);
     HMG_TRY(check_launch());
-    HMG_CUDA(cudaMemcpyAsync(H.scal_host, H.scal, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
     HMG_CUDA(cudaStreamSynchronize(s));
     const double bn = std::sqrt(H.scal_host->bb);
     if (bn == 0.0) {
@@ -339,7 +350,6 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
             launch_update_xr(H, F, x, pc, s);      // x += alpha p, r -= alpha q, partial <r, r>
         launch_finalize(H, kFinRR, s);
         HMG_TRY(check_launch());
-        HMG_CUDA(cudaMemcpyAsync(H.scal_host, H.scal, sizeof(PcgScalars), cudaMemcpyDeviceToHost, s));
         HMG_CUDA(cudaStreamSynchronize(s));
         if (H.scal_host->bad != ~0ull) return check_bad(H, s);
         const double rn = std::sqrt(H.scal_host->rr);
@@ -702,7 +712,8 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     H->npartials = partials_needed(F.n, nlayers) + 148 * 8 + 64;
     BCUDA(cudaMalloc(&H->partials, sizeof(double) * H->npartials));
     BCUDA(cudaMalloc(&H->scal, sizeof(PcgScalars)));
-    BCUDA(cudaMallocHost(&H->scal_host, sizeof(PcgScalars)));
+    BCUDA(cudaHostAlloc(&H->scal_host, sizeof(PcgScalars), cudaHostAllocMapped));
+    BCUDA(cudaHostGetDevicePointer(&H->scal_pub, H->scal_host, 0));
     PcgScalars init{};
     init.bad = ~0ull;
     BCUDA(cudaMemcpy(H->scal, &init, sizeof(init), cudaMemcpyHostToDevice));
@@ -926,8 +937,8 @@ hmg_status hmg_pcg_solve(const hmg_hierarchy* h, const hmg_mg_params* p, const d
     HMG_TRY(check_params(p));
     HMG_TRY(check_ptr(b, "b"));
     HMG_TRY(check_ptr(x, "x"));
-    HMG_TRY(check_ptr(iters, "iters"));
-    HMG_TRY(check_ptr(relres, "relres"));
+    HMG_TRY(check_out(iters, "iters"));
+    HMG_TRY(check_out(relres, "relres"));
     if (b == x) return fail(HMG_ERR_INVALID_ARG, "x: must not alias b");
     if (!(rtol >= 0)) return fail(HMG_ERR_INVALID_ARG, "rtol: must be >= 0");
     if (maxit < 0) return fail(HMG_ERR_INVALID_ARG, "maxit: must be >= 0");
@@ -942,8 +953,8 @@ hmg_status hmg_pcg_solve_single_level(const hmg_hierarchy* h, int nsweeps, doubl
     if (!std::isfinite(omega)) return fail(HMG_ERR_INVALID_ARG, "omega: must be finite");
     HMG_TRY(check_ptr(b, "b"));
     HMG_TRY(check_ptr(x, "x"));
-    HMG_TRY(check_ptr(iters, "iters"));
-    HMG_TRY(check_ptr(relres, "relres"));
+    HMG_TRY(check_out(iters, "iters"));
+    HMG_TRY(check_out(relres, "relres"));
     if (b == x) return fail(HMG_ERR_INVALID_ARG, "x: must not alias b");
     if (!(rtol >= 0)) return fail(HMG_ERR_INVALID_ARG, "rtol: must be >= 0");
     if (maxit < 0) return fail(HMG_ERR_INVALID_ARG, "maxit: must be >= 0");
@@ -954,8 +965,8 @@ hmg_status hmg_pcg_solve_host(const hmg_hierarchy* h, const hmg_mg_params* p, co
                               double rtol, int maxit, int* iters, double* relres, void* stream) {
     HMG_TRY(check_h(h));
     Hierarchy& H = const_cast<Hierarchy&>(HH(h));
-    HMG_TRY(check_ptr(b_host, "b_host"));
-    HMG_TRY(check_ptr(x_host, "x_host"));
+    HMG_TRY(check_out(b_host, "b_host"));
+    HMG_TRY(check_out(x_host, "x_host"));
     const DevLevel& F = H.lev[H.fine_ref];
     const size_t vb = sizeof(double) * H.nz * F.ld;
     if (!H.hb) {
@@ -973,6 +984,89 @@ hmg_status hmg_pcg_solve_host(const hmg_hierarchy* h, const hmg_mg_params* p, co
     HMG_CUDA(cudaStreamSynchronize(s));
     g_err = msg;
     return st;
+}
+
+hmg_status hmg_pcg_solve_host_batch(const hmg_hierarchy* h, const hmg_mg_params* p, int nrhs,
+                                    const double* const* b_host, double* const* x_host, double rtol, int maxit,
+                                    int* iters, double* relres, void* stream) {
+    HMG_TRY(check_h(h));
+    Hierarchy& H = const_cast<Hierarchy&>(HH(h));
+    if (nrhs < 0) return fail(HMG_ERR_INVALID_ARG, "nrhs: must be >= 0");
+    if (nrhs == 0) return HMG_OK;
+    HMG_TRY(check_out(b_host, "b_host"));
+    HMG_TRY(check_out(x_host, "x_host"));
+    HMG_TRY(check_out(iters, "iters"));
+    HMG_TRY(check_out(relres, "relres"));
+    for (int i = 0; i < nrhs; ++i) {
+        if (!b_host[i]) return fail(HMG_ERR_INVALID_ARG, "b_host[" + std::to_string(i) + "]: null pointer");
+        if (!x_host[i]) return fail(HMG_ERR_INVALID_ARG, "x_host[" + std::to_string(i) + "]: null pointer");
+    }
+    HMG_CUDA(cudaSetDevice(H.device));
+    const DevLevel& F = H.lev[H.fine_ref];
+    const size_t vb = sizeof(double) * H.nz * F.ld;
+    if (!H.hb) {
+        HMG_CUDA(cudaMalloc(&H.hb, vb));
+        HMG_CUDA(cudaMalloc(&H.hx, vb));
+    }
+    if (!H.hb1) {
+        HMG_CUDA(cudaMalloc(&H.hb1, vb));
+        HMG_CUDA(cudaMalloc(&H.hx1, vb));
+        HMG_CUDA(cudaStreamCreateWithFlags(&H.cs_in, cudaStreamNonBlocking));
+        HMG_CUDA(cudaStreamCreateWithFlags(&H.cs_out, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            HMG_CUDA(cudaEventCreateWithFlags(&H.ev_in[i], cudaEventDisableTiming));
+            HMG_CUDA(cudaEventCreateWithFlags(&H.ev_solved[i], cudaEventDisableTiming));
+            HMG_CUDA(cudaEventCreateWithFlags(&H.ev_out[i], cudaEventDisableTiming));
+        }
+    }
+    double* const dB[2] = {H.hb, H.hb1};
+    double* const dX[2] = {H.hx, H.hx1};
+    cudaStream_t s = S(stream);
+    const size_t hp = sizeof(double) * F.n, dp = sizeof(double) * F.ld;
+    // Solve i runs on `stream` from dB[i % 2] into dX[i % 2]; the copy of b_{i+1}
+    // in (cs_in) and of x_{i-1} out (cs_out) overlap it.  Buffer reuse is
+    // ordered by events: b_{i+1} lands in the buffer solve i-1 read, after that
+    // solve; solve i writes the x buffer whose copy-out (x_{i-2}) it waits for.
+    HMG_CUDA(cudaEventRecord(H.ev_solved[1], s));   // the calling stream's prior work (buffers may be in use)
+    HMG_CUDA(cudaStreamWaitEvent(H.cs_in, H.ev_solved[1], 0));
+    HMG_CUDA(cudaMemcpy2DAsync(dB[0], dp, b_host[0], hp, hp, H.nz, cudaMemcpyHostToDevice, H.cs_in));
+    HMG_CUDA(cudaEventRecord(H.ev_in[0], H.cs_in));
+    hmg_status worst = HMG_OK;
+    std::string msg;
+    for (int i = 0; i < nrhs; ++i) {
+        const int c = i & 1, o = c ^ 1;
+        if (i + 1 < nrhs) {
+            if (i >= 1) HMG_CUDA(cudaStreamWaitEvent(H.cs_in, H.ev_solved[o], 0));
+            HMG_CUDA(cudaMemcpy2DAsync(dB[o], dp, b_host[i + 1], hp, hp, H.nz, cudaMemcpyHostToDevice, H.cs_in));
+            HMG_CUDA(cudaEventRecord(H.ev_in[o], H.cs_in));
+        }
+        HMG_CUDA(cudaStreamWaitEvent(s, H.ev_in[c], 0));
+        if (i >= 2) HMG_CUDA(cudaStreamWaitEvent(s, H.ev_out[c], 0));
+        int it = 0;
+        double rr = 0.0;
+        const hmg_status st = hmg_pcg_solve(h, p, dB[c], dX[c], rtol, maxit, &it, &rr, stream);
+        iters[i] = it;
+        relres[i] = rr;
+        if (st != HMG_OK && st != HMG_ERR_NOT_CONVERGED) {
+            cudaStreamSynchronize(H.cs_in);
+            cudaStreamSynchronize(H.cs_out);
+            return st;
+        }
+        if (st != HMG_OK && worst == HMG_OK) {
+            worst = st;
+            msg = g_err;
+        }
+        HMG_CUDA(cudaEventRecord(H.ev_solved[c], s));
+        HMG_CUDA(cudaStreamWaitEvent(H.cs_out, H.ev_solved[c], 0));
+        HMG_CUDA(cudaMemcpy2DAsync(x_host[i], hp, dX[c], dp, hp, H.nz, cudaMemcpyDeviceToHost, H.cs_out));
+        HMG_CUDA(cudaEventRecord(H.ev_out[c], H.cs_out));
+    }
+    HMG_CUDA(cudaStreamSynchronize(H.cs_out));
+    HMG_CUDA(cudaStreamSynchronize(H.cs_in));
+    // the caller's stream is ordered after the last copy-out
+    HMG_CUDA(cudaStreamWaitEvent(s, H.ev_out[(nrhs - 1) & 1], 0));
+    g_err = msg;
+    return worst;
 }
 
 hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, double* geom, double* bands, double* lam) {

@@ -151,8 +151,14 @@ struct Hierarchy {
     double* partials = nullptr; // per-block partial sums (deterministic reductions)
     int npartials = 0;
     PcgScalars* scal = nullptr; // device
-    PcgScalars* scal_host = nullptr;  // pinned
+    PcgScalars* scal_host = nullptr;  // mapped pinned host memory, written by the finalize kernels
+    PcgScalars* scal_pub = nullptr;   // its device alias
     double *hb = nullptr, *hx = nullptr;  // device staging for the host entry point
+    // pipelined host batch (hmg_pcg_solve_host_batch): second staging pair,
+    // copy-in / copy-out streams and their events
+    double *hb1 = nullptr, *hx1 = nullptr;
+    cudaStream_t cs_in = nullptr, cs_out = nullptr;
+    cudaEvent_t ev_in[2] = {}, ev_solved[2] = {}, ev_out[2] = {};
     int tail_ref = -1;          // levels <= tail_ref run in one coarse-tail launch (-1: off)
     bool tail_grid = false;     // the tail is a cooperative multi-CTA launch (false: one CTA)
     int tail_threads = 64;      // threads per CTA of the cooperative tail

@@ -521,8 +521,16 @@ __device__ __forceinline__ void scalar_op(PcgScalars* sc, int op, double S) {
     }
 }
 
+// pub: non-null for the scalars the host reads (||b||^2, ||r||^2 with the
+// singular-pivot flag): the updated struct is also written to mapped pinned
+// host memory, so the host's read needs no copy-engine transfer (which would
+// queue behind a large device->host copy on another stream)
+__device__ __forceinline__ void publish(const PcgScalars* sc, PcgScalars* pub) {
+    if (pub) *pub = *sc;
+}
+
 __global__ void __launch_bounds__(kFinThreads) k_finalize(const double* __restrict__ partial, int np, int op,
-                                                          PcgScalars* __restrict__ sc) {
+                                                          PcgScalars* __restrict__ sc, PcgScalars* pub) {
     __shared__ double red[kFinThreads / 32];
     double s = 0.0;
     for (int i = threadIdx.x; i < np; i += kFinThreads) s = s + partial[i];
@@ -533,9 +541,13 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(const double* __restri
         return;
     }
     scalar_op(sc, op, S);
+    publish(sc, pub);
 }
 
-__global__ void k_scalar_op(PcgScalars* __restrict__ sc, int op) { scalar_op(sc, op, sc->tmp); }
+__global__ void k_scalar_op(PcgScalars* __restrict__ sc, int op, PcgScalars* pub) {
+    scalar_op(sc, op, sc->tmp);
+    publish(sc, pub);
+}
 
 __global__ void k_copy_rows(const double* __restrict__ src, int64_t sld, double* __restrict__ dst, int64_t dld,
                             int64_t n) {
@@ -604,15 +616,16 @@ ProfScope::~ProfScope() {
 // Sum of the per-block partials into the PCG scalar `op`; across ranks
 // (multi-GPU) the rank-local totals are all-reduced first.
 void finalize_parts(const Hierarchy& H, int nparts, int op, cudaStream_t s) {
+    PcgScalars* pub = (op == kFinBB || op == kFinRR) ? H.scal_pub : nullptr;
     if (!H.comm || (H.nranks == 1 && !H.force_coll)) {
-        k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, op, H.scal);
+        k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, op, H.scal, pub);
         ++H.launches;
         return;
     }
-    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, -1, H.scal);
+    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, -1, H.scal, nullptr);
     ++H.launches;
     dist_allreduce_tmp(H, s);
-    k_scalar_op<<<1, 1, 0, s>>>(H.scal, op);
+    k_scalar_op<<<1, 1, 0, s>>>(H.scal, op, pub);
     ++H.launches;
 }
 
@@ -763,12 +776,12 @@ void launch_finalize(const Hierarchy& H, int op, cudaStream_t s) {
 }
 
 void launch_finalize_local(const Hierarchy& H, int nparts, cudaStream_t s) {
-    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, -1, H.scal);
+    k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, -1, H.scal, nullptr);
     ++H.launches;
 }
 
 void launch_scalar_op(const Hierarchy& H, int op, cudaStream_t s) {
-    k_scalar_op<<<1, 1, 0, s>>>(H.scal, op);
+    k_scalar_op<<<1, 1, 0, s>>>(H.scal, op, nullptr);
     ++H.launches;
 }
 

@@ -148,6 +148,28 @@ def test_host_entry_point(pair):
     assert np.array_equal(x, g.to_host(cfg.fine_ref, xd))
 
 
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_batch_entry_point(pair, pinned):
+    """Pipelined batch (copies on their own streams, two staging pairs): every
+    solve bitwise equal to the one-at-a-time solve, for 5 different right-hand
+    sides (odd count: both staging buffers reused), pinned and pageable."""
+    cfg, g, o, lam, b = pair
+    bs = [np.ascontiguousarray(b * (1.0 + 0.25 * i) + hi.uniform_vector(b.shape, 100 + i) * (i % 2))
+          for i in range(5)]
+    if pinned:
+        bs = [torch.from_numpy(v).pin_memory().numpy() for v in bs]
+        xs = [torch.empty(b.shape, dtype=torch.float64).pin_memory().numpy() for _ in bs]
+    else:
+        xs = [np.empty_like(v) for v in bs]
+    its, rrs, st = g.pcg_solve_host_batch(bs, xs)
+    assert st == "HMG_OK"
+    for v, x, it, rr in zip(bs, xs, its, rrs):
+        x1, it1, rr1, st1 = g.pcg_solve_host(v)
+        assert st1 == "HMG_OK" and it == it1 and rr == rr1
+        assert np.array_equal(x, x1)
+    assert g.pcg_solve_host_batch([], []) == ([], [], "HMG_OK")
+
+
 def test_padding_untouched_and_ignored():
     """ref 0 (20 cells, ld 32) and ref 1 (80 cells, ld 96): padding entries are
     never read (NaN there changes nothing) and never written."""
