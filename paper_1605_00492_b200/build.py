@@ -10,6 +10,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -34,15 +35,29 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp, "-ldl"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(HERE, "build")
+    os.makedirs(objdir, exist_ok=True)
+    # one nvcc per translation unit, in parallel, then one link
+    jobs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, src + f".{os.getpid()}.o")
+        jobs.append(([NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj], obj))
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(lambda j: subprocess.run(j[0], capture_output=True, text=True), jobs))
+    link = [NVCC, *ARCH, "-shared", *[o for _, o in jobs], "-o", tmp, "-ldl"]
+    results.append(subprocess.run(link, capture_output=True, text=True) if all(r.returncode == 0 for r in results)
+                   else subprocess.CompletedProcess(link, 1, "", "link skipped: compile failed\n"))
+    log = "".join(" ".join(c) + "\n" + r.stdout + r.stderr for c, r in zip([j[0] for j in jobs] + [link], results))
     with open(os.path.join(HERE, "build.log"), "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+        fh.write(log)
+    for _, o in jobs:
+        if os.path.exists(o):
+            os.remove(o)
+    if any(r.returncode != 0 for r in results):
+        sys.stderr.write(log)
         raise RuntimeError("nvcc failed building libhmg.so (see paper_1605_00492_b200/build.log)")
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write(log)
     os.replace(tmp, LIB)
     return LIB
 
