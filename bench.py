@@ -485,7 +485,7 @@ def run_c1(args):
         "config": {"workload": "C1: ref 5 x 64 layers, 1,310,720 dofs; t 0.01, w2 1e-4",
                    "cache": "L2 evicted (256 MB read) before every launch; 'warm': 100 launches back to back, "
                             "working set (84 MB) L2-resident"},
-        "roofline": {"kernel": "k_apply_t (operator apply, ref 5)", "bound": "hbm", "achieved": a["GB/s"],
+        "roofline": {"kernel": "k_apply_st (operator apply, ref 5)", "bound": "hbm", "achieved": a["GB/s"],
                      "peak": peak, "unit": "GB/s", "frac": a["frac"], "peak_source": peak_note},
         "kernels": out}))
 

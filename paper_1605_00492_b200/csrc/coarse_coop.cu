@@ -178,6 +178,26 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         l1 = (loc >> 8) & 0xff;
         l2 = (loc >> 16) & 0xff;
     };
+    // What the vector planes hold: sb = tile res_t of res_b, su = the same tile
+    // of res_u (the iterate this CTA last wrote or read for it).  A CTA that
+    // owns a single tile of a level keeps both across that level's steps and
+    // gathers only the off-tile neighbours again.
+    const double* res_b = nullptr;
+    const double* res_u = nullptr;
+    int res_t = -1;
+    auto load_vectors = [&](const CoopLevel& L, int t, const double* bl, const double* uin) {
+        const bool keep_b = t == res_t && bl == res_b;
+        if (!keep_b) cp_rows(sb, bl, L.V.ld, (int64_t)t * TW, TW);
+        if (uin) {
+            if (!(keep_b && uin == res_u)) cp_rows(su, uin, L.V.ld, (int64_t)t * TW, TW);
+            cp_halo(shu, uin, L, t, 0, L.V.ld);
+        }
+    };
+    auto resident = [&](int t, const double* bl, const double* u) {
+        res_t = t;
+        res_b = bl;
+        res_u = u;
+    };
     // one damped sweep of level l from iterate uin (nullptr: zero guess) to uout, all tiles
     auto sweep_step = [&](int l, const double* bl, const double* uin, double* uout) {
         const CoopLevel& L = LV[l];
@@ -186,17 +206,14 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
             int l0, l1, l2;
             slots(L, c, l0, l1, l2);
             __syncthreads();                           // every thread is done with the previous tile's planes
-            cp_rows(sb, bl, L.V.ld, (int64_t)t * TW, TW);
-            if (uin) {
-                cp_rows(su, uin, L.V.ld, (int64_t)t * TW, TW);
-                cp_halo(shu, uin, L, t, 0, L.V.ld);
-            }
+            load_vectors(L, t, bl, uin);
             load_static(l, t);
             cp_wait();
             CSTAMP();
             tile_sweep_cta<TW>(S, nz, warp, j, l0, l1, l2, uin == nullptr, P.omega, jlane && c < L.V.n);
             CSTAMP();
             store_own(uout, L, c);
+            resident(t, bl, uout);
         }
     };
 
@@ -220,13 +237,10 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
             int l0, l1, l2;
             slots(L, c, l0, l1, l2);
             __syncthreads();
-            cp_rows(sb, bl, L.V.ld, (int64_t)t * TW, TW);
-            if (c_in) {
-                cp_rows(su, c_in, L.V.ld, (int64_t)t * TW, TW);
-                cp_halo(shu, c_in, L, t, 0, L.V.ld);
-            }
+            load_vectors(L, t, bl, c_in);
             load_static(l, t);
             cp_wait();
+            resident(t, bl, c_in);
             CSTAMP();
             tile_residuals_cta<TW>(S, nz, warp, j, l0, l1, l2, c_in == nullptr);   // r = b - H^ u (r = b from zero)
             __syncthreads();
@@ -264,6 +278,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
                     tile_sweep_cta<TW>(S, nz, warp, j, l0, l1, l2, s == 0, P.omega, jlane && c < L.V.n);
                 CSTAMP();
                 store_own(out, L, c);
+                resident(0, bl, out);
             }
         } else {
             const double* c_in = nullptr;
@@ -319,6 +334,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
             if (P.nu_post > 0) tile_sweep_cta<TW>(S, nz, warp, j, l0, l1, l2, false, P.omega, jlane && valid);
             CSTAMP();
             store_own(dst, L, c);
+            resident(t, bl, dst);
         }
         grid.sync();
         CSTAMP();
