@@ -72,6 +72,18 @@ def _load():
             lib.ora_pcg.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                     ctypes.c_double, P, P, ctypes.c_double, ctypes.c_int,
                                     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), P]
+            lib.ora_mixed_nedges.argtypes = [P]
+            lib.ora_mixed_nedges.restype = ctypes.c_int64
+            lib.ora_mixed_size.argtypes = [P]
+            lib.ora_mixed_size.restype = ctypes.c_int64
+            lib.ora_mixed_edges.argtypes = [P, P, P, P]
+            lib.ora_mixed_part.argtypes = [P, ctypes.c_int, P, P, P, P, P, P]
+            lib.ora_mixed_apply.argtypes = [P, P, P]
+            lib.ora_mixed_precond.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                              ctypes.c_double, P, P]
+            lib.ora_mixed_gmres.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_int, P, P,
+                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), P]
             lib.ora_last_error.restype = ctypes.c_char_p
             _lib = lib
     return _lib
@@ -210,5 +222,76 @@ class Hierarchy:
         code = _load().ora_pcg(self._h, kind, nu_pre, nu_post, n_coarse, omega, _ptr(b), _ptr(x),
                                rtol, maxit, ctypes.byref(it), ctypes.byref(rr), _ptr(hist))
         if code not in (0, NOT_CONVERGED) or (raise_on_fail and code):
+            _check(code)
+        return x, it.value, rr.value, hist[: it.value + 1], code
+
+    # ---- NEXT-4: mixed velocity-pressure system (readings R15-R20) ----
+    def mixed_sizes(self):
+        """(ne, N): fine-level edge count and the mixed vector length
+        nz*ne + (nz-1)*n + nz*n (blocks [U_h | U_z | P])."""
+        lib = _load()
+        return int(lib.ora_mixed_nedges(self._h)), int(lib.ora_mixed_size(self._h))
+
+    def mixed_split(self, x):
+        """Views (U_h [nz][ne], U_z [nz-1][n], P [nz][n]) of a mixed vector."""
+        ne, _ = self.mixed_sizes()
+        nz, n = self.nz, self.n(self.fine_ref)
+        a, b = nz * ne, nz * ne + (nz - 1) * n
+        return x[:a].reshape(nz, ne), x[a:b].reshape(nz - 1, n), x[b:].reshape(nz, n)
+
+    def mixed_edges(self):
+        """Edge table (reading R16): ec [ne][2] cells (a < b), es [ne][2]
+        slots, ce [n][3] edge across each slot."""
+        ne, _ = self.mixed_sizes()
+        n = self.n(self.fine_ref)
+        ec, es, ce = np.empty((ne, 2), np.int32), np.empty((ne, 2), np.int32), np.empty((n, 3), np.int32)
+        _check(_load().ora_mixed_edges(self._h, _ptr(ec), _ptr(es), _ptr(ce)))
+        return ec, es, ce
+
+    def mixed_part(self, which: str, Uh=None, Uz=None, P=None):
+        """One operator of the mixed system: 'div' (U -> p), 'divT' (P -> U),
+        'mass' (M2), 'lumped_inv' (L^-1), 'gram' (RT0 Gram matrices [n][3][3])."""
+        ne, _ = self.mixed_sizes()
+        nz, n = self.nz, self.n(self.fine_ref)
+        code = {"div": 0, "divT": 1, "mass": 2, "lumped_inv": 3, "gram": 4}[which]
+        Uh = None if Uh is None else _f64(Uh)
+        Uz = None if Uz is None else _f64(Uz)
+        P = None if P is None else _f64(P)
+        yh = np.zeros((n, 3, 3)) if which == "gram" else np.zeros((nz, ne))
+        yz, yp = np.zeros((max(nz - 1, 0), n)), np.zeros((nz, n))
+        _check(_load().ora_mixed_part(self._h, code, _ptr(Uh), _ptr(Uz), _ptr(P), _ptr(yh), _ptr(yz), _ptr(yp)))
+        if which == "div":
+            return yp
+        if which == "gram":
+            return yh
+        return yh, yz
+
+    def mixed_apply(self, x) -> np.ndarray:
+        """y = A x, A = [[M2, -omega D^T], [omega D, M3]], omega = sqrt(w2)."""
+        x = _f64(x)
+        y = np.empty_like(x)
+        _check(_load().ora_mixed_apply(self._h, _ptr(x), _ptr(y)))
+        return y
+
+    def mixed_precond(self, f, precond="schur", nu_pre=2, nu_post=2, n_coarse=20, omega=0.8) -> np.ndarray:
+        """Schur-complement preconditioner (Eq. 6, lumped mass, one V-cycle)."""
+        f = _f64(f)
+        x = np.empty_like(f)
+        kind = {"none": 0, "schur": 1}[precond]
+        _check(_load().ora_mixed_precond(self._h, kind, nu_pre, nu_post, n_coarse, omega, _ptr(f), _ptr(x)))
+        return x
+
+    def mixed_gmres(self, F, rtol=1e-5, restart=30, maxit=300, precond="schur", nu_pre=2, nu_post=2, n_coarse=20,
+                    omega=0.8):
+        """Right-preconditioned GMRES(restart), x0 = 0.  Returns (x, iters, relres, history, status)."""
+        F = _f64(F)
+        x = np.empty_like(F)
+        it = ctypes.c_int(0)
+        rr = ctypes.c_double(0.0)
+        hist = np.zeros(maxit + 1)
+        kind = {"none": 0, "schur": 1}[precond]
+        code = _load().ora_mixed_gmres(self._h, kind, nu_pre, nu_post, n_coarse, omega, restart, rtol, maxit,
+                                       _ptr(F), _ptr(x), ctypes.byref(it), ctypes.byref(rr), _ptr(hist))
+        if code not in (0, NOT_CONVERGED):
             _check(code)
         return x, it.value, rr.value, hist[: it.value + 1], code

@@ -692,3 +692,411 @@ done:
     if (st == ORA_ERR_NOT_CONVERGED) snprintf(ora_msg, sizeof ora_msg, "not converged after %d iterations", maxit);
     return st;
 }
+
+/* ================================================================== */
+/* NEXT-4: the mixed velocity-pressure system around    */
+/* the V-cycle -- Eq. 5 with omega_N = 0, its Schur-       */
+/* complement preconditioner (Eq. 6) with a lumped velocity */
+/* mass, and restarted GMRES(30).  Readings R15-R20 of     */
+/* DESIGN.md; every loop below is per (edge, layer), per (column,      */
+/* interface) or per (cell, layer) in the canonical order stated.      */
+/*                                                                    */
+/* Unknowns (reading R15): U_h [nz][ne] normal flux through the        */
+/* vertical face of edge e in layer k, positive from cell a to cell b  */
+/* (a < b); U_z [nz-1][n] flux through interface i = 1..nz-1 of column */
+/* c (row i-1), positive upward (u.n = 0 removes i = 0 and i = nz,     */
+/* P:415-418); P [nz][n].  omega = sqrt(w2) (omega_c^2 = w2).          */
+/*   A = [[M2, -omega D^T], [omega D, M3]]                              */
+/* ================================================================== */
+
+/* Edge table of the fine level (reading R16): edges in order of their  */
+/* lower cell a, then a's slot j; b = nbr[a][j]; slot_b = the slot of b */
+/* whose neighbour is a.  ce[c][j] = edge across slot j of cell c.      */
+typedef struct {
+    int64_t ne;
+    int32_t *ec, *es, *ce;   /* [ne][2] cells (a, b), [ne][2] slots, [n][3] edges */
+} ora_edges;
+
+static void free_edges(ora_edges* E) { free(E->ec); free(E->es); free(E->ce); }
+
+static int fine_edges(const ora_h* h, ora_edges* E) {
+    const ora_level* L = &h->lev[h->fine_ref];
+    int64_t n = L->n;
+    E->ne = 3 * n / 2;
+    E->ec = (int32_t*)malloc(sizeof(int32_t) * 2 * E->ne);
+    E->es = (int32_t*)malloc(sizeof(int32_t) * 2 * E->ne);
+    E->ce = (int32_t*)malloc(sizeof(int32_t) * 3 * n);
+    if (!E->ec || !E->es || !E->ce) { free_edges(E); return ORA_ERR_OOM; }
+    int64_t e = 0;
+    for (int64_t c = 0; c < n; c++)
+        for (int j = 0; j < 3; j++) {
+            int32_t o = L->mesh.nbr[3 * c + j];
+            if (c < o) {
+                int jo = 0;
+                while (L->mesh.nbr[3 * o + jo] != (int32_t)c) jo++;
+                E->ec[2 * e] = (int32_t)c; E->ec[2 * e + 1] = o;
+                E->es[2 * e] = j; E->es[2 * e + 1] = jo;
+                E->ce[3 * c + j] = (int32_t)e;
+                E->ce[3 * o + jo] = (int32_t)e;
+                e++;
+            }
+        }
+    return ORA_OK;
+}
+
+/* sigma_{c,j}: +1 if the flux of the edge across slot j leaves c (c is  */
+/* the lower cell a), -1 otherwise.                                     */
+static double edge_sign(const ora_level* L, int64_t c, int j) {
+    return (c < L->mesh.nbr[3 * c + j]) ? 1.0 : -1.0;
+}
+
+/* Gram matrix of the outward flux-normalised RT0 functions of cell c    */
+/* (reading R17): psi_j(x) = (x - P_{j+2}) / (2|T|) on the flat chordal  */
+/* triangle (P_0, P_1, P_2), edge j = (P_j, P_{j+1}) opposite P_{j+2};    */
+/* G_{jl} = int_T psi_j . psi_l dA by the edge-midpoint rule (exact for  */
+/* quadratics): G_{jl} = ((s_0 + s_1) + s_2) / (12 |T|),                 */
+/* s_q = (m_q - P_{j+2}) . (m_q - P_{l+2}), m_q = 0.5 (P_q + P_{q+1}).    */
+static void rt0_gram(const ora_level* L, int64_t c, double G[3][3]) {
+    const double* V = L->mesh.v;
+    const int32_t* F = L->mesh.f;
+    const double* Pv[3] = {&V[3 * F[3 * c]], &V[3 * F[3 * c + 1]], &V[3 * F[3 * c + 2]]};
+    double m[3][3];
+    for (int q = 0; q < 3; q++)
+        for (int d = 0; d < 3; d++) m[q][d] = 0.5 * (Pv[q][d] + Pv[(q + 1) % 3][d]);
+    for (int j = 0; j < 3; j++)
+        for (int l = 0; l < 3; l++) {
+            const double* A = Pv[(j + 2) % 3];
+            const double* B = Pv[(l + 2) % 3];
+            double s[3];
+            for (int q = 0; q < 3; q++) {
+                double ax = m[q][0] - A[0], ay = m[q][1] - A[1], az = m[q][2] - A[2];
+                double bx = m[q][0] - B[0], by = m[q][1] - B[1], bz = m[q][2] - B[2];
+                s[q] = (ax * bx + ay * by) + az * bz;
+            }
+            G[j][l] = ((s[0] + s[1]) + s[2]) / (12.0 * L->area[c]);
+        }
+}
+
+/* Mixed-system parts (reading R18), used by the apply, the             */
+/* preconditioner and the pins:                                          */
+/*  div:   (D U)[k][c] = (((s0 U_h[E0] + s1 U_h[E1]) + s2 U_h[E2])       */
+/*                        + U_z[k+1]) - U_z[k]   (absent U_z skipped)     */
+/*  divT:  (D^T P)_h[k][e] = P[k][a] - P[k][b];                           */
+/*         (D^T P)_z[i][c] = P[i-1][c] - P[i][c]                          */
+/*  mass:  (M2 U)_h[k][e] = t_a/(dz lam_a) + t_b/(dz lam_b),              */
+/*         t_c = ((g0 U_h[E0] + g1 U_h[E1]) + g2 U_h[E2]),                */
+/*         g_l = (s_j s_l) G^c_{j l}, j = the slot of e in c;              */
+/*         (M2 U)_z[i] = ((dg W_i + lo W_{i-1}) + hi W_{i+1}),             */
+/*         dg = ((dz/3)/(area lam_{i-1})) + ((dz/3)/(area lam_i)),          */
+/*         lo = (dz/6)/(area lam_{i-1}), hi = (dz/6)/(area lam_i)           */
+/*         (P1 vertical mass of unit-flux hats, weight 1/lam per cell)     */
+/*  lumped inverse (reading R19, the two-point lumping whose Schur        */
+/*  complement is BASELINE's H^): (L^-1 U)_h = U_h ((len dz) lamf)/cd,     */
+/*  (L^-1 U)_z = U_z (area lamf)/dz, lamf = 0.5 (lam_a + lam_b).            */
+static void mixed_div(const ora_h* h, const ora_edges* E, const double* Uh, const double* Uz, double* y) {
+    const ora_level* L = &h->lev[h->fine_ref];
+    int nz = h->nz;
+    int64_t n = L->n, ne = E->ne;
+    for (int k = 0; k < nz; k++)
+        for (int64_t c = 0; c < n; c++) {
+            double d = edge_sign(L, c, 0) * Uh[(int64_t)k * ne + E->ce[3 * c]];
+            d = d + edge_sign(L, c, 1) * Uh[(int64_t)k * ne + E->ce[3 * c + 1]];
+            d = d + edge_sign(L, c, 2) * Uh[(int64_t)k * ne + E->ce[3 * c + 2]];
+            if (k + 1 <= nz - 1) d = d + Uz[(int64_t)k * n + c];         /* interface k+1: row k */
+            if (k >= 1) d = d - Uz[(int64_t)(k - 1) * n + c];             /* interface k: row k-1 */
+            y[(int64_t)k * n + c] = d;
+        }
+}
+
+static void mixed_divT(const ora_h* h, const ora_edges* E, const double* P, double* yh, double* yz) {
+    const ora_level* L = &h->lev[h->fine_ref];
+    int nz = h->nz;
+    int64_t n = L->n, ne = E->ne;
+    for (int k = 0; k < nz; k++)
+        for (int64_t e = 0; e < ne; e++)
+            yh[(int64_t)k * ne + e] = P[(int64_t)k * n + E->ec[2 * e]] - P[(int64_t)k * n + E->ec[2 * e + 1]];
+    for (int i = 1; i <= nz - 1; i++)
+        for (int64_t c = 0; c < n; c++)
+            yz[(int64_t)(i - 1) * n + c] = P[(int64_t)(i - 1) * n + c] - P[(int64_t)i * n + c];
+}
+
+static void mixed_mass(const ora_h* h, const ora_edges* E, const double* Uh, const double* Uz, double* yh,
+                       double* yz) {
+    const ora_level* L = &h->lev[h->fine_ref];
+    int nz = h->nz;
+    int64_t n = L->n, ne = E->ne;
+    double dz = h->dz;
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < ne; e++) {
+        double G[2][3][3];
+        rt0_gram(L, E->ec[2 * e], G[0]);
+        rt0_gram(L, E->ec[2 * e + 1], G[1]);
+        for (int k = 0; k < nz; k++) {
+            double m[2];
+            for (int s = 0; s < 2; s++) {
+                int64_t c = E->ec[2 * e + s];
+                int j = E->es[2 * e + s];
+                double g[3];
+                for (int l = 0; l < 3; l++) g[l] = (edge_sign(L, c, j) * edge_sign(L, c, l)) * G[s][j][l];
+                double t = g[0] * Uh[(int64_t)k * ne + E->ce[3 * c]];
+                t = t + g[1] * Uh[(int64_t)k * ne + E->ce[3 * c + 1]];
+                t = t + g[2] * Uh[(int64_t)k * ne + E->ce[3 * c + 2]];
+                m[s] = t / (dz * L->lam[(int64_t)k * n + c]);
+            }
+            yh[(int64_t)k * ne + e] = m[0] + m[1];
+        }
+    }
+    for (int i = 1; i <= nz - 1; i++)
+        for (int64_t c = 0; c < n; c++) {
+            double slo = L->area[c] * L->lam[(int64_t)(i - 1) * n + c];
+            double shi = L->area[c] * L->lam[(int64_t)i * n + c];
+            double dg = ((dz / 3.0) / slo) + ((dz / 3.0) / shi);
+            double v = dg * Uz[(int64_t)(i - 1) * n + c];
+            if (i - 1 >= 1) v = v + ((dz / 6.0) / slo) * Uz[(int64_t)(i - 2) * n + c];
+            if (i + 1 <= nz - 1) v = v + ((dz / 6.0) / shi) * Uz[(int64_t)i * n + c];
+            yz[(int64_t)(i - 1) * n + c] = v;
+        }
+}
+
+static void mixed_lumped_inv(const ora_h* h, const ora_edges* E, const double* Uh, const double* Uz, double* yh,
+                             double* yz) {
+    const ora_level* L = &h->lev[h->fine_ref];
+    int nz = h->nz;
+    int64_t n = L->n, ne = E->ne;
+    double dz = h->dz;
+    for (int k = 0; k < nz; k++)
+        for (int64_t e = 0; e < ne; e++) {
+            int64_t a = E->ec[2 * e], b = E->ec[2 * e + 1];
+            int j = E->es[2 * e];
+            double lamf = 0.5 * (L->lam[(int64_t)k * n + a] + L->lam[(int64_t)k * n + b]);
+            double il = ((L->len[3 * a + j] * dz) * lamf) / L->cd[3 * a + j];
+            yh[(int64_t)k * ne + e] = Uh[(int64_t)k * ne + e] * il;
+        }
+    for (int i = 1; i <= nz - 1; i++)
+        for (int64_t c = 0; c < n; c++) {
+            double lamf = 0.5 * (L->lam[(int64_t)(i - 1) * n + c] + L->lam[(int64_t)i * n + c]);
+            double il = (L->area[c] * lamf) / dz;
+            yz[(int64_t)(i - 1) * n + c] = Uz[(int64_t)(i - 1) * n + c] * il;
+        }
+}
+
+int64_t ora_mixed_nedges(const ora_h* h) { return 3 * h->lev[h->fine_ref].n / 2; }
+
+int ora_mixed_edges(const ora_h* h, int32_t* ec, int32_t* es, int32_t* ce) {
+    ora_edges E;
+    int st = fine_edges(h, &E);
+    if (st) return st;
+    int64_t n = h->lev[h->fine_ref].n;
+    if (ec) memcpy(ec, E.ec, sizeof(int32_t) * 2 * E.ne);
+    if (es) memcpy(es, E.es, sizeof(int32_t) * 2 * E.ne);
+    if (ce) memcpy(ce, E.ce, sizeof(int32_t) * 3 * n);
+    free_edges(&E);
+    return ORA_OK;
+}
+
+/* One part of the mixed system: which = 0 div (Uh, Uz -> yp), 1 divT    */
+/* (P -> yh, yz), 2 mass (Uh, Uz -> yh, yz), 3 lumped inverse,            */
+/* 4 RT0 Gram matrices of all fine cells ([n][3][3] into yh).            */
+int ora_mixed_part(const ora_h* h, int which, const double* Uh, const double* Uz, const double* P, double* yh,
+                   double* yz, double* yp) {
+    ora_edges E;
+    int st = fine_edges(h, &E);
+    if (st) return st;
+    if (which == 0) mixed_div(h, &E, Uh, Uz, yp);
+    else if (which == 1) mixed_divT(h, &E, P, yh, yz);
+    else if (which == 2) mixed_mass(h, &E, Uh, Uz, yh, yz);
+    else if (which == 3) mixed_lumped_inv(h, &E, Uh, Uz, yh, yz);
+    else if (which == 4) {
+        const ora_level* L = &h->lev[h->fine_ref];
+        for (int64_t c = 0; c < L->n; c++) rt0_gram(L, c, (double(*)[3])&yh[9 * c]);
+    } else st = ORA_ERR_ARG;
+    free_edges(&E);
+    return st;
+}
+
+/* y = A x (reading R18): y_h = M2h U_h - omega (D^T P)_h,                */
+/* y_z = M2z U_z - omega (D^T P)_z, y_p = omega (D U) + vol P              */
+/* (vol = area dz).  Vectors concatenated [U_h | U_z | P].                 */
+static void mixed_apply(const ora_h* h, const ora_edges* E, const double* x, double* y, double* tmp) {
+    const ora_level* L = &h->lev[h->fine_ref];
+    int nz = h->nz;
+    int64_t n = L->n, ne = E->ne;
+    int64_t nh = (int64_t)nz * ne, nzz = (int64_t)(nz - 1) * n, np = (int64_t)nz * n;
+    double om = sqrt(h->w2);
+    const double *Uh = x, *Uz = x + nh, *P = x + nh + nzz;
+    double *yh = y, *yz = y + nh, *yp = y + nh + nzz;
+    double *th = tmp, *tz = tmp + nh, *tp = tmp + nh + nzz;
+    mixed_mass(h, E, Uh, Uz, yh, yz);
+    mixed_divT(h, E, P, th, tz);
+    for (int64_t q = 0; q < nh; q++) yh[q] = yh[q] - om * th[q];
+    for (int64_t q = 0; q < nzz; q++) yz[q] = yz[q] - om * tz[q];
+    mixed_div(h, E, Uh, Uz, tp);
+    for (int k = 0; k < nz; k++)
+        for (int64_t c = 0; c < n; c++) {
+            int64_t q = (int64_t)k * n + c;
+            yp[q] = om * tp[q] + (L->area[c] * h->dz) * P[q];
+        }
+    (void)np;
+}
+
+int64_t ora_mixed_size(const ora_h* h) {
+    int64_t n = h->lev[h->fine_ref].n;
+    return (int64_t)h->nz * (3 * n / 2) + (int64_t)(h->nz - 1) * n + (int64_t)h->nz * n;
+}
+
+int ora_mixed_apply(const ora_h* h, const double* x, double* y) {
+    ora_edges E;
+    int st = fine_edges(h, &E);
+    if (st) return st;
+    double* tmp = (double*)malloc(sizeof(double) * ora_mixed_size(h));
+    if (!tmp) { free_edges(&E); return ORA_ERR_OOM; }
+    mixed_apply(h, &E, x, y, tmp);
+    free(tmp);
+    free_edges(&E);
+    return ORA_OK;
+}
+
+/* Schur-complement preconditioner (Eq. 6 with M2^-1 -> L^-1 and H^-1 ->  */
+/* one V-cycle; reading R19), applied right to left:                       */
+/*   g_p = f_p - omega (D (L^-1 f_u));  x_p = V(g_p);                      */
+/*   x_u = L^-1 (f_u + omega (D^T x_p)).                                   */
+/* kind 1: V-cycle; kind 0: identity (no preconditioner).                  */
+static int mixed_precond(ora_h* h, const ora_edges* E, int kind, int nu_pre, int nu_post, int n_coarse,
+                         double omega_s, const double* f, double* x, double* tmp) {
+    const ora_level* L = &h->lev[h->fine_ref];
+    int nz = h->nz;
+    int64_t n = L->n, ne = E->ne;
+    int64_t nh = (int64_t)nz * ne, nzz = (int64_t)(nz - 1) * n, np = (int64_t)nz * n;
+    if (kind == 0) { memcpy(x, f, sizeof(double) * (nh + nzz + np)); return ORA_OK; }
+    double om = sqrt(h->w2);
+    const double *fh = f, *fz = f + nh, *fp = f + nh + nzz;
+    double *xh = x, *xz = x + nh, *xp = x + nh + nzz;
+    double *th = tmp, *tz = tmp + nh, *tp = tmp + nh + nzz;
+    mixed_lumped_inv(h, E, fh, fz, th, tz);
+    mixed_div(h, E, th, tz, tp);
+    for (int64_t q = 0; q < np; q++) tp[q] = fp[q] - om * tp[q];
+    int st = ora_vcycle(h, nu_pre, nu_post, n_coarse, omega_s, tp, xp);
+    if (st) return st;
+    mixed_divT(h, E, xp, th, tz);
+    for (int64_t q = 0; q < nh; q++) th[q] = fh[q] + om * th[q];
+    for (int64_t q = 0; q < nzz; q++) tz[q] = fz[q] + om * tz[q];
+    mixed_lumped_inv(h, E, th, tz, xh, xz);
+    return ORA_OK;
+}
+
+int ora_mixed_precond(ora_h* h, int kind, int nu_pre, int nu_post, int n_coarse, double omega_s, const double* f,
+                      double* x) {
+    ora_edges E;
+    int st = fine_edges(h, &E);
+    if (st) return st;
+    double* tmp = (double*)malloc(sizeof(double) * ora_mixed_size(h));
+    if (!tmp) { free_edges(&E); return ORA_ERR_OOM; }
+    st = mixed_precond(h, &E, kind, nu_pre, nu_post, n_coarse, omega_s, f, x, tmp);
+    free(tmp);
+    free_edges(&E);
+    return st;
+}
+
+/* Restarted right-preconditioned GMRES(m) (reading R20; Saad & Schultz,  */
+/* the paper's GMRES(30) to ||r||/||r_0|| < 1e-5), x0 = 0:       */
+/*   r = F, beta = ||r||; per cycle: v_0 = r / beta, g = beta e_0;          */
+/*   for j < m: w = A M^-1 v_j; classical Gram-Schmidt h_ij = <v_i, w>      */
+/*   (i <= j, all against the same w), w = w - sum_i h_ij v_i in order i;   */
+/*   h_{j+1,j} = ||w||, v_{j+1} = w / h_{j+1,j}; previous Givens rotations  */
+/*   applied to column j in order, new rotation (c, s) = (h_jj, h_{j+1,j})  */
+/*   / sqrt(h_jj^2 + h_{j+1,j}^2); g_{j+1} = -s g_j, g_j = c g_j;            */
+/*   stop the cycle when |g_{j+1}| <= rtol ||F|| (count = Arnoldi steps).   */
+/*   Then y = H^-1 g (back substitution), x = x + M^-1 (sum_i y_i v_i);    */
+/*   r = F - A x, beta = ||r||; converged when beta <= rtol ||F||.          */
+/* dot = sequential sum in index order.                                    */
+int ora_mixed_gmres(ora_h* h, int kind, int nu_pre, int nu_post, int n_coarse, double omega_s, int m, double rtol,
+                    int maxit, const double* F, double* X, int* iters, double* relres, double* hist) {
+    ora_edges E;
+    int st = fine_edges(h, &E);
+    if (st) return st;
+    int64_t N = ora_mixed_size(h);
+    double* V = (double*)malloc(sizeof(double) * N * (m + 1));
+    double* w = (double*)malloc(sizeof(double) * N);
+    double* z = (double*)malloc(sizeof(double) * N);
+    double* tmp = (double*)malloc(sizeof(double) * N);
+    double* H = (double*)calloc((size_t)(m + 1) * m, sizeof(double));
+    double* cs = (double*)malloc(sizeof(double) * m);
+    double* sn = (double*)malloc(sizeof(double) * m);
+    double* g = (double*)malloc(sizeof(double) * (m + 1));
+    double* yv = (double*)malloc(sizeof(double) * m);
+    if (!V || !w || !z || !tmp || !H || !cs || !sn || !g || !yv) { st = ORA_ERR_OOM; goto out; }
+    *iters = 0;
+    *relres = 0.0;
+    for (int64_t q = 0; q < N; q++) X[q] = 0.0;
+    double fn = sqrt(dot(N, F, F));
+    if (hist) hist[0] = fn == 0.0 ? 0.0 : 1.0;
+    if (fn == 0.0) { st = ORA_OK; goto out; }
+    memcpy(w, F, sizeof(double) * N);
+    double beta = fn;
+    int total = 0;
+    st = ORA_ERR_NOT_CONVERGED;
+    while (total < maxit) {
+        for (int64_t q = 0; q < N; q++) V[q] = w[q] / beta;
+        for (int i = 0; i <= m; i++) g[i] = 0.0;
+        g[0] = beta;
+        int j, done = 0;
+        for (j = 0; j < m && total < maxit; j++) {
+            double* vj = V + (int64_t)j * N;
+            int s2 = mixed_precond(h, &E, kind, nu_pre, nu_post, n_coarse, omega_s, vj, z, tmp);
+            if (s2) { st = s2; goto out; }
+            mixed_apply(h, &E, z, w, tmp);
+            for (int i = 0; i <= j; i++) H[i * m + j] = dot(N, V + (int64_t)i * N, w);
+            for (int i = 0; i <= j; i++) {
+                const double* vi = V + (int64_t)i * N;
+                double hij = H[i * m + j];
+                for (int64_t q = 0; q < N; q++) w[q] = w[q] - hij * vi[q];
+            }
+            double hn = sqrt(dot(N, w, w));
+            H[(j + 1) * m + j] = hn;
+            double* vn = V + (int64_t)(j + 1) * N;
+            for (int64_t q = 0; q < N; q++) vn[q] = w[q] / hn;
+            for (int i = 0; i < j; i++) {
+                double a = H[i * m + j], b = H[(i + 1) * m + j];
+                H[i * m + j] = cs[i] * a + sn[i] * b;
+                H[(i + 1) * m + j] = -sn[i] * a + cs[i] * b;
+            }
+            double a = H[j * m + j], b = H[(j + 1) * m + j];
+            double rr = sqrt(a * a + b * b);
+            cs[j] = a / rr;
+            sn[j] = b / rr;
+            H[j * m + j] = rr;
+            H[(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            total++;
+            if (hist) hist[total] = fabs(g[j + 1]) / fn;
+            if (fabs(g[j + 1]) <= rtol * fn) { j++; done = 1; break; }
+        }
+        /* y = H^-1 g on the leading j x j block, x += M^-1 (V y) */
+        for (int i = j - 1; i >= 0; i--) {
+            double s = g[i];
+            for (int l = i + 1; l < j; l++) s = s - H[i * m + l] * yv[l];
+            yv[i] = s / H[i * m + i];
+        }
+        for (int64_t q = 0; q < N; q++) w[q] = 0.0;
+        for (int i = 0; i < j; i++) {
+            const double* vi = V + (int64_t)i * N;
+            for (int64_t q = 0; q < N; q++) w[q] = w[q] + yv[i] * vi[q];
+        }
+        int s2 = mixed_precond(h, &E, kind, nu_pre, nu_post, n_coarse, omega_s, w, z, tmp);
+        if (s2) { st = s2; goto out; }
+        for (int64_t q = 0; q < N; q++) X[q] = X[q] + z[q];
+        mixed_apply(h, &E, X, z, tmp);
+        for (int64_t q = 0; q < N; q++) w[q] = F[q] - z[q];
+        beta = sqrt(dot(N, w, w));
+        *iters = total;
+        *relres = beta / fn;
+        if (beta <= rtol * fn) { st = ORA_OK; break; }
+        (void)done;
+    }
+out:
+    free(V); free(w); free(z); free(tmp); free(H); free(cs); free(sn); free(g); free(yv);
+    free_edges(&E);
+    if (st == ORA_ERR_NOT_CONVERGED) snprintf(ora_msg, sizeof ora_msg, "GMRES not converged after %d iterations", maxit);
+    return st;
+}
