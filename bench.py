@@ -332,6 +332,36 @@ def run_hmg(args, ws, rank, local):
               "status": st_sl, "solve_ms": e0.elapsed_time(e1), "final_relres": rr_sl,
               "multigrid_pcg_iterations": iters, "multigrid_solve_ms": ms}
 
+    # ---- NEXT-4: the paper's outer solve -- the mixed velocity-pressure system
+    # (Eq. 5, omega_N = 0) by right-preconditioned GMRES(30) to 1e-5 with the
+    # Schur-complement preconditioner (Eq. 6, lumped mass + one V-cycle) ----
+    mixed = None
+    if ws == 1:
+        lay = h.mixed_layout()
+        unknowns = lay["ne"] * cfg.nz + (cfg.nz - 1) * cfg.n + cfg.nz * cfg.n
+        Fm = hi.uniform_vector(unknowns, 67)      # seeded U(-1, 1) over every unknown (reading R15)
+        Fd = h.mixed_to_device(Fm)
+        del Fm
+        Xd = h.mixed_empty()
+        h.mixed_gmres(Fd, Xd, rtol=1e-5, restart=30, maxit=300, params=params)
+        barrier()
+        h.profile_select(None)
+        h.profile_begin()
+        e0.record(stream)
+        _, it_m, rr_m, st_m = h.mixed_gmres(Fd, Xd, rtol=1e-5, restart=30, maxit=300, params=params)
+        e1.record(stream)
+        barrier()
+        h.profile_end()
+        ms_m = e0.elapsed_time(e1)
+        share = {k: round(h.profile_query(k, -1)[1] / ms_m, 4) for k in ("sweep", "sweep_zero", "sweep_prolong",
+                                                                          "resid_restrict", "coarse_tail", "mixed")}
+        mixed = {"solver": "right-preconditioned GMRES(30), CGS2, to ||r|| <= 1e-5 ||F||",
+                 "preconditioner": "Schur complement (Eq. 6) with two-point lumped velocity mass + one V(2,2)",
+                 "unknowns": unknowns, "gmres_iterations": it_m, "status": st_m, "final_relres": rr_m,
+                 "solve_ms": ms_m, "ms_per_iteration": ms_m / max(it_m, 1),
+                 "unknowns_per_s_per_iteration": unknowns * it_m / (ms_m * 1e-3), "time_share": share}
+        del Fd, Xd
+
     # ---- end to end: host buffers through hmg_pcg_solve_host ----------------
     hb = torch.from_numpy(b).pin_memory()
     hx = torch.empty_like(hb).pin_memory()
@@ -393,6 +423,7 @@ def run_hmg(args, ws, rank, local):
             "time_share": shares,
             "cpu_baseline": cpu,
             "single_level_comparison": sl,
+            "next4_mixed_outer_solve": mixed,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * cfg.nz * n * ws),
                     "d2h_bytes_per_step": int(8 * cfg.nz * n * ws), "ms_per_step": ms_e2e,
                     "api": "hmg_pcg_solve_host_batch (copies of neighbouring steps overlap the solve)",

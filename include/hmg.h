@@ -231,7 +231,9 @@ int64_t hmg_launch_count(const hmg_hierarchy* h);
  * 0 apply, 1 zero-guess sweep, 2 sweep, 3 sweep with fused prolongation,
  * 4 residual+restriction, 5 restriction, 6 prolongation, 7 CG vector kernels,
  * 8 coarse-tail V-cycle (all levels <= the tail level in one launch),
- * 9 operator apply with the CG direction update p = z + beta p fused. */
+ * 9 operator apply with the CG direction update p = z + beta p fused,
+ * 10 the mixed system's kernels (hmg_mixed_*: apply, preconditioner steps,
+ * GMRES vector operations; the preconditioner's V-cycle keeps its classes). */
 hmg_status hmg_profile_begin(hmg_hierarchy* h);
 hmg_status hmg_profile_end(hmg_hierarchy* h);
 /* Restrict recording to one kernel class on one level (-1: any); an event pair
@@ -246,6 +248,52 @@ hmg_status hmg_profile_query(const hmg_hierarchy* h, int kernel_class, int ref, 
  * (the compiler's div.rn.f64).  The two must be bitwise equal. */
 hmg_status hmg_selftest_div(const double* a, const double* b, double* fast, double* ref, int64_t n,
                             void* stream);
+
+/* ---------------------------------------------------------------------------
+ * NEXT-4: the mixed velocity-pressure system around the V-cycle.
+ * Eq. 5 with omega_N = 0 at lowest order, on the hierarchy's
+ * finest level (single-GPU hierarchies; a distributed one is rejected with
+ * HMG_ERR_INVALID_ARG):
+ *     A [U; P] = [[M2, -omega D^T], [omega D, M3]] [U; P],   omega = sqrt(w2),
+ * U = RT0 normal fluxes through the vertical faces (edge e, layer k; positive
+ * from the edge's lower cell to its upper cell) and P1-in-the-vertical fluxes
+ * through the interior interfaces (positive upward; u.n = 0 at top and bottom,
+ * P:415-418), P = the DG0 pressure; M2 = the consistent velocity mass with
+ * weight 1/lam per cell, M3 = diag(vol), D = the net outward flux (DESIGN.md
+ * readings R15-R18).  Device vectors, fp64, caller-owned, one contiguous
+ * array of ntot doubles:
+ *     [0, off_z)        U_h  [nlayers][ldh]      (entries e >= ne are padding)
+ *     [off_z, off_p)    U_z  [nlayers-1][ld]     (interface i = row i-1)
+ *     [off_p, ntot)     P    [nlayers][ld]       (ld of the finest level)
+ * Padding entries of inputs must be zero; outputs keep them zero.  The tables
+ * (edge list, RT0 mass rows, lumped inverse) are built on the first call of
+ * any hmg_mixed_* function and owned by the hierarchy. */
+hmg_status hmg_mixed_layout(const hmg_hierarchy* h, int64_t* ne, int64_t* ldh, int64_t* off_z, int64_t* off_p,
+                            int64_t* ntot);
+/* Edge table to HOST buffers (tests; either may be NULL): ec int32 [ne][2] the
+ * two cells of edge e (lower first), ce int32 [ncells][3] the edge across each
+ * neighbour slot.  Edges are numbered by lower cell, then its slot (R16). */
+hmg_status hmg_mixed_export_edges(const hmg_hierarchy* h, int32_t* ec, int32_t* ce);
+/* y = A x (x, y must not alias). */
+hmg_status hmg_mixed_apply(const hmg_hierarchy* h, const double* x, double* y, void* stream);
+/* x = B f, the Schur-complement preconditioner of Eq. 6 with the
+ * velocity mass replaced by its two-point lumping L (whose Schur complement
+ * M3 + omega^2 D L^-1 D^T is exactly this library's H^) and H^-1 by one
+ * V-cycle with parameters p (reading R19):
+ *     g = f_P - omega D L^-1 f_U,  x_P = V(g),  x_U = L^-1 (f_U + omega D^T x_P).
+ * p = NULL: x = f (no preconditioner). */
+hmg_status hmg_mixed_precond(const hmg_hierarchy* h, const hmg_mg_params* p, const double* f, double* x,
+                             void* stream);
+/* Restarted right-preconditioned GMRES(restart) for A X = F from X = 0, the
+ * paper's outer solver ("GMRES(k=30) to ||r||/||r_0|| < 1e-5", P:791-796;
+ * reading R20): stops when the true residual ||F - A X||_2 <= rtol ||F||_2
+ * (checked at the end of each cycle; within a cycle the Givens estimate ends
+ * the cycle early).  iters = Arnoldi steps (preconditioner applications
+ * excluding the one per cycle that forms X).  restart in [1, 31].
+ * Synchronises once per Arnoldi step (the Hessenberg column).  Returns
+ * HMG_ERR_NOT_CONVERGED with X, iters, relres filled after maxit steps. */
+hmg_status hmg_mixed_gmres(const hmg_hierarchy* h, const hmg_mg_params* p, const double* F, double* X, double rtol,
+                           int restart, int maxit, int* iters, double* relres, void* stream);
 
 /* Message for the last error on this thread ("" if none). */
 const char* hmg_last_error(void);

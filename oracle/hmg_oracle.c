@@ -1000,8 +1000,9 @@ int ora_mixed_precond(ora_h* h, int kind, int nu_pre, int nu_post, int n_coarse,
 /* Restarted right-preconditioned GMRES(m) (reading R20; Saad & Schultz,  */
 /* the paper's GMRES(30) to ||r||/||r_0|| < 1e-5), x0 = 0:       */
 /*   r = F, beta = ||r||; per cycle: v_0 = r / beta, g = beta e_0;          */
-/*   for j < m: w = A M^-1 v_j; classical Gram-Schmidt h_ij = <v_i, w>      */
-/*   (i <= j, all against the same w), w = w - sum_i h_ij v_i in order i;   */
+/*   for j < m: w = A M^-1 v_j; classical Gram-Schmidt applied twice      */
+/*   (CGS2): per pass c_i = <v_i, w> (i <= j, all against the same w), then */
+/*   w = w - sum_i c_i v_i in order i; h_ij = c_i(pass 1) + c_i(pass 2);    */
 /*   h_{j+1,j} = ||w||, v_{j+1} = w / h_{j+1,j}; previous Givens rotations  */
 /*   applied to column j in order, new rotation (c, s) = (h_jj, h_{j+1,j})  */
 /*   / sqrt(h_jj^2 + h_{j+1,j}^2); g_{j+1} = -s g_j, g_j = c g_j;            */
@@ -1045,11 +1046,14 @@ int ora_mixed_gmres(ora_h* h, int kind, int nu_pre, int nu_post, int n_coarse, d
             int s2 = mixed_precond(h, &E, kind, nu_pre, nu_post, n_coarse, omega_s, vj, z, tmp);
             if (s2) { st = s2; goto out; }
             mixed_apply(h, &E, z, w, tmp);
-            for (int i = 0; i <= j; i++) H[i * m + j] = dot(N, V + (int64_t)i * N, w);
-            for (int i = 0; i <= j; i++) {
-                const double* vi = V + (int64_t)i * N;
-                double hij = H[i * m + j];
-                for (int64_t q = 0; q < N; q++) w[q] = w[q] - hij * vi[q];
+            for (int pass = 0; pass < 2; pass++) {       /* CGS2: Gram-Schmidt twice */
+                for (int i = 0; i <= j; i++) yv[i] = dot(N, V + (int64_t)i * N, w);
+                for (int i = 0; i <= j; i++) {
+                    const double* vi = V + (int64_t)i * N;
+                    double hij = yv[i];
+                    for (int64_t q = 0; q < N; q++) w[q] = w[q] - hij * vi[q];
+                }
+                for (int i = 0; i <= j; i++) H[i * m + j] = pass == 0 ? yv[i] : H[i * m + j] + yv[i];
             }
             double hn = sqrt(dot(N, w, w));
             H[(j + 1) * m + j] = hn;

@@ -88,6 +88,11 @@ def load_library():
         "hmg_build_hierarchy_dist": [I, I, I, D, D, P, I, P, ctypes.POINTER(P)],
         "hmg_nccl_unique_id": [P],
         "hmg_partition_plan": [I, I, I, I, pI64, pI64, pI64, pI, pI64, P, P, P, P, P, P, P],
+        "hmg_mixed_layout": [P, pI64, pI64, pI64, pI64, pI64],
+        "hmg_mixed_export_edges": [P, P, P],
+        "hmg_mixed_apply": [P, P, P, P],
+        "hmg_mixed_precond": [P, pP, P, P, P],
+        "hmg_mixed_gmres": [P, pP, P, P, D, I, I, pI, pD, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -308,7 +313,8 @@ class Hierarchy:
 
     # -- diagnostics -----------------------------------------------------------
     KERNEL_CLASSES = {"apply": 0, "sweep_zero": 1, "sweep": 2, "sweep_prolong": 3, "resid_restrict": 4,
-                      "restrict": 5, "prolong": 6, "vector": 7, "coarse_tail": 8, "apply_pupdate": 9}
+                      "restrict": 5, "prolong": 6, "vector": 7, "coarse_tail": 8, "apply_pupdate": 9,
+                      "mixed": 10}
 
     def profile_begin(self):
         _check(load_library().hmg_profile_begin(self._h))
@@ -327,6 +333,74 @@ class Hierarchy:
         _check(load_library().hmg_profile_query(self._h, self.KERNEL_CLASSES[kernel_class], ref, ctypes.byref(n),
                                                 ctypes.byref(ms)))
         return n.value, ms.value
+
+    # -- NEXT-4: mixed velocity-pressure system (include/hmg.h hmg_mixed_*) ----
+    def mixed_layout(self) -> dict:
+        """ne, ldh, off_z, off_p, ntot of the mixed vectors [U_h | U_z | P]."""
+        v = [ctypes.c_int64() for _ in range(5)]
+        _check(load_library().hmg_mixed_layout(self._h, *[ctypes.byref(x) for x in v]))
+        return dict(zip(("ne", "ldh", "off_z", "off_p", "ntot"), (x.value for x in v)))
+
+    def mixed_edges(self):
+        """(ec [ne][2], ce [n][3]) host int32 arrays."""
+        lay = self.mixed_layout()
+        n, _ = self.level_info(self.fine_ref)
+        ec, ce = np.empty((lay["ne"], 2), np.int32), np.empty((n, 3), np.int32)
+        _check(load_library().hmg_mixed_export_edges(self._h, ec.ctypes.data_as(ctypes.c_void_p),
+                                                     ce.ctypes.data_as(ctypes.c_void_p)))
+        return ec, ce
+
+    def mixed_to_device(self, x: np.ndarray):
+        """Oracle-layout mixed vector (nz*ne | (nz-1)*n | nz*n) -> padded device vector."""
+        import torch
+        lay = self.mixed_layout()
+        n, ld = self.level_info(self.fine_ref)
+        nz, ne = self.nz, lay["ne"]
+        t = torch.zeros(lay["ntot"], dtype=torch.float64, device=f"cuda:{self.device}")
+        a, b = nz * ne, nz * ne + (nz - 1) * n
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        t[: lay["off_z"]].view(nz, lay["ldh"])[:, :ne] = torch.from_numpy(x[:a].reshape(nz, ne))
+        if nz > 1:
+            t[lay["off_z"]: lay["off_p"]].view(nz - 1, ld)[:, :n] = torch.from_numpy(x[a:b].reshape(nz - 1, n))
+        t[lay["off_p"]:].view(nz, ld)[:, :n] = torch.from_numpy(x[b:].reshape(nz, n))
+        return t
+
+    def mixed_to_host(self, t) -> np.ndarray:
+        lay = self.mixed_layout()
+        n, ld = self.level_info(self.fine_ref)
+        nz, ne = self.nz, lay["ne"]
+        parts = [t[: lay["off_z"]].view(nz, lay["ldh"])[:, :ne]]
+        if nz > 1:
+            parts.append(t[lay["off_z"]: lay["off_p"]].view(nz - 1, ld)[:, :n])
+        parts.append(t[lay["off_p"]:].view(nz, ld)[:, :n])
+        return np.concatenate([p.cpu().numpy().ravel() for p in parts])
+
+    def mixed_empty(self):
+        import torch
+        return torch.zeros(self.mixed_layout()["ntot"], dtype=torch.float64, device=f"cuda:{self.device}")
+
+    def mixed_apply(self, x, y=None):
+        y = self.mixed_empty() if y is None else y
+        _check(load_library().hmg_mixed_apply(self._h, _dptr(x, "x"), _dptr(y, "y"), _stream()))
+        return y
+
+    def mixed_precond(self, f, x=None, params: MGParams | None = MGParams()):
+        x = self.mixed_empty() if x is None else x
+        p = None if params is None else params.c()
+        _check(load_library().hmg_mixed_precond(self._h, None if p is None else ctypes.byref(p), _dptr(f, "f"),
+                                                _dptr(x, "x"), _stream()))
+        return x
+
+    def mixed_gmres(self, F, X=None, rtol: float = 1e-5, restart: int = 30, maxit: int = 300,
+                    params: MGParams | None = MGParams()):
+        """Returns (X, iters, relres, status_name)."""
+        X = self.mixed_empty() if X is None else X
+        p = None if params is None else params.c()
+        it, rr = ctypes.c_int(0), ctypes.c_double(0.0)
+        code = _check(load_library().hmg_mixed_gmres(self._h, None if p is None else ctypes.byref(p), _dptr(F, "F"),
+                                                     _dptr(X, "X"), rtol, restart, maxit, ctypes.byref(it),
+                                                     ctypes.byref(rr), _stream()), allow=(5,))
+        return X, it.value, rr.value, STATUS[code]
 
     def export_level(self, ref: int) -> dict:
         n, _ = self.level_info(ref)

@@ -15,7 +15,7 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhmg.so")
-SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "sweep_st.cu", "apply_st.cu", "sweep_small.cu", "coarse_tail.cu", "coarse_coop.cu", "mesh.cpp", "dist.cpp", "nccl_dyn.cpp", "local_transport.cu"]
+SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "sweep_st.cu", "apply_st.cu", "sweep_small.cu", "coarse_tail.cu", "coarse_coop.cu", "mesh.cpp", "dist.cpp", "nccl_dyn.cpp", "local_transport.cu", "mixed.cu"]
 HEADERS = ["hmg_internal.h", "mf_ops.cuh", "small_tile.cuh", "mesh.h", "sm100_ptx.cuh", "dist.h", "nccl_dyn.h", os.path.join("..", "..", "include", "hmg.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

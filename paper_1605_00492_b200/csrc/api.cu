@@ -134,6 +134,7 @@ void free_hierarchy(Hierarchy* H) {
     if (H->scal_host) cudaFreeHost(H->scal_host);
     for (cudaEvent_t e : H->prof.pool) cudaEventDestroy(e);
     cudaFree(H->gbuf_send); cudaFree(H->gbuf_recv);
+    mixed_free(H->mix);
     if (H->comm) {
         std::string err;
         if (const Nccl* N = nccl(&err)) N->CommDestroy(H->comm);
@@ -761,7 +762,124 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     return HMG_OK;
 }
 
+// NEXT-4 (mixed.cu): restarted right-preconditioned GMRES(m) on the mixed
+// system (reading R20), the oracle's ora_mixed_gmres step for step: classical
+// Gram-Schmidt applied twice (CGS2) against one w, Givens rotations and the small triangular solve
+// on the host, every vector operation in mixed.cu's kernels.  Dot products
+// are deterministic block trees (the oracle's are sequential): parity is the
+// iteration count.
+hmg_status mixed_gmres_impl(const Hierarchy& H, const hmg_mg_params* p, const double* F, double* X, double rtol,
+                            int m, int maxit, int* iters, double* relres, cudaStream_t s) {
+    MixedSystem& M = *H.mix;
+    const int64_t N = M.ntot;
+    if (M.m < m) {
+        cudaFree(M.V); cudaFree(M.w); cudaFree(M.z); cudaFree(M.t);
+        M.V = M.w = M.z = M.t = nullptr;
+        M.m = 0;
+        HMG_CUDA(cudaMalloc(&M.V, sizeof(double) * N * (m + 1)));
+        HMG_CUDA(cudaMalloc(&M.w, sizeof(double) * N));
+        HMG_CUDA(cudaMalloc(&M.z, sizeof(double) * N));
+        HMG_CUDA(cudaMalloc(&M.t, sizeof(double) * N));
+        M.m = m;
+    }
+    // padding entries of every work vector stay zero
+    HMG_CUDA(cudaMemsetAsync(M.V, 0, sizeof(double) * N * (M.m + 1), s));
+    HMG_CUDA(cudaMemsetAsync(M.z, 0, sizeof(double) * N, s));
+    HMG_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * N, s));
+    *iters = 0;
+    *relres = 0.0;
+    auto fetch = [&](int nv) -> hmg_status {
+        HMG_CUDA(cudaMemcpyAsync(M.dots_host, M.dots, sizeof(double) * nv, cudaMemcpyDeviceToHost, s));
+        HMG_TRY(check_launch());
+        HMG_CUDA(cudaStreamSynchronize(s));
+        return HMG_OK;
+    };
+    auto norm = [&](const double* a, double* out) -> hmg_status {
+        mixed_mdot(H, &a, 1, a, s);
+        HMG_TRY(fetch(1));
+        *out = std::sqrt(M.dots_host[0]);
+        return HMG_OK;
+    };
+    double fn = 0.0;
+    HMG_TRY(norm(F, &fn));
+    if (fn == 0.0) return HMG_OK;
+    HMG_CUDA(cudaMemcpyAsync(M.w, F, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    std::vector<double> Hm((size_t)(m + 1) * m, 0.0), cs(m), sn(m), g(m + 1), yv(m);
+    std::vector<const double*> vp(m + 1);
+    for (int i = 0; i <= m; ++i) vp[i] = M.V + (int64_t)i * N;
+    double beta = fn;
+    int total = 0;
+    while (total < maxit) {
+        mixed_vec(H, 0, M.w, nullptr, beta, M.V, s);          // v_0 = r / beta
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int j;
+        for (j = 0; j < m && total < maxit; ++j) {
+            mixed_precond(H, p, vp[j], M.z, s);                // w = A M^-1 v_j
+            launch_mixed_apply(H, M.z, M.w, s);
+            for (int pass = 0; pass < 2; ++pass) {             // CGS2: Gram-Schmidt twice
+                mixed_mdot(H, vp.data(), j + 1, M.w, s);       // c_i = <v_i, w>, i <= j
+                HMG_TRY(fetch(j + 1));
+                for (int i = 0; i <= j; ++i) {
+                    yv[i] = M.dots_host[i];
+                    Hm[(size_t)i * m + j] = pass == 0 ? yv[i] : Hm[(size_t)i * m + j] + yv[i];
+                }
+                mixed_lincomb(H, true, M.w, vp.data(), yv.data(), j + 1, M.w, s);
+            }
+            double hn = 0.0;
+            HMG_TRY(norm(M.w, &hn));
+            Hm[(size_t)(j + 1) * m + j] = hn;
+            mixed_vec(H, 0, M.w, nullptr, hn, const_cast<double*>(vp[j + 1]), s);
+            for (int i = 0; i < j; ++i) {
+                const double a = Hm[(size_t)i * m + j], b = Hm[(size_t)(i + 1) * m + j];
+                Hm[(size_t)i * m + j] = cs[i] * a + sn[i] * b;
+                Hm[(size_t)(i + 1) * m + j] = -sn[i] * a + cs[i] * b;
+            }
+            const double a = Hm[(size_t)j * m + j], b = Hm[(size_t)(j + 1) * m + j];
+            const double rr = std::sqrt(a * a + b * b);
+            cs[j] = a / rr;
+            sn[j] = b / rr;
+            Hm[(size_t)j * m + j] = rr;
+            Hm[(size_t)(j + 1) * m + j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            ++total;
+            if (std::fabs(g[j + 1]) <= rtol * fn) {
+                ++j;
+                break;
+            }
+        }
+        for (int i = j - 1; i >= 0; --i) {                    // y = H^-1 g
+            double sm = g[i];
+            for (int l = i + 1; l < j; ++l) sm = sm - Hm[(size_t)i * m + l] * yv[l];
+            yv[i] = sm / Hm[(size_t)i * m + i];
+        }
+        mixed_lincomb(H, false, nullptr, vp.data(), yv.data(), j, M.w, s);   // w = V y
+        mixed_precond(H, p, M.w, M.z, s);                      // x += M^-1 (V y)
+        mixed_vec(H, 2, M.z, nullptr, 0.0, X, s);
+        launch_mixed_apply(H, X, M.z, s);                      // r = F - A x
+        mixed_vec(H, 1, F, M.z, 0.0, M.w, s);
+        HMG_TRY(norm(M.w, &beta));
+        *iters = total;
+        *relres = beta / fn;
+        if (beta <= rtol * fn) return HMG_OK;
+    }
+    return fail(HMG_ERR_NOT_CONVERGED, "GMRES not converged after " + std::to_string(maxit) + " iterations (relres " +
+                                           std::to_string(*relres) + ")");
+}
+
+hmg_status ensure_mixed(const Hierarchy& H) {
+    if (H.mix) return HMG_OK;
+    const std::string e = mixed_setup(H);
+    if (!e.empty()) return fail(e.find("single-GPU") != std::string::npos ? HMG_ERR_INVALID_ARG : HMG_ERR_CUDA, e);
+    return check_launch();
+}
+
 }  // namespace
+
+void hmg::vcycle_fine(const Hierarchy& H, const hmg_mg_params& p, const double* b, double* out, cudaStream_t s) {
+    vcycle_level(H, H.fine_ref, p, b, out, s);
+}
 
 extern "C" {
 
@@ -1149,6 +1267,86 @@ hmg_status hmg_selftest_div(const double* a, const double* b, double* fast, doub
     if (n == 0) return HMG_OK;
     launch_selftest_div(n, a, b, fast, ref, S(stream));
     return check_launch();
+}
+
+hmg_status hmg_mixed_layout(const hmg_hierarchy* h, int64_t* ne, int64_t* ldh, int64_t* off_z, int64_t* off_p,
+                            int64_t* ntot) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(ensure_mixed(H));
+    const MixedSystem& M = *H.mix;
+    if (ne) *ne = M.ne;
+    if (ldh) *ldh = M.ldh;
+    if (off_z) *off_z = M.off_z;
+    if (off_p) *off_p = M.off_p;
+    if (ntot) *ntot = M.ntot;
+    return HMG_OK;
+}
+
+hmg_status hmg_mixed_export_edges(const hmg_hierarchy* h, int32_t* ec, int32_t* ce) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(ensure_mixed(H));
+    const MixedSystem& M = *H.mix;
+    const DevLevel& L = H.lev[H.fine_ref];
+    if (ec) {
+        std::vector<int32_t> a(M.ne), b(M.ne);
+        HMG_CUDA(cudaMemcpy(a.data(), M.eca, sizeof(int32_t) * M.ne, cudaMemcpyDeviceToHost));
+        HMG_CUDA(cudaMemcpy(b.data(), M.ecb, sizeof(int32_t) * M.ne, cudaMemcpyDeviceToHost));
+        for (int64_t e = 0; e < M.ne; ++e) {
+            ec[2 * e] = a[e];
+            ec[2 * e + 1] = b[e];
+        }
+    }
+    if (ce) {
+        std::vector<int32_t> t(3 * L.ld);
+        HMG_CUDA(cudaMemcpy(t.data(), M.ce, sizeof(int32_t) * 3 * L.ld, cudaMemcpyDeviceToHost));
+        for (int64_t c = 0; c < L.n; ++c)
+            for (int j = 0; j < 3; ++j) ce[3 * c + j] = t[j * L.ld + c];
+    }
+    return HMG_OK;
+}
+
+hmg_status hmg_mixed_apply(const hmg_hierarchy* h, const double* x, double* y, void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_ptr(x, "x"));
+    HMG_TRY(check_ptr(y, "y"));
+    if (x == y) return fail(HMG_ERR_INVALID_ARG, "y: must not alias x");
+    HMG_TRY(ensure_mixed(H));
+    launch_mixed_apply(H, x, y, S(stream));
+    return check_launch();
+}
+
+hmg_status hmg_mixed_precond(const hmg_hierarchy* h, const hmg_mg_params* p, const double* f, double* x,
+                             void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    if (p) HMG_TRY(check_params(p));
+    HMG_TRY(check_ptr(f, "f"));
+    HMG_TRY(check_ptr(x, "x"));
+    if (f == x) return fail(HMG_ERR_INVALID_ARG, "x: must not alias f");
+    HMG_TRY(ensure_mixed(H));
+    mixed_precond(H, p, f, x, S(stream));
+    return check_launch();
+}
+
+hmg_status hmg_mixed_gmres(const hmg_hierarchy* h, const hmg_mg_params* p, const double* F, double* X, double rtol,
+                           int restart, int maxit, int* iters, double* relres, void* stream) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    if (p) HMG_TRY(check_params(p));
+    HMG_TRY(check_ptr(F, "F"));
+    HMG_TRY(check_ptr(X, "X"));
+    HMG_TRY(check_out(iters, "iters"));
+    HMG_TRY(check_out(relres, "relres"));
+    if (F == X) return fail(HMG_ERR_INVALID_ARG, "X: must not alias F");
+    if (!(rtol >= 0)) return fail(HMG_ERR_INVALID_ARG, "rtol: must be >= 0");
+    if (restart < 1 || restart > mixed_lin_max() - 1)
+        return fail(HMG_ERR_INVALID_ARG, "restart: must be in [1, " + std::to_string(mixed_lin_max() - 1) + "]");
+    if (maxit < 0) return fail(HMG_ERR_INVALID_ARG, "maxit: must be >= 0");
+    HMG_TRY(ensure_mixed(H));
+    return mixed_gmres_impl(H, p, F, X, rtol, restart, maxit, iters, relres, S(stream));
 }
 
 }  // extern "C"

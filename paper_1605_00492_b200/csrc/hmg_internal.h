@@ -132,7 +132,7 @@ struct PcgScalars {
 // (kernel class, level).  Off by default; the benchmark turns it on for the
 // timed region to report the dominant kernel's live duration.
 enum KernelClass { kKApply = 0, kKSweepZero, kKSweep, kKSweepProlong, kKResidRestrict, kKRestrict, kKProlong,
-                   kKVector, kKCoarseTail, kKApplyP, kKNumClasses };
+                   kKVector, kKCoarseTail, kKApplyP, kKMixed, kKNumClasses };
 struct Profiler {
     bool on = false;
     int only_cls = -1, only_ref = -1;   // hmg_profile_select: record only this class / level (-1: all)
@@ -141,7 +141,26 @@ struct Profiler {
     std::vector<int> cls, ref;       // per pair
 };
 
+// NEXT-4 mixed velocity-pressure system (mixed.cu): tables of the fine level,
+// built on first use.  Vectors [U_h: nz x ldh | U_z: (nz-1) x ld | P: nz x ld].
+struct MixedSystem {
+    int64_t ne = 0, ldh = 0, off_z = 0, off_p = 0, ntot = 0;
+    double omega = 0;
+    int32_t *eca = nullptr, *ecb = nullptr, *esa = nullptr;   // [ldh]: cells a < b, slot of the edge in a
+    int32_t* ee = nullptr;      // [6][ldh] edges of a's slots, then b's
+    double* eg = nullptr;       // [6][ldh] RT0 mass rows (sign-adjusted Gram entries)
+    int32_t* ce = nullptr;      // [3][ld] edge across each slot of a cell
+    double* cs = nullptr;       // [3][ld] +1 / -1: the edge's flux leaves / enters the cell
+    double* IL = nullptr;       // [off_p] lumped inverse mass of every velocity dof
+    double* g = nullptr;        // [nz][ld] preconditioner: V-cycle right-hand side
+    int nblocks = 0;
+    double *part = nullptr, *dots = nullptr, *dots_host = nullptr;
+    int m = 0;                  // GMRES workspace: basis V [m+1][ntot], w, z, t
+    double *V = nullptr, *w = nullptr, *z = nullptr, *t = nullptr;
+};
+
 struct Hierarchy {
+    mutable MixedSystem* mix = nullptr;
     int device = 0;
     int fine_ref = 0, coarsest_ref = 0, nz = 0;
     double thickness = 0, w2 = 0, dz = 0;
@@ -190,6 +209,19 @@ struct Hierarchy {
     bool use_small_sweep = true;
     int l2_prefetch_groups = 0;   // measured: the ring alone is as fast at ref 7 and faster at ref 6
 };
+
+// mixed.cu (NEXT-4)
+std::string mixed_setup(const Hierarchy& H);   // "" on success
+void mixed_free(MixedSystem* M);
+void launch_mixed_apply(const Hierarchy& H, const double* x, double* y, cudaStream_t s);
+void mixed_precond(const Hierarchy& H, const hmg_mg_params* p, const double* f, double* x, cudaStream_t s);
+void mixed_mdot(const Hierarchy& H, const double* const* v, int nv, const double* w, cudaStream_t s);
+void mixed_lincomb(const Hierarchy& H, bool sub, const double* base, const double* const* v, const double* c, int nv,
+                   double* w, cudaStream_t s);
+void mixed_vec(const Hierarchy& H, int op, const double* x, const double* b, double sc, double* y, cudaStream_t s);
+int mixed_lin_max();
+// api.cu: one V-cycle on the finest level (Alg. 1)
+void vcycle_fine(const Hierarchy& H, const hmg_mg_params& p, const double* b, double* out, cudaStream_t s);
 
 // kernels.cu
 void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
