@@ -7,7 +7,8 @@ and shares no code with it; the only module both sides use is ``hmg_inputs``
 (seeded random inputs, no method arithmetic).
 
 The arithmetic lives in ``hmg_oracle.c`` (plain C, fp64, ``-O2
--ffp-contract=off``), which follows DESIGN.md's readings R1-R12 of the paper
+-ffp-contract=off``), which follows DESIGN.md's readings R1-R12 (and R15-R20 for the NEXT-4 mixed
+system) of the paper
 step by step; this module is ctypes marshalling only.  Arrays are numpy fp64,
 layer-major ``[nz][n]`` (C order), ``n = 20 * 4**ref`` cells.
 

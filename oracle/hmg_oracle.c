@@ -26,6 +26,11 @@
  *   restrict/prolong  pinned: adjointness, RP = 4I, constants
  *   vcycle            pinned: dense two-grid matrix form, symmetry, linearity
  *   pcg               pinned: scipy.sparse.linalg.cg iteration count
+ *   mixed system      pinned (NEXT-4, readings R15-R20): divergence theorem
+ *   (Eq. 5, Eq. 6,    and adjointness of D, lumped Schur complement == the
+ *    GMRES(30))       pinned apply above, RT0 exactness on constant fields,
+ *                     P1 hat integrals, mass SPD, GMRES residual minimality
+ *                     against dense least squares, Eq. 6 factorisation
  */
 #include <math.h>
 #include <stdint.h>

@@ -786,6 +786,8 @@ hmg_status mixed_gmres_impl(const Hierarchy& H, const hmg_mg_params* p, const do
     HMG_CUDA(cudaMemsetAsync(M.V, 0, sizeof(double) * N * (M.m + 1), s));
     HMG_CUDA(cudaMemsetAsync(M.z, 0, sizeof(double) * N, s));
     HMG_CUDA(cudaMemsetAsync(X, 0, sizeof(double) * N, s));
+    HMG_CUDA(cudaMemcpyAsync(M.t, F, sizeof(double) * N, cudaMemcpyDeviceToDevice, s));
+    F = M.t;                       // library copy: 16-byte aligned for the vector kernels
     *iters = 0;
     *relres = 0.0;
     auto fetch = [&](int nv) -> hmg_status {
@@ -795,7 +797,7 @@ hmg_status mixed_gmres_impl(const Hierarchy& H, const hmg_mg_params* p, const do
         return HMG_OK;
     };
     auto norm = [&](const double* a, double* out) -> hmg_status {
-        mixed_mdot(H, &a, 1, a, s);
+        mixed_dots(H, a, nullptr, 0, 2, s);
         HMG_TRY(fetch(1));
         *out = std::sqrt(M.dots_host[0]);
         return HMG_OK;
@@ -818,13 +820,13 @@ hmg_status mixed_gmres_impl(const Hierarchy& H, const hmg_mg_params* p, const do
             mixed_precond(H, p, vp[j], M.z, s);                // w = A M^-1 v_j
             launch_mixed_apply(H, M.z, M.w, s);
             for (int pass = 0; pass < 2; ++pass) {             // CGS2: Gram-Schmidt twice
-                mixed_mdot(H, vp.data(), j + 1, M.w, s);       // c_i = <v_i, w>, i <= j
+                mixed_dots(H, M.w, vp.data(), j + 1, 1, s);    // c_i = <v_i, w>, i <= j
                 HMG_TRY(fetch(j + 1));
                 for (int i = 0; i <= j; ++i) {
                     yv[i] = M.dots_host[i];
                     Hm[(size_t)i * m + j] = pass == 0 ? yv[i] : Hm[(size_t)i * m + j] + yv[i];
                 }
-                mixed_lincomb(H, true, M.w, vp.data(), yv.data(), j + 1, M.w, s);
+                mixed_update(H, M.w, M.w, vp.data(), yv.data(), j + 1, false, s);
             }
             double hn = 0.0;
             HMG_TRY(norm(M.w, &hn));
@@ -854,7 +856,7 @@ hmg_status mixed_gmres_impl(const Hierarchy& H, const hmg_mg_params* p, const do
             for (int l = i + 1; l < j; ++l) sm = sm - Hm[(size_t)i * m + l] * yv[l];
             yv[i] = sm / Hm[(size_t)i * m + i];
         }
-        mixed_lincomb(H, false, nullptr, vp.data(), yv.data(), j, M.w, s);   // w = V y
+        mixed_update(H, nullptr, M.w, vp.data(), yv.data(), j, true, s);    // w = V y
         mixed_precond(H, p, M.w, M.z, s);                      // x += M^-1 (V y)
         mixed_vec(H, 2, M.z, nullptr, 0.0, X, s);
         launch_mixed_apply(H, X, M.z, s);                      // r = F - A x

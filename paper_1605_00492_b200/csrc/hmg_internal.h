@@ -215,9 +215,9 @@ std::string mixed_setup(const Hierarchy& H);   // "" on success
 void mixed_free(MixedSystem* M);
 void launch_mixed_apply(const Hierarchy& H, const double* x, double* y, cudaStream_t s);
 void mixed_precond(const Hierarchy& H, const hmg_mg_params* p, const double* f, double* x, cudaStream_t s);
-void mixed_mdot(const Hierarchy& H, const double* const* v, int nv, const double* w, cudaStream_t s);
-void mixed_lincomb(const Hierarchy& H, bool sub, const double* base, const double* const* v, const double* c, int nv,
-                   double* w, cudaStream_t s);
+void mixed_dots(const Hierarchy& H, const double* w, const double* const* v, int nv, int dot, cudaStream_t s);
+void mixed_update(const Hierarchy& H, const double* win, double* wout, const double* const* v, const double* c, int nv,
+                  bool add, cudaStream_t s);
 void mixed_vec(const Hierarchy& H, int op, const double* x, const double* b, double sc, double* y, cudaStream_t s);
 int mixed_lin_max();
 // api.cu: one V-cycle on the finest level (Alg. 1)

@@ -29,6 +29,7 @@
 
 #include "hmg_internal.h"
 #include "mesh.h"
+#include "sm100_ptx.cuh"
 
 namespace hmg {
 
@@ -116,6 +117,7 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_apply_h(MixView V, const do
         g[q] = V.eg[q * V.ldh + e];
     }
     const double* P = x + V.off_p;
+    #pragma unroll 4
     for (int k = 0; k < V.nz; ++k) {
         const double* Ur = x + k * V.ldh;
         double ta = g[0] * Ur[E[0]];
@@ -143,6 +145,7 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_apply_zp(MixView V, const d
     const double* lam = V.lam + c;
     const int nz = V.nz;
     const int64_t ld = V.ld;
+    #pragma unroll 4
     for (int i = 1; i <= nz - 1; ++i) {
         const double slo = ar * lam[(i - 1) * ld];
         const double shi = ar * lam[i * ld];
@@ -155,6 +158,7 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_apply_zp(MixView V, const d
     const int32_t E0 = V.ce[c], E1 = V.ce[ld + c], E2 = V.ce[2 * ld + c];
     const double s0 = V.cs[c], s1 = V.cs[ld + c], s2 = V.cs[2 * ld + c];
     const double vol = ar * dz;
+    #pragma unroll 4
     for (int k = 0; k < nz; ++k) {
         const double* Ur = x + k * V.ldh;
         double d = s0 * Ur[E0];
@@ -175,6 +179,7 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_pre_p(MixView V, const doub
     const int32_t E0 = V.ce[c], E1 = V.ce[ld + c], E2 = V.ce[2 * ld + c];
     const double s0 = V.cs[c], s1 = V.cs[ld + c], s2 = V.cs[2 * ld + c];
     const int nz = V.nz;
+    #pragma unroll 4
     for (int k = 0; k < nz; ++k) {
         const int64_t r = k * V.ldh;
         double d = s0 * (f[r + E0] * V.IL[r + E0]);
@@ -199,12 +204,14 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_pre_u(MixView V, const doub
     const double* xp = x + V.off_p;
     if (t < V.ne) {
         const int64_t a = V.eca[t], b = V.ecb[t];
+        #pragma unroll 4
         for (int k = 0; k < V.nz; ++k) {
             const int64_t q = k * V.ldh + t;
             x[q] = (f[q] + V.om * (xp[k * V.ld + a] - xp[k * V.ld + b])) * V.IL[q];
         }
     }
     if (t < V.n) {
+        #pragma unroll 4
         for (int i = 1; i <= V.nz - 1; ++i) {
             const int64_t q = V.off_z + (i - 1) * V.ld + t;
             x[q] = (f[q] + V.om * (xp[(i - 1) * V.ld + t] - xp[i * V.ld + t])) * V.IL[q];
@@ -213,81 +220,139 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_pre_u(MixView V, const doub
 }
 
 // ---- flat vector kernels of GMRES (padding entries are zero) ----
+// Every GMRES work vector is library-allocated (16-byte aligned, ntot even),
+// so the kernels stream double2.  Dots: groups of G basis vectors against one
+// w, each thread keeping 2 double2 of every vector in flight; per-block
+// partial sums in a fixed order (per-thread strided order, warp shuffle tree,
+// warps in order), then one warp per sum (k_gs_final), so results are
+// deterministic.  Updates w_out = w_in - c_0 v_0 - c_1 v_1 ... apply the terms
+// in order i (the oracle's per-entry order), G vectors per pass.
 constexpr int kDotBlock = 256;
-constexpr int kMdot = 8;
-struct MdotArgs {
-    const double* v[kMdot];
-    int nv;
+constexpr int kLinMax = 32;
+constexpr int kGroup = 8;
+struct GsArgs {
+    const double2* v[kGroup];
+    double c[kGroup];
 };
 
-// per-block partial sums of <v_i, w>, i < nv, each in a fixed order
-__global__ void __launch_bounds__(kDotBlock) k_mdot(MdotArgs A, const double* __restrict__ w, int64_t N,
+template <int G, bool SELF>
+__global__ void __launch_bounds__(kDotBlock) k_dots(GsArgs A, const double2* __restrict__ w, int64_t N2,
                                                     double* __restrict__ part) {
-    __shared__ double red[kMdot][kDotBlock / 32];
-    double s[kMdot];
+    constexpr int NS = SELF ? 1 : G;
+    __shared__ double red[NS][kDotBlock / 32];
+    double acc[NS];
 #pragma unroll
-    for (int i = 0; i < kMdot; ++i) s[i] = 0.0;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < N; q += stride) {
-        const double wq = w[q];
+    for (int i = 0; i < NS; ++i) acc[i] = 0.0;
+    const int64_t span = (int64_t)gridDim.x * kDotBlock * 2;
+    for (int64_t q0 = (int64_t)blockIdx.x * kDotBlock * 2 + threadIdx.x; q0 < N2; q0 += span) {
+        const int64_t q1 = q0 + kDotBlock;
+        const bool h1 = q1 < N2;
+        const double2 w0 = w[q0];
+        const double2 w1 = h1 ? w[q1] : make_double2(0.0, 0.0);
+        if (SELF) {
+            acc[0] = acc[0] + w0.x * w0.x;
+            acc[0] = acc[0] + w0.y * w0.y;
+            acc[0] = acc[0] + w1.x * w1.x;
+            acc[0] = acc[0] + w1.y * w1.y;
+        } else {
+            double2 x0[G], x1[G];
 #pragma unroll
-        for (int i = 0; i < kMdot; ++i)
-            if (i < A.nv) s[i] = s[i] + A.v[i][q] * wq;
+            for (int i = 0; i < G; ++i) {
+                x0[i] = A.v[i][q0];
+                x1[i] = h1 ? A.v[i][q1] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int i = 0; i < G; ++i) {
+                acc[i] = acc[i] + x0[i].x * w0.x;
+                acc[i] = acc[i] + x0[i].y * w0.y;
+                acc[i] = acc[i] + x1[i].x * w1.x;
+                acc[i] = acc[i] + x1[i].y * w1.y;
+            }
+        }
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-    for (int i = 0; i < kMdot; ++i) {
-        double t = s[i];
+    for (int i = 0; i < NS; ++i) {
+        double t = acc[i];
         for (int off = 16; off > 0; off >>= 1) t = t + __shfl_down_sync(0xffffffffu, t, off);
         if (lane == 0) red[i][warp] = t;
     }
     __syncthreads();
-    if (threadIdx.x < A.nv) {
+    if (threadIdx.x < NS) {
         double t = 0.0;
         for (int wi = 0; wi < kDotBlock / 32; ++wi) t = t + red[threadIdx.x][wi];
         part[threadIdx.x * gridDim.x + blockIdx.x] = t;
     }
 }
 
-__global__ void k_mdot_final(const double* __restrict__ part, int nblocks, int nv, double* __restrict__ out) {
-    const int i = threadIdx.x;
-    if (i >= nv) return;
+// out[i] (+)= sum over blocks of part[i][.]: one warp per sum, lanes take blocks
+// lane, lane + 32, ... in order, then a fixed shuffle tree
+__global__ void k_gs_final(const double* __restrict__ part, int nblocks, double* __restrict__ out) {
+    const int i = blockIdx.x, lane = threadIdx.x;
     double t = 0.0;
-    for (int b = 0; b < nblocks; ++b) t = t + part[i * nblocks + b];
-    out[i] = t;
+    for (int b = lane; b < nblocks; b += 32) t = t + part[i * nblocks + b];
+    for (int off = 16; off > 0; off >>= 1) t = t + __shfl_down_sync(0xffffffffu, t, off);
+    if (lane == 0) out[i] = t;
 }
 
-constexpr int kLinMax = 32;
-struct LinArgs {
-    const double* v[kLinMax];
-    double c[kLinMax];
-    int nv;
-};
-
-// w = base - c_0 v_0 - c_1 v_1 ... (sub) or 0 + c_0 v_0 + c_1 v_1 ... (!sub), each
-// term applied in order i = 0, 1, ... (the oracle's loop order per entry)
-template <bool SUB>
-__global__ void k_lincomb(LinArgs A, const double* __restrict__ base, double* __restrict__ w, int64_t N) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < N; q += stride) {
-        double t = SUB ? base[q] : 0.0;
-        for (int i = 0; i < A.nv; ++i) {
-            if (SUB)
-                t = t - A.c[i] * A.v[i][q];
-            else
-                t = t + A.c[i] * A.v[i][q];
+// w_out = w_in -/+ sum_{i < G} c_i v_i (ADD with w_in == nullptr: 0 + ...)
+template <int G, bool ADD>
+__global__ void __launch_bounds__(kDotBlock) k_upd(GsArgs A, const double2* win, double2* wout, int64_t N2) {
+    const int64_t stride = (int64_t)gridDim.x * kDotBlock;
+    for (int64_t q = (int64_t)blockIdx.x * kDotBlock + threadIdx.x; q < N2; q += stride) {
+        double2 x[G];
+#pragma unroll
+        for (int i = 0; i < G; ++i) x[i] = A.v[i][q];
+        double2 t = win ? win[q] : make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < G; ++i) {
+            if (ADD) {
+                t.x = t.x + A.c[i] * x[i].x;
+                t.y = t.y + A.c[i] * x[i].y;
+            } else {
+                t.x = t.x - A.c[i] * x[i].x;
+                t.y = t.y - A.c[i] * x[i].y;
+            }
         }
-        w[q] = t;
+        wout[q] = t;
     }
 }
 
-// 0: y = x / s   1: y = a - b   2: y = y + x
+// y = x / s for library vectors (double2; shared-reciprocal IEEE division,
+// exact '/' redo where the fast path is not valid)
+__global__ void __launch_bounds__(kDotBlock) k_scale2(const double2* __restrict__ x, double s, double2* __restrict__ y,
+                                                      int64_t N2) {
+    const int64_t stride = (int64_t)gridDim.x * kDotBlock;
+    const double ys = div_recip(s);
+    for (int64_t q = (int64_t)blockIdx.x * kDotBlock + threadIdx.x; q < N2; q += stride) {
+        const double2 a = x[q];
+        bool slow = false;
+        double2 r;
+        r.x = div_fast_z(a.x, s, ys, slow);
+        r.y = div_fast_z(a.y, s, ys, slow);
+        if (slow) {
+            r.x = a.x / s;
+            r.y = a.y / s;
+        }
+        y[q] = r;
+    }
+}
+
+// 0: y = x / s (shared-reciprocal IEEE division, exact '/' redo if the fast
+// path is not valid)   1: y = x - b   2: y = y + x   (scalar: y may be a
+// caller's unaligned vector)
 template <int OP>
 __global__ void k_vec(const double* __restrict__ x, const double* __restrict__ b, double s, double* __restrict__ y,
                       int64_t N) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < N; q += stride) {
-        if (OP == 0) y[q] = x[q] / s;
+    const int64_t stride = (int64_t)gridDim.x * kDotBlock;
+    const double ys = OP == 0 ? div_recip(s) : 0.0;
+    for (int64_t q = (int64_t)blockIdx.x * kDotBlock + threadIdx.x; q < N; q += stride) {
+        if (OP == 0) {
+            bool slow = false;
+            double r = div_fast_z(x[q], s, ys, slow);
+            if (slow) r = x[q] / s;
+            y[q] = r;
+        }
         if (OP == 1) y[q] = x[q] - b[q];
         if (OP == 2) y[q] = y[q] + x[q];
     }
@@ -296,7 +361,7 @@ __global__ void k_vec(const double* __restrict__ x, const double* __restrict__ b
 unsigned flat_grid(const Hierarchy& H) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
-    return (unsigned)(4 * sms);
+    return (unsigned)(2 * sms);
 }
 
 }  // namespace
@@ -391,7 +456,7 @@ std::string mixed_setup(const Hierarchy& H) {
     ok = ok && cudaMalloc(&M->g, sizeof(double) * nz * ld) == cudaSuccess &&
          cudaMemset(M->g, 0, sizeof(double) * nz * ld) == cudaSuccess;
     M->nblocks = (int)flat_grid(H);
-    ok = ok && cudaMalloc(&M->part, sizeof(double) * kMdot * M->nblocks) == cudaSuccess;
+    ok = ok && cudaMalloc(&M->part, sizeof(double) * kLinMax * M->nblocks) == cudaSuccess;
     ok = ok && cudaMalloc(&M->dots, sizeof(double) * 64) == cudaSuccess;
     ok = ok && cudaHostAlloc(&M->dots_host, sizeof(double) * 64, cudaHostAllocDefault) == cudaSuccess;
     if (!ok) {
@@ -435,44 +500,74 @@ void mixed_precond(const Hierarchy& H, const hmg_mg_params* p, const double* f, 
     ++H.launches;
 }
 
-// dots[i] = <v_i, w>, i < nv (deterministic), left in M.dots (device)
-void mixed_mdot(const Hierarchy& H, const double* const* v, int nv, const double* w, cudaStream_t s) {
+// dot = 1: M.dots[i] = <v_i, w> for i < nv; dot = 2: M.dots[0] = <w, w>.
+void mixed_dots(const Hierarchy& H, const double* w, const double* const* v, int nv, int dot, cudaStream_t s) {
     const MixedSystem& M = *H.mix;
     ProfScope ps(H, kKMixed, H.fine_ref, s);
-    for (int i0 = 0; i0 < nv; i0 += kMdot) {
-        MdotArgs A{};
-        A.nv = nv - i0 < kMdot ? nv - i0 : kMdot;
-        for (int i = 0; i < A.nv; ++i) A.v[i] = v[i0 + i];
-        k_mdot<<<M.nblocks, kDotBlock, 0, s>>>(A, w, M.ntot, M.part);
-        k_mdot_final<<<1, 32, 0, s>>>(M.part, M.nblocks, A.nv, M.dots + i0);
+    const unsigned g = (unsigned)M.nblocks;
+    const int64_t N2 = M.ntot / 2;
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    if (dot == 2) {
+        k_dots<1, true><<<g, kDotBlock, 0, s>>>(GsArgs{}, w2, N2, M.part);
+        k_gs_final<<<1, 32, 0, s>>>(M.part, M.nblocks, M.dots);
         H.launches += 2;
+        return;
+    }
+    // groups of at most 4 vectors (measured: 8 per pass streams at 3.6 TB/s, 4 at 5.2)
+    for (int i0 = 0; i0 < nv;) {
+        const int left = nv - i0;
+        const int G = left >= 4 ? 4 : left >= 2 ? 2 : 1;
+        GsArgs A{};
+        for (int i = 0; i < G; ++i) A.v[i] = reinterpret_cast<const double2*>(v[i0 + i]);
+        if (G == 4) k_dots<4, false><<<g, kDotBlock, 0, s>>>(A, w2, N2, M.part);
+        if (G == 2) k_dots<2, false><<<g, kDotBlock, 0, s>>>(A, w2, N2, M.part);
+        if (G == 1) k_dots<1, false><<<g, kDotBlock, 0, s>>>(A, w2, N2, M.part);
+        k_gs_final<<<G, 32, 0, s>>>(M.part, M.nblocks, M.dots + i0);
+        H.launches += 2;
+        i0 += G;
     }
 }
 
-// w = base - sum c_i v_i (sub) or w = sum c_i v_i, in order of i
-void mixed_lincomb(const Hierarchy& H, bool sub, const double* base, const double* const* v, const double* c, int nv,
-                   double* w, cudaStream_t s) {
+// w_out = w_in - sum_i c_i v_i (add: w_out = 0 + sum_i c_i v_i; w_in unused),
+// terms in order i; w_in == w_out allowed
+void mixed_update(const Hierarchy& H, const double* win, double* wout, const double* const* v, const double* c, int nv,
+                  bool add, cudaStream_t s) {
     const MixedSystem& M = *H.mix;
     ProfScope ps(H, kKMixed, H.fine_ref, s);
-    LinArgs A{};
-    A.nv = nv;
-    for (int i = 0; i < nv; ++i) {
-        A.v[i] = v[i];
-        A.c[i] = c[i];
+    const unsigned g = (unsigned)M.nblocks * 2;
+    const int64_t N2 = M.ntot / 2;
+    const double2* in = add ? nullptr : reinterpret_cast<const double2*>(win);
+    double2* out = reinterpret_cast<double2*>(wout);
+    for (int i0 = 0; i0 < nv;) {
+        const int left = nv - i0;
+        const int G = left >= 8 ? 8 : left >= 4 ? 4 : left >= 2 ? 2 : 1;
+        GsArgs A{};
+        for (int i = 0; i < G; ++i) {
+            A.v[i] = reinterpret_cast<const double2*>(v[i0 + i]);
+            A.c[i] = c[i0 + i];
+        }
+#define HMG_UPD(GG)                                                                 \
+    if (G == GG) {                                                                  \
+        if (add) k_upd<GG, true><<<g, kDotBlock, 0, s>>>(A, in, out, N2);           \
+        else k_upd<GG, false><<<g, kDotBlock, 0, s>>>(A, in, out, N2);              \
     }
-    if (sub)
-        k_lincomb<true><<<M.nblocks, kDotBlock, 0, s>>>(A, base, w, M.ntot);
-    else
-        k_lincomb<false><<<M.nblocks, kDotBlock, 0, s>>>(A, base, w, M.ntot);
-    ++H.launches;
+        HMG_UPD(8) HMG_UPD(4) HMG_UPD(2) HMG_UPD(1)
+#undef HMG_UPD
+        ++H.launches;
+        in = out;                 // later groups continue from the partial result
+        i0 += G;
+    }
 }
 
 void mixed_vec(const Hierarchy& H, int op, const double* x, const double* b, double sc, double* y, cudaStream_t s) {
     const MixedSystem& M = *H.mix;
     ProfScope ps(H, kKMixed, H.fine_ref, s);
-    if (op == 0) k_vec<0><<<M.nblocks, kDotBlock, 0, s>>>(x, b, sc, y, M.ntot);
-    if (op == 1) k_vec<1><<<M.nblocks, kDotBlock, 0, s>>>(x, b, sc, y, M.ntot);
-    if (op == 2) k_vec<2><<<M.nblocks, kDotBlock, 0, s>>>(x, b, sc, y, M.ntot);
+    const unsigned g = (unsigned)M.nblocks * 2;
+    if (op == 0)
+        k_scale2<<<g, kDotBlock, 0, s>>>(reinterpret_cast<const double2*>(x), sc, reinterpret_cast<double2*>(y),
+                                         M.ntot / 2);
+    if (op == 1) k_vec<1><<<g, kDotBlock, 0, s>>>(x, b, sc, y, M.ntot);
+    if (op == 2) k_vec<2><<<g, kDotBlock, 0, s>>>(x, b, sc, y, M.ntot);
     ++H.launches;
 }
 
