@@ -336,8 +336,13 @@ def run_hmg(args, ws, rank, local):
     # (Eq. 5, omega_N = 0) by right-preconditioned GMRES(30) to 1e-5 with the
     # Schur-complement preconditioner (Eq. 6, lumped mass + one V-cycle) ----
     mixed = None
-    if ws == 1:
-        lay = h.mixed_layout()
+    lay = h.mixed_layout() if ws == 1 else None
+    # GMRES(30) keeps 31 basis vectors + 3 work vectors of the mixed system
+    # (C2: 20 GB; C4 whole on one GPU would need 160 GB next to the hierarchy)
+    need = 34 * 8 * lay["ntot"] if lay else 0
+    if lay and need > 0.9 * torch.cuda.mem_get_info(local)[0]:
+        mixed = {"skipped": f"GMRES(30) workspace {need / 1e9:.0f} GB does not fit next to the hierarchy"}
+    elif lay:
         unknowns = lay["ne"] * cfg.nz + (cfg.nz - 1) * cfg.n + cfg.nz * cfg.n
         Fm = hi.uniform_vector(unknowns, 67)      # seeded U(-1, 1) over every unknown (reading R15)
         Fd = h.mixed_to_device(Fm)
