@@ -104,8 +104,8 @@ __global__ void k_mixed_il(MixView V, const double* __restrict__ geom, const int
 
 // y_h = M2h U_h - omega (P_a - P_b) per (edge, layer) (reading R18):
 // t_s = ((g0 U[E0] + g1 U[E1]) + g2 U[E2]), m_s = t_s / (dz lam_s), y = (m_a + m_b) - omega (P_a - P_b)
-__global__ void __launch_bounds__(kMixBlock) k_mixed_apply_h(MixView V, const double* __restrict__ x,
-                                                             double* __restrict__ y) {
+__global__ void __launch_bounds__(kMixBlock, 8) k_mixed_apply_h(MixView V, const double* __restrict__ x,
+                                                                double* __restrict__ y) {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= V.ne) return;
     const int64_t a = V.eca[e], b = V.ecb[e];
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_apply_h(MixView V, const do
         g[q] = V.eg[q * V.ldh + e];
     }
     const double* P = x + V.off_p;
-    #pragma unroll 4
+#pragma unroll 1
     for (int k = 0; k < V.nz; ++k) {
         const double* Ur = x + k * V.ldh;
         double ta = g[0] * Ur[E[0]];
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_apply_zp(MixView V, const d
     const double* lam = V.lam + c;
     const int nz = V.nz;
     const int64_t ld = V.ld;
-    #pragma unroll 4
+#pragma unroll 4
     for (int i = 1; i <= nz - 1; ++i) {
         const double slo = ar * lam[(i - 1) * ld];
         const double shi = ar * lam[i * ld];
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_apply_zp(MixView V, const d
     const int32_t E0 = V.ce[c], E1 = V.ce[ld + c], E2 = V.ce[2 * ld + c];
     const double s0 = V.cs[c], s1 = V.cs[ld + c], s2 = V.cs[2 * ld + c];
     const double vol = ar * dz;
-    #pragma unroll 4
+#pragma unroll 4
     for (int k = 0; k < nz; ++k) {
         const double* Ur = x + k * V.ldh;
         double d = s0 * Ur[E0];
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_pre_p(MixView V, const doub
     const int32_t E0 = V.ce[c], E1 = V.ce[ld + c], E2 = V.ce[2 * ld + c];
     const double s0 = V.cs[c], s1 = V.cs[ld + c], s2 = V.cs[2 * ld + c];
     const int nz = V.nz;
-    #pragma unroll 4
+#pragma unroll 4
     for (int k = 0; k < nz; ++k) {
         const int64_t r = k * V.ldh;
         double d = s0 * (f[r + E0] * V.IL[r + E0]);
@@ -200,18 +200,19 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_pre_p(MixView V, const doub
 // Preconditioner step 3: x_u = L^-1 (f_u + omega D^T x_p); x_p is already in x.
 __global__ void __launch_bounds__(kMixBlock) k_mixed_pre_u(MixView V, const double* __restrict__ f,
                                                            double* __restrict__ x) {
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const double* xp = x + V.off_p;
-    if (t < V.ne) {
+    const int64_t t = t0 < V.ne ? t0 : t0 - V.ne;   // threads [0, ne): edges; [ne, ne + n): columns
+    if (t0 < V.ne) {
         const int64_t a = V.eca[t], b = V.ecb[t];
-        #pragma unroll 4
+#pragma unroll 4
         for (int k = 0; k < V.nz; ++k) {
             const int64_t q = k * V.ldh + t;
             x[q] = (f[q] + V.om * (xp[k * V.ld + a] - xp[k * V.ld + b])) * V.IL[q];
         }
     }
-    if (t < V.n) {
-        #pragma unroll 4
+    if (t0 >= V.ne && t < V.n) {
+#pragma unroll 4
         for (int i = 1; i <= V.nz - 1; ++i) {
             const int64_t q = V.off_z + (i - 1) * V.ld + t;
             x[q] = (f[q] + V.om * (xp[(i - 1) * V.ld + t] - xp[i * V.ld + t])) * V.IL[q];
@@ -361,7 +362,7 @@ __global__ void k_vec(const double* __restrict__ x, const double* __restrict__ b
 unsigned flat_grid(const Hierarchy& H) {
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
-    return (unsigned)(2 * sms);
+    return (unsigned)(4 * sms);
 }
 
 }  // namespace
@@ -494,9 +495,8 @@ void mixed_precond(const Hierarchy& H, const hmg_mg_params* p, const double* f, 
         ++H.launches;
     }
     vcycle_fine(H, *p, M.g, x + M.off_p, s);
-    const int64_t nt = V.ne > V.n ? V.ne : V.n;
     ProfScope ps(H, kKMixed, H.fine_ref, s);
-    k_mixed_pre_u<<<nblk(nt), kMixBlock, 0, s>>>(V, f, x);
+    k_mixed_pre_u<<<nblk(V.ne + V.n), kMixBlock, 0, s>>>(V, f, x);
     ++H.launches;
 }
 
@@ -534,7 +534,7 @@ void mixed_update(const Hierarchy& H, const double* win, double* wout, const dou
                   bool add, cudaStream_t s) {
     const MixedSystem& M = *H.mix;
     ProfScope ps(H, kKMixed, H.fine_ref, s);
-    const unsigned g = (unsigned)M.nblocks * 2;
+    const unsigned g = (unsigned)M.nblocks;
     const int64_t N2 = M.ntot / 2;
     const double2* in = add ? nullptr : reinterpret_cast<const double2*>(win);
     double2* out = reinterpret_cast<double2*>(wout);
@@ -562,7 +562,7 @@ void mixed_update(const Hierarchy& H, const double* win, double* wout, const dou
 void mixed_vec(const Hierarchy& H, int op, const double* x, const double* b, double sc, double* y, cudaStream_t s) {
     const MixedSystem& M = *H.mix;
     ProfScope ps(H, kKMixed, H.fine_ref, s);
-    const unsigned g = (unsigned)M.nblocks * 2;
+    const unsigned g = (unsigned)M.nblocks;
     if (op == 0)
         k_scale2<<<g, kDotBlock, 0, s>>>(reinterpret_cast<const double2*>(x), sc, reinterpret_cast<double2*>(y),
                                          M.ntot / 2);
