@@ -366,6 +366,23 @@ def run_hmg(args, ws, rank, local):
                  "solve_ms": ms_m, "ms_per_iteration": ms_m / max(it_m, 1),
                  "unknowns_per_s_per_iteration": unknowns * it_m / (ms_m * 1e-3), "time_share": share}
         del Fd, Xd
+        if rank == 0 and not args.no_cpu_baseline:
+            # the oracle beside it: one preconditioner application + mixed apply on the
+            # host cores (the part of a GMRES iteration outside Gram-Schmidt), bounded sample
+            import oracle
+            cores = len(os.sched_getaffinity(0))
+            os.environ["OMP_NUM_THREADS"] = str(cores)
+            o = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+            Fm = hi.uniform_vector(unknowns, 67)
+            t0 = time.perf_counter()
+            o.mixed_apply(o.mixed_precond(Fm))
+            dt = time.perf_counter() - t0
+            o.close()
+            del Fm
+            mixed["cpu_baseline"] = {"value": unknowns / dt, "unit": "unknowns/s per (preconditioner + apply)",
+                                     "cores": cores, "kind": "oracle",
+                                     "sample": f"one oracle Schur preconditioner application (incl. one V(2,2)) + "
+                                               f"one mixed apply over all {unknowns} unknowns: {dt:.2f} s"}
 
     # ---- end to end: host buffers through hmg_pcg_solve_host ----------------
     hb = torch.from_numpy(b).pin_memory()

@@ -128,6 +128,23 @@ def test_gmres_restart_and_unpreconditioned():
     o.close()
 
 
+@pytest.mark.parametrize("name", ["C0", "C2b_r4"])
+def test_gmres_paper_cycle(name):
+    """The paper's own cycle, V(1,1) with 2 coarse sweeps, as the
+    Schur complement's pressure solve: same GMRES iteration count as the oracle."""
+    cfg = CASES[name]
+    lam, _ = hi.make_inputs(cfg)
+    g = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    o = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    _, N = o.mixed_sizes()
+    F = hi.uniform_vector(N, 68)
+    _, it, rr, st = g.mixed_gmres(g.mixed_to_device(F), rtol=1e-5, params=MGParams(1, 1, 2, 0.8))
+    _, it_o, rr_o, _, st_o = o.mixed_gmres(F, rtol=1e-5, nu_pre=1, nu_post=1, n_coarse=2, omega=0.8)
+    assert st == "HMG_OK" and st_o == 0 and it == it_o, (it, it_o)
+    g.close()
+    o.close()
+
+
 def test_mixed_errors():
     cfg = hi.CONFIGS["C0"]
     lam, _ = hi.make_inputs(cfg)
