@@ -126,6 +126,9 @@ void free_hierarchy(Hierarchy* H) {
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q); cudaFree(H->p2);
     cudaFree(H->partials); cudaFree(H->scal); cudaFree(H->hb); cudaFree(H->hx);
     cudaFree(H->hb1); cudaFree(H->hx1);
+    if (H->xs) cudaStreamDestroy(H->xs);
+    if (H->ev_x_go) cudaEventDestroy(H->ev_x_go);
+    if (H->ev_x_done) cudaEventDestroy(H->ev_x_done);
     if (H->cs_in) cudaStreamDestroy(H->cs_in);
     if (H->cs_out) cudaStreamDestroy(H->cs_out);
     for (int i = 0; i < 2; ++i)
@@ -230,18 +233,41 @@ const double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b,
 
 // Alg. 1 recursively (reading R9): out = V_l(b_l) with zero initial guess.
 // `out` is never the level's wa/wb (it is the coarse level's u or the caller's z).
+// The PCG's deferred x = x + alpha p (pcg_impl): on the side stream xs once
+// the stream reaches the V-cycle's coarse part, where HBM is idle and the
+// cooperative kernel leaves SMs free; `side` = false runs it on s itself.
+// The side stream has low priority and its kernel is enqueued after the
+// coarse-part launch, so the (cooperative) coarse kernel gets its SMs first.
+void flush_pending_x(const Hierarchy& H, cudaStream_t s, bool side, bool go_recorded = false) {
+    if (!H.px.pending) return;
+    const DevLevel& F = H.lev[H.fine_ref];
+    if (side) {
+        if (!go_recorded) cudaEventRecord(H.ev_x_go, s);
+        cudaStreamWaitEvent(H.xs, H.ev_x_go, 0);
+        launch_update_part(H, F, 2, H.px.first, H.px.x, H.px.p, nullptr, H.xs);
+        cudaEventRecord(H.ev_x_done, H.xs);
+    } else {
+        launch_update_part(H, F, 2, H.px.first, H.px.x, H.px.p, nullptr, s);
+    }
+    H.px.pending = false;
+}
+
 void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const double* b, double* out,
                   cudaStream_t s) {
     const DevLevel& L = H.lev[ref];
     if (ref == H.coop_ref && coarse_coop_supported(H)) {   // levels <= coop_ref: one cooperative launch
+        if (H.px.pending) cudaEventRecord(H.ev_x_go, s);
         launch_coarse_coop(H, p, b, out, s);
+        flush_pending_x(H, s, true, true);
         return;
     }
     if (ref == H.tail_ref) {                    // levels <= tail_ref: one launch
+        flush_pending_x(H, s, true);
         launch_coarse_tail(H, p, b, out, s);
         return;
     }
     if (ref == H.coarsest_ref) {
+        flush_pending_x(H, s, true);
         // whole coarsest level in one CTA's shared memory when it fits (ref 0: 20 columns)
         if (H.use_small_sweep && L.n <= kSmallTile && sweep_small_supported(H, L)) {
             ProfScope ps(H, kKCoarseTail, L.ref, s);
@@ -332,7 +358,18 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     // addition from the halos of z and p_old (k_halo_pupdate).
     double* pc = H.z;                              // current search direction
     double* zb = H.z;                              // buffer holding the current z
+    // x = x + alpha p is needed only at the end: with defer_x it leaves the
+    // critical path (r = r - alpha q and <r, r> stay on s), runs on the side
+    // stream under the next V-cycle's coarse part, and s waits for it before
+    // the next apply (which overwrites alpha and, an iteration later, p).
+    bool x_inflight = false;
+    auto join_x = [&]() {
+        if (x_inflight) cudaStreamWaitEvent(s, H.ev_x_done, 0);
+        x_inflight = false;
+    };
+    H.px.pending = false;
     for (int it = 1; it <= maxit; ++it) {
+        join_x();
         if (it == 1) {
             if (dist) halo_exchange(H, F, pc, s);
             launch_apply_dot(H, F, pc, H.q, s);    // q = H^ p, alpha = rho / <p, q>
@@ -345,21 +382,41 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
             launch_apply_pupdate_dot(H, F, zb, pc, pn, H.q, s);
             pc = pn;
         }
-        if (it == 1)
+        if (H.defer_x) {
+            launch_update_part(H, F, 1, it == 1, x, pc, b, s);   // r = r - alpha q (b - alpha q), partial <r, r>
+            H.px.pending = true;
+            H.px.first = it == 1;
+            H.px.x = x;
+            H.px.p = pc;
+        } else if (it == 1) {
             launch_update_xr_first(H, F, x, pc, b, s);   // x = 0 + alpha p, r = b - alpha q, partial <r, r>
-        else
+        } else {
             launch_update_xr(H, F, x, pc, s);      // x += alpha p, r -= alpha q, partial <r, r>
+        }
         launch_finalize(H, kFinRR, s);
         HMG_TRY(check_launch());
         HMG_CUDA(cudaStreamSynchronize(s));
-        if (H.scal_host->bad != ~0ull) return check_bad(H, s);
+        if (H.scal_host->bad != ~0ull) {
+            H.px.pending = false;
+            return check_bad(H, s);
+        }
         const double rn = std::sqrt(H.scal_host->rr);
         *iters = it;
         *relres = rn / bn;
-        if (rn <= rtol * bn) return HMG_OK;
+        if (rn <= rtol * bn) {
+            flush_pending_x(H, s, false);          // the last x update, in stream order
+            HMG_TRY(check_launch());
+            return HMG_OK;
+        }
         zb = (pc != H.z) ? H.z : H.p;              // a buffer that is not p
+        x_inflight = H.px.pending;                 // launched on xs inside the V-cycle (or below)
         precond_dot(H.r, zb, kFinRZ);              // beta = rho' / rho, rho = rho' (p updated in the next apply)
+        if (H.px.pending) {                        // preconditioner without a coarse part
+            flush_pending_x(H, s, false);
+            x_inflight = false;
+        }
     }
+    join_x();
     return fail(HMG_ERR_NOT_CONVERGED, "not converged after " + std::to_string(maxit) +
                                            " iterations (relres " + std::to_string(*relres) + ")");
 }
@@ -434,6 +491,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_FACT_MAX")) H->fact_max_cells = std::atoll(e);
     if (const char* e = std::getenv("HMG_CHECK_SKIP")) H->check_skip = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
+    if (const char* e = std::getenv("HMG_DEFER_X")) H->defer_x = std::string(e) != "0";
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at
         // most kCoopMaxCells cells runs in one cooperative launch -- those levels
@@ -712,6 +770,13 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     }
     H->npartials = partials_needed(F.n, nlayers) + 148 * 8 + 64;
     BCUDA(cudaMalloc(&H->partials, sizeof(double) * H->npartials));
+    {
+        int lo = 0, hi = 0;
+        BCUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));   // lo: the least urgent
+        BCUDA(cudaStreamCreateWithPriority(&H->xs, cudaStreamNonBlocking, lo));
+    }
+    BCUDA(cudaEventCreateWithFlags(&H->ev_x_go, cudaEventDisableTiming));
+    BCUDA(cudaEventCreateWithFlags(&H->ev_x_done, cudaEventDisableTiming));
     BCUDA(cudaMalloc(&H->scal, sizeof(PcgScalars)));
     BCUDA(cudaHostAlloc(&H->scal_host, sizeof(PcgScalars), cudaHostAllocMapped));
     BCUDA(cudaHostGetDevicePointer(&H->scal_pub, H->scal_host, 0));

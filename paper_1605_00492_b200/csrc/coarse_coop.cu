@@ -386,9 +386,14 @@ void launch_coop_tw(const Hierarchy& H, CoopParams& P, cudaStream_t s) {
     int per_sm = 0, sms = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_coarse_coop<TW>, kCoopThreads, smem);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
-    int grid = P.lev[H.coop_ref - H.coarsest_ref].ntiles;
+    // as many rounds of tiles on the top level as the resident CTAs need, the
+    // tiles dealt evenly (C2b: 160 tiles -> 80 CTAs x 2 instead of 148 CTAs of
+    // which 12 take a second tile -- the same critical path, and 68 SMs stay
+    // free for the PCG's deferred x update on the side stream)
+    const int ntop = P.lev[H.coop_ref - H.coarsest_ref].ntiles;
     const int cap = (per_sm < 1 ? 1 : per_sm) * sms;
-    if (grid > cap) grid = cap;
+    const int rounds = (ntop + cap - 1) / cap;
+    const int grid = (ntop + rounds - 1) / rounds;
     ProfScope ps(H, kKCoarseTail, H.coop_ref, s);
     void* args[] = {&P};
     cudaLaunchCooperativeKernel((const void*)k_coarse_coop<TW>, dim3(grid), dim3(kCoopThreads), args, smem, s);

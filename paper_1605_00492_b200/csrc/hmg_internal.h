@@ -177,6 +177,17 @@ struct Hierarchy {
     // copy-in / copy-out streams and their events
     double *hb1 = nullptr, *hx1 = nullptr;
     cudaStream_t cs_in = nullptr, cs_out = nullptr;
+    // PCG: x = x + alpha p deferred to the side stream xs, launched when the
+    // V-cycle reaches its latency-bound coarse part (idle HBM, free SMs)
+    cudaStream_t xs = nullptr;
+    cudaEvent_t ev_x_go = nullptr, ev_x_done = nullptr;
+    struct PendingX {
+        bool pending = false, first = false;
+        double* x = nullptr;
+        const double* p = nullptr;
+    };
+    mutable PendingX px;
+    bool defer_x = true;        // HMG_DEFER_X=0: x and r updated by one kernel on the solve stream
     cudaEvent_t ev_in[2] = {}, ev_solved[2] = {}, ev_out[2] = {};
     int tail_ref = -1;          // levels <= tail_ref run in one coarse-tail launch (-1: off)
     bool tail_grid = false;     // the tail is a cooperative multi-CTA launch (false: one CTA)
@@ -241,6 +252,8 @@ void launch_prolong_add(const Hierarchy& H, const DevLevel& F, const double* uin
 void launch_dot(const Hierarchy& H, const DevLevel& L, const double* a, const double* b, cudaStream_t s);
 void launch_finalize(const Hierarchy& H, int op, cudaStream_t s);
 void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, const double* p, cudaStream_t s);
+void launch_update_part(const Hierarchy& H, const DevLevel& L, int part, bool first, double* x, const double* p,
+                        const double* b, cudaStream_t s);
 // first iteration from x = 0, r = b: x = 0 + alpha p, r = b - alpha q (reads b, not x or r)
 void launch_update_xr_first(const Hierarchy& H, const DevLevel& L, double* x, const double* p, const double* b,
                             cudaStream_t s);

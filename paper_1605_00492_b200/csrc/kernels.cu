@@ -477,7 +477,9 @@ __global__ void __launch_bounds__(kVecBlock) k_dot(const double* __restrict__ a,
 
 // FIRST: the first iteration from x = 0, r = b -- reads b instead of r and does
 // not read x; x = 0 + alpha p and r = b - alpha q are the same operations.
-template <bool FIRST>
+// PART: 0 both updates, 1 r only (with the partial <r, r>), 2 x only (the
+// PCG defers it to a side stream under the V-cycle's coarse tail).
+template <bool FIRST, int PART = 0>
 __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x, double* __restrict__ r,
                                                          const double* __restrict__ p, const double* __restrict__ q,
                                                          const double* __restrict__ rin, int64_t n, int64_t ld, int nz,
@@ -493,20 +495,25 @@ __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x,
             const int64_t c = v.c0 + h * 2 * kVecBlock;
             if (c < n) {
                 const int64_t i = k * ld + c;
-                double2 xx = FIRST ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(x + i);
-                double2 rr = *reinterpret_cast<const double2*>((FIRST ? rin : r) + i);
-                const double2 pp = *reinterpret_cast<const double2*>(p + i);
-                const double2 qq = *reinterpret_cast<const double2*>(q + i);
-                xx.x = xx.x + alpha * pp.x;
-                xx.y = xx.y + alpha * pp.y;
-                rr.x = rr.x - alpha * qq.x;
-                rr.y = rr.y - alpha * qq.y;
-                *reinterpret_cast<double2*>(x + i) = xx;
-                *reinterpret_cast<double2*>(r + i) = rr;
-                s = s + rr.x * rr.x;
-                s = s + rr.y * rr.y;
+                if (PART != 1) {
+                    double2 xx = FIRST ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(x + i);
+                    const double2 pp = *reinterpret_cast<const double2*>(p + i);
+                    xx.x = xx.x + alpha * pp.x;
+                    xx.y = xx.y + alpha * pp.y;
+                    *reinterpret_cast<double2*>(x + i) = xx;
+                }
+                if (PART != 2) {
+                    double2 rr = *reinterpret_cast<const double2*>((FIRST ? rin : r) + i);
+                    const double2 qq = *reinterpret_cast<const double2*>(q + i);
+                    rr.x = rr.x - alpha * qq.x;
+                    rr.y = rr.y - alpha * qq.y;
+                    *reinterpret_cast<double2*>(r + i) = rr;
+                    s = s + rr.x * rr.x;
+                    s = s + rr.y * rr.y;
+                }
             }
         }
+    if (PART == 2) return;
     const double tot = block_sum(s, red);
     if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = tot;
 }
@@ -832,6 +839,19 @@ void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, const do
     ProfScope ps(H, kKVector, H.fine_ref, s);
     k_update_xr<false><<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(x, H.r, p, H.q, nullptr, L.n, L.ld, H.nz, H.scal,
                                                                  H.partials);
+    ++H.launches;
+}
+
+// part 1: r = r - alpha q (first: r = b - alpha q) with partial <r, r>;
+// part 2: x = x + alpha p (first: x = 0 + alpha p)
+void launch_update_part(const Hierarchy& H, const DevLevel& L, int part, bool first, double* x, const double* p,
+                        const double* b, cudaStream_t s) {
+    ProfScope ps(H, kKVector, H.fine_ref, s);
+    const dim3 g = vec_grid(L.n, H.nz);
+    if (part == 1 && first) k_update_xr<true, 1><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
+    if (part == 1 && !first) k_update_xr<false, 1><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
+    if (part == 2 && first) k_update_xr<true, 2><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
+    if (part == 2 && !first) k_update_xr<false, 2><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
     ++H.launches;
 }
 
