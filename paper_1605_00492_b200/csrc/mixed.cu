@@ -339,21 +339,11 @@ __global__ void __launch_bounds__(kDotBlock) k_scale2(const double2* __restrict_
     }
 }
 
-// 0: y = x / s (shared-reciprocal IEEE division, exact '/' redo if the fast
-// path is not valid)   1: y = x - b   2: y = y + x   (scalar: y may be a
-// caller's unaligned vector)
+// 1: y = x - b   2: y = y + x   (scalar: y may be a caller's unaligned vector)
 template <int OP>
-__global__ void k_vec(const double* __restrict__ x, const double* __restrict__ b, double s, double* __restrict__ y,
-                      int64_t N) {
+__global__ void k_vec(const double* __restrict__ x, const double* __restrict__ b, double* __restrict__ y, int64_t N) {
     const int64_t stride = (int64_t)gridDim.x * kDotBlock;
-    const double ys = OP == 0 ? div_recip(s) : 0.0;
     for (int64_t q = (int64_t)blockIdx.x * kDotBlock + threadIdx.x; q < N; q += stride) {
-        if (OP == 0) {
-            bool slow = false;
-            double r = div_fast_z(x[q], s, ys, slow);
-            if (slow) r = x[q] / s;
-            y[q] = r;
-        }
         if (OP == 1) y[q] = x[q] - b[q];
         if (OP == 2) y[q] = y[q] + x[q];
     }
@@ -566,8 +556,8 @@ void mixed_vec(const Hierarchy& H, int op, const double* x, const double* b, dou
     if (op == 0)
         k_scale2<<<g, kDotBlock, 0, s>>>(reinterpret_cast<const double2*>(x), sc, reinterpret_cast<double2*>(y),
                                          M.ntot / 2);
-    if (op == 1) k_vec<1><<<g, kDotBlock, 0, s>>>(x, b, sc, y, M.ntot);
-    if (op == 2) k_vec<2><<<g, kDotBlock, 0, s>>>(x, b, sc, y, M.ntot);
+    if (op == 1) k_vec<1><<<g, kDotBlock, 0, s>>>(x, b, y, M.ntot);
+    if (op == 2) k_vec<2><<<g, kDotBlock, 0, s>>>(x, b, y, M.ntot);
     ++H.launches;
 }
 
