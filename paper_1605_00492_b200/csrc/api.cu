@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <type_traits>
 #include <string>
 
 #include "dist.h"
@@ -121,6 +122,8 @@ void free_hierarchy(Hierarchy* H) {
         cudaFree(L.fden);
         cudaFree(L.small_cells); cudaFree(L.small_count); cudaFree(L.small_loc);
         cudaFree(L.coop_cells); cudaFree(L.coop_count); cudaFree(L.coop_loc);
+        cudaFree(L.hedge); cudaFree(L.edge_e0); cudaFree(L.edge_ne); cudaFree(L.edge_hcells);
+        cudaFree(L.edge_hcount); cudaFree(L.edge_loc); cudaFree(L.edge_own); cudaFree(L.edge_cell);
         cudaFree(L.dist.send_idx); cudaFree(L.dist.sendbuf); cudaFree(L.dist.recvbuf);
     }
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q); cudaFree(H->p2);
@@ -492,6 +495,9 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_CHECK_SKIP")) H->check_skip = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     if (const char* e = std::getenv("HMG_DEFER_X")) H->defer_x = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_EDGE_H")) H->edge_h = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_EDGE_MIN_DOFS")) H->edge_min_dofs = std::atoll(e);
+    if (const char* e = std::getenv("HMG_EDGE_RESID")) H->edge_resid = std::string(e) != "0";
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at
         // most kCoopMaxCells cells runs in one cooperative launch -- those levels
@@ -741,6 +747,98 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
                 L.small.count = L.small_count;
                 L.small.loc = L.small_loc;
             }
+            // edge-deduplicated couplings for the streamed sweep (levels without
+            // precomputed Thomas factors, i.e. the ones k_sweep_st serves)
+            // only where the streamed kernels are bound by HBM bandwidth (>= 16M dofs
+            // on the level); on smaller levels they are bound by the consumers' per-layer
+            // work and the extra copies cost more than the bytes saved (measured at ref 6)
+            if (H->edge_h && L.n > H->fact_max_cells && L.halo.loc && L.n * nlayers >= H->edge_min_dofs) {
+                const int64_t n = L.n, ntl = (n + kSweepTile - 1) / kSweepTile;
+                std::vector<int64_t> eown(n + 1, 0);
+                for (int64_t c = 0; c < n; ++c) {
+                    int cnt = 0;
+                    for (int j = 0; j < 3; ++j) cnt += nbl[c * 3 + j] > c;
+                    eown[c + 1] = eown[c] + cnt;
+                }
+                const int64_t nE = eown[n], ldE = round_up32(nE);
+                std::vector<int32_t> eid(3 * n), own(2 * ldE, 0);
+                for (int64_t c = 0; c < n; ++c) {
+                    int64_t q = eown[c];
+                    for (int j = 0; j < 3; ++j) {
+                        const int32_t o = nbl[c * 3 + j];
+                        if (o > c) {
+                            eid[3 * c + j] = (int32_t)q;
+                            own[q] = (int32_t)c;
+                            own[ldE + q] = j;
+                            ++q;
+                        }
+                    }
+                }
+                for (int64_t c = 0; c < n; ++c)
+                    for (int j = 0; j < 3; ++j) {
+                        const int32_t o = nbl[c * 3 + j];
+                        if (o < c) {                     // owned by o (< c, so owned, not a halo slot)
+                            int jo = 0;
+                            while (jo < 3 && nbl[o * 3 + jo] != (int32_t)c) ++jo;
+                            int64_t q = eown[o];
+                            for (int i = 0; i < jo; ++i) q += nbl[o * 3 + i] > o;
+                            eid[3 * c + j] = (int32_t)q;
+                        }
+                    }
+                std::vector<int32_t> e0(ntl), nel(ntl), hc(ntl * kEdgeHalo, 0), hn(ntl, 0);
+                std::vector<uint32_t> eloc(L.ld, 0);
+                bool ok = true;
+                for (int64_t t = 0; t < ntl && ok; ++t) {
+                    const int64_t a = t * kSweepTile, e = std::min<int64_t>(n, a + kSweepTile);
+                    const int64_t lo = eown[a] & ~int64_t(1), hi = (eown[e] + 1) & ~int64_t(1);
+                    if (hi - lo > kEdgeRange) ok = false;
+                    e0[t] = (int32_t)lo;
+                    nel[t] = (int32_t)(hi - lo);
+                    for (int64_t c = a; c < e && ok; ++c) {
+                        uint32_t packed = 0;
+                        for (int j = 0; j < 3; ++j) {
+                            const int32_t id = eid[3 * c + j];
+                            uint32_t off;
+                            if (id >= eown[a] && id < eown[e]) {
+                                off = (uint32_t)(id - lo);
+                            } else {
+                                if (hn[t] >= kEdgeHalo) { ok = false; break; }
+                                hc[t * kEdgeHalo + hn[t]] = id;
+                                off = (uint32_t)(kEdgeRange + hn[t]);
+                                ++hn[t];
+                            }
+                            packed |= off << (8 * j);
+                        }
+                        eloc[c] = packed;
+                    }
+                }
+                if (ok) {
+                    auto up = [&](auto** dst, const auto& src) -> bool {
+                        using T = typename std::decay_t<decltype(src)>::value_type;
+                        return cudaMalloc(reinterpret_cast<void**>(dst), sizeof(T) * src.size()) == cudaSuccess &&
+                               cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice) ==
+                                   cudaSuccess;
+                    };
+                    std::vector<int32_t> ecell(3 * L.ld, 0);
+                    for (int64_t c = 0; c < n; ++c)
+                        for (int j = 0; j < 3; ++j) ecell[j * L.ld + c] = eid[3 * c + j];
+                    if (!(up(&L.edge_e0, e0) && up(&L.edge_ne, nel) && up(&L.edge_hcells, hc) &&
+                          up(&L.edge_hcount, hn) && up(&L.edge_loc, eloc) && up(&L.edge_own, own) &&
+                          up(&L.edge_cell, ecell)))
+                        return cleanup(fail(HMG_ERR_OOM, "edge tables: device allocation failed"));
+                    BCUDA(cudaMalloc(&L.hedge, sizeof(double) * nlayers * ldE));
+                    BCUDA(cudaMemset(L.hedge, 0, sizeof(double) * nlayers * ldE));
+                    L.edge.H = L.hedge;
+                    L.edge.ldE = ldE;
+                    L.edge.e0 = L.edge_e0;
+                    L.edge.ne = L.edge_ne;
+                    L.edge.hcells = L.edge_hcells;
+                    L.edge.hcount = L.edge_hcount;
+                    L.edge.loc = L.edge_loc;
+                    L.edge.cell = L.edge_cell;
+                    L.edge_count = nE;
+                }
+            }
             const int ctw = coarse_coop_tile_width(nlayers);
             if (r <= H->coop_ref && ctw == kSmallTile) {
                 L.coop_halo = L.small;
@@ -761,7 +859,10 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
                            cudaMemcpyHostToDevice));
         for (int r = fine_ref - 1; r >= coarsest_ref; --r) launch_coarsen_lam(*H, H->lev[r + 1], H->lev[r], s);
     }
-    for (int r = coarsest_ref; r <= fine_ref; ++r) launch_assemble(*H, H->lev[r], s);
+    for (int r = coarsest_ref; r <= fine_ref; ++r) {
+        launch_assemble(*H, H->lev[r], s);
+        if (H->lev[r].hedge) launch_edge_h(*H, H->lev[r], H->lev[r].edge_count, s);
+    }
     // PCG workspace
     const size_t fb = sizeof(double) * nlayers * F.ld;
     for (double** v : {&H->r, &H->z, &H->p, &H->q, &H->p2}) {

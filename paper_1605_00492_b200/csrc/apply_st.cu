@@ -45,26 +45,30 @@ struct ApMaps {
 };
 
 struct ApLayout {
-    int x, z, hx, hz, stage;
+    int x, z, hx, hz, eh, stage;
 };
-__host__ __device__ constexpr ApLayout ap_layout(bool pupd, int G) {
+// eh: the band box carries D and U only; couplings from the edge store (one
+// row of kEdgeRow doubles per layer: contiguous range, then gathered edges)
+__host__ __device__ constexpr ApLayout ap_layout(bool pupd, int G, bool eh = false) {
     ApLayout L{};
-    L.x = 5 * G * kTile;
+    L.x = (eh ? 2 : 5) * G * kTile;
     L.z = L.x + (G + 1) * kTile;
     L.hx = L.z + (pupd ? (G + 1) * kTile : 0);
     L.hz = L.hx + G * kHaloMax;
-    L.stage = L.hz + (pupd ? G * kHaloMax : 0);
+    L.eh = L.hz + (pupd ? G * kHaloMax : 0);
+    L.stage = L.eh + (eh ? G * kEdgeRow : 0);
     return L;
 }
 
-template <bool DOT, bool PUPD, int G>
+template <bool DOT, bool PUPD, int G, bool EH = false>
 __global__ void __launch_bounds__(kThreads, 2)
-    k_apply_st(const __grid_constant__ ApMaps maps, LevelView L, TileHalo th, const double* __restrict__ xin,
+    k_apply_st(const __grid_constant__ ApMaps maps, LevelView L, TileHalo th, EdgeTiles et,
+               const double* __restrict__ xin,
                const double* __restrict__ zv, double* __restrict__ y, double* __restrict__ pnew,
                double* __restrict__ partial, const PcgScalars* __restrict__ sc, int S) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ double red[kThreads / 32];
-    constexpr ApLayout AL = ap_layout(PUPD, G);
+    constexpr ApLayout AL = ap_layout(PUPD, G, EH);
     const int nz = L.nz;
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
@@ -95,18 +99,25 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (warp == kConsumerWarps) {
         // ======================= producer warp =======================
         const uint64_t pol = ptx::policy_evict_first();
-        const uint32_t bytes = (uint32_t)(sizeof(double) * (5 * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile));
+        const uint32_t bytes =
+            (uint32_t)(sizeof(double) * ((EH ? 2 : 5) * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile));
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int x = tile * kTile;
             const int hcount = th.count[tile];
             const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
             const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
+            const int32_t ee0 = EH ? et.e0[tile] : 0;
+            const uint32_t ebytes = EH ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
+            const int ehc = EH ? et.hcount[tile] : 0;
+            const int32_t eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
                 ptx::mbar_wait(&empty[s], phase ^ 1u);
                 double* st = stages + (size_t)s * AL.stage;
                 for (int kk = 0; kk < G; ++kk) {
                     const int k = gi * G + kk;
                     if (k >= nz) break;
+                    if (EH && lane < ehc)
+                        ptx::cp_async8(st + AL.eh + kk * kEdgeRow + kEdgeRange + lane, et.H + (int64_t)k * et.ldE + eh0);
                     const double* src = xin + (int64_t)k * ld;
                     if (lane < hcount) ptx::cp_async8(st + AL.hx + kk * kHaloMax + lane, src + h0);
                     if (lane + 32 < hcount) ptx::cp_async8(st + AL.hx + kk * kHaloMax + lane + 32, src + h1);
@@ -119,7 +130,13 @@ __global__ void __launch_bounds__(kThreads, 2)
                 ptx::cp_async_arrive(&full[s]);
                 __syncwarp();
                 if (lane == 0) {
-                    ptx::mbar_arrive_expect_tx(&full[s], bytes);
+                    int nl = nz - gi * G;
+                    nl = nl < G ? nl : G;
+                    ptx::mbar_arrive_expect_tx(&full[s], bytes + (EH ? (uint32_t)nl * ebytes : 0u));
+                    if (EH)
+                        for (int kk = 0; kk < nl; ++kk)
+                            ptx::bulk_g2s(st + AL.eh + kk * kEdgeRow, et.H + (int64_t)(gi * G + kk) * et.ldE + ee0,
+                                          ebytes, &full[s]);
                     ptx::tma_load_3d_hint(st, &maps.bands, x, gi * G, 0, &full[s], pol);
                     ptx::tma_load_2d(st + AL.x, &maps.x, x, gi * G, &full[s]);
                     if (PUPD) ptx::tma_load_2d(st + AL.z, &maps.z, x, gi * G, &full[s]);
@@ -135,6 +152,13 @@ __global__ void __launch_bounds__(kThreads, 2)
             const bool valid = c < L.n;
             const uint32_t loc = th.loc[valid ? c : L.n - 1];
             const int l0 = loc & 0xff, l1 = (loc >> 8) & 0xff, l2 = (loc >> 16) & 0xff;
+            int eo0 = 0, eo1 = 0, eo2 = 0;             // the faces' offsets in an edge row
+            if (EH) {
+                const uint32_t el = et.loc[valid ? c : L.n - 1];
+                eo0 = el & 0xff;
+                eo1 = (el >> 8) & 0xff;
+                eo2 = (el >> 16) & 0xff;
+            }
             double xm = 0.0, Um = 0.0;
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
                 ptx::mbar_wait(&full[s], phase);
@@ -164,9 +188,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                     double acc = Dk * xk;
                     if (IN || k > 0) acc = acc + Um * xm;
                     if (IN || k < nz - 1) acc = acc + Uk * xp;
-                    acc = acc + sr[2 * G * kTile] * XV(kk, l0);
-                    acc = acc + sr[3 * G * kTile] * XV(kk, l1);
-                    acc = acc + sr[4 * G * kTile] * XV(kk, l2);
+                    const double* er = st + AL.eh + kk * kEdgeRow;
+                    acc = acc + (EH ? er[eo0] : sr[2 * G * kTile]) * XV(kk, l0);
+                    acc = acc + (EH ? er[eo1] : sr[3 * G * kTile]) * XV(kk, l1);
+                    acc = acc + (EH ? er[eo2] : sr[4 * G * kTile]) * XV(kk, l2);
                     if (valid) {
                         const int64_t i = (int64_t)k * ld + c;
                         y[i] = acc;
@@ -203,11 +228,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
-template <bool DOT, bool PUPD, int G>
+template <bool DOT, bool PUPD, int G, bool EH = false>
 int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const double* z, double* y, double* pnew,
               cudaStream_t s) {
     const int nz = H.nz;
-    constexpr ApLayout AL = ap_layout(PUPD, G);
+    constexpr ApLayout AL = ap_layout(PUPD, G, EH);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
     const size_t budget = 110 * 1024;
@@ -216,20 +241,20 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     const size_t smem = 1024 + sizeof(double) * (size_t)S * AL.stage;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_apply_st<DOT, PUPD, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_apply_st<DOT, PUPD, G, EH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     ApMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     const LevelView V = L.view(nz);
-    maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, 5);
+    maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, EH ? 2 : 5);
     maps.x = make_tensor_map(x, L.ld, nz, kTile, G + 1, 1);
     if (PUPD) maps.z = make_tensor_map(z, L.ld, nz, kTile, G + 1, 1);
     const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
     const unsigned cap = (unsigned)(2 * sms);
     const unsigned grid = ntiles < cap ? ntiles : cap;
-    launch_pdl(H, k_apply_st<DOT, PUPD, G>, dim3(grid), dim3(kThreads), smem, s, maps, V, L.halo, x, z, y, pnew,
-               H.partials, H.scal, S);
+    launch_pdl(H, k_apply_st<DOT, PUPD, G, EH>, dim3(grid), dim3(kThreads), smem, s, maps, V, L.halo, L.edge, x, z, y,
+               pnew, H.partials, H.scal, S);
     return (int)grid;
 }
 
@@ -243,8 +268,13 @@ bool apply_st_supported(const Hierarchy& H, const DevLevel& L) {
 int launch_apply_st(const Hierarchy& H, const DevLevel& L, const double* x, double* y, bool dot, cudaStream_t s) {
     int n = 0;
     try {
-        if (dot)
+        const bool eh = L.edge.H != nullptr;
+        if (dot && eh)
+            n = launch_ap<true, false, 2, true>(H, L, x, nullptr, y, nullptr, s);
+        else if (dot)
             n = launch_ap<true, false, 2>(H, L, x, nullptr, y, nullptr, s);
+        else if (eh)
+            launch_ap<false, false, 2, true>(H, L, x, nullptr, y, nullptr, s);
         else
             launch_ap<false, false, 2>(H, L, x, nullptr, y, nullptr, s);
     } catch (const std::exception& e) {
@@ -259,7 +289,10 @@ int launch_apply_pupdate_st(const Hierarchy& H, const DevLevel& L, const double*
                             double* q, cudaStream_t s) {
     int n = 0;
     try {
-        n = launch_ap<true, true, 2>(H, L, pold, z, q, pnew, s);
+        if (L.edge.H)
+            n = launch_ap<true, true, 2, true>(H, L, pold, z, q, pnew, s);
+        else
+            n = launch_ap<true, true, 2>(H, L, pold, z, q, pnew, s);
     } catch (const std::exception& e) {
         g_launch_error = std::string("apply launch: ") + e.what();
     }

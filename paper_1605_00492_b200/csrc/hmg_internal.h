@@ -31,6 +31,25 @@ struct TileHalo {
     const uint32_t* loc = nullptr;    // [ld]
 };
 
+// Edge-deduplicated horizontal couplings for the streamed sweep (each face
+// coupling stored once, 1.5 per cell instead of 3).  Edges are numbered by
+// their lower cell, then its slot, so the edges owned by a 128-cell tile are
+// one contiguous range (176-216 at ref >= 5; streamed with one bulk copy per
+// layer); the <= 32 faces whose lower cell lies before the tile are gathered.
+constexpr int kEdgeRange = 224;   // contiguous part of a stage row (doubles)
+constexpr int kEdgeHalo = 32;     // gathered part
+constexpr int kEdgeRow = kEdgeRange + kEdgeHalo;
+struct EdgeTiles {
+    const double* H = nullptr;        // [nz][ldE] coupling of each edge and layer
+    int64_t ldE = 0;
+    const int32_t* e0 = nullptr;      // [ntiles] first edge of the tile's range (even)
+    const int32_t* ne = nullptr;      // [ntiles] edges per layer to copy (even)
+    const int32_t* hcells = nullptr;  // [ntiles][kEdgeHalo] edges owned before the tile
+    const int32_t* hcount = nullptr;  // [ntiles]
+    const uint32_t* loc = nullptr;    // [ld] per cell: 3 x 8-bit offsets into a stage row
+    const int32_t* cell = nullptr;    // [3][ld] edge across each face of a cell (thread-per-column kernels)
+};
+
 // Same for the 32-column tiles of the small-level sweep.
 struct SmallHalo {
     const int32_t* cells = nullptr;   // [ntiles][kSmallHaloMax]
@@ -92,6 +111,14 @@ struct DevLevel {
     int32_t* coop_count = nullptr;
     uint32_t* coop_loc = nullptr;
     SmallHalo coop_halo;
+    // edge-deduplicated couplings (streamed-sweep levels; HMG_EDGE_H=0 disables)
+    double* hedge = nullptr;
+    int32_t *edge_e0 = nullptr, *edge_ne = nullptr, *edge_hcells = nullptr, *edge_hcount = nullptr;
+    uint32_t* edge_loc = nullptr;
+    int32_t* edge_own = nullptr;      // [2][ldE] owner cell and slot of each edge (setup)
+    int32_t* edge_cell = nullptr;     // [3][ld] edge across each face
+    int64_t edge_count = 0;
+    EdgeTiles edge;
     // Thomas factors (coarse-tail levels only): pivots, refined reciprocals, multipliers
     double* fden = nullptr;
     double* fy = nullptr;
@@ -218,6 +245,9 @@ struct Hierarchy {
     bool use_st_apply = true;   // HMG_APPLY_ST=0: thread-per-column k_apply_t instead of k_apply_st
     bool matrix_free = false;   // operator applies recompute the couplings from lam + geometry (NEXT-2)   // HMG_SWEEP_ST=0: non-zero-guess sweeps by k_sweep_tc instead of k_sweep_st
     bool use_small_sweep = true;
+    bool edge_h = true;         // HMG_EDGE_H=0: streamed sweeps read the per-cell H bands
+    bool edge_resid = true;     // HMG_EDGE_RESID=0: residual + restriction reads the per-cell bands
+    int64_t edge_min_dofs = 16LL << 20;   // levels with fewer dofs keep the per-cell bands (HMG_EDGE_MIN_DOFS)
     int l2_prefetch_groups = 0;   // measured: the ring alone is as fast at ref 7 and faster at ref 6
 };
 
@@ -235,6 +265,7 @@ int mixed_lin_max();
 void vcycle_fine(const Hierarchy& H, const hmg_mg_params& p, const double* b, double* out, cudaStream_t s);
 
 // kernels.cu
+void launch_edge_h(const Hierarchy& H, const DevLevel& L, int64_t nedges, cudaStream_t s);
 void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
 void launch_coarsen_lam(const Hierarchy& H, const DevLevel& F, const DevLevel& C, cudaStream_t s);
 void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s);

@@ -330,7 +330,10 @@ __global__ void k_restrict(const double* __restrict__ r, int64_t ldf, double* __
 // Residual of the current iterate restricted to the coarse level: each lane
 // computes r = b - H^ u for its column; groups of 4 lanes (the 4 children of
 // one parent) combine in child order through shuffles.
-__global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, const double* __restrict__ b,
+// EH: the couplings are read from the edge store (1.5 per cell instead of 3;
+// the same values bit for bit)
+template <bool EH>
+__global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, EdgeTiles et, const double* __restrict__ b,
                                                                 const double* __restrict__ u,
                                                                 double* __restrict__ bc, int64_t ldc, int64_t coff) {
     const int64_t cc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -341,6 +344,12 @@ __global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, con
     const int kc = (nz + gridDim.y - 1) / gridDim.y;
     const int k0 = blockIdx.y * kc, k1 = min(nz, k0 + kc);
     const int32_t n0 = L.nbr[c], n1 = L.nbr[ld + c], n2 = L.nbr[2 * ld + c];
+    int32_t e0 = 0, e1 = 0, e2 = 0;
+    if (EH) {
+        e0 = et.cell[c];
+        e1 = et.cell[ld + c];
+        e2 = et.cell[2 * ld + c];
+    }
     const int lane = threadIdx.x & 31;
     if (k0 >= k1) return;                 // uniform across the block
     double um = k0 > 0 ? u[(int64_t)(k0 - 1) * ld + c] : 0.0;
@@ -354,9 +363,10 @@ __global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, con
         double acc = L.D[i] * uk;
         if (k > 0) acc = acc + Um * um;
         if (k < nz - 1) acc = acc + Uk * up;
-        acc = acc + L.H0[i] * u[row + n0];
-        acc = acc + L.H1[i] * u[row + n1];
-        acc = acc + L.H2[i] * u[row + n2];
+        const double* eh = et.H + k * et.ldE;
+        acc = acc + (EH ? eh[e0] : L.H0[i]) * u[row + n0];
+        acc = acc + (EH ? eh[e1] : L.H1[i]) * u[row + n1];
+        acc = acc + (EH ? eh[e2] : L.H2[i]) * u[row + n2];
         const double r = b[i] - acc;
         const double r1 = __shfl_down_sync(0xffffffffu, r, 1);
         const double r2 = __shfl_down_sync(0xffffffffu, r, 2);
@@ -647,6 +657,24 @@ void launch_coarsen_lam(const Hierarchy& H, const DevLevel& F, const DevLevel& C
     ++H.launches;
 }
 
+// Edge-deduplicated couplings: H_e[k][e] = H_j[k][a] for the owner (a, j) of
+// edge e (a copy of the band value; the other cell's band holds the same
+// bits, the assembly being bitwise symmetric).
+__global__ void k_edge_h(const int32_t* __restrict__ own, int64_t ne, int64_t ldE, int64_t ld, int nz,
+                         const double* __restrict__ bands, double* __restrict__ hedge) {
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int k = blockIdx.y;
+    if (e >= ne) return;
+    const int64_t a = own[e], j = own[ldE + e];
+    hedge[k * ldE + e] = bands[((2 + j) * nz + k) * ld + a];
+}
+
+void launch_edge_h(const Hierarchy& H, const DevLevel& L, int64_t nedges, cudaStream_t s) {
+    dim3 g(blocks(nedges, 256), H.nz);
+    k_edge_h<<<g, 256, 0, s>>>(L.edge_own, nedges, L.edge.ldE, L.ld, H.nz, L.bands, L.hedge);
+    ++H.launches;
+}
+
 void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
     dim3 g(blocks(L.n, 256), H.nz);
     k_assemble<<<g, 256, 0, s>>>(L.n, L.ld, H.nz, L.nbr, L.geom, L.lam, H.w2, H.dz, L.bands);
@@ -749,7 +777,10 @@ void launch_resid_restrict(const Hierarchy& H, const DevLevel& F, const double* 
     ProfScope ps(H, kKResidRestrict, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
     dim3 g(blocks(F.n, kApplyBlock), vchunks(F.n, H.nz));
-    k_resid_restrict<<<g, kApplyBlock, 0, s>>>(F.view(H.nz), b, u, bc, C.ld, F.dist.coff);
+    if (F.edge.H && H.edge_resid)
+        k_resid_restrict<true><<<g, kApplyBlock, 0, s>>>(F.view(H.nz), F.edge, b, u, bc, C.ld, F.dist.coff);
+    else
+        k_resid_restrict<false><<<g, kApplyBlock, 0, s>>>(F.view(H.nz), F.edge, b, u, bc, C.ld, F.dist.coff);
     ++H.launches;
 }
 

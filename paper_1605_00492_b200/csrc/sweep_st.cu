@@ -73,19 +73,23 @@ struct StMaps {
 // of u (+ u_c), off-tile neighbour values (u, u_c, lam) of the G layers.
 // Backward stage: [0, 8 kTile) u rows, then 8 kTile/4 u_c rows.
 struct StLayout {
-    int op, band, b, u, uc, hu, huc, hlam, fwd, bwd, stage;
+    int op, band, b, u, uc, hu, huc, hlam, eh, fwd, bwd, stage;
 };
-__host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool mf, int G, bool dot = false) {
+// eh: the band box carries D and U only; the couplings come from the edge
+// store, one row of kEdgeRow doubles per layer (contiguous range, then gathered)
+__host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool mf, int G, bool dot = false,
+                                                 bool eh = false) {
     StLayout L{};
     L.op = 0;                                        // band rows (stored), or lam rows (matrix-free)
     L.band = mf ? (G + 1) * kTile : 0;               // band rows as the consumers read them
-    L.b = L.band + 5 * G * kTile;
+    L.b = L.band + (eh ? 2 : 5) * G * kTile;
     L.u = L.b + G * kTile;
     L.uc = L.u + (zero ? 0 : (G + 1) * kTile);
     L.hu = L.uc + (prolong ? (G + 1) * (kTile / 4) : 0);
     L.huc = L.hu + (zero ? 0 : G * kHaloMax);
     L.hlam = L.huc + (prolong ? G * kHaloMax : 0);
-    L.fwd = L.hlam + (mf ? G * kHaloMax : 0);
+    L.eh = L.hlam + (mf ? G * kHaloMax : 0);
+    L.fwd = L.eh + (eh ? G * kEdgeRow : 0);
     L.bwd = zero ? 0 : kBack * kTile + (prolong ? kBack * (kTile / 4) : 0) + (dot ? kBack * kTile : 0);
     L.stage = L.fwd > L.bwd ? L.fwd : L.bwd;
     return L;
@@ -99,15 +103,17 @@ struct StOp {
     double w2, dz;
 };
 
-template <bool ZERO, bool PROLONG, bool MF, int G, bool CHK, bool DOT = false>
+template <bool ZERO, bool PROLONG, bool MF, int G, bool CHK, bool DOT = false, bool EH = false>
 __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
-    k_sweep_st(const __grid_constant__ StMaps maps, LevelView L, StOp op, TileHalo th, const double* __restrict__ bvec,
+    k_sweep_st(const __grid_constant__ StMaps maps, LevelView L, StOp op, TileHalo th, EdgeTiles et,
+               const double* __restrict__ bvec,
                const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc, double* __restrict__ uout,
                double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols, int pf_groups,
                double* __restrict__ partial) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ double dred[kThreads / 32];
-    constexpr StLayout SL = st_layout(ZERO, PROLONG, MF, G, DOT);
+    static_assert(!(EH && (ZERO || MF)), "edge store: general stored-band sweeps only");
+    constexpr StLayout SL = st_layout(ZERO, PROLONG, MF, G, DOT, EH);
     double dotacc = 0.0;                               // DOT: this thread's sum of b_k u'_k
 #ifdef HMG_TIMING
     long long tt0 = 0, wf = 0, wb = 0, ntl = 0, tfw = 0, tbk = 0, tfw0 = 0, tws = 0;
@@ -214,7 +220,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
         // ======================= producer warp =======================
         const uint64_t pol_stream = ptx::policy_evict_first();
         const uint64_t pol_keep = ptx::policy_evict_last();
-        constexpr int op_rows = MF ? (G + 1) * kTile : 5 * G * kTile;
+        constexpr int op_rows = MF ? (G + 1) * kTile : (EH ? 2 : 5) * G * kTile;
         const uint32_t fwd_bytes =
             (uint32_t)(sizeof(double) * (op_rows + G * kTile + (ZERO ? 0 : (G + 1) * kTile) +
                                          (PROLONG ? (G + 1) * (kTile / 4) : 0)));
@@ -233,9 +239,22 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
             const int hcount = HALO ? th.count[tile] : 0;
             const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
             const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
+            // edge store: the tile's contiguous edge range and its gathered edges
+            const int32_t ee0 = EH ? et.e0[tile] : 0;
+            const uint32_t ebytes = EH ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
+            const int ehc = EH ? et.hcount[tile] : 0;
+            const int32_t eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
                 ptx::mbar_wait(&empty[s], phase ^ 1u);
                 double* st = stages + (size_t)s * SL.stage;
+                if (EH) {
+                    for (int kk = 0; kk < G; ++kk) {
+                        const int k = gi * G + kk;
+                        if (k >= nz) break;
+                        if (lane < ehc) ptx::cp_async8(st + SL.eh + kk * kEdgeRow + kEdgeRange + lane,
+                                                       et.H + (int64_t)k * et.ldE + eh0);
+                    }
+                }
                 if (HALO) {
                     for (int kk = 0; kk < G; ++kk) {          // off-tile neighbours of the G layers
                         const int k = gi * G + kk;
@@ -270,7 +289,13 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         ptx::tma_prefetch_2d(&maps.b, x, gp * G);
                         if (!ZERO) ptx::tma_prefetch_2d(&maps.uf, x, gp * G);
                     }
-                    ptx::mbar_arrive_expect_tx(&full[s], fwd_bytes);
+                    int nl = nz - gi * G;
+                    nl = nl < G ? nl : G;
+                    ptx::mbar_arrive_expect_tx(&full[s], fwd_bytes + (EH ? (uint32_t)nl * ebytes : 0u));
+                    if (EH)
+                        for (int kk = 0; kk < nl; ++kk)
+                            ptx::bulk_g2s(st + SL.eh + kk * kEdgeRow, et.H + (int64_t)(gi * G + kk) * et.ldE + ee0,
+                                          ebytes, &full[s]);
                     if (MF)
                         ptx::tma_load_2d_hint(st + SL.op, &maps.lam, x, gi * G, &full[s], pol_stream);
                     else
@@ -322,6 +347,13 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 l0 = loc & 0xff;
                 l1 = (loc >> 8) & 0xff;
                 l2 = (loc >> 16) & 0xff;
+            }
+            int eo0 = 0, eo1 = 0, eo2 = 0;                 // the faces' offsets in an edge row
+            if (EH) {
+                const uint32_t el = et.loc[cv];
+                eo0 = el & 0xff;
+                eo1 = (el >> 8) & 0xff;
+                eo2 = (el >> 16) & 0xff;
             }
             ColumnGeom cg{};
 
@@ -380,9 +412,10 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     const double* sr = st + SL.band + kk * kTile + j;
                     const double Dk = sr[0];
                     const double Uk = sr[G * kTile];
-                    const double H0 = sr[2 * G * kTile];
-                    const double H1 = sr[3 * G * kTile];
-                    const double H2 = sr[4 * G * kTile];
+                    const double* er = st + SL.eh + kk * kEdgeRow;
+                    const double H0 = EH ? er[eo0] : sr[2 * G * kTile];
+                    const double H1 = EH ? er[eo1] : sr[3 * G * kTile];
+                    const double H2 = EH ? er[eo2] : sr[4 * G * kTile];
                     const double bk = st[SL.b + kk * kTile + j];
                     double r;
                     if (ZERO) {
@@ -631,12 +664,12 @@ uint32_t st_tmem_cols(int nz) {
     return c;
 }
 
-template <bool Z, bool P, bool M, int G, bool CK = true, bool DOT = false>
+template <bool Z, bool P, bool M, int G, bool CK = true, bool DOT = false, bool EH = false>
 int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
               double* uout, double omega, cudaStream_t s) {
     const int nz = H.nz;
     const uint32_t cols = st_tmem_cols(nz);
-    constexpr StLayout SL = st_layout(Z, P, M, G, DOT);
+    constexpr StLayout SL = st_layout(Z, P, M, G, DOT, EH);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
     const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
@@ -649,7 +682,8 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
     if (smem < floor_smem) smem = floor_smem;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_sweep_st<Z, P, M, G, CK, DOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        cudaFuncSetAttribute(k_sweep_st<Z, P, M, G, CK, DOT, EH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             220 * 1024);
         attr = true;
     }
     StMaps maps;
@@ -658,7 +692,7 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
     if (M)
         maps.lam = make_tensor_map(L.lam, L.ld, nz, kTile, G + 1, 1);
     else
-        maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, 5);
+        maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, EH ? 2 : 5);
     maps.b = make_tensor_map(b, L.ld, nz, kTile, G, 1);
     if (!Z) {
         maps.uf = make_tensor_map(uin, L.ld, nz, kTile, G + 1, 1);
@@ -679,8 +713,9 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
     const unsigned cap = (unsigned)((two ? 2 : 1) * sms);
     const unsigned rounds = (ntiles + cap - 1) / cap;
     const unsigned grid = (ntiles + rounds - 1) / rounds;
-    launch_pdl(H, k_sweep_st<Z, P, M, G, CK, DOT>, dim3(grid), dim3(M ? kThreadsMf : kThreads), smem, s, maps, V, op,
-               L.halo, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups, H.partials);
+    launch_pdl(H, k_sweep_st<Z, P, M, G, CK, DOT, EH>, dim3(grid), dim3(M ? kThreadsMf : kThreads), smem, s, maps, V,
+               op, L.halo, L.edge, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups,
+               H.partials);
     return (int)grid;
 }
 
@@ -692,6 +727,13 @@ namespace {
 
 }  // namespace
 
+// The sweep reads the edge store only where two CTAs share an SM (nz <= 64):
+// with one CTA per SM (nz = 128) its consumers are the bottleneck and the
+// extra copies made the C4 sweep 25% slower (measured); the apply uses it always.
+bool sweep_edge_store(const Hierarchy& H, const DevLevel& L) {
+    return L.edge.H != nullptr && st_tmem_cols(H.nz) <= 256;
+}
+
 bool sweep_st_supported(const Hierarchy& H, const DevLevel& L) {
     return H.use_st_sweep && H.nz <= 128 && L.halo.loc != nullptr;
 }
@@ -700,8 +742,13 @@ int launch_sweep_st_dot(const Hierarchy& H, const DevLevel& L, const double* b, 
                         double omega, cudaStream_t s) {
     int n = 0;
     try {
-        if (L.g_safe)
+        const bool eh = sweep_edge_store(H, L);
+        if (L.g_safe && eh)
+            n = launch_st<false, false, false, 2, false, true, true>(H, L, b, uin, nullptr, uout, omega, s);
+        else if (L.g_safe)
             n = launch_st<false, false, false, 2, false, true>(H, L, b, uin, nullptr, uout, omega, s);
+        else if (eh)
+            n = launch_st<false, false, false, 2, true, true, true>(H, L, b, uin, nullptr, uout, omega, s);
         else
             n = launch_st<false, false, false, 2, true, true>(H, L, b, uin, nullptr, uout, omega, s);
     } catch (const std::exception& e) {
@@ -728,6 +775,15 @@ void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, con
                 launch_st<false, true, true, 2>(H, L, b, uin, uc, uout, omega, s);
             else
                 launch_st<false, false, true, 2>(H, L, b, uin, nullptr, uout, omega, s);
+        } else if (uin && sweep_edge_store(H, L)) {   // edge-deduplicated couplings
+            if (L.g_safe && uc)
+                launch_st<false, true, false, 2, false, false, true>(H, L, b, uin, uc, uout, omega, s);
+            else if (L.g_safe)
+                launch_st<false, false, false, 2, false, false, true>(H, L, b, uin, nullptr, uout, omega, s);
+            else if (uc)
+                launch_st<false, true, false, 2, true, false, true>(H, L, b, uin, uc, uout, omega, s);
+            else
+                launch_st<false, false, false, 2, true, false, true>(H, L, b, uin, nullptr, uout, omega, s);
         } else if (L.g_safe) {
             if (!uin)
                 launch_st<true, false, false, 2, false>(H, L, b, nullptr, nullptr, uout, omega, s);
