@@ -219,6 +219,14 @@ hmg_status hmg_pcg_solve_single_level(const hmg_hierarchy* h, int nsweeps, doubl
 hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, double* geom,
                             double* bands, double* lam);
 
+/* Diagnostic: which kernels of level `ref` read the edge-deduplicated coupling
+ * store (each face coupling stored once per layer instead of once per cell
+ * side; built on levels of >= 16M dofs): bit 0 the streamed sweep, bit 1 the
+ * streamed apply, bit 2 residual + restriction (then formed by the streamed
+ * apply with a restriction epilogue).  Their algorithmic bytes per dof drop
+ * by 12 (1.5 instead of 3 couplings); results are bitwise unchanged. */
+hmg_status hmg_edge_store(const hmg_hierarchy* h, int ref, int* kernels);
+
 /* Kernel launches issued by the library since the hierarchy was built
  * (diagnostic counter used by the benchmark's gpu_launches claim). */
 int64_t hmg_launch_count(const hmg_hierarchy* h);

@@ -89,6 +89,7 @@ def load_library():
         "hmg_nccl_unique_id": [P],
         "hmg_partition_plan": [I, I, I, I, pI64, pI64, pI64, pI, pI64, P, P, P, P, P, P, P],
         "hmg_mixed_layout": [P, pI64, pI64, pI64, pI64, pI64],
+        "hmg_edge_store": [P, I, pI],
         "hmg_mixed_export_edges": [P, P, P],
         "hmg_mixed_apply": [P, P, P, P],
         "hmg_mixed_precond": [P, pP, P, P, P],
@@ -333,6 +334,12 @@ class Hierarchy:
         _check(load_library().hmg_profile_query(self._h, self.KERNEL_CLASSES[kernel_class], ref, ctypes.byref(n),
                                                 ctypes.byref(ms)))
         return n.value, ms.value
+
+    def edge_store(self, ref: int) -> dict:
+        """Which kernels of level ``ref`` read the edge-deduplicated coupling store."""
+        k = ctypes.c_int(0)
+        _check(load_library().hmg_edge_store(self._h, ref, ctypes.byref(k)))
+        return {"sweep": bool(k.value & 1), "apply": bool(k.value & 2), "resid_restrict": bool(k.value & 4)}
 
     # -- NEXT-4: mixed velocity-pressure system (include/hmg.h hmg_mixed_*) ----
     def mixed_layout(self) -> dict:
