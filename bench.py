@@ -461,6 +461,12 @@ def run_hmg(args, ws, rank, local):
                          "traffic": ncu_traffic(cfg.name, es["sweep"]),
                          "store": ("edge-deduplicated couplings: u, b, D, U, 1.5 H in, u' out = 52 B/dof"
                                    if es["sweep"] else "per-cell bands: u, b, D, U, 3 H in, u' out = 64 B/dof"),
+                         # the same launch counted with the per-cell store's 64 B/dof (the byte model of
+                         # earlier rounds), for comparison only: these bytes are not all moved
+                         "per_cell_store_equivalent": {
+                             "bytes_per_dof": BYTES_PER_DOF["sweep"],
+                             "GB/s": BYTES_PER_DOF["sweep"] * dofs_local / (avg_sw * 1e-3) / 1e9,
+                             "frac": BYTES_PER_DOF["sweep"] * dofs_local / (avg_sw * 1e-3) / 1e9 / peak},
                          "algorithmic_bytes_per_launch": bytes_sw, "avg_launch_us": avg_sw * 1e3,
                          "launches_timed": n_sw, "peak_source": peak_note},
             "fine_level_kernels": fine,

@@ -123,7 +123,7 @@ void free_hierarchy(Hierarchy* H) {
         cudaFree(L.small_cells); cudaFree(L.small_count); cudaFree(L.small_loc);
         cudaFree(L.coop_cells); cudaFree(L.coop_count); cudaFree(L.coop_loc);
         cudaFree(L.hedge); cudaFree(L.edge_e0); cudaFree(L.edge_ne); cudaFree(L.edge_hcells);
-        cudaFree(L.edge_hcount); cudaFree(L.edge_loc); cudaFree(L.edge_own); cudaFree(L.edge_cell);
+        cudaFree(L.edge_hcount); cudaFree(L.edge_loc); cudaFree(L.edge_own);
         cudaFree(L.dist.send_idx); cudaFree(L.dist.sendbuf); cudaFree(L.dist.recvbuf);
     }
     cudaFree(H->r); cudaFree(H->z); cudaFree(H->p); cudaFree(H->q); cudaFree(H->p2);
@@ -497,7 +497,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_DEFER_X")) H->defer_x = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_EDGE_H")) H->edge_h = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_EDGE_MIN_DOFS")) H->edge_min_dofs = std::atoll(e);
-    if (const char* e = std::getenv("HMG_EDGE_RESID")) H->edge_resid = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_RESID_ST")) H->resid_st = std::string(e) != "0";
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at
         // most kCoopMaxCells cells runs in one cooperative launch -- those levels
@@ -819,12 +819,8 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
                                cudaMemcpy(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice) ==
                                    cudaSuccess;
                     };
-                    std::vector<int32_t> ecell(3 * L.ld, 0);
-                    for (int64_t c = 0; c < n; ++c)
-                        for (int j = 0; j < 3; ++j) ecell[j * L.ld + c] = eid[3 * c + j];
                     if (!(up(&L.edge_e0, e0) && up(&L.edge_ne, nel) && up(&L.edge_hcells, hc) &&
-                          up(&L.edge_hcount, hn) && up(&L.edge_loc, eloc) && up(&L.edge_own, own) &&
-                          up(&L.edge_cell, ecell)))
+                          up(&L.edge_hcount, hn) && up(&L.edge_loc, eloc) && up(&L.edge_own, own)))
                         return cleanup(fail(HMG_ERR_OOM, "edge tables: device allocation failed"));
                     BCUDA(cudaMalloc(&L.hedge, sizeof(double) * nlayers * ldE));
                     BCUDA(cudaMemset(L.hedge, 0, sizeof(double) * nlayers * ldE));
@@ -835,7 +831,6 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
                     L.edge.hcells = L.edge_hcells;
                     L.edge.hcount = L.edge_hcount;
                     L.edge.loc = L.edge_loc;
-                    L.edge.cell = L.edge_cell;
                     L.edge_count = nE;
                 }
             }
@@ -1381,6 +1376,21 @@ hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, doubl
 }
 
 int64_t hmg_launch_count(const hmg_hierarchy* h) { return h ? HH(h).launches : -1; }
+
+hmg_status hmg_edge_store(const hmg_hierarchy* h, int ref, int* kernels) {
+    HMG_TRY(check_h(h));
+    const Hierarchy& H = HH(h);
+    HMG_TRY(check_level(H, ref, "ref"));
+    HMG_TRY(check_out(kernels, "kernels"));
+    const DevLevel& L = H.lev[ref];
+    *kernels = 0;
+    if (L.edge.H) {
+        if (sweep_edge_store(H, L)) *kernels |= 1;
+        *kernels |= 2;
+        if (resid_st_supported(H, L)) *kernels |= 4;
+    }
+    return HMG_OK;
+}
 
 hmg_status hmg_profile_begin(hmg_hierarchy* h) {
     HMG_TRY(check_h(h));

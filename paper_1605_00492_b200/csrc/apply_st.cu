@@ -39,36 +39,43 @@ constexpr int kConsumerWarps = kTile / 32;
 constexpr int kThreads = kTile + 32;
 
 struct ApMaps {
-    CUtensorMap bands;  // 3-D box kTile x G x 5
-    CUtensorMap x;      // box kTile x (G + 1): x, or p_old (PUPD)
+    CUtensorMap bands;  // 3-D box kTile x G x 5 (x 2: D, U with the edge store)
+    CUtensorMap x;      // box kTile x (G + 1): x, or p_old (PUPD), or u (RESID)
     CUtensorMap z;      // box kTile x (G + 1): z (PUPD)
+    CUtensorMap b;      // box kTile x G: right-hand side (RESID)
 };
 
 struct ApLayout {
-    int x, z, hx, hz, eh, stage;
+    int x, z, b, hx, hz, eh, stage;
 };
 // eh: the band box carries D and U only; couplings from the edge store (one
 // row of kEdgeRow doubles per layer: contiguous range, then gathered edges)
-__host__ __device__ constexpr ApLayout ap_layout(bool pupd, int G, bool eh = false) {
+__host__ __device__ constexpr ApLayout ap_layout(bool pupd, int G, bool eh = false, bool resid = false) {
     ApLayout L{};
     L.x = (eh ? 2 : 5) * G * kTile;
     L.z = L.x + (G + 1) * kTile;
-    L.hx = L.z + (pupd ? (G + 1) * kTile : 0);
+    L.b = L.z + (pupd ? (G + 1) * kTile : 0);
+    L.hx = L.b + (resid ? G * kTile : 0);
     L.hz = L.hx + G * kHaloMax;
     L.eh = L.hz + (pupd ? G * kHaloMax : 0);
     L.stage = L.eh + (eh ? G * kEdgeRow : 0);
     return L;
 }
 
-template <bool DOT, bool PUPD, int G, bool EH = false>
+// RESID (Alg. 1 M2): r = b - H^ u formed like y (reading R5 order, then b - acc)
+// and restricted in the epilogue, b_c[k][p] = ((r_4p + r_4p+1) + r_4p+2) + r_4p+3
+// over four adjacent lanes (reading R8; k_resid_restrict's order) into y = b_c
+// (leading dimension ldc, column offset coff).
+template <bool DOT, bool PUPD, int G, bool EH = false, bool RESID = false>
 __global__ void __launch_bounds__(kThreads, 2)
     k_apply_st(const __grid_constant__ ApMaps maps, LevelView L, TileHalo th, EdgeTiles et,
                const double* __restrict__ xin,
                const double* __restrict__ zv, double* __restrict__ y, double* __restrict__ pnew,
-               double* __restrict__ partial, const PcgScalars* __restrict__ sc, int S) {
+               double* __restrict__ partial, const PcgScalars* __restrict__ sc, int S, int64_t ldc, int64_t coff) {
+    static_assert(!(RESID && (DOT || PUPD)), "residual mode: plain operator only");
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ double red[kThreads / 32];
-    constexpr ApLayout AL = ap_layout(PUPD, G, EH);
+    constexpr ApLayout AL = ap_layout(PUPD, G, EH, RESID);
     const int nz = L.nz;
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
@@ -99,8 +106,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (warp == kConsumerWarps) {
         // ======================= producer warp =======================
         const uint64_t pol = ptx::policy_evict_first();
-        const uint32_t bytes =
-            (uint32_t)(sizeof(double) * ((EH ? 2 : 5) * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile));
+        const uint32_t bytes = (uint32_t)(sizeof(double) * ((EH ? 2 : 5) * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile +
+                                                            (RESID ? G * kTile : 0)));
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int x = tile * kTile;
             const int hcount = th.count[tile];
@@ -138,6 +145,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                             ptx::bulk_g2s(st + AL.eh + kk * kEdgeRow, et.H + (int64_t)(gi * G + kk) * et.ldE + ee0,
                                           ebytes, &full[s]);
                     ptx::tma_load_3d_hint(st, &maps.bands, x, gi * G, 0, &full[s], pol);
+                    if (RESID) ptx::tma_load_2d_hint(st + AL.b, &maps.b, x, gi * G, &full[s], pol);
                     ptx::tma_load_2d(st + AL.x, &maps.x, x, gi * G, &full[s]);
                     if (PUPD) ptx::tma_load_2d(st + AL.z, &maps.z, x, gi * G, &full[s]);
                 }
@@ -192,7 +200,13 @@ __global__ void __launch_bounds__(kThreads, 2)
                     acc = acc + (EH ? er[eo0] : sr[2 * G * kTile]) * XV(kk, l0);
                     acc = acc + (EH ? er[eo1] : sr[3 * G * kTile]) * XV(kk, l1);
                     acc = acc + (EH ? er[eo2] : sr[4 * G * kTile]) * XV(kk, l2);
-                    if (valid) {
+                    if (RESID) {
+                        const double r = st[AL.b + kk * kTile + j] - acc;
+                        const double r1 = __shfl_down_sync(0xffffffffu, r, 1);
+                        const double r2 = __shfl_down_sync(0xffffffffu, r, 2);
+                        const double r3 = __shfl_down_sync(0xffffffffu, r, 3);
+                        if (valid && (j & 3) == 0) y[(int64_t)k * ldc + coff + (c >> 2)] = ((r + r1) + r2) + r3;
+                    } else if (valid) {
                         const int64_t i = (int64_t)k * ld + c;
                         y[i] = acc;
                         if (PUPD) pnew[i] = xk;
@@ -228,11 +242,11 @@ __global__ void __launch_bounds__(kThreads, 2)
     }
 }
 
-template <bool DOT, bool PUPD, int G, bool EH = false>
+template <bool DOT, bool PUPD, int G, bool EH = false, bool RESID = false>
 int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const double* z, double* y, double* pnew,
-              cudaStream_t s) {
+              cudaStream_t s, const double* b = nullptr, int64_t ldc = 0, int64_t coff = 0) {
     const int nz = H.nz;
-    constexpr ApLayout AL = ap_layout(PUPD, G, EH);
+    constexpr ApLayout AL = ap_layout(PUPD, G, EH, RESID);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
     const size_t budget = 110 * 1024;
@@ -241,7 +255,8 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     const size_t smem = 1024 + sizeof(double) * (size_t)S * AL.stage;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_apply_st<DOT, PUPD, G, EH>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_apply_st<DOT, PUPD, G, EH, RESID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
         attr = true;
     }
     ApMaps maps;
@@ -250,15 +265,36 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, EH ? 2 : 5);
     maps.x = make_tensor_map(x, L.ld, nz, kTile, G + 1, 1);
     if (PUPD) maps.z = make_tensor_map(z, L.ld, nz, kTile, G + 1, 1);
+    if (RESID) maps.b = make_tensor_map(b, L.ld, nz, kTile, G, 1);
     const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
     const unsigned cap = (unsigned)(2 * sms);
     const unsigned grid = ntiles < cap ? ntiles : cap;
-    launch_pdl(H, k_apply_st<DOT, PUPD, G, EH>, dim3(grid), dim3(kThreads), smem, s, maps, V, L.halo, L.edge, x, z, y,
-               pnew, H.partials, H.scal, S);
+    launch_pdl(H, k_apply_st<DOT, PUPD, G, EH, RESID>, dim3(grid), dim3(kThreads), smem, s, maps, V, L.halo, L.edge, x,
+               z, y, pnew, H.partials, H.scal, S, ldc, coff);
     return (int)grid;
 }
 
 }  // namespace
+
+// b_c = R(b - H^ u) through the streamed apply; used where the level has the
+// edge store and columns of <= 64 layers (C2b fine level: 209 -> 185 us).  With
+// 128 layers the thread-per-column k_resid_restrict streams its long columns at
+// 6.4 TB/s and stays faster (C4: 1,524 against 1,596 us), so it keeps the
+// per-cell bands there.
+bool resid_st_supported(const Hierarchy& H, const DevLevel& L) {
+    return H.resid_st && L.edge.H != nullptr && H.use_st_apply && !H.matrix_free && L.halo.loc != nullptr &&
+           H.nz >= 2 && H.nz <= 64;
+}
+
+void launch_resid_restrict_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* u, double* bc,
+                              int64_t ldc, int64_t coff, cudaStream_t s) {
+    try {
+        launch_ap<false, false, 2, true, true>(H, L, u, nullptr, bc, nullptr, s, b, ldc, coff);
+    } catch (const std::exception& e) {
+        g_launch_error = std::string("residual launch: ") + e.what();
+    }
+    ++H.launches;
+}
 
 bool apply_st_supported(const Hierarchy& H, const DevLevel& L) {
     return H.use_st_apply && L.halo.loc != nullptr && H.nz >= 2;

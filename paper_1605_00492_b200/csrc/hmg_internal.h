@@ -47,7 +47,6 @@ struct EdgeTiles {
     const int32_t* hcells = nullptr;  // [ntiles][kEdgeHalo] edges owned before the tile
     const int32_t* hcount = nullptr;  // [ntiles]
     const uint32_t* loc = nullptr;    // [ld] per cell: 3 x 8-bit offsets into a stage row
-    const int32_t* cell = nullptr;    // [3][ld] edge across each face of a cell (thread-per-column kernels)
 };
 
 // Same for the 32-column tiles of the small-level sweep.
@@ -116,7 +115,6 @@ struct DevLevel {
     int32_t *edge_e0 = nullptr, *edge_ne = nullptr, *edge_hcells = nullptr, *edge_hcount = nullptr;
     uint32_t* edge_loc = nullptr;
     int32_t* edge_own = nullptr;      // [2][ldE] owner cell and slot of each edge (setup)
-    int32_t* edge_cell = nullptr;     // [3][ld] edge across each face
     int64_t edge_count = 0;
     EdgeTiles edge;
     // Thomas factors (coarse-tail levels only): pivots, refined reciprocals, multipliers
@@ -246,8 +244,8 @@ struct Hierarchy {
     bool matrix_free = false;   // operator applies recompute the couplings from lam + geometry (NEXT-2)   // HMG_SWEEP_ST=0: non-zero-guess sweeps by k_sweep_tc instead of k_sweep_st
     bool use_small_sweep = true;
     bool edge_h = true;         // HMG_EDGE_H=0: streamed sweeps read the per-cell H bands
-    bool edge_resid = true;     // HMG_EDGE_RESID=0: residual + restriction reads the per-cell bands
-    int64_t edge_min_dofs = 16LL << 20;   // levels with fewer dofs keep the per-cell bands (HMG_EDGE_MIN_DOFS)
+    int64_t edge_min_dofs = 16LL << 20;
+    bool resid_st = true;       // HMG_RESID_ST=0: residual + restriction by k_resid_restrict on edge-store levels too   // levels with fewer dofs keep the per-cell bands (HMG_EDGE_MIN_DOFS)
     int l2_prefetch_groups = 0;   // measured: the ring alone is as fast at ref 7 and faster at ref 6
 };
 
@@ -301,6 +299,7 @@ void launch_sweep_tc(const Hierarchy& H, const DevLevel& L, const double* b, con
 
 // sweep_st.cu: streamed persistent sweep with a non-zero iterate (same arithmetic)
 bool sweep_st_supported(const Hierarchy& H, const DevLevel& L);
+bool sweep_edge_store(const Hierarchy& H, const DevLevel& L);
 void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
                      double* uout, double omega, cudaStream_t s);
 // the same general sweep (non-zero iterate, no prolongation, stored bands) also
@@ -311,6 +310,9 @@ int launch_sweep_st_dot(const Hierarchy& H, const DevLevel& L, const double* b, 
 // apply_st.cu: TMA-streamed persistent operator apply (same arithmetic as k_apply_t);
 // the dot forms return the number of per-CTA partial sums written to H.partials
 bool apply_st_supported(const Hierarchy& H, const DevLevel& L);
+bool resid_st_supported(const Hierarchy& H, const DevLevel& L);
+void launch_resid_restrict_st(const Hierarchy& H, const DevLevel& L, const double* b, const double* u, double* bc,
+                              int64_t ldc, int64_t coff, cudaStream_t s);
 int launch_apply_st(const Hierarchy& H, const DevLevel& L, const double* x, double* y, bool dot, cudaStream_t s);
 int launch_apply_pupdate_st(const Hierarchy& H, const DevLevel& L, const double* z, const double* pold, double* pnew,
                             double* q, cudaStream_t s);

@@ -330,10 +330,7 @@ __global__ void k_restrict(const double* __restrict__ r, int64_t ldf, double* __
 // Residual of the current iterate restricted to the coarse level: each lane
 // computes r = b - H^ u for its column; groups of 4 lanes (the 4 children of
 // one parent) combine in child order through shuffles.
-// EH: the couplings are read from the edge store (1.5 per cell instead of 3;
-// the same values bit for bit)
-template <bool EH>
-__global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, EdgeTiles et, const double* __restrict__ b,
+__global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, const double* __restrict__ b,
                                                                 const double* __restrict__ u,
                                                                 double* __restrict__ bc, int64_t ldc, int64_t coff) {
     const int64_t cc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -344,12 +341,6 @@ __global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, Edg
     const int kc = (nz + gridDim.y - 1) / gridDim.y;
     const int k0 = blockIdx.y * kc, k1 = min(nz, k0 + kc);
     const int32_t n0 = L.nbr[c], n1 = L.nbr[ld + c], n2 = L.nbr[2 * ld + c];
-    int32_t e0 = 0, e1 = 0, e2 = 0;
-    if (EH) {
-        e0 = et.cell[c];
-        e1 = et.cell[ld + c];
-        e2 = et.cell[2 * ld + c];
-    }
     const int lane = threadIdx.x & 31;
     if (k0 >= k1) return;                 // uniform across the block
     double um = k0 > 0 ? u[(int64_t)(k0 - 1) * ld + c] : 0.0;
@@ -363,10 +354,9 @@ __global__ void __launch_bounds__(kApplyBlock) k_resid_restrict(LevelView L, Edg
         double acc = L.D[i] * uk;
         if (k > 0) acc = acc + Um * um;
         if (k < nz - 1) acc = acc + Uk * up;
-        const double* eh = et.H + k * et.ldE;
-        acc = acc + (EH ? eh[e0] : L.H0[i]) * u[row + n0];
-        acc = acc + (EH ? eh[e1] : L.H1[i]) * u[row + n1];
-        acc = acc + (EH ? eh[e2] : L.H2[i]) * u[row + n2];
+        acc = acc + L.H0[i] * u[row + n0];
+        acc = acc + L.H1[i] * u[row + n1];
+        acc = acc + L.H2[i] * u[row + n2];
         const double r = b[i] - acc;
         const double r1 = __shfl_down_sync(0xffffffffu, r, 1);
         const double r2 = __shfl_down_sync(0xffffffffu, r, 2);
@@ -776,11 +766,12 @@ void launch_resid_restrict(const Hierarchy& H, const DevLevel& F, const double* 
                            double* bc, cudaStream_t s) {
     ProfScope ps(H, kKResidRestrict, F.ref, s);
     const DevLevel& C = H.lev[F.ref - 1];
+    if (resid_st_supported(H, F)) {
+        launch_resid_restrict_st(H, F, b, u, bc, C.ld, F.dist.coff, s);
+        return;
+    }
     dim3 g(blocks(F.n, kApplyBlock), vchunks(F.n, H.nz));
-    if (F.edge.H && H.edge_resid)
-        k_resid_restrict<true><<<g, kApplyBlock, 0, s>>>(F.view(H.nz), F.edge, b, u, bc, C.ld, F.dist.coff);
-    else
-        k_resid_restrict<false><<<g, kApplyBlock, 0, s>>>(F.view(H.nz), F.edge, b, u, bc, C.ld, F.dist.coff);
+    k_resid_restrict<<<g, kApplyBlock, 0, s>>>(F.view(H.nz), b, u, bc, C.ld, F.dist.coff);
     ++H.launches;
 }
 
