@@ -86,7 +86,9 @@ __host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool m
     L.u = L.b + G * kTile;
     L.uc = L.u + (zero ? 0 : (G + 1) * kTile);
     L.hu = L.uc + (prolong ? (G + 1) * (kTile / 4) : 0);
-    L.huc = L.hu + (zero ? 0 : G * kHaloMax);
+    // halo rows of u: stride kTile where no prolongation / matrix-free parts use
+    // them, so a neighbour is read at (tile or halo offset) + kk * kTile alike
+    L.huc = L.hu + (zero ? 0 : G * ((prolong || mf) ? kHaloMax : kTile));
     L.hlam = L.huc + (prolong ? G * kHaloMax : 0);
     L.eh = L.hlam + (mf ? G * kHaloMax : 0);
     L.fwd = L.eh + (eh ? G * kEdgeRow : 0);
@@ -119,6 +121,8 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
     long long tt0 = 0, wf = 0, wb = 0, ntl = 0, tfw = 0, tbk = 0, tfw0 = 0, tws = 0;
 #endif
     constexpr bool HALO = !ZERO || MF;       // off-tile neighbour values needed
+    constexpr int HS = (PROLONG || MF) ? kHaloMax : kTile;   // stride of the halo rows of u
+    constexpr bool FLAT = !PROLONG && !MF && !ZERO;         // neighbours read at one offset per tile
     const int nz = L.nz;
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
@@ -261,8 +265,8 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         if (k >= nz) break;
                         if (!ZERO) {
                             const double* src = uin + (int64_t)k * ld;
-                            if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * kHaloMax + lane, src + h0);
-                            if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * kHaloMax + lane + 32, src + h1);
+                            if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane, src + h0);
+                            if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane + 32, src + h1);
                         }
                         if (PROLONG) {
                             const double* srcc = uc + (int64_t)k * ldc;
@@ -348,6 +352,10 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 l1 = (loc >> 8) & 0xff;
                 l2 = (loc >> 16) & 0xff;
             }
+            // FLAT: stage offsets of the three neighbours' u at row 0 (tile row or halo row)
+            const int no0 = l0 < kTile ? SL.u + l0 : SL.hu + (l0 - kTile);
+            const int no1 = l1 < kTile ? SL.u + l1 : SL.hu + (l1 - kTile);
+            const int no2 = l2 < kTile ? SL.u + l2 : SL.hu + (l2 - kTile);
             int eo0 = 0, eo1 = 0, eo2 = 0;                 // the faces' offsets in an edge row
             if (EH) {
                 const uint32_t el = et.loc[cv];
@@ -400,9 +408,13 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 };
                 auto NBR = [&](int kk, int l) -> double {
                     if (l < kTile) return UV(kk, l);
-                    double v = hu[kk * kHaloMax + l - kTile];
+                    double v = hu[kk * HS + l - kTile];
                     if (PROLONG) v = v + huc[kk * kHaloMax + l - kTile];
                     return v;
+                };
+                auto NBRF = [&](int kk, int q, int l) -> double {   // neighbour q (slot l) of the column
+                    if (FLAT) return st[(q == 0 ? no0 : q == 1 ? no1 : no2) + kk * kTile];
+                    return NBR(kk, l);
                 };
                 // One layer: residual row (reading R5 order) and Thomas step.  IN
                 // (interior: 0 < k < nz - 1) drops every boundary test.
@@ -427,9 +439,9 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         double acc = Dk * uk;
                         if (IN || k > 0) acc = acc + Um * um;
                         if (IN || k < nz - 1) acc = acc + Uk * up;
-                        acc = acc + H0 * NBR(kk, l0);
-                        acc = acc + H1 * NBR(kk, l1);
-                        acc = acc + H2 * NBR(kk, l2);
+                        acc = acc + H0 * NBRF(kk, 0, l0);
+                        acc = acc + H1 * NBRF(kk, 1, l1);
+                        acc = acc + H2 * NBRF(kk, 2, l2);
                         r = bk - acc;
                         um = uk;
                     }
