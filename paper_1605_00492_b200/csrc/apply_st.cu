@@ -51,13 +51,18 @@ struct ApLayout {
 // eh: the band box carries D and U only; couplings from the edge store (one
 // row of kEdgeRow doubles per layer: contiguous range, then gathered edges)
 __host__ __device__ constexpr ApLayout ap_layout(bool pupd, int G, bool eh = false, bool resid = false) {
+    static_assert(kTile % 2 == 0, "");
     ApLayout L{};
     L.x = (eh ? 2 : 5) * G * kTile;
     L.z = L.x + (G + 1) * kTile;
     L.b = L.z + (pupd ? (G + 1) * kTile : 0);
     L.hx = L.b + (resid ? G * kTile : 0);
-    L.hz = L.hx + G * kHaloMax;
-    L.eh = L.hz + (pupd ? G * kHaloMax : 0);
+    // halo rows with the tile rows' stride kTile: a neighbour's operand is read at
+    // one per-tile offset (tile or halo part) + kk * kTile
+    // (with the p update the halo rows of z sit as far after those of p_old as the
+    // tile rows of z after those of p_old: (G + 1) rows)
+    L.hz = L.hx + (pupd ? (G + 1) : G) * kTile;
+    L.eh = L.hz + (pupd ? G * kTile : 0);
     L.stage = L.eh + (eh ? G * kEdgeRow : 0);
     return L;
 }
@@ -126,12 +131,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (EH && lane < ehc)
                         ptx::cp_async8(st + AL.eh + kk * kEdgeRow + kEdgeRange + lane, et.H + (int64_t)k * et.ldE + eh0);
                     const double* src = xin + (int64_t)k * ld;
-                    if (lane < hcount) ptx::cp_async8(st + AL.hx + kk * kHaloMax + lane, src + h0);
-                    if (lane + 32 < hcount) ptx::cp_async8(st + AL.hx + kk * kHaloMax + lane + 32, src + h1);
+                    if (lane < hcount) ptx::cp_async8(st + AL.hx + kk * kTile + lane, src + h0);
+                    if (lane + 32 < hcount) ptx::cp_async8(st + AL.hx + kk * kTile + lane + 32, src + h1);
                     if (PUPD) {
                         const double* srz = zv + (int64_t)k * ld;
-                        if (lane < hcount) ptx::cp_async8(st + AL.hz + kk * kHaloMax + lane, srz + h0);
-                        if (lane + 32 < hcount) ptx::cp_async8(st + AL.hz + kk * kHaloMax + lane + 32, srz + h1);
+                        if (lane < hcount) ptx::cp_async8(st + AL.hz + kk * kTile + lane, srz + h0);
+                        if (lane + 32 < hcount) ptx::cp_async8(st + AL.hz + kk * kTile + lane + 32, srz + h1);
                     }
                 }
                 ptx::cp_async_arrive(&full[s]);
@@ -160,6 +165,11 @@ __global__ void __launch_bounds__(kThreads, 2)
             const bool valid = c < L.n;
             const uint32_t loc = th.loc[valid ? c : L.n - 1];
             const int l0 = loc & 0xff, l1 = (loc >> 8) & 0xff, l2 = (loc >> 16) & 0xff;
+            // stage offsets of the neighbours' x (p_old) at row 0; their z lies at the same
+            // offset + (AL.z - AL.x) (tile and halo rows of z both sit that far after x's)
+            const int ox0 = l0 < kTile ? AL.x + l0 : AL.hx + (l0 - kTile);
+            const int ox1 = l1 < kTile ? AL.x + l1 : AL.hx + (l1 - kTile);
+            const int ox2 = l2 < kTile ? AL.x + l2 : AL.hx + (l2 - kTile);
             int eo0 = 0, eo1 = 0, eo2 = 0;             // the faces' offsets in an edge row
             if (EH) {
                 const uint32_t el = et.loc[valid ? c : L.n - 1];
@@ -180,8 +190,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                         if (PUPD) return sz[kk * kTile + l] + beta * sx[kk * kTile + l];
                         return sx[kk * kTile + l];
                     }
-                    if (PUPD) return hz[kk * kHaloMax + l - kTile] + beta * hx[kk * kHaloMax + l - kTile];
-                    return hx[kk * kHaloMax + l - kTile];
+                    if (PUPD) return hz[kk * kTile + l - kTile] + beta * hx[kk * kTile + l - kTile];
+                    return hx[kk * kTile + l - kTile];
+                };
+                // the three neighbours' operands at the per-tile offsets (same values as XV)
+                auto XN = [&](int kk, int q) -> double {
+                    const int ox = q == 0 ? ox0 : q == 1 ? ox1 : ox2;
+                    if (PUPD) return st[ox + (AL.z - AL.x) + kk * kTile] + beta * st[ox + kk * kTile];
+                    return st[ox + kk * kTile];
                 };
                 // one layer; IN (interior, 0 < k < nz - 1) drops the boundary tests
                 auto step = [&](int kk, auto interior) {
@@ -197,9 +213,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                     if (IN || k > 0) acc = acc + Um * xm;
                     if (IN || k < nz - 1) acc = acc + Uk * xp;
                     const double* er = st + AL.eh + kk * kEdgeRow;
-                    acc = acc + (EH ? er[eo0] : sr[2 * G * kTile]) * XV(kk, l0);
-                    acc = acc + (EH ? er[eo1] : sr[3 * G * kTile]) * XV(kk, l1);
-                    acc = acc + (EH ? er[eo2] : sr[4 * G * kTile]) * XV(kk, l2);
+                    acc = acc + (EH ? er[eo0] : sr[2 * G * kTile]) * XN(kk, 0);
+                    acc = acc + (EH ? er[eo1] : sr[3 * G * kTile]) * XN(kk, 1);
+                    acc = acc + (EH ? er[eo2] : sr[4 * G * kTile]) * XN(kk, 2);
                     if (RESID) {
                         const double r = st[AL.b + kk * kTile + j] - acc;
                         const double r1 = __shfl_down_sync(0xffffffffu, r, 1);
