@@ -247,7 +247,7 @@ void flush_pending_x(const Hierarchy& H, cudaStream_t s, bool side, bool go_reco
     if (side) {
         if (!go_recorded) cudaEventRecord(H.ev_x_go, s);
         cudaStreamWaitEvent(H.xs, H.ev_x_go, 0);
-        launch_update_part(H, F, 2, H.px.first, H.px.x, H.px.p, nullptr, H.xs);
+        launch_update_part(H, F, H.x_slow_blocks > 0 ? 3 : 2, H.px.first, H.px.x, H.px.p, nullptr, H.xs);
         cudaEventRecord(H.ev_x_done, H.xs);
     } else {
         launch_update_part(H, F, 2, H.px.first, H.px.x, H.px.p, nullptr, s);
@@ -495,6 +495,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_CHECK_SKIP")) H->check_skip = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     if (const char* e = std::getenv("HMG_DEFER_X")) H->defer_x = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_X_BLOCKS")) H->x_slow_blocks = std::atoi(e);
     if (const char* e = std::getenv("HMG_EDGE_H")) H->edge_h = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_EDGE_MIN_DOFS")) H->edge_min_dofs = std::atoll(e);
     if (const char* e = std::getenv("HMG_RESID_ST")) H->resid_st = std::string(e) != "0";

@@ -213,6 +213,7 @@ struct Hierarchy {
     };
     mutable PendingX px;
     bool defer_x = true;        // HMG_DEFER_X=0: x and r updated by one kernel on the solve stream
+    int x_slow_blocks = 148;    // HMG_X_BLOCKS=n: the deferred update by n grid-stride CTAs (0: the full vector grid)
     cudaEvent_t ev_in[2] = {}, ev_solved[2] = {}, ev_out[2] = {};
     int tail_ref = -1;          // levels <= tail_ref run in one coarse-tail launch (-1: off)
     bool tail_grid = false;     // the tail is a cooperative multi-CTA launch (false: one CTA)

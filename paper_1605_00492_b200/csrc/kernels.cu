@@ -864,8 +864,30 @@ void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, const do
     ++H.launches;
 }
 
+// x = x + alpha p (FIRST: x = 0 + alpha p) over every padded row, grid-stride:
+// the deferred CG update on the side stream, launched with few CTAs so that it
+// trickles through the V-cycle's latency-bound coarse part instead of
+// contending with it at full bandwidth (same values as k_update_xr's x part)
+template <bool FIRST>
+__global__ void __launch_bounds__(256) k_update_x_slow(double* __restrict__ x, const double* __restrict__ p,
+                                                       int64_t n, int64_t ld, int nz, const PcgScalars* __restrict__ sc) {
+    const double alpha = sc->alpha;
+    double2* x2 = reinterpret_cast<double2*>(x);
+    const double2* p2 = reinterpret_cast<const double2*>(p);
+    const int64_t hn = n / 2, total = hn * nz;          // pairs of cells per layer (n is even); padding untouched
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = t / hn, q = k * (ld / 2) + (t - k * hn);
+        double2 xx = FIRST ? make_double2(0.0, 0.0) : x2[q];
+        const double2 pp = p2[q];
+        xx.x = xx.x + alpha * pp.x;
+        xx.y = xx.y + alpha * pp.y;
+        x2[q] = xx;
+    }
+}
+
 // part 1: r = r - alpha q (first: r = b - alpha q) with partial <r, r>;
-// part 2: x = x + alpha p (first: x = 0 + alpha p)
+// part 2: x = x + alpha p (first: x = 0 + alpha p); part 3: the same as 2 by
+// k_update_x_slow with `slow_blocks` CTAs
 void launch_update_part(const Hierarchy& H, const DevLevel& L, int part, bool first, double* x, const double* p,
                         const double* b, cudaStream_t s) {
     ProfScope ps(H, kKVector, H.fine_ref, s);
@@ -874,6 +896,11 @@ void launch_update_part(const Hierarchy& H, const DevLevel& L, int part, bool fi
     if (part == 1 && !first) k_update_xr<false, 1><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
     if (part == 2 && first) k_update_xr<true, 2><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
     if (part == 2 && !first) k_update_xr<false, 2><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
+    if (part == 3) {
+        const unsigned nb = (unsigned)(H.x_slow_blocks > 0 ? H.x_slow_blocks : 1);
+        if (first) k_update_x_slow<true><<<nb, 256, 0, s>>>(x, p, L.n, L.ld, H.nz, H.scal);
+        else k_update_x_slow<false><<<nb, 256, 0, s>>>(x, p, L.n, L.ld, H.nz, H.scal);
+    }
     ++H.launches;
 }
 
