@@ -247,7 +247,10 @@ void flush_pending_x(const Hierarchy& H, cudaStream_t s, bool side, bool go_reco
     if (side) {
         if (!go_recorded) cudaEventRecord(H.ev_x_go, s);
         cudaStreamWaitEvent(H.xs, H.ev_x_go, 0);
-        launch_update_part(H, F, H.x_slow_blocks > 0 ? 3 : 2, H.px.first, H.px.x, H.px.p, nullptr, H.xs);
+        // few CTAs only while the update fits the coarse part's duration (C2: 21M dofs,
+        // ~300 us); a C4-size update (168M dofs) runs at full width
+        const bool trickle = H.x_slow_blocks > 0 && (int64_t)H.nz * F.n <= (32LL << 20);
+        launch_update_part(H, F, trickle ? 3 : 2, H.px.first, H.px.x, H.px.p, nullptr, H.xs);
         cudaEventRecord(H.ev_x_done, H.xs);
     } else {
         launch_update_part(H, F, 2, H.px.first, H.px.x, H.px.p, nullptr, s);
