@@ -50,6 +50,8 @@ constexpr int kThreads = kTile + 32;       // + one producer warp
 constexpr int kMfWarps = kTile / 32;       // matrix-free: warps forming the couplings of each stage
 constexpr int kThreadsMf = kThreads + 32 * kMfWarps;
 constexpr int kBack = 8;                   // layers per backward stage
+constexpr int kUcRow = 64;                 // forward u_c rows: 32 parents of the tile + the next 32 (so the
+                                           // tile and halo parts of u_c share the row stride kHaloMax)
 
 #ifdef HMG_TIMING
 __device__ long long g_st_timing[8];   // CTA 0, thread 0: [0] total, [1] forward wait, [2] backward wait, [3] tiles
@@ -85,10 +87,10 @@ __host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool m
     L.b = L.band + (eh ? 2 : 5) * G * kTile;
     L.u = L.b + G * kTile;
     L.uc = L.u + (zero ? 0 : (G + 1) * kTile);
-    L.hu = L.uc + (prolong ? (G + 1) * (kTile / 4) : 0);
+    L.hu = L.uc + (prolong ? (G + 1) * kUcRow : 0);
     // halo rows of u: stride kTile where no prolongation / matrix-free parts use
     // them, so a neighbour is read at (tile or halo offset) + kk * kTile alike
-    L.huc = L.hu + (zero ? 0 : G * ((prolong || mf) ? kHaloMax : kTile));
+    L.huc = L.hu + (zero ? 0 : G * (mf ? kHaloMax : kTile));
     L.hlam = L.huc + (prolong ? G * kHaloMax : 0);
     L.eh = L.hlam + (mf ? G * kHaloMax : 0);
     L.fwd = L.eh + (eh ? G * kEdgeRow : 0);
@@ -121,8 +123,9 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
     long long tt0 = 0, wf = 0, wb = 0, ntl = 0, tfw = 0, tbk = 0, tfw0 = 0, tws = 0;
 #endif
     constexpr bool HALO = !ZERO || MF;       // off-tile neighbour values needed
-    constexpr int HS = (PROLONG || MF) ? kHaloMax : kTile;   // stride of the halo rows of u
-    constexpr bool FLAT = !PROLONG && !MF && !ZERO;         // neighbours read at one offset per tile
+    constexpr int HS = MF ? kHaloMax : kTile;   // stride of the halo rows of u
+    constexpr bool FLAT = !MF && !ZERO;         // neighbours read at per-tile offsets
+    static_assert(kUcRow == kHaloMax, "u_c tile and halo rows share one stride");
     const int nz = L.nz;
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
@@ -227,7 +230,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
         constexpr int op_rows = MF ? (G + 1) * kTile : (EH ? 2 : 5) * G * kTile;
         const uint32_t fwd_bytes =
             (uint32_t)(sizeof(double) * (op_rows + G * kTile + (ZERO ? 0 : (G + 1) * kTile) +
-                                         (PROLONG ? (G + 1) * (kTile / 4) : 0)));
+                                         (PROLONG ? (G + 1) * kUcRow : 0)));
         const uint32_t bwd_bytes = (uint32_t)(sizeof(double) * (kBack * kTile + (PROLONG ? kBack * (kTile / 4) : 0) +
                                                                 (DOT ? kBack * kTile : 0)));
         int s = 0;
@@ -356,6 +359,10 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
             const int no0 = l0 < kTile ? SL.u + l0 : SL.hu + (l0 - kTile);
             const int no1 = l1 < kTile ? SL.u + l1 : SL.hu + (l1 - kTile);
             const int no2 = l2 < kTile ? SL.u + l2 : SL.hu + (l2 - kTile);
+            // PROLONG: offsets of the neighbours' u_c (parent in the tile's rows, or halo row)
+            const int nc0 = l0 < kTile ? SL.uc + (l0 >> 2) : SL.huc + (l0 - kTile);
+            const int nc1 = l1 < kTile ? SL.uc + (l1 >> 2) : SL.huc + (l1 - kTile);
+            const int nc2 = l2 < kTile ? SL.uc + (l2 >> 2) : SL.huc + (l2 - kTile);
             int eo0 = 0, eo1 = 0, eo2 = 0;                 // the faces' offsets in an edge row
             if (EH) {
                 const uint32_t el = et.loc[cv];
@@ -403,7 +410,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 // u value (with the fused prolongation) of local slot l at stage row kk
                 auto UV = [&](int kk, int l) -> double {
                     double v = su[kk * kTile + l];
-                    if (PROLONG) v = v + suc[kk * (kTile / 4) + (l >> 2)];
+                    if (PROLONG) v = v + suc[kk * kUcRow + (l >> 2)];
                     return v;
                 };
                 auto NBR = [&](int kk, int l) -> double {
@@ -413,7 +420,11 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     return v;
                 };
                 auto NBRF = [&](int kk, int q, int l) -> double {   // neighbour q (slot l) of the column
-                    if (FLAT) return st[(q == 0 ? no0 : q == 1 ? no1 : no2) + kk * kTile];
+                    if (FLAT) {
+                        double v = st[(q == 0 ? no0 : q == 1 ? no1 : no2) + kk * kTile];
+                        if (PROLONG) v = v + st[(q == 0 ? nc0 : q == 1 ? nc1 : nc2) + kk * kUcRow];
+                        return v;
+                    }
                     return NBR(kk, l);
                 };
                 // One layer: residual row (reading R5 order) and Thomas step.  IN
@@ -714,7 +725,7 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
     if (P) {
         const DevLevel& C = H.lev[L.ref - 1];
         ldc = C.ld;
-        maps.ucf = make_tensor_map(uc, C.ld, nz, kTile / 4, G + 1, 1);
+        maps.ucf = make_tensor_map(uc, C.ld, nz, kUcRow, G + 1, 1);
         maps.ucb = make_tensor_map(uc, C.ld, nz, kTile / 4, kBack, 1);
     }
     if (DOT) maps.bb = make_tensor_map(b, L.ld, nz, kTile, kBack, 1);
