@@ -446,3 +446,32 @@ def test_streamed_kernels_layer_counts(nz):
     assert st == "HMG_OK" and it == o.pcg(b)[1]
     g.close()
     o.close()
+
+
+@pytest.mark.parametrize("nz", [64, 128])
+def test_edge_store_forced_on_small_levels(monkeypatch, nz):
+    """The edge-deduplicated coupling store is built only on
+    levels of >= 16M dofs by default; forced onto ref 5 (HMG_EDGE_MIN_DOFS), the
+    streamed apply, sweeps (with and without the fused prolongation), the
+    streamed residual + restriction and the V-cycle stay bitwise equal to the
+    oracle, and PCG takes its iteration count."""
+    monkeypatch.setenv("HMG_EDGE_MIN_DOFS", "1000000")
+    cfg = hi.Config("edge", 5, 0, nz, 0.001, 1e-5)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(5, 0, nz, 0.001, 1e-5, lam)
+    o = oracle.Hierarchy(5, 0, nz, 0.001, 1e-5, lam)
+    es = g.edge_store(5)
+    assert es["apply"] and es["sweep"] == (nz <= 64) and es["resid_restrict"] == (nz <= 64)
+    x = hi.uniform_vector(b.shape, 71)
+    bd, xd = g.to_device(5, b), g.to_device(5, x)
+    assert np.array_equal(g.to_host(5, g.apply_helmholtz(5, xd)), o.apply(5, x))
+    u = g.to_device(5, x)
+    g.line_smooth(5, bd, u, 2, 0.8, False)
+    assert np.array_equal(g.to_host(5, u), o.sweep(5, b, x, 2, 0.8))
+    assert np.array_equal(g.to_host(4, g.residual_restrict(5, bd, xd)), o.restrict(5, o.residual(5, b, x)))
+    assert np.array_equal(g.to_host(5, g.vcycle(bd)), o.vcycle(b))
+    _, it, _, st = g.pcg_solve(bd)
+    _, it_o, _, _, st_o = o.pcg(b)
+    assert st == "HMG_OK" and st_o == 0 and it == it_o
+    g.close()
+    o.close()
