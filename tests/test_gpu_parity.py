@@ -475,3 +475,35 @@ def test_edge_store_forced_on_small_levels(monkeypatch, nz):
     assert st == "HMG_OK" and st_o == 0 and it == it_o
     g.close()
     o.close()
+
+
+@pytest.mark.parametrize("env", [{}, {"HMG_DEFER_X": "0"}, {"HMG_X_BLOCKS": "0"}, {"HMG_X_BLOCKS": "7"}])
+def test_deferred_x_update_paths(monkeypatch, env):
+    """The CG update x = x + alpha p runs deferred on a side stream (default), on
+    the solve stream (HMG_DEFER_X=0), at full width (HMG_X_BLOCKS=0) or trickled
+    by a few CTAs: every variant gives the same x bit for bit, also when PCG
+    stops at maxit (NOT_CONVERGED, the last update still lands)."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    cfg = hi.Config("defx", 5, 0, 64, 0.001, 1e-5)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(5, 0, 64, 0.001, 1e-5, lam)
+    o = oracle.Hierarchy(5, 0, 64, 0.001, 1e-5, lam)
+    bd = g.to_device(5, b)
+    x, it, rr, st = g.pcg_solve(bd, rtol=1e-8)
+    xo, it_o, _, _, st_o = o.pcg(b, rtol=1e-8)
+    assert st == "HMG_OK" and it == it_o
+    x = g.to_host(5, x)
+    assert rel(x, xo) <= 1e-9                      # x differs from the oracle's only by dot rounding
+    x2, it2, _, st2 = g.pcg_solve(bd, rtol=1e-30, maxit=2)
+    xo2, _, _, _, st_o2 = o.pcg(b, rtol=1e-30, maxit=2)
+    assert st2 == "HMG_ERR_NOT_CONVERGED" and st_o2 == oracle.NOT_CONVERGED and it2 == 2
+    assert rel(g.to_host(5, x2), xo2) <= 1e-9
+    # reference for the bitwise comparison across variants: the solve-stream update
+    monkeypatch.setenv("HMG_DEFER_X", "0")
+    g0 = Hierarchy(5, 0, 64, 0.001, 1e-5, lam)
+    x0, _, _, _ = g0.pcg_solve(g0.to_device(5, b), rtol=1e-8)
+    assert np.array_equal(x, g0.to_host(5, x0))
+    g.close()
+    g0.close()
+    o.close()
