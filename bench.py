@@ -450,8 +450,8 @@ def run_hmg(args, ws, rank, local):
                        "pcg_iterations": iters, "vcycles_per_step": nv, "final_relres": relres,
                        "parallelism": (f"domain decomposition x{ws} (NCCL halos, all-reduce, coarse gather at ref "
                                        f"{min(args.gather_ref, cfg.fine_ref)})") if ws > 1 else "single GPU",
-                       "cache": f"inputs larger than L2 (fine bands {5 * 8 * cfg.ndofs // ws / 1e6:.0f} MB + vectors "
-                                f"per level)"},
+                       "cache": f"inputs larger than L2 (fine-level operator {(3.5 if es['sweep'] else 5) * 8 * cfg.ndofs // ws / 1e6:.0f}"
+                                f" MB + vectors per level)"},
             "pcg_solve_ms": ms,
             "vcycle_only": {"value": cfg.ndofs / (ms_vc * 1e-3), "unit": UNIT, "ms": ms_vc},
             "setup_s": setup_s,
