@@ -352,6 +352,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
 #ifdef HMG_TIMING
 }  // namespace
 extern "C" void hmg_debug_coop_timing(long long* out) { cudaMemcpyFromSymbol(out, g_coop_timing, sizeof(long long) * 512); }
+extern "C" void hmg_debug_tile_phase(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, g_tile_phase, sizeof(unsigned long long) * 4);
+}
 extern "C" unsigned long long hmg_debug_tile_slow() {
     unsigned long long v = 0;
     cudaMemcpyFromSymbol(&v, g_tile_slow_count, sizeof(v));

@@ -23,6 +23,12 @@ constexpr int kHaloW = kSmallHaloMax;  // width of the halo plane (<= 32 off-til
 
 #ifdef HMG_TIMING
 __device__ unsigned long long g_tile_slow_count;   // diagnostics: exact-division redos
+__device__ unsigned long long g_tile_phase[4];     // CTA 0 thread 0: residual pass, forward, backward cycles; calls
+#define TSTAMP(v) long long v = clock64()
+#define TACC(i, a, b) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_tile_phase[i] += (unsigned long long)((b) - (a)); } while (0)
+#else
+#define TSTAMP(v) do {} while (0)
+#define TACC(i, a, b) do {} while (0)
 #endif
 
 // Shared-memory planes of one tile, each [nzp][TW] (nzp = nz rounded up to 8);
@@ -200,8 +206,11 @@ template <int TW = kTileW>
 __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int warp, int j, int l0, int l1, int l2,
                                                bool zero, double omega, bool valid) {
     const int nzp = (nz + 7) & ~7;
+    TSTAMP(p0);
     tile_residuals_cta<TW>(S, nz, warp, j, l0, l1, l2, zero);
     __syncthreads();
+    TSTAMP(p1);
+    TACC(0, p0, p1);
     if (warp == 0) {
         bool slow = false;
         double zprev = 0.0;
@@ -229,6 +238,8 @@ __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int wa
 #pragma unroll
             for (int i = 0; i < 8; ++i) S.z[(k0 + i) * TW + j] = rr[i];
         }
+        TSTAMP(p2);
+        TACC(1, p1, p2);
         if (__any_sync(0xffffffffu, slow && valid)) {  // rare: recompute with '/' (bitwise the same as the oracle)
 #ifdef HMG_TIMING
             if (j == 0) atomicAdd(&g_tile_slow_count, 1ull);
@@ -264,6 +275,9 @@ __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int wa
 #pragma unroll
             for (int i = 0; i < 8; ++i) S.u[(k1 - i) * TW + j] = uo[i];
         }
+        TSTAMP(p3);
+        TACC(2, p2, p3);
+        if (blockIdx.x == 0 && threadIdx.x == 0) TACC(3, 0, 1);
     }
     __syncthreads();
 }

@@ -41,3 +41,9 @@ print(" ".join(str(x) for x in d))
 f = B.load_library().hmg_debug_tile_slow
 f.restype = ctypes.c_ulonglong
 print("exact-division redos over 3 V-cycles (all CTAs):", f())
+
+ph = (ctypes.c_ulonglong * 4)()
+B.load_library().hmg_debug_tile_phase(ph)
+n = max(ph[3], 1)
+print(f"tile_sweep_cta calls (CTA 0) {ph[3]}: residual pass {ph[0] / n:.0f} cyc, forward chain {ph[1] / n:.0f} cyc, "
+      f"backward {ph[2] / n:.0f} cyc per call")
