@@ -502,6 +502,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     if (const char* e = std::getenv("HMG_EDGE_H")) H->edge_h = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_EDGE_MIN_DOFS")) H->edge_min_dofs = std::atoll(e);
     if (const char* e = std::getenv("HMG_RESID_ST")) H->resid_st = std::string(e) != "0";
+    if (const char* e = std::getenv("HMG_APPLY_CTAS")) H->apply_ctas_per_sm = std::atoi(e);
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at
         // most kCoopMaxCells cells runs in one cooperative launch -- those levels

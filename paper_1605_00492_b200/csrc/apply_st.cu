@@ -72,7 +72,7 @@ __host__ __device__ constexpr ApLayout ap_layout(bool pupd, int G, bool eh = fal
 // over four adjacent lanes (reading R8; k_resid_restrict's order) into y = b_c
 // (leading dimension ldc, column offset coff).
 template <bool DOT, bool PUPD, int G, bool EH = false, bool RESID = false>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 3)
     k_apply_st(const __grid_constant__ ApMaps maps, LevelView L, TileHalo th, EdgeTiles et,
                const double* __restrict__ xin,
                const double* __restrict__ zv, double* __restrict__ y, double* __restrict__ pnew,
@@ -265,7 +265,11 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     constexpr ApLayout AL = ap_layout(PUPD, G, EH, RESID);
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
-    const size_t budget = 110 * 1024;
+    // resident CTAs per SM (shared memory split evenly): three for the p-update
+    // and residual variants (more consumer warps: C2b 244 -> 225 us and 183 -> 172
+    // us), two for the plain apply (C1 19.0 against 20.3 us with three)
+    const int per_sm = (PUPD || RESID) ? H.apply_ctas_per_sm : 2;
+    const size_t budget = (size_t)(per_sm >= 3 ? 72 : 110) * 1024;
     int S = (int)((budget - 1024) / (sizeof(double) * AL.stage));
     S = S < 2 ? 2 : (S > 32 ? 32 : S);
     const size_t smem = 1024 + sizeof(double) * (size_t)S * AL.stage;
@@ -283,7 +287,7 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     if (PUPD) maps.z = make_tensor_map(z, L.ld, nz, kTile, G + 1, 1);
     if (RESID) maps.b = make_tensor_map(b, L.ld, nz, kTile, G, 1);
     const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
-    const unsigned cap = (unsigned)(2 * sms);
+    const unsigned cap = (unsigned)((per_sm >= 3 ? 3 : 2) * sms);
     const unsigned grid = ntiles < cap ? ntiles : cap;
     launch_pdl(H, k_apply_st<DOT, PUPD, G, EH, RESID>, dim3(grid), dim3(kThreads), smem, s, maps, V, L.halo, L.edge, x,
                z, y, pnew, H.partials, H.scal, S, ldc, coff);

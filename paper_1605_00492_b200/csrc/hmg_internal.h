@@ -246,7 +246,8 @@ struct Hierarchy {
     bool use_small_sweep = true;
     bool edge_h = true;         // HMG_EDGE_H=0: streamed sweeps read the per-cell H bands
     int64_t edge_min_dofs = 16LL << 20;
-    bool resid_st = true;       // HMG_RESID_ST=0: residual + restriction by k_resid_restrict on edge-store levels too   // levels with fewer dofs keep the per-cell bands (HMG_EDGE_MIN_DOFS)
+    bool resid_st = true;
+    int apply_ctas_per_sm = 3;  // HMG_APPLY_CTAS=2: two CTAs per SM for the p-update / residual applies too       // HMG_RESID_ST=0: residual + restriction by k_resid_restrict on edge-store levels too   // levels with fewer dofs keep the per-cell bands (HMG_EDGE_MIN_DOFS)
     int l2_prefetch_groups = 0;   // measured: the ring alone is as fast at ref 7 and faster at ref 6
 };
 
