@@ -229,11 +229,16 @@ def run_hmg(args, ws, rank, local):
         if rank == 0:
             nid.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(nid, 0)
+        # the finest level is always distributed (gather_ref < fine_ref), so each
+        # rank passes its owned part of lam and b (include/hmg.h)
+        gref = max(2, min(args.gather_ref, cfg.fine_ref - 1))
+        if cfg.fine_ref <= 2:
+            raise SystemExit(f"{cfg.name}: fine ref {cfg.fine_ref} has no level to distribute (needs ref > 2)")
         per = cfg.n // ws
         own = slice(rank * per, (rank + 1) * per)
         lam, b = np.ascontiguousarray(lam[:, own]), np.ascontiguousarray(b[:, own])
         h = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, device=local,
-                      dist=(rank, ws, bytes(nid.cpu().numpy()), min(args.gather_ref, cfg.fine_ref)))
+                      dist=(rank, ws, bytes(nid.cpu().numpy()), gref))
     setup_s = time.perf_counter() - t0
     r = cfg.fine_ref
     bd = h.to_device(r, b)
@@ -449,7 +454,7 @@ def run_hmg(args, ws, rank, local):
                        "dofs": cfg.ndofs, "dofs_per_gpu": cfg.ndofs // ws, "thickness": cfg.thickness, "w2": cfg.w2,
                        "pcg_iterations": iters, "vcycles_per_step": nv, "final_relres": relres,
                        "parallelism": (f"domain decomposition x{ws} (NCCL halos, all-reduce, coarse gather at ref "
-                                       f"{min(args.gather_ref, cfg.fine_ref)})") if ws > 1 else "single GPU",
+                                       f"{max(2, min(args.gather_ref, cfg.fine_ref - 1))})") if ws > 1 else "single GPU",
                        "cache": f"inputs larger than L2 (fine-level operator {(3.5 if es['sweep'] else 5) * 8 * cfg.ndofs // ws / 1e6:.0f}"
                                 f" MB + vectors per level)"},
             "pcg_solve_ms": ms,
@@ -571,9 +576,35 @@ def run_c1(args):
         "kernels": out}))
 
 
+def launch_ranks(args) -> int:
+    """`bench.py --gpus N` started without torchrun: start the N ranks here
+    (one process per GPU, torch.distributed.run on 127.0.0.1) and return their
+    exit code.  Fails loudly when fewer than N GPUs are visible."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        print(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible", file=sys.stderr)
+        return 1
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
     ws, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and not (args.impl == "reference" or args.config == "C1"):
+        sys.exit(launch_ranks(args))
+    if ws > 1 and ws != args.gpus:
+        raise SystemExit(f"WORLD_SIZE={ws} but --gpus {args.gpus}: launch one rank per GPU")
+    if ws > 1:
+        # NCCL's communicator lines (rank / nranks / device per rank) on stderr
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     if args.impl == "reference":
         run_reference(args, ws, rank)
     elif args.config == "C1":

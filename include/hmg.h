@@ -136,8 +136,10 @@ hmg_status hmg_free_hierarchy(hmg_hierarchy* h);
 hmg_status hmg_level_info(const hmg_hierarchy* h, int ref, int64_t* ncells, int64_t* ld);
 
 /* y = H^ x on level `ref` (Eq. 8; "v = H^ u = H^_z u + H^_h u").
- * x, y: device [nlayers][ld].  Row order of reading R5. */
-hmg_status hmg_apply_helmholtz(const hmg_hierarchy* h, int ref, const double* x, double* y,
+ * x, y: device [nlayers][ld].  Row order of reading R5.  x is non-const: on a
+ * distributed level the library writes x's halo slots (the neighbours' owned
+ * values) before reading them; its owned entries are not modified. */
+hmg_status hmg_apply_helmholtz(const hmg_hierarchy* h, int ref, double* x, double* y,
                                void* stream);
 
 /* nsweeps damped line-Jacobi sweeps on level `ref` (Eq. 10 read with Eq. 13,
@@ -154,13 +156,20 @@ hmg_status hmg_line_smooth(const hmg_hierarchy* h, int ref, const double* b, dou
                            int nsweeps, double omega, int u_is_zero, void* stream);
 
 /* b_c = R r_f: 4-child sum restriction from fine_ref to fine_ref-1
- * (reading R8).  r_f: [nlayers][ld_fine], b_c: [nlayers][ld_coarse]. */
+ * (reading R8).  r_f: [nlayers][ld_fine], b_c: [nlayers][ld_coarse].
+ * Distributed hierarchy: restriction is rank-local; when level fine_ref-1 is
+ * replicated (fine_ref-1 <= gather_ref < fine_ref) b_c receives the WHOLE
+ * coarse vector on every rank (the coarse all-gather; collective). */
 hmg_status hmg_restrict(const hmg_hierarchy* h, int fine_ref, const double* r_f, double* b_c,
                         void* stream);
 
-/* b_c = R (b - H^ u): fused residual + restriction on level fine_ref. */
+/* b_c = R (b - H^ u): fused residual + restriction on level fine_ref
+ * (residual in the row order of reading R5, then the sum of reading R8).
+ * u is non-const for the same reason as x of hmg_apply_helmholtz (halo slots
+ * written on a distributed level, owned entries untouched); b_c as for
+ * hmg_restrict (whole coarse vector when the coarser level is replicated). */
 hmg_status hmg_residual_restrict(const hmg_hierarchy* h, int fine_ref, const double* b,
-                                 const double* u, double* b_c, void* stream);
+                                 double* u, double* b_c, void* stream);
 
 /* u_f += P u_c: injection prolongation ("natural embedding"). */
 hmg_status hmg_prolong_add(const hmg_hierarchy* h, int fine_ref, const double* u_c, double* u_f,

@@ -175,6 +175,11 @@ class Hierarchy:
         level when gather_ref < fine_ref."""
         lib = load_library()
         lam = np.ascontiguousarray(np.asarray(lam, dtype=np.float64))
+        n = 20 * 4 ** fine_ref if 0 <= fine_ref <= 10 else 0
+        if dist is not None and dist[3] < fine_ref:
+            n //= max(int(dist[1]), 1)                # this rank's owned part of the finest level
+        if lam.size != nlayers * n:
+            raise ValueError(f"lam: expected {nlayers} x {n} values, got shape {lam.shape}")
         h = ctypes.c_void_p()
         if dist is None:
             _check(lib.hmg_build_hierarchy(fine_ref, coarsest_ref, nlayers, thickness, w2,

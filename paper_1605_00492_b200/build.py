@@ -15,7 +15,11 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhmg.so")
-SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "sweep_st.cu", "apply_st.cu", "sweep_small.cu", "coarse_tail.cu", "coarse_coop.cu", "mesh.cpp", "dist.cpp", "nccl_dyn.cpp", "local_transport.cu", "mixed.cu"]
+SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "sweep_st.cu", "apply_st.cu", "sweep_small.cu", "thomas_factor.cu",
+           "coarse_coop.cu", "mesh.cpp", "dist.cpp", "nccl_dyn.cpp", "mixed.cu"]
+# test-only in-process collective transport (HMG_TRANSPORT=local), its own library
+TEST_SOURCES = ["local_transport.cu"]
+TEST_LIB = os.path.join(HERE, "libhmg_localtx.so")
 HEADERS = ["hmg_internal.h", "mf_ops.cuh", "small_tile.cuh", "mesh.h", "sm100_ptx.cuh", "dist.h", "nccl_dyn.h", os.path.join("..", "..", "include", "hmg.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -24,10 +28,10 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC,-
 
 
 def _stale() -> bool:
-    if not os.path.exists(LIB):
+    if not (os.path.exists(LIB) and os.path.exists(TEST_LIB)):
         return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [__file__]
+    t = min(os.path.getmtime(LIB), os.path.getmtime(TEST_LIB))
+    deps = [os.path.join(CSRC, f) for f in SOURCES + TEST_SOURCES + HEADERS] + [__file__]
     return any(os.path.getmtime(d) > t for d in deps)
 
 
@@ -47,7 +51,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
     link = [NVCC, *ARCH, "-shared", *[o for _, o in jobs], "-o", tmp, "-ldl"]
     results.append(subprocess.run(link, capture_output=True, text=True) if all(r.returncode == 0 for r in results)
                    else subprocess.CompletedProcess(link, 1, "", "link skipped: compile failed\n"))
-    log = "".join(" ".join(c) + "\n" + r.stdout + r.stderr for c, r in zip([j[0] for j in jobs] + [link], results))
+    # the test-only transport library (not linked into libhmg.so)
+    tmp_test = TEST_LIB + f".tmp{os.getpid()}"
+    test_cmd = [NVCC, *ARCH, *FLAGS, "-shared", *[os.path.join(CSRC, f) for f in TEST_SOURCES], "-o", tmp_test]
+    results.append(subprocess.run(test_cmd, capture_output=True, text=True))
+    log = "".join(" ".join(c) + "\n" + r.stdout + r.stderr
+                  for c, r in zip([j[0] for j in jobs] + [link, test_cmd], results))
     with open(os.path.join(HERE, "build.log"), "w") as fh:
         fh.write(log)
     for _, o in jobs:
@@ -59,6 +68,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose:
         sys.stderr.write(log)
     os.replace(tmp, LIB)
+    os.replace(tmp_test, TEST_LIB)
     return LIB
 
 

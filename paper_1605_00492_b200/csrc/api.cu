@@ -164,10 +164,9 @@ void nccl_check(int r, const char* what) {
 
 // Fill the halo slots of vector v on a distributed level from the owners:
 // pack my owned cells each peer needs, grouped send/recv, unpack.
-void halo_exchange(const Hierarchy& H, const DevLevel& L, const double* v_const, cudaStream_t s) {
+void halo_exchange(const Hierarchy& H, const DevLevel& L, double* v, cudaStream_t s) {
     const DistLevel& D = L.dist;
     if (!D.on || D.peer_rank.empty()) return;
-    double* v = const_cast<double*>(v_const);     // halo slots are library scratch (include/hmg.h)
     const Nccl* N = nccl(nullptr);
     launch_halo_pack(H, L, v, s);
     const int nz = H.nz;
@@ -213,9 +212,9 @@ namespace {
 // sweep writes `out` if given (it must not be wa/wb), else wa or wb.
 // Returns the buffer holding the result.
 // -------------------------------------------------------------------------
-const double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b, const double* uin, const double* uc,
-                         int count, double* out, double omega, cudaStream_t s) {
-    const double* cur = uin;
+double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b, double* uin, const double* uc,
+                   int count, double* out, double omega, cudaStream_t s) {
+    double* cur = uin;
     for (int i = 0; i < count; ++i) {
         double* dst = (i == count - 1 && out) ? out : (cur == L.wa ? L.wb : L.wa);
         if (cur) halo_exchange(H, L, cur, s);      // neighbours' old values (Jacobi)
@@ -267,11 +266,6 @@ void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const dou
         flush_pending_x(H, s, true, true);
         return;
     }
-    if (ref == H.tail_ref) {                    // levels <= tail_ref: one launch
-        flush_pending_x(H, s, true);
-        launch_coarse_tail(H, p, b, out, s);
-        return;
-    }
     if (ref == H.coarsest_ref) {
         flush_pending_x(H, s, true);
         // whole coarsest level in one CTA's shared memory when it fits (ref 0: 20 columns)
@@ -286,7 +280,7 @@ void vcycle_level(const Hierarchy& H, int ref, const hmg_mg_params& p, const dou
     }
     const DevLevel& C = H.lev[ref - 1];
     // M1 presmooth from zero: the iterate stays in wa/wb through M2-M3
-    const double* cur = nullptr;
+    double* cur = nullptr;
     if (p.nu_pre > 0) cur = run_sweeps(H, L, b, nullptr, nullptr, p.nu_pre, nullptr, p.omega, s);
     // M2 restrict the residual (b itself when u = 0)
     if (cur) {
@@ -338,9 +332,11 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     HMG_TRY(check_launch());
     HMG_CUDA(cudaStreamSynchronize(s));
     const double bn = std::sqrt(H.scal_host->bb);
-    if (bn == 0.0) {
+    if (bn == 0.0 || maxit == 0) {            // x = x0 = 0 (and r = b: relres 1 when b != 0)
         HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
-        return HMG_OK;
+        if (bn == 0.0) return HMG_OK;
+        *relres = 1.0;
+        return fail(HMG_ERR_NOT_CONVERGED, "not converged after 0 iterations (relres 1)");
     }
     // <r, z> after each preconditioner application: fused into its last sweep
     // when that is a streamed fine-level sweep (a fixed-order per-CTA sum, like
@@ -400,8 +396,18 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
             launch_update_xr(H, F, x, pc, s);      // x += alpha p, r -= alpha q, partial <r, r>
         }
         launch_finalize(H, kFinRR, s);
-        HMG_TRY(check_launch());
-        HMG_CUDA(cudaStreamSynchronize(s));
+        {
+            // an error leaves no deferred x update behind (nor a side stream the
+            // caller's stream does not wait for)
+            hmg_status st = check_launch();
+            const cudaError_t e = cudaStreamSynchronize(s);
+            if (st != HMG_OK || e != cudaSuccess) {
+                H.px.pending = false;
+                join_x();
+                if (st != HMG_OK) return st;
+                return fail(HMG_ERR_CUDA, std::string("cudaStreamSynchronize: ") + cudaGetErrorString(e));
+            }
+        }
         if (H.scal_host->bad != ~0ull) {
             H.px.pending = false;
             return check_bad(H, s);
@@ -455,6 +461,8 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
         if (!dist->nccl_id) return fail(HMG_ERR_INVALID_ARG, "dist->nccl_id: null pointer");
         if (gather_ref < std::max(2, coarsest_ref) || gather_ref > fine_ref)
             return fail(HMG_ERR_INVALID_ARG, "dist->gather_ref: must be in [max(2, coarsest_ref), fine_ref]");
+        if (nranks > 1 && gather_ref >= fine_ref)   // every level replicated: nothing to distribute
+            return fail(HMG_ERR_INVALID_ARG, "dist->gather_ref: must be < fine_ref when nranks > 1");
     }
     // lam_host: the finest level, [nlayers][20*4^fine_ref] (single GPU) or this
     // rank's owned cells [nlayers][20*4^fine_ref/nranks] (distributed, when
@@ -515,19 +523,6 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
         while (coop < fine_ref && 20LL * (1LL << (2 * (coop + 1))) <= coop_max) ++coop;
         if (const char* e = std::getenv("HMG_COOP_REF")) coop = std::atoi(e);
         H->coop_ref = coop < 0 ? -1 : std::min(std::max(coop, coarsest_ref), dist ? gather_ref : fine_ref);
-        // Diagnostic alternative (HMG_TAIL_REF=r): levels <= r in the global-memory
-        // tail kernel (coarse_tail.cu); HMG_TAIL_GRID=1 makes it cooperative.
-        int tail = -1;
-        if (const char* e = std::getenv("HMG_TAIL_REF")) tail = std::atoi(e);
-        if (const char* e = std::getenv("HMG_TAIL_GRID")) H->tail_grid = std::string(e) != "0";
-        if (const char* e = std::getenv("HMG_TAIL_THREADS")) H->tail_threads = std::max(32, std::min(128, std::atoi(e)));
-        if (tail < 0) {
-            H->tail_ref = -1;
-        } else {
-            H->coop_ref = -1;
-            tail = std::max(tail, coarsest_ref);
-            H->tail_ref = std::min(tail, dist ? gather_ref : fine_ref);   // the tail never spans distributed levels
-        }
     }
     if (H->use_tc_sweep && !tensor_maps_available()) {
         delete H;
@@ -894,7 +889,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     // for every level too small to fill the GPU (latency-bound sweeps)
     for (int r = coarsest_ref; r <= fine_ref; ++r) {
         DevLevel& L = H->lev[r];
-        if (!(r <= H->tail_ref || r <= H->coop_ref || L.n <= H->fact_max_cells)) continue;
+        if (!(r <= H->coop_ref || L.n <= H->fact_max_cells)) continue;
         const size_t vb = sizeof(double) * nlayers * L.ld;
         BCUDA(cudaMalloc(&L.fden, 3 * vb));          // [3][nz][ld]: den, y, g (one TMA box)
         L.fy = L.fden + (size_t)nlayers * L.ld;
@@ -1129,7 +1124,7 @@ hmg_status hmg_level_info(const hmg_hierarchy* h, int ref, int64_t* ncells, int6
     return HMG_OK;
 }
 
-hmg_status hmg_apply_helmholtz(const hmg_hierarchy* h, int ref, const double* x, double* y, void* stream) {
+hmg_status hmg_apply_helmholtz(const hmg_hierarchy* h, int ref, double* x, double* y, void* stream) {
     HMG_TRY(check_h(h));
     const Hierarchy& H = HH(h);
     HMG_TRY(check_level(H, ref, "ref"));
@@ -1177,11 +1172,14 @@ hmg_status hmg_restrict(const hmg_hierarchy* h, int fine_ref, const double* r_f,
     if (fine_ref == H.coarsest_ref) return fail(HMG_ERR_INVALID_ARG, "fine_ref: no coarser level in hierarchy");
     HMG_TRY(check_ptr(r_f, "r_f"));
     HMG_TRY(check_ptr(b_c, "b_c"));
-    launch_restrict(H, H.lev[fine_ref], r_f, b_c, S(stream));
+    const DevLevel& L = H.lev[fine_ref];
+    const DevLevel& C = H.lev[fine_ref - 1];
+    launch_restrict(H, L, r_f, b_c, S(stream));
+    if (L.dist.on && !C.dist.on) coarse_gather(H, C, b_c, S(stream));   // replicated coarse level: whole vector
     return check_launch();
 }
 
-hmg_status hmg_residual_restrict(const hmg_hierarchy* h, int fine_ref, const double* b, const double* u, double* b_c,
+hmg_status hmg_residual_restrict(const hmg_hierarchy* h, int fine_ref, const double* b, double* u, double* b_c,
                                  void* stream) {
     HMG_TRY(check_h(h));
     const Hierarchy& H = HH(h);
@@ -1190,7 +1188,11 @@ hmg_status hmg_residual_restrict(const hmg_hierarchy* h, int fine_ref, const dou
     HMG_TRY(check_ptr(b, "b"));
     HMG_TRY(check_ptr(u, "u"));
     HMG_TRY(check_ptr(b_c, "b_c"));
-    launch_resid_restrict(H, H.lev[fine_ref], b, u, b_c, S(stream));
+    const DevLevel& L = H.lev[fine_ref];
+    const DevLevel& C = H.lev[fine_ref - 1];
+    halo_exchange(H, L, u, S(stream));             // neighbours' values of u (halo slots are library scratch)
+    launch_resid_restrict(H, L, b, u, b_c, S(stream));
+    if (L.dist.on && !C.dist.on) coarse_gather(H, C, b_c, S(stream));   // replicated coarse level: whole vector
     return check_launch();
 }
 

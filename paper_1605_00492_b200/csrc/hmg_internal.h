@@ -130,21 +130,6 @@ struct DevLevel {
     }
 };
 
-// One level as seen by the coarse-tail kernel (coarse_tail.cu).
-struct TailLevel {
-    LevelView V;
-    double *wa, *wb, *b, *u;
-    const double *den, *y, *g;
-    int64_t ldc;                // coarse leading dimension for the fused prolongation (set in-kernel)
-};
-struct TailParams {
-    TailLevel lev[kMaxRef + 1];
-    int nz, top, coarsest, nu_pre, nu_post, n_coarse;
-    double omega;
-    const double* b_top;
-    double* out_top;
-};
-
 // Device-resident PCG scalars: one struct so a single 64-byte D2H read per
 // iteration returns the residual norm and the singular-pivot flag together.
 struct PcgScalars {
@@ -215,9 +200,6 @@ struct Hierarchy {
     bool defer_x = true;        // HMG_DEFER_X=0: x and r updated by one kernel on the solve stream
     int x_slow_blocks = 148;    // HMG_X_BLOCKS=n: the deferred update by n grid-stride CTAs (0: the full vector grid)
     cudaEvent_t ev_in[2] = {}, ev_solved[2] = {}, ev_out[2] = {};
-    int tail_ref = -1;          // levels <= tail_ref run in one coarse-tail launch (-1: off)
-    bool tail_grid = false;     // the tail is a cooperative multi-CTA launch (false: one CTA)
-    int tail_threads = 64;      // threads per CTA of the cooperative tail
     int coop_ref = -1;          // levels <= coop_ref run in one cooperative smem-tile launch (-1: off)
     // multi-GPU (hmg_build_hierarchy_dist): levels > gather_ref are distributed
     int rank = 0, nranks = 1, gather_ref = -1;
@@ -320,11 +302,9 @@ int launch_apply_pupdate_st(const Hierarchy& H, const DevLevel& L, const double*
                             double* q, cudaStream_t s);
 void finalize_parts(const Hierarchy& H, int nparts, int op, cudaStream_t s);
 
-// coarse_tail.cu
+// thomas_factor.cu
 void launch_factor(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
 void launch_pivot_check(const Hierarchy& H, const DevLevel& L, unsigned int* gslow, cudaStream_t s);
-void launch_coarse_tail(const Hierarchy& H, const hmg_mg_params& p, const double* b_top, double* out_top,
-                        cudaStream_t s);
 // coarse_coop.cu: levels <= H.coop_ref in one cooperative launch (32-column smem tiles)
 bool coarse_coop_supported(const Hierarchy& H);
 int coarse_coop_tile_width(int nz);   // 32, 16 or 8 columns per tile (0: no fit)

@@ -1,5 +1,8 @@
-// In-process transport with NCCL's interface, for testing the multi-GPU code
-// path of this library on ONE GPU (HMG_TRANSPORT=local).
+// TEST-ONLY in-process transport with NCCL's interface, for testing the
+// multi-GPU code path of this library on ONE GPU (HMG_TRANSPORT=local).  It is
+// NOT part of the product library: build.py compiles it into its own
+// libhmg_localtx.so, which libhmg.so dlopens only when HMG_TRANSPORT=local
+// (tests/test_dist_local.py).
 //
 // Every rank is a host thread of the same process, all on the same device,
 // each enqueuing its work on its own stream.  The collectives the library uses
@@ -289,7 +292,10 @@ const char* l_error_string(int r) {
 
 }  // namespace
 
-const Nccl* local_transport() {
+}  // namespace hmg
+
+extern "C" const void* hmg_local_transport_table() {
+    using namespace hmg;
     static Nccl t;
     t.GetUniqueId = l_get_unique_id;
     t.CommInitRank = l_comm_init_rank;
@@ -303,5 +309,3 @@ const Nccl* local_transport() {
     t.GetErrorString = l_error_string;
     return &t;
 }
-
-}  // namespace hmg

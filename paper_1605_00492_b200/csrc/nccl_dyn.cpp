@@ -8,15 +8,48 @@
 
 namespace hmg {
 
-const Nccl* local_transport();   // local_transport.cu
+namespace {
+
+// HMG_TRANSPORT=local (tests only): every rank a thread of this process on one
+// GPU, collectives through the test transport of local_transport.cu, which is
+// built into its own libhmg_localtx.so next to this library (not part of it).
+const Nccl* local_transport(std::string* err) {
+    static const Nccl* table = nullptr;
+    static std::string load_err;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        Dl_info info{};
+        std::string dir = ".";
+        if (dladdr(reinterpret_cast<void*>(&local_transport), &info) && info.dli_fname) {
+            dir = info.dli_fname;
+            const size_t slash = dir.rfind('/');
+            dir = slash == std::string::npos ? "." : dir.substr(0, slash);
+        }
+        const std::string path = dir + "/libhmg_localtx.so";
+        void* h = dlopen(path.c_str(), RTLD_NOW | RTLD_LOCAL);
+        if (!h) {
+            load_err = "HMG_TRANSPORT=local: cannot load " + path + " (test-only transport; build.py builds it)";
+            return;
+        }
+        auto fn = reinterpret_cast<const void* (*)()>(dlsym(h, "hmg_local_transport_table"));
+        if (!fn) {
+            load_err = path + " lacks hmg_local_transport_table";
+            return;
+        }
+        table = static_cast<const Nccl*>(fn());
+    });
+    if (!table && err) *err = load_err;
+    return table;
+}
+
+}  // namespace
 
 const Nccl* nccl(std::string* err) {
-    // HMG_TRANSPORT=local: every rank a thread of this process on one GPU (tests)
     static const bool local = [] {
         const char* e = std::getenv("HMG_TRANSPORT");
         return e && std::string(e) == "local";
     }();
-    if (local) return local_transport();
+    if (local) return local_transport(err);
     static Nccl table;
     static bool ok = false;
     static std::string load_err;

@@ -28,8 +28,9 @@ struct Nccl {
 };
 
 // Loaded table, or nullptr with `err` set.  HMG_TRANSPORT=local selects the
-// in-process transport of local_transport.cu (all ranks threads of one
-// process on one GPU; for testing the multi-GPU path on a single device).
+// TEST-ONLY in-process transport (local_transport.cu, built separately into
+// libhmg_localtx.so and loaded from next to this library: all ranks threads
+// of one process on one GPU, for testing the multi-GPU path on one device).
 const Nccl* nccl(std::string* err);
 
 }  // namespace hmg
