@@ -307,10 +307,15 @@ hmg_status hmg_mixed_precond(const hmg_hierarchy* h, const hmg_mg_params* p, con
  * (checked at the end of each cycle; within a cycle the Givens estimate ends
  * the cycle early).  iters = Arnoldi steps (preconditioner applications
  * excluding the one per cycle that forms X).  restart in [1, 31].
- * Synchronises once per Arnoldi step (the Hessenberg column).  Returns
+ * gs_passes: classical Gram-Schmidt passes per Arnoldi step -- 1 = CGS (what
+ * PETSc's GMRES does by default, so most likely the paper's), 2 = CGS2 (the
+ * recommended setting: one pass loses the basis' orthogonality on the
+ * anisotropic problems, max|<v_a,v_b> - delta_ab| ~ 1e-1 at ref 5 x 64 C2b
+ * against ~1e-12 with two; R20).  Other values: HMG_ERR_INVALID_ARG.
+ * Synchronises once per Gram-Schmidt pass (the Hessenberg column).  Returns
  * HMG_ERR_NOT_CONVERGED with X, iters, relres filled after maxit steps. */
 hmg_status hmg_mixed_gmres(const hmg_hierarchy* h, const hmg_mg_params* p, const double* F, double* X, double rtol,
-                           int restart, int maxit, int* iters, double* relres, void* stream);
+                           int restart, int maxit, int gs_passes, int* iters, double* relres, void* stream);
 
 /* Message for the last error on this thread ("" if none). */
 const char* hmg_last_error(void);

@@ -83,8 +83,9 @@ def _load():
             lib.ora_mixed_precond.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                               ctypes.c_double, P, P]
             lib.ora_mixed_gmres.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                            ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_int, P, P,
-                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), P]
+                                            ctypes.c_double, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                            ctypes.c_int, P, P, ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_double), P, ctypes.POINTER(ctypes.c_double)]
             lib.ora_last_error.restype = ctypes.c_char_p
             _lib = lib
     return _lib
@@ -283,16 +284,23 @@ class Hierarchy:
         return x
 
     def mixed_gmres(self, F, rtol=1e-5, restart=30, maxit=300, precond="schur", nu_pre=2, nu_post=2, n_coarse=20,
-                    omega=0.8):
-        """Right-preconditioned GMRES(restart), x0 = 0.  Returns (x, iters, relres, history, status)."""
+                    omega=0.8, gs_passes=2, orth=False):
+        """Right-preconditioned GMRES(restart), x0 = 0, classical Gram-Schmidt
+        applied ``gs_passes`` times per Arnoldi step (1 = CGS, PETSc's default;
+        2 = CGS2, reading R20).  Returns (x, iters, relres, history, status), plus
+        the basis' worst orthogonality error max|<v_a, v_b> - delta_ab| over all
+        cycles when ``orth``."""
         F = _f64(F)
         x = np.empty_like(F)
         it = ctypes.c_int(0)
         rr = ctypes.c_double(0.0)
+        oe = ctypes.c_double(0.0)
         hist = np.zeros(maxit + 1)
         kind = {"none": 0, "schur": 1}[precond]
         code = _load().ora_mixed_gmres(self._h, kind, nu_pre, nu_post, n_coarse, omega, restart, rtol, maxit,
-                                       _ptr(F), _ptr(x), ctypes.byref(it), ctypes.byref(rr), _ptr(hist))
+                                       gs_passes, _ptr(F), _ptr(x), ctypes.byref(it), ctypes.byref(rr), _ptr(hist),
+                                       ctypes.byref(oe) if orth else None)
         if code not in (0, NOT_CONVERGED):
             _check(code)
-        return x, it.value, rr.value, hist[: it.value + 1], code
+        out = (x, it.value, rr.value, hist[: it.value + 1], code)
+        return out + (oe.value,) if orth else out

@@ -1016,7 +1016,8 @@ int ora_mixed_precond(ora_h* h, int kind, int nu_pre, int nu_post, int n_coarse,
 /*   r = F - A x, beta = ||r||; converged when beta <= rtol ||F||.          */
 /* dot = sequential sum in index order.                                    */
 int ora_mixed_gmres(ora_h* h, int kind, int nu_pre, int nu_post, int n_coarse, double omega_s, int m, double rtol,
-                    int maxit, const double* F, double* X, int* iters, double* relres, double* hist) {
+                    int maxit, int gs_passes, const double* F, double* X, int* iters, double* relres, double* hist,
+                    double* orth) {
     ora_edges E;
     int st = fine_edges(h, &E);
     if (st) return st;
@@ -1033,6 +1034,8 @@ int ora_mixed_gmres(ora_h* h, int kind, int nu_pre, int nu_post, int n_coarse, d
     if (!V || !w || !z || !tmp || !H || !cs || !sn || !g || !yv) { st = ORA_ERR_OOM; goto out; }
     *iters = 0;
     *relres = 0.0;
+    if (orth) *orth = 0.0;
+    if (gs_passes < 1) { st = ORA_ERR_ARG; snprintf(ora_msg, sizeof ora_msg, "gs_passes must be >= 1"); goto out; }
     for (int64_t q = 0; q < N; q++) X[q] = 0.0;
     double fn = sqrt(dot(N, F, F));
     if (hist) hist[0] = fn == 0.0 ? 0.0 : 1.0;
@@ -1051,7 +1054,9 @@ int ora_mixed_gmres(ora_h* h, int kind, int nu_pre, int nu_post, int n_coarse, d
             int s2 = mixed_precond(h, &E, kind, nu_pre, nu_post, n_coarse, omega_s, vj, z, tmp);
             if (s2) { st = s2; goto out; }
             mixed_apply(h, &E, z, w, tmp);
-            for (int pass = 0; pass < 2; pass++) {       /* CGS2: Gram-Schmidt twice */
+            /* classical Gram-Schmidt, gs_passes times: 1 = CGS (PETSc's default,
+               refinement "never"), 2 = CGS2 ("twice is enough"; reading R20) */
+            for (int pass = 0; pass < gs_passes; pass++) {
                 for (int i = 0; i <= j; i++) yv[i] = dot(N, V + (int64_t)i * N, w);
                 for (int i = 0; i <= j; i++) {
                     const double* vi = V + (int64_t)i * N;
@@ -1080,6 +1085,13 @@ int ora_mixed_gmres(ora_h* h, int kind, int nu_pre, int nu_post, int n_coarse, d
             total++;
             if (hist) hist[total] = fabs(g[j + 1]) / fn;
             if (fabs(g[j + 1]) <= rtol * fn) { j++; done = 1; break; }
+        }
+        if (orth) {   /* diagnostic: max |<v_a, v_b> - delta_ab| over the cycle's j + 1 basis vectors */
+            for (int a2 = 0; a2 <= j; a2++)
+                for (int b2 = 0; b2 <= a2; b2++) {
+                    double e = dot(N, V + (int64_t)a2 * N, V + (int64_t)b2 * N) - (a2 == b2 ? 1.0 : 0.0);
+                    if (fabs(e) > *orth) *orth = fabs(e);
+                }
         }
         /* y = H^-1 g on the leading j x j block, x += M^-1 (V y) */
         for (int i = j - 1; i >= 0; i--) {

@@ -93,7 +93,7 @@ def load_library():
         "hmg_mixed_export_edges": [P, P, P],
         "hmg_mixed_apply": [P, P, P, P],
         "hmg_mixed_precond": [P, pP, P, P, P],
-        "hmg_mixed_gmres": [P, pP, P, P, D, I, I, pI, pD, P],
+        "hmg_mixed_gmres": [P, pP, P, P, D, I, I, I, pI, pD, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -404,13 +404,13 @@ class Hierarchy:
         return x
 
     def mixed_gmres(self, F, X=None, rtol: float = 1e-5, restart: int = 30, maxit: int = 300,
-                    params: MGParams | None = MGParams()):
-        """Returns (X, iters, relres, status_name)."""
+                    params: MGParams | None = MGParams(), gs_passes: int = 2):
+        """gs_passes: 1 = CGS, 2 = CGS2.  Returns (X, iters, relres, status_name)."""
         X = self.mixed_empty() if X is None else X
         p = None if params is None else params.c()
         it, rr = ctypes.c_int(0), ctypes.c_double(0.0)
         code = _check(load_library().hmg_mixed_gmres(self._h, None if p is None else ctypes.byref(p), _dptr(F, "F"),
-                                                     _dptr(X, "X"), rtol, restart, maxit, ctypes.byref(it),
+                                                     _dptr(X, "X"), rtol, restart, maxit, gs_passes, ctypes.byref(it),
                                                      ctypes.byref(rr), _stream()), allow=(5,))
         return X, it.value, rr.value, STATUS[code]
 

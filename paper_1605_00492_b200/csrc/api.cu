@@ -925,12 +925,12 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
 
 // NEXT-4 (mixed.cu): restarted right-preconditioned GMRES(m) on the mixed
 // system (reading R20), the oracle's ora_mixed_gmres step for step: classical
-// Gram-Schmidt applied twice (CGS2) against one w, Givens rotations and the small triangular solve
+// Gram-Schmidt applied gs_passes times (2 = CGS2, the default) against one w, Givens rotations and the small triangular solve
 // on the host, every vector operation in mixed.cu's kernels.  Dot products
 // are deterministic block trees (the oracle's are sequential): parity is the
 // iteration count.
 hmg_status mixed_gmres_impl(const Hierarchy& H, const hmg_mg_params* p, const double* F, double* X, double rtol,
-                            int m, int maxit, int* iters, double* relres, cudaStream_t s) {
+                            int m, int maxit, int gs_passes, int* iters, double* relres, cudaStream_t s) {
     MixedSystem& M = *H.mix;
     const int64_t N = M.ntot;
     if (M.m < m) {
@@ -980,7 +980,7 @@ hmg_status mixed_gmres_impl(const Hierarchy& H, const hmg_mg_params* p, const do
         for (j = 0; j < m && total < maxit; ++j) {
             mixed_precond(H, p, vp[j], M.z, s);                // w = A M^-1 v_j
             launch_mixed_apply(H, M.z, M.w, s);
-            for (int pass = 0; pass < 2; ++pass) {             // CGS2: Gram-Schmidt twice
+            for (int pass = 0; pass < gs_passes; ++pass) {     // CGS (1) or CGS2 (2, the default)
                 mixed_dots(H, M.w, vp.data(), j + 1, 1, s);    // c_i = <v_i, w>, i <= j
                 HMG_TRY(fetch(j + 1));
                 for (int i = 0; i <= j; ++i) {
@@ -1517,7 +1517,7 @@ hmg_status hmg_mixed_precond(const hmg_hierarchy* h, const hmg_mg_params* p, con
 }
 
 hmg_status hmg_mixed_gmres(const hmg_hierarchy* h, const hmg_mg_params* p, const double* F, double* X, double rtol,
-                           int restart, int maxit, int* iters, double* relres, void* stream) {
+                           int restart, int maxit, int gs_passes, int* iters, double* relres, void* stream) {
     HMG_TRY(check_h(h));
     const Hierarchy& H = HH(h);
     if (p) HMG_TRY(check_params(p));
@@ -1530,8 +1530,9 @@ hmg_status hmg_mixed_gmres(const hmg_hierarchy* h, const hmg_mg_params* p, const
     if (restart < 1 || restart > mixed_lin_max() - 1)
         return fail(HMG_ERR_INVALID_ARG, "restart: must be in [1, " + std::to_string(mixed_lin_max() - 1) + "]");
     if (maxit < 0) return fail(HMG_ERR_INVALID_ARG, "maxit: must be >= 0");
+    if (gs_passes < 1 || gs_passes > 2) return fail(HMG_ERR_INVALID_ARG, "gs_passes: must be 1 (CGS) or 2 (CGS2)");
     HMG_TRY(ensure_mixed(H));
-    return mixed_gmres_impl(H, p, F, X, rtol, restart, maxit, iters, relres, S(stream));
+    return mixed_gmres_impl(H, p, F, X, rtol, restart, maxit, gs_passes, iters, relres, S(stream));
 }
 
 }  // extern "C"

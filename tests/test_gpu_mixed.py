@@ -90,12 +90,15 @@ def test_precond_bitwise(pair, params):
     assert np.array_equal(g.mixed_to_host(g.mixed_precond(g.mixed_to_device(f), params=None)), f)
 
 
-def test_gmres_iterations_match_oracle(pair):
+@pytest.mark.parametrize("gs_passes", [2, 1], ids=["CGS2", "CGS"])
+def test_gmres_iterations_match_oracle(pair, gs_passes):
+    """Both Gram-Schmidt variants (R20: CGS2 the default, CGS = PETSc's default
+    and most likely the paper's) take the oracle's iteration count."""
     cfg, g, o = pair
     _, N = o.mixed_sizes()
     F = hi.uniform_vector(N, 65)
-    X, it, rr, st = g.mixed_gmres(g.mixed_to_device(F), rtol=1e-5)
-    Xo, it_o, rr_o, _, st_o = o.mixed_gmres(F, rtol=1e-5)
+    X, it, rr, st = g.mixed_gmres(g.mixed_to_device(F), rtol=1e-5, gs_passes=gs_passes)
+    Xo, it_o, rr_o, _, st_o = o.mixed_gmres(F, rtol=1e-5, gs_passes=gs_passes)
     assert st == "HMG_OK" and st_o == 0
     assert it == it_o, (it, it_o, rr, rr_o)
     assert rr <= 1e-5 and rr == pytest.approx(rr_o, rel=1e-2)
@@ -154,6 +157,8 @@ def test_mixed_errors():
         g.mixed_apply(x, x)
     with pytest.raises(HmgError, match="restart"):
         g.mixed_gmres(x, restart=0)
+    with pytest.raises(HmgError, match="gs_passes"):
+        g.mixed_gmres(x, gs_passes=3)
     X, it, rr, st = g.mixed_gmres(x)          # zero right-hand side: zero iterations, X = 0
     assert it == 0 and st == "HMG_OK" and torch.all(X == 0)
     g.close()

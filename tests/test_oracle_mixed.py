@@ -244,3 +244,51 @@ def test_gmres_c0_converges_like_the_paper(c0):
     assert rel <= 1e-5
     _, it0, _, _, st0 = h.mixed_gmres(F, rtol=1e-5, maxit=60, precond="none")
     assert st0 != 0 or it0 > 3 * it
+
+
+@pytest.mark.parametrize("gs_passes", [1, 2], ids=["CGS", "CGS2"])
+def test_gmres_both_gram_schmidt_variants_minimise(gs_passes):
+    """On a small, well-conditioned case one and two Gram-Schmidt passes both
+    give the least-squares-minimal residual history (checked against an
+    independent dense solve): the variant only matters once orthogonality is
+    lost (next test)."""
+    cfg, h = _tiny()
+    ne, N = h.mixed_sizes()
+    A = _dense(h.mixed_apply, N)
+    Minv = _dense(lambda f: h.mixed_precond(f), N)
+    B = A @ Minv
+    F = hi.uniform_vector(N, 33)
+    x, it, rel, hist, st = h.mixed_gmres(F, rtol=1e-10, restart=30, maxit=60, gs_passes=gs_passes)
+    assert st == 0
+    K = np.empty((N, 0))
+    v = F / np.linalg.norm(F)
+    for j in range(1, min(it, 6) + 1):
+        K, _ = np.linalg.qr(np.column_stack([K, v]))
+        y, *_ = np.linalg.lstsq(B @ K, F, rcond=None)
+        assert hist[j] == pytest.approx(np.linalg.norm(F - B @ K @ y) / np.linalg.norm(F), rel=1e-7, abs=1e-14)
+        v = B @ K[:, -1]
+    h.close()
+
+
+def test_gmres_cgs_loses_orthogonality_cgs2_keeps_it():
+    """Why reading R20 departs from PETSc's default (one classical Gram-Schmidt
+    pass, most likely what the paper's GMRES(30) ran): on the
+    anisotropic problems one pass loses the Arnoldi basis' orthogonality --
+    the loss of CGS grows like eps * kappa^2 of the Krylov matrix -- while two
+    passes keep it at the rounding level ("twice is enough": ||I - V^T V|| =
+    O(eps), independent of kappa).  Measured on the oracle alone, no GPU
+    involved: C2c's anisotropy at ref 4 x 64 and C2b's at ref 3 x 16; at ref 5 x
+    64 (C2b) CGS's basis is ~1e-1 from orthogonal (13 s, not run here)."""
+    for name, ref, nz, loss_cgs in (("C2c", 4, 64, 1e-3), ("C2b", 3, 16, 1e-7)):
+        c = hi.CONFIGS[name]
+        cfg = hi.Config("orth", ref, 0, nz, c.thickness, c.w2)
+        lam, _ = hi.make_inputs(cfg)
+        h = oracle.Hierarchy(ref, 0, nz, cfg.thickness, cfg.w2, lam)
+        _, N = h.mixed_sizes()
+        F = hi.uniform_vector(N, 65)
+        _, it1, rel1, _, st1, orth1 = h.mixed_gmres(F, rtol=1e-5, gs_passes=1, orth=True)
+        _, it2, rel2, _, st2, orth2 = h.mixed_gmres(F, rtol=1e-5, gs_passes=2, orth=True)
+        assert st1 == 0 and st2 == 0
+        assert orth2 <= 1000 * EPS, (name, orth2)
+        assert orth1 >= loss_cgs, (name, orth1)
+        h.close()
