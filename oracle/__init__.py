@@ -28,6 +28,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "hmg_oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "band_oracle.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -37,9 +38,9 @@ CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-s
 
 def build(force: bool = False) -> str:
     """Compile the oracle shared library (gcc).  Returns its path."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+    if force or not os.path.exists(_LIB) or any(os.path.getmtime(_LIB) < os.path.getmtime(f) for f in _SRCS):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", *CFLAGS, _SRC, "-o", tmp, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, *_SRCS, "-o", tmp, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -87,6 +88,16 @@ def _load():
                                             ctypes.c_int, P, P, ctypes.POINTER(ctypes.c_int),
                                             ctypes.POINTER(ctypes.c_double), P, ctypes.POINTER(ctypes.c_double)]
             lib.ora_last_error.restype = ctypes.c_char_p
+            # NEXT-3 core (band_oracle.c)
+            lib.ora_gbtrf.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P]
+            lib.ora_gbtrs.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P, P, P]
+            lib.ora_gbtrs.restype = None
+            lib.ora_gbmv.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, P]
+            lib.ora_gbmv.restype = None
+            lib.ora_p_restrict.argtypes = [ctypes.c_int64, ctypes.c_int, P, P]
+            lib.ora_p_restrict.restype = None
+            lib.ora_p_prolong_add.argtypes = [ctypes.c_int64, ctypes.c_int, P, P]
+            lib.ora_p_prolong_add.restype = None
             _lib = lib
     return _lib
 
@@ -304,3 +315,55 @@ class Hierarchy:
             _check(code)
         out = (x, it.value, rr.value, hist[: it.value + 1], code)
         return out + (oe.value,) if orth else out
+
+
+# ---- NEXT-3 core: per-column banded LU (dgbtrf / dgbtrs) and DG1 <-> DG0 ----
+def gbtrf(ab, kl: int, ku: int):
+    """dgbtrf (unblocked dgbtf2 order) of ONE m x m banded matrix in LAPACK band
+    storage ``ab`` [ldab][m] (ldab >= 2 kl + ku + 1, A(i, j) = ab[kl + ku + i - j, j]).
+    Returns (lu [ldab][m], ipiv [m] 0-based int32, info)."""
+    a = np.asfortranarray(ab, dtype=np.float64)          # column j contiguous, as LAPACK
+    ldab, m = a.shape
+    flat = np.ascontiguousarray(a.T)                      # [m][ldab]
+    ipiv = np.zeros(m, np.int32)
+    info = _load().ora_gbtrf(m, kl, ku, _ptr(flat), ldab, _ptr(ipiv))
+    return flat.T.copy(), ipiv, int(info)
+
+
+def gbtrs(lu, kl: int, ku: int, ipiv, b) -> np.ndarray:
+    """dgbtrs ('N', one right-hand side) from gbtrf's factors."""
+    ldab, m = lu.shape
+    flat = np.ascontiguousarray(np.asarray(lu, dtype=np.float64).T)
+    ip = np.ascontiguousarray(ipiv, dtype=np.int32)
+    b = _f64(b)
+    x = np.empty_like(b)
+    _load().ora_gbtrs(m, kl, ku, _ptr(flat), ldab, _ptr(ip), _ptr(b), _ptr(x))
+    return x
+
+
+def gbmv(ab_rows, kl: int, ku: int, x) -> np.ndarray:
+    """y = A x, the paper's row-wise band storage ab_rows [m][kl + ku + 1]."""
+    a = _f64(ab_rows)
+    m = a.shape[0]
+    assert a.shape[1] == kl + ku + 1
+    x = _f64(x)
+    y = np.empty(m)
+    _load().ora_gbmv(m, kl, ku, _ptr(a), _ptr(x), _ptr(y))
+    return y
+
+
+def p_restrict(r1) -> np.ndarray:
+    """DG1 -> DG0: r1 [ncol][6 nz] -> b0 [ncol][nz], the 6 nodal values summed."""
+    r1 = _f64(r1)
+    ncol, m = r1.shape
+    b0 = np.empty((ncol, m // 6))
+    _load().ora_p_restrict(ncol, m // 6, _ptr(r1), _ptr(b0))
+    return b0
+
+
+def p_prolong_add(u0, u1) -> np.ndarray:
+    """u1 + P u0: every nodal value of cell k gets the cell's DG0 value."""
+    u0, u1 = _f64(u0), _f64(u1).copy()
+    ncol, nz = u0.shape
+    _load().ora_p_prolong_add(ncol, nz, _ptr(u0), _ptr(u1))
+    return u1
