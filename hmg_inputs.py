@@ -67,3 +67,47 @@ def make_inputs(cfg: Config, seed: int | None = None, extra: int = 0):
 def uniform_vector(shape, seed: int) -> np.ndarray:
     """An extra seeded U(-1,1) vector (test vectors, not part of a config)."""
     return np.random.default_rng(seed).uniform(-1.0, 1.0, shape)
+
+
+# ---- NEXT-3 core inputs: batched banded column matrices ----------------------
+# The NLO column operator (P:1099-1106): m = 6 nz rows, kl = ku = 13.  Its
+# entries depend on the BDFM1 velocity mass the paper does not print (DESIGN.md
+# R21), so the banded solver is driven by seeded random band matrices of that
+# shape: entries U(-1, 1) inside the band (not diagonally dominant, so partial
+# pivoting really interchanges rows), zero outside and in the fill-in rows.
+NLO_CONFIGS = {
+    # name: (fine ref, layers) -> ncol = 20 * 4**ref columns, m = 6 * layers rows
+    "N0": (2, 8),     # tiny: 320 columns x 48 rows
+    "N1": (4, 64),    # the paper's NLO mesh (5,120 cells x 64 layers, P:838-839): m = 384
+    "N2": (6, 64),    # a B200-sized NLO problem: 81,920 columns x 384 rows = 31.5M DG1 dofs
+}
+
+
+def band_lu_storage(ncol: int, m: int, kl: int, ku: int, seed: int, ld: int | None = None) -> np.ndarray:
+    """Seeded band matrices in the batched LAPACK LU layout [m][2kl+ku+1][ld]
+    (A(i, j) at [j][kl+ku+i-j][c]; columns c >= ncol and entries outside the
+    band zero)."""
+    ld = ncol if ld is None else ld
+    ldab = 2 * kl + ku + 1
+    rng = np.random.default_rng(seed)
+    ab = np.zeros((m, ldab, ld))
+    ab[:, kl:, :ncol] = rng.uniform(-1.0, 1.0, (m, kl + ku + 1, ncol))
+    r = np.arange(kl, ldab)
+    j = np.arange(m)
+    i = j[:, None] + r[None, :] - (kl + ku)          # matrix row of each band slot
+    ab[:, kl:, :][(i < 0) | (i >= m)] = 0.0
+    return ab
+
+
+def band_row_storage(ncol: int, m: int, kl: int, ku: int, seed: int, ld: int | None = None) -> np.ndarray:
+    """Seeded band matrices in the paper's row-wise layout [m][kl+ku+1][ld]
+    (A(i, j) at [i][kl+j-i][c]; slots with j outside [0, m) zero)."""
+    ld = ncol if ld is None else ld
+    bw = kl + ku + 1
+    rng = np.random.default_rng(seed)
+    ar = np.zeros((m, bw, ld))
+    ar[:, :, :ncol] = rng.uniform(-1.0, 1.0, (m, bw, ncol))
+    i = np.arange(m)
+    j = i[:, None] + np.arange(bw)[None, :] - kl
+    ar[(j < 0) | (j >= m)] = 0.0
+    return ar

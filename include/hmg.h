@@ -317,6 +317,54 @@ hmg_status hmg_mixed_precond(const hmg_hierarchy* h, const hmg_mg_params* p, con
 hmg_status hmg_mixed_gmres(const hmg_hierarchy* h, const hmg_mg_params* p, const double* F, double* X, double rtol,
                            int restart, int maxit, int gs_passes, int* iters, double* relres, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * NEXT-3 core: batched per-column banded linear algebra of the
+ * next-to-lowest-order discretisation.  There the column operator H^_z of
+ * each vertical column is a banded matrix with m = 6 nz rows (DG1: 6 unknowns
+ * per prism cell, ordered cell by cell) and bandwidth n_BW = kl + ku + 1 = 27
+ * (P:1099-1106), inverted with a precomputed LU factorisation with partial
+ * pivoting (LAPACK dgbtrf) and its solve (dgbtrs); the first
+ * coarsening step is the p-coarsening DG1 -> DG0 by the natural embedding
+ * (P:645-648).  These calls need no hierarchy.  Results are those of LAPACK's
+ * algorithms in their operation order (oracle/band_oracle.c), every grid
+ * column independent.
+ *
+ * Batched layouts (device, fp64 unless noted; c = grid column, ld >= ncol a
+ * multiple of 32; pointers 16-byte aligned):
+ *   ab    [m][2 kl + ku + 1][ld]   LU storage, LAPACK band format per column:
+ *                                   A(i, j) at ab[(j*(2kl+ku+1) + kl+ku+i-j)*ld + c]
+ *                                   (rows 0..kl-1 of each j: room for U's fill-in)
+ *   ipiv  [m][ld] int32             0-based row interchanged with row j
+ *   ar    [m][kl + ku + 1][ld]      the paper's row-wise band storage of the
+ *                                   product kernel:
+ *                                   A(i, j) at ar[(i*(kl+ku+1) + kl+j-i)*ld + c]
+ *   vectors [m][ld]; a DG1 vector is [nz][6][ld], a DG0 one [nz][ld].
+ * Compiled (kl, ku) pairs: (13, 13) (the NLO operator), (1, 1) (the LO one),
+ * (2, 2), (3, 5), (5, 2), (0, 0); others -> HMG_ERR_INVALID_ARG.  m <= 4096. */
+
+/* In-place LU factorisation of every column (dgbtrf; setup, synchronous).  On
+ * an exactly zero pivot the factorisation is completed (as LAPACK's info > 0)
+ * and HMG_ERR_SINGULAR_COLUMN names the first such grid column; *singular
+ * (may be NULL) receives it, or -1. */
+hmg_status hmg_band_factor(int64_t ncol, int m, int kl, int ku, double* ab, int64_t ld, int32_t* ipiv,
+                           int64_t* singular, void* stream);
+/* x = A^-1 b per column from hmg_band_factor's output (dgbtrs, 'N').  b, x
+ * must not alias.  Useful bytes per column (Eq. 15):
+ * 4 m (3 n_BW + 4). */
+hmg_status hmg_band_solve(int64_t ncol, int m, int kl, int ku, const double* ab, int64_t ld,
+                          const int32_t* ipiv, const double* b, double* x, void* stream);
+/* y = A x per column, A in the row-wise storage ar (Eq. 14's 8 m (n_BW + 2)
+ * bytes per column).  y(i) = sum over j in increasing order. */
+hmg_status hmg_band_apply(int64_t ncol, int m, int kl, int ku, const double* ar, int64_t ld, const double* x,
+                          double* y, void* stream);
+/* DG1 -> DG0 restriction (transpose of the natural embedding; reading R21):
+ * b0[k][c] = sum_{d=0..5} r1[6k+d][c], summed in d order.  r1 [6 nz][ld],
+ * b0 [nz][ld]. */
+hmg_status hmg_p_restrict(int64_t ncol, int nz, const double* r1, int64_t ld, double* b0, void* stream);
+/* DG0 -> DG1 prolongation-add (natural embedding: a cell constant has every
+ * nodal DG1 value equal to it): u1[6k+d][c] += u0[k][c]. */
+hmg_status hmg_p_prolong_add(int64_t ncol, int nz, const double* u0, int64_t ld, double* u1, void* stream);
+
 /* Message for the last error on this thread ("" if none). */
 const char* hmg_last_error(void);
 

@@ -6,8 +6,8 @@ of ``include/hmg.h``; this package is a thin ctypes binding (argument
 marshalling only).  There is no CPU fallback: importing works without a GPU,
 but every call that computes needs the CUDA library and a device.
 """
-from .binding import (HmgError, Hierarchy, MGParams, STATUS, lib_path, load_library, nccl_unique_id,
-                      partition_plan)
+from .binding import (HmgError, Hierarchy, MGParams, STATUS, band_apply, band_factor, band_solve, lib_path,
+                      load_library, nccl_unique_id, p_prolong_add, p_restrict, partition_plan)
 
-__all__ = ["HmgError", "Hierarchy", "MGParams", "STATUS", "lib_path", "load_library", "nccl_unique_id",
-           "partition_plan"]
+__all__ = ["HmgError", "Hierarchy", "MGParams", "STATUS", "band_apply", "band_factor", "band_solve", "lib_path",
+           "load_library", "nccl_unique_id", "p_prolong_add", "p_restrict", "partition_plan"]

@@ -94,6 +94,11 @@ def load_library():
         "hmg_mixed_apply": [P, P, P, P],
         "hmg_mixed_precond": [P, pP, P, P, P],
         "hmg_mixed_gmres": [P, pP, P, P, D, I, I, I, pI, pD, P],
+        "hmg_band_factor": [I64, I, I, I, P, I64, P, pI64, P],
+        "hmg_band_solve": [I64, I, I, I, P, I64, P, P, P, P],
+        "hmg_band_apply": [I64, I, I, I, P, I64, P, P, P],
+        "hmg_p_restrict": [I64, I, P, I64, P, P],
+        "hmg_p_prolong_add": [I64, I, P, I64, P, P],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -123,6 +128,61 @@ def _dptr(t, name: str):
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or not t.is_contiguous():
         raise TypeError(f"{name}: expected a contiguous float64 CUDA tensor")
     return ctypes.c_void_p(t.data_ptr())
+
+
+def _tptr(t, name: str, dtype_name: str):
+    import torch
+    dt = {"float64": torch.float64, "int32": torch.int32}[dtype_name]
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != dt or not t.is_contiguous():
+        raise TypeError(f"{name}: expected a contiguous {dtype_name} CUDA tensor")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+# ---- NEXT-3 core: batched per-column banded algebra (include/hmg.h hmg_band_*) ----
+def band_factor(ab, ipiv, ncol: int, kl: int, ku: int) -> int:
+    """In-place LU (dgbtrf) of every column: ab [m][2kl+ku+1][ld] float64,
+    ipiv [m][ld] int32 (CUDA tensors).  Raises HmgError (HMG_ERR_SINGULAR_COLUMN)
+    naming the first column with a zero pivot (the factorisation is completed)."""
+    m, ldab, ld = ab.shape
+    assert ldab == 2 * kl + ku + 1 and tuple(ipiv.shape) == (m, ld)
+    sing = ctypes.c_int64(-1)
+    _check(load_library().hmg_band_factor(ncol, m, kl, ku, _tptr(ab, "ab", "float64"), ld,
+                                          _tptr(ipiv, "ipiv", "int32"), ctypes.byref(sing), _stream()))
+    return sing.value
+
+
+def band_solve(ab, ipiv, b, x, ncol: int, kl: int, ku: int):
+    """x = A^-1 b per column (dgbtrs) from band_factor's output; b, x [m][ld]."""
+    m, ldab, ld = ab.shape
+    _check(load_library().hmg_band_solve(ncol, m, kl, ku, _tptr(ab, "ab", "float64"), ld,
+                                         _tptr(ipiv, "ipiv", "int32"), _tptr(b, "b", "float64"),
+                                         _tptr(x, "x", "float64"), _stream()))
+    return x
+
+
+def band_apply(ar, x, y, ncol: int, kl: int, ku: int):
+    """y = A x per column, ar [m][kl+ku+1][ld] the paper's row-wise band storage."""
+    m, bw, ld = ar.shape
+    assert bw == kl + ku + 1
+    _check(load_library().hmg_band_apply(ncol, m, kl, ku, _tptr(ar, "ar", "float64"), ld,
+                                         _tptr(x, "x", "float64"), _tptr(y, "y", "float64"), _stream()))
+    return y
+
+
+def p_restrict(r1, b0, ncol: int):
+    """DG1 -> DG0: b0 [nz][ld] = sum of the 6 nodal values, r1 [6 nz][ld]."""
+    nz, ld = b0.shape
+    _check(load_library().hmg_p_restrict(ncol, nz, _tptr(r1, "r1", "float64"), ld, _tptr(b0, "b0", "float64"),
+                                         _stream()))
+    return b0
+
+
+def p_prolong_add(u0, u1, ncol: int):
+    """DG0 -> DG1: u1 [6 nz][ld] += the cell value on each of its 6 nodes."""
+    nz, ld = u0.shape
+    _check(load_library().hmg_p_prolong_add(ncol, nz, _tptr(u0, "u0", "float64"), ld, _tptr(u1, "u1", "float64"),
+                                            _stream()))
+    return u1
 
 
 def nccl_unique_id() -> bytes:

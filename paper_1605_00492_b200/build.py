@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhmg.so")
 SOURCES = ["api.cu", "kernels.cu", "sweep_tc.cu", "sweep_st.cu", "apply_st.cu", "sweep_small.cu", "thomas_factor.cu",
-           "coarse_coop.cu", "mesh.cpp", "dist.cpp", "nccl_dyn.cpp", "mixed.cu"]
+           "coarse_coop.cu", "mesh.cpp", "dist.cpp", "nccl_dyn.cpp", "mixed.cu", "band.cu"]
 # test-only in-process collective transport (HMG_TRANSPORT=local), its own library
 TEST_SOURCES = ["local_transport.cu"]
 TEST_LIB = os.path.join(HERE, "libhmg_localtx.so")

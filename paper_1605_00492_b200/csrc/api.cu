@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <new>
+#include <stdexcept>
 #include <type_traits>
 #include <string>
 
@@ -1533,6 +1534,110 @@ hmg_status hmg_mixed_gmres(const hmg_hierarchy* h, const hmg_mg_params* p, const
     if (gs_passes < 1 || gs_passes > 2) return fail(HMG_ERR_INVALID_ARG, "gs_passes: must be 1 (CGS) or 2 (CGS2)");
     HMG_TRY(ensure_mixed(H));
     return mixed_gmres_impl(H, p, F, X, rtol, restart, maxit, gs_passes, iters, relres, S(stream));
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-3 core: batched per-column banded algebra (band.cu; include/hmg.h)
+// ---------------------------------------------------------------------------
+static hmg_status check_band(int64_t ncol, int m, int kl, int ku, int64_t ld) {
+    if (ncol < 0) return fail(HMG_ERR_INVALID_ARG, "ncol: must be >= 0");
+    if (m < 1 || m > 4096) return fail(HMG_ERR_INVALID_ARG, "m: must be in [1, 4096]");
+    if (!band_shape_supported(kl, ku))
+        return fail(HMG_ERR_INVALID_ARG, "kl, ku: (" + std::to_string(kl) + ", " + std::to_string(ku) +
+                                             ") not compiled; supported: (13,13) (1,1) (2,2) (3,5) (5,2) (0,0)");
+    if (ld < ncol || ld % 32 != 0) return fail(HMG_ERR_INVALID_ARG, "ld: must be >= ncol and a multiple of 32");
+    if ((int64_t)m * (2 * kl + ku + 1) > (int64_t)1 << 31) return fail(HMG_ERR_INVALID_ARG, "m: band too large");
+    return HMG_OK;
+}
+
+hmg_status hmg_band_factor(int64_t ncol, int m, int kl, int ku, double* ab, int64_t ld, int32_t* ipiv,
+                           int64_t* singular, void* stream) {
+    g_err.clear();
+    HMG_TRY(check_band(ncol, m, kl, ku, ld));
+    HMG_TRY(check_ptr(ab, "ab"));
+    HMG_TRY(check_ptr(ipiv, "ipiv"));
+    if (singular) *singular = -1;
+    if (ncol == 0) return HMG_OK;
+    unsigned long long* bad = nullptr;
+    HMG_CUDA(cudaMalloc(&bad, sizeof(*bad)));
+    const unsigned long long none = ~0ull;
+    HMG_CUDA(cudaMemcpyAsync(bad, &none, sizeof(none), cudaMemcpyHostToDevice, S(stream)));
+    launch_band_factor(ncol, m, kl, ku, ab, ld, ipiv, bad, S(stream));
+    hmg_status st = check_launch();
+    unsigned long long got = none;
+    if (st == HMG_OK) {
+        cudaError_t e = cudaMemcpyAsync(&got, bad, sizeof(got), cudaMemcpyDeviceToHost, S(stream));
+        if (e == cudaSuccess) e = cudaStreamSynchronize(S(stream));
+        if (e != cudaSuccess) st = fail(HMG_ERR_CUDA, std::string("hmg_band_factor: ") + cudaGetErrorString(e));
+    }
+    cudaFree(bad);
+    if (st != HMG_OK) return st;
+    if (got != none) {
+        const int64_t col = (int64_t)(got >> 24), row = (int64_t)(got & ((1ull << 24) - 1));
+        if (singular) *singular = col;
+        return fail(HMG_ERR_SINGULAR_COLUMN, "singular column: column " + std::to_string(col) + " (U(" +
+                                                 std::to_string(row) + ", " + std::to_string(row) + ") = 0)");
+    }
+    return HMG_OK;
+}
+
+hmg_status hmg_band_solve(int64_t ncol, int m, int kl, int ku, const double* ab, int64_t ld, const int32_t* ipiv,
+                          const double* b, double* x, void* stream) {
+    g_err.clear();
+    HMG_TRY(check_band(ncol, m, kl, ku, ld));
+    HMG_TRY(check_ptr(ab, "ab"));
+    HMG_TRY(check_ptr(ipiv, "ipiv"));
+    HMG_TRY(check_ptr(b, "b"));
+    HMG_TRY(check_ptr(x, "x"));
+    if (b == x) return fail(HMG_ERR_INVALID_ARG, "x: must not alias b");
+    if (ncol == 0) return HMG_OK;
+    try {
+        launch_band_solve(ncol, m, kl, ku, ab, ld, ipiv, b, x, S(stream));
+    } catch (const std::exception& e) {
+        return fail(HMG_ERR_CUDA, std::string("hmg_band_solve: ") + e.what());
+    }
+    return check_launch();
+}
+
+hmg_status hmg_band_apply(int64_t ncol, int m, int kl, int ku, const double* ar, int64_t ld, const double* x, double* y,
+                          void* stream) {
+    g_err.clear();
+    HMG_TRY(check_band(ncol, m, kl, ku, ld));
+    HMG_TRY(check_ptr(ar, "ar"));
+    HMG_TRY(check_ptr(x, "x"));
+    HMG_TRY(check_ptr(y, "y"));
+    if (x == y) return fail(HMG_ERR_INVALID_ARG, "y: must not alias x");
+    if (ncol == 0) return HMG_OK;
+    try {
+        launch_band_apply(ncol, m, kl, ku, ar, ld, x, y, S(stream));
+    } catch (const std::exception& e) {
+        return fail(HMG_ERR_CUDA, std::string("hmg_band_apply: ") + e.what());
+    }
+    return check_launch();
+}
+
+hmg_status hmg_p_restrict(int64_t ncol, int nz, const double* r1, int64_t ld, double* b0, void* stream) {
+    g_err.clear();
+    if (ncol < 0) return fail(HMG_ERR_INVALID_ARG, "ncol: must be >= 0");
+    if (nz < 1 || nz > 65535) return fail(HMG_ERR_INVALID_ARG, "nz: must be in [1, 65535]");
+    if (ld < ncol) return fail(HMG_ERR_INVALID_ARG, "ld: must be >= ncol");
+    HMG_TRY(check_ptr(r1, "r1"));
+    HMG_TRY(check_ptr(b0, "b0"));
+    if (ncol == 0) return HMG_OK;
+    launch_p_restrict(ncol, nz, r1, ld, b0, S(stream));
+    return check_launch();
+}
+
+hmg_status hmg_p_prolong_add(int64_t ncol, int nz, const double* u0, int64_t ld, double* u1, void* stream) {
+    g_err.clear();
+    if (ncol < 0) return fail(HMG_ERR_INVALID_ARG, "ncol: must be >= 0");
+    if (nz < 1 || nz > 65535) return fail(HMG_ERR_INVALID_ARG, "nz: must be in [1, 65535]");
+    if (ld < ncol) return fail(HMG_ERR_INVALID_ARG, "ld: must be >= ncol");
+    HMG_TRY(check_ptr(u0, "u0"));
+    HMG_TRY(check_ptr(u1, "u1"));
+    if (ncol == 0) return HMG_OK;
+    launch_p_prolong_add(ncol, nz, u0, ld, u1, S(stream));
+    return check_launch();
 }
 
 }  // extern "C"

@@ -302,6 +302,17 @@ int launch_apply_pupdate_st(const Hierarchy& H, const DevLevel& L, const double*
                             double* q, cudaStream_t s);
 void finalize_parts(const Hierarchy& H, int nparts, int op, cudaStream_t s);
 
+// band.cu (NEXT-3 core: batched banded LU / solve / product, DG1 <-> DG0)
+bool band_shape_supported(int kl, int ku);
+void launch_band_factor(int64_t ncol, int m, int kl, int ku, double* ab, int64_t ld, int32_t* ipiv,
+                        unsigned long long* bad, cudaStream_t s);
+void launch_band_solve(int64_t ncol, int m, int kl, int ku, const double* ab, int64_t ld, const int32_t* ipiv,
+                       const double* b, double* x, cudaStream_t s);
+void launch_band_apply(int64_t ncol, int m, int kl, int ku, const double* ar, int64_t ld, const double* x, double* y,
+                       cudaStream_t s);
+void launch_p_restrict(int64_t ncol, int nz, const double* r1, int64_t ld, double* b0, cudaStream_t s);
+void launch_p_prolong_add(int64_t ncol, int nz, const double* u0, int64_t ld, double* u1, cudaStream_t s);
+
 // thomas_factor.cu
 void launch_factor(const Hierarchy& H, const DevLevel& L, cudaStream_t s);
 void launch_pivot_check(const Hierarchy& H, const DevLevel& L, unsigned int* gslow, cudaStream_t s);
