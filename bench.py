@@ -147,18 +147,42 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def oracle_sample(cfg, lam, b, threads: int, nv: int = 2):
-    """Bounded oracle sample: ``nv`` V(2,2) cycles of the oracle on the same
-    workload (the metric's unit of work: one V-cycle over every fine dof)."""
-    os.environ["OMP_NUM_THREADS"] = str(threads)
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_baseline(cfg, lam, b, cores: int) -> dict:
+    """The oracle as it stands on the host cores: the full PCG +
+    V(2,2) solve to 1e-8 on all cores (the metric's own unit: fine dofs x
+    V-cycles / solve time), and one V(2,2) cycle on ONE thread.  Bounded: about
+    10-30 s of CPU work at C2 size."""
     import oracle
     h = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam)
+    oracle.set_threads(cores)
     t0 = time.perf_counter()
-    for _ in range(nv):
-        h.vcycle(b, 2, 2, 20, 0.8)
-    dt = time.perf_counter() - t0
+    _, it, rel, hist, st = h.pcg(b, rtol=1e-8)
+    t_pcg = time.perf_counter() - t0
+    oracle.set_threads(1)
+    t0 = time.perf_counter()
+    h.vcycle(b, 2, 2, 20, 0.8)
+    t_one = time.perf_counter() - t0
+    oracle.set_threads(cores)
     h.close()
-    return cfg.ndofs * nv / dt, dt, nv
+    nv = it                      # V-cycles in the solve: 1 before the loop + 1 per non-final iteration
+    return {"value": cfg.ndofs * nv / t_pcg, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"one oracle PCG + V(2,2) solve of {cfg.name} to 1e-8 ({it} iterations, {nv} V-cycles, "
+                      f"{cfg.ndofs} dofs) on {cores} threads: {t_pcg:.2f} s",
+            "pcg_solve_s": t_pcg, "pcg_iterations": it, "residual_history": [float(v) for v in hist],
+            "single_thread": {"value": cfg.ndofs / t_one, "unit": UNIT, "cores": 1,
+                              "sample": f"one oracle V(2,2) cycle over {cfg.ndofs} dofs on 1 thread: {t_one:.2f} s"}}
 
 
 def run_reference(args, ws, rank):
@@ -327,6 +351,9 @@ def run_hmg(args, ws, rank, local):
             fine[k] = {"us": round(avg * 1e3, 2), "bytes_per_dof": bpd[k],
                        "GB/s": round(bpd[k] * dofs_local / (avg * 1e-3) / 1e9, 1)}
 
+    hist = [float(v) for v in h.pcg_history()]
+    levels = level_table(h, cfg, ws, bpd, r) if ws == 1 else None
+
     # ---- V-cycle alone -------------------------------------------------------
     z = h.empty(r)
     for _ in range(3):
@@ -384,7 +411,10 @@ def run_hmg(args, ws, rank, local):
         ms_m = e0.elapsed_time(e1)
         share = {k: round(h.profile_query(k, -1)[1] / ms_m, 4) for k in ("sweep", "sweep_zero", "sweep_prolong",
                                                                           "resid_restrict", "coarse_tail", "mixed")}
+        # the same solve with ONE Gram-Schmidt pass (CGS, PETSc's default; reading R20)
+        _, it_c, rr_c, st_c = h.mixed_gmres(Fd, Xd, rtol=1e-5, restart=30, maxit=300, params=params, gs_passes=1)
         mixed = {"solver": "right-preconditioned GMRES(30), CGS2, to ||r|| <= 1e-5 ||F||",
+                 "single_pass_cgs": {"gmres_iterations": it_c, "status": st_c, "final_relres": rr_c},
                  "preconditioner": "Schur complement (Eq. 6) with two-point lumped velocity mass + one V(2,2)",
                  "unknowns": unknowns, "gmres_iterations": it_m, "status": st_m, "final_relres": rr_m,
                  "solve_ms": ms_m, "ms_per_iteration": ms_m / max(it_m, 1),
@@ -407,6 +437,10 @@ def run_hmg(args, ws, rank, local):
                                      "cores": cores, "kind": "oracle",
                                      "sample": f"one oracle Schur preconditioner application (incl. one V(2,2)) + "
                                                f"one mixed apply over all {unknowns} unknowns: {dt:.2f} s"}
+
+    # ---- NEXT-3 core: the NLO column operator's banded LU solve (P:736-741,
+    # m = 384, n_BW = 27) on the B200-sized NLO problem N2 ----
+    nlo = nlo_section(args, stream, local) if ws == 1 else None
 
     # ---- end to end: host buffers through hmg_pcg_solve_host ----------------
     hb = torch.from_numpy(b).pin_memory()
@@ -440,10 +474,7 @@ def run_hmg(args, ws, rank, local):
     # ---- oracle on the host cores (rank 0, N = 1 only) -----------------------
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cores = len(os.sched_getaffinity(0))
-        v, dt, nvo = oracle_sample(cfg, lam, b, cores)
-        cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-               "sample": f"{nvo} oracle V(2,2) cycles over all {cfg.ndofs} dofs of {cfg.name}: {dt:.2f} s"}
+        cpu = oracle_baseline(cfg, lam, b, len(os.sched_getaffinity(0)))
 
     if rank == 0:
         out = {
@@ -475,10 +506,13 @@ def run_hmg(args, ws, rank, local):
                          "algorithmic_bytes_per_launch": bytes_sw, "avg_launch_us": avg_sw * 1e3,
                          "launches_timed": n_sw, "peak_source": peak_note},
             "fine_level_kernels": fine,
+            "pcg_residual_history": hist,
+            "multigrid_breakdown": levels,
             "time_share": shares,
             "cpu_baseline": cpu,
             "single_level_comparison": sl,
             "next4_mixed_outer_solve": mixed,
+            "next3_banded_column_solve": nlo,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(8 * cfg.nz * n * ws),
                     "d2h_bytes_per_step": int(8 * cfg.nz * n * ws), "ms_per_step": ms_e2e,
                     "api": "hmg_pcg_solve_host_batch (copies of neighbouring steps overlap the solve)",
@@ -491,6 +525,172 @@ def run_hmg(args, ws, rank, local):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def level_table(h, cfg, ws, bpd_fine, fine_ref) -> dict:
+    """The paper's per-level breakdown (Tab. "MultigridBreakdown", P:1011-1038,
+    and "usefulBandwidth") for this build: per level, the time of
+    one operator application H^ (H^_h + H^_z fused), of one H^_z^-1 (the
+    zero-guess sweep, omega T^-1 b: the Thomas solve alone), of one fused sweep
+    (residual + H^_z^-1 + update), each launched alone, with useful GB/s from
+    the byte model of the store the kernel reads; and the time each level takes
+    inside one V(2,2) cycle (all kernels recorded with that level; the levels
+    of the cooperative coarse kernel are reported together)."""
+    import torch
+    from paper_1605_00492_b200 import MGParams
+    peak, _ = measured_peak()
+    rows = []
+    reps = 20
+    for ref in range(fine_ref, cfg.coarsest_ref - 1, -1):
+        n_r, _ = h.level_info(ref)
+        dofs = n_r * cfg.nz
+        x = h.empty(ref)
+        x[:, :n_r] = torch.rand((cfg.nz, n_r), dtype=torch.float64, device=x.device) * 2 - 1
+        y, u = h.empty(ref), h.empty(ref)
+        for _ in range(2):
+            h.apply_helmholtz(ref, x, y)
+            h.line_smooth(ref, x, u, 1, 0.8, True)
+        torch.cuda.synchronize()
+        h.profile_select(None)
+        h.profile_begin()
+        for _ in range(reps):
+            h.apply_helmholtz(ref, x, y)
+        for _ in range(reps):
+            h.line_smooth(ref, x, u, 1, 0.8, True)
+        for _ in range(reps):
+            h.line_smooth(ref, x, u, 1, 0.8, False)
+        torch.cuda.synchronize()
+        h.profile_end()
+        row = {"ref": ref, "cells": n_r, "dofs": dofs}
+        es = h.edge_store(ref)
+        for key, cls, bpd in (("H", "apply", 44.0 if es["apply"] else 56.0),
+                              ("Hz_inv", "sweep_zero", 32.0),
+                              ("sweep", "sweep", 52.0 if es["sweep"] else 64.0)):
+            nk, ms = h.profile_query(cls, ref)
+            if nk:
+                us = ms * 1e3 / nk
+                gbs = bpd * dofs / (us * 1e-6) / 1e9
+                row[key] = {"us": round(us, 2), "bytes_per_dof": bpd, "GB/s": round(gbs, 1),
+                            "frac": round(gbs / peak, 3)}
+        rows.append(row)
+    # time per level inside one V-cycle
+    bd = h.empty(fine_ref)
+    bd[:, :cfg.n // ws] = torch.rand((cfg.nz, cfg.n // ws), dtype=torch.float64, device=bd.device) * 2 - 1
+    z = h.empty(fine_ref)
+    h.vcycle(bd, z, MGParams())
+    torch.cuda.synchronize()
+    h.profile_select(None)
+    h.profile_begin()
+    nvc = 5
+    for _ in range(nvc):
+        h.vcycle(bd, z, MGParams())
+    torch.cuda.synchronize()
+    h.profile_end()
+    in_cycle = {}
+    for ref in range(fine_ref, cfg.coarsest_ref - 1, -1):
+        tot = 0.0
+        for cls in ("sweep", "sweep_zero", "sweep_prolong", "apply", "resid_restrict", "restrict", "prolong",
+                    "coarse_tail"):
+            tot += h.profile_query(cls, ref)[1]
+        if tot > 0:
+            in_cycle[str(ref)] = round(tot * 1e3 / nvc, 2)
+    return {"per_level_single_launch": rows, "vcycle_us_per_level": in_cycle,
+            "note": "H = fused H^_h + H^_z apply; Hz_inv = zero-guess sweep (Thomas solve only); sweep = fused "
+                    "residual + Thomas + update; vcycle_us_per_level: the cooperative coarse kernel's levels are "
+                    "listed under its top level"}
+
+
+def nlo_section(args, stream, local):
+    """NEXT-3 core at the N2 size (81,920 columns x m = 384 rows, kl = ku = 13):
+    the batched LU factorisation (setup, timed once), the dgbtrs solve and the
+    paper's banded product (timed per launch with CUDA events on the launching
+    stream; inputs of 10.1 / 6.8 GB, far beyond L2), the DG1 <-> DG0 transfers,
+    with the paper's useful-byte models: Eq. 15, 4 m (3 n_BW + 4) B per column
+    for the solve; Eq. 14, 8 m (n_BW + 2) for the product.  Matrices: seeded
+    U(-1, 1) inside the band (reading R21: the BDFM1 operator is not built)."""
+    import torch
+    from paper_1605_00492_b200 import band_apply, band_factor, band_solve, p_prolong_add, p_restrict
+
+    ref, nz = hi.NLO_CONFIGS["N2"]
+    ncol, m, kl, ku = 20 * 4 ** ref, 6 * nz, 13, 13
+    nbw = kl + ku + 1
+    ld = (ncol + 31) // 32 * 32
+    dev = f"cuda:{local}"
+    g = torch.Generator(device=dev)
+    g.manual_seed(2)
+    ldab = 2 * kl + ku + 1
+    ab = torch.zeros((m, ldab, ld), dtype=torch.float64, device=dev)
+    ab[:, kl:, :ncol] = torch.rand((m, kl + ku + 1, ncol), generator=g, dtype=torch.float64, device=dev) * 2 - 1
+    jj = torch.arange(m, device=dev)[:, None]
+    rr = torch.arange(kl, ldab, device=dev)[None, :]
+    ab[:, kl:, :][(jj + rr - (kl + ku) < 0) | (jj + rr - (kl + ku) >= m)] = 0.0
+    ipiv = torch.zeros((m, ld), dtype=torch.int32, device=dev)
+    b = torch.rand((m, ld), generator=g, dtype=torch.float64, device=dev) * 2 - 1
+    x = torch.zeros_like(b)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    band_factor(ab, ipiv, ncol, kl, ku)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    factor_ms = e0.elapsed_time(e1)
+    peak, peak_note = measured_peak()
+
+    def timed(fn, reps):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for a0, a1 in evs:
+            a0.record(stream)
+            fn()
+            a1.record(stream)
+        torch.cuda.synchronize()
+        return float(np.mean([a0.elapsed_time(a1) for a0, a1 in evs]))
+
+    reps = max(10, min(args.steps, 30))
+    solve_ms = timed(lambda: band_solve(ab, ipiv, b, x, ncol, kl, ku), reps)
+    solve_bytes = ncol * 4 * m * (3 * nbw + 4)
+    del ab, ipiv
+    ar = torch.rand((m, nbw, ld), generator=g, dtype=torch.float64, device=dev) * 2 - 1
+    y = torch.zeros_like(b)
+    apply_ms = timed(lambda: band_apply(ar, b, y, ncol, kl, ku), reps)
+    apply_bytes = ncol * 8 * m * (nbw + 2)
+    del ar
+    b0 = torch.zeros((nz, ld), dtype=torch.float64, device=dev)
+    restr_ms = timed(lambda: p_restrict(b, b0, ncol), reps)
+    prol_ms = timed(lambda: p_prolong_add(b0, y, ncol), reps)
+    gbs = solve_bytes / (solve_ms * 1e-3) / 1e9
+    out = {"workload": f"N2: {ncol} columns x m = {m} rows (ref {ref}, {nz} layers x 6 DG1 dofs), kl = ku = {kl}, "
+                       f"n_BW = {nbw}; seeded U(-1, 1) band matrices",
+           "factor_ms": factor_ms,
+           "solve": {"us": solve_ms * 1e3, "bytes_per_column": 4 * m * (3 * nbw + 4), "GB/s": gbs,
+                     "dofs_per_s": ncol * m / (solve_ms * 1e-3)},
+           "apply": {"us": apply_ms * 1e3, "bytes_per_column": 8 * m * (nbw + 2),
+                     "GB/s": apply_bytes / (apply_ms * 1e-3) / 1e9},
+           "p_restrict_us": restr_ms * 1e3, "p_prolong_us": prol_ms * 1e3,
+           "roofline": {"kernel": "k_gbtrs<13, 13> (dgbtrs per column, Eq. 15 bytes)", "bound": "hbm",
+                        "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak, "peak_source": peak_note},
+           "paper_context": "ARCHER NLO finest level: H^_z^-1 12.36 GB/s, H^_z 45.92 GB/s (P:1166)"}
+    del b, x, y, b0
+    torch.cuda.empty_cache()
+    if not args.no_cpu_baseline:
+        # the oracle beside it: dgbtrs on a bounded sample of columns, one thread
+        import oracle
+        rng = np.random.default_rng(0)
+        nsample = 400
+        t_cpu = 0.0
+        for c in range(nsample):
+            abc = hi.band_lu_storage(1, m, kl, ku, seed=1000 + c)[:, :, 0].T.copy()
+            lu, ip, _ = oracle.gbtrf(abc, kl, ku)
+            bc = rng.uniform(-1, 1, m)
+            t0 = time.perf_counter()
+            oracle.gbtrs(lu, kl, ku, ip, bc)
+            t_cpu += time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": nsample * m / t_cpu, "unit": "dofs/s (solve)", "cores": 1, "kind": "oracle",
+                               "sample": f"oracle dgbtrs of {nsample} columns (m = {m}, kl = ku = {kl}), one thread, "
+                                         f"{t_cpu:.3f} s incl. ctypes call overhead"}
+    return out
 
 
 def run_c1(args):

@@ -213,6 +213,13 @@ hmg_status hmg_pcg_solve_host_batch(const hmg_hierarchy* h, const hmg_mg_params*
                                     const double* const* b_host, double* const* x_host, double rtol,
                                     int maxit, int* iters, double* relres, void* stream);
 
+/* Residual history of the last hmg_pcg_solve* call on this hierarchy (host,
+ * no synchronisation): hist[k] = ||r_k||_2 / ||b||_2 for k = 0 .. iters (the
+ * recursively updated residual the stopping test reads; hist[0] = 1, or 0 for
+ * b = 0).  *n receives iters + 1; at most cap values are written (hist may be
+ * NULL to query n). */
+hmg_status hmg_pcg_history(const hmg_hierarchy* h, double* hist, int cap, int* n);
+
 /* Same as hmg_pcg_solve but preconditioned by `nsweeps` line-Jacobi sweeps
  * from zero on the finest level: the paper's single-level method
  * ("two iterations of Block-Jacobi vertical line relaxation"). */

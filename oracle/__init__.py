@@ -88,6 +88,8 @@ def _load():
                                             ctypes.c_int, P, P, ctypes.POINTER(ctypes.c_int),
                                             ctypes.POINTER(ctypes.c_double), P, ctypes.POINTER(ctypes.c_double)]
             lib.ora_last_error.restype = ctypes.c_char_p
+            lib.ora_set_threads.argtypes = [ctypes.c_int]
+            lib.ora_set_threads.restype = None
             # NEXT-3 core (band_oracle.c)
             lib.ora_gbtrf.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P]
             lib.ora_gbtrs.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.c_int, P, P, P]
@@ -100,6 +102,11 @@ def _load():
             lib.ora_p_prolong_add.restype = None
             _lib = lib
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """OpenMP threads of the oracle's column loops (results are independent of it)."""
+    _load().ora_set_threads(int(n))
 
 
 class OracleError(RuntimeError):

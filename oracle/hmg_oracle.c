@@ -33,6 +33,7 @@
  *                     against dense least squares, Eq. 6 factorisation
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -1121,3 +1122,6 @@ out:
     if (st == ORA_ERR_NOT_CONVERGED) snprintf(ora_msg, sizeof ora_msg, "GMRES not converged after %d iterations", maxit);
     return st;
 }
+
+/* Thread count of the OpenMP column loops (results do not depend on it). */
+void ora_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }

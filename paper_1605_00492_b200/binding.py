@@ -94,6 +94,7 @@ def load_library():
         "hmg_mixed_apply": [P, P, P, P],
         "hmg_mixed_precond": [P, pP, P, P, P],
         "hmg_mixed_gmres": [P, pP, P, P, D, I, I, I, pI, pD, P],
+        "hmg_pcg_history": [P, P, I, pI],
         "hmg_band_factor": [I64, I, I, I, P, I64, P, pI64, P],
         "hmg_band_solve": [I64, I, I, I, P, I64, P, P, P, P],
         "hmg_band_apply": [I64, I, I, I, P, I64, P, P, P],
@@ -335,6 +336,15 @@ class Hierarchy:
                                                    maxit, ctypes.byref(it), ctypes.byref(rr), _stream()),
                       allow=(5,))
         return x, it.value, rr.value, STATUS[code]
+
+    def pcg_history(self) -> np.ndarray:
+        """||r_k|| / ||b||, k = 0 .. iters, of the last PCG solve (hmg_pcg_history)."""
+        n = ctypes.c_int(0)
+        _check(load_library().hmg_pcg_history(self._h, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value)
+        _check(load_library().hmg_pcg_history(self._h, out.ctypes.data_as(ctypes.c_void_p), n.value,
+                                              ctypes.byref(n)))
+        return out
 
     def pcg_solve_single_level(self, b, x=None, nsweeps: int = 2, omega: float = 0.8, rtol: float = 1e-8,
                                maxit: int = 500):

@@ -333,6 +333,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     HMG_TRY(check_launch());
     HMG_CUDA(cudaStreamSynchronize(s));
     const double bn = std::sqrt(H.scal_host->bb);
+    H.res_hist.assign(1, bn == 0.0 ? 0.0 : 1.0);
     if (bn == 0.0 || maxit == 0) {            // x = x0 = 0 (and r = b: relres 1 when b != 0)
         HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
         if (bn == 0.0) return HMG_OK;
@@ -416,6 +417,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         const double rn = std::sqrt(H.scal_host->rr);
         *iters = it;
         *relres = rn / bn;
+        H.res_hist.push_back(rn / bn);
         if (rn <= rtol * bn) {
             flush_pending_x(H, s, false);          // the last x update, in stream order
             HMG_TRY(check_launch());
@@ -1356,6 +1358,17 @@ hmg_status hmg_pcg_solve_host_batch(const hmg_hierarchy* h, const hmg_mg_params*
     HMG_CUDA(cudaStreamWaitEvent(s, H.ev_out[(nrhs - 1) & 1], 0));
     g_err = msg;
     return worst;
+}
+
+hmg_status hmg_pcg_history(const hmg_hierarchy* h, double* hist, int cap, int* n) {
+    HMG_TRY(check_h(h));
+    HMG_TRY(check_out(n, "n"));
+    if (cap < 0) return fail(HMG_ERR_INVALID_ARG, "cap: must be >= 0");
+    const std::vector<double>& v = HH(h).res_hist;
+    *n = (int)v.size();
+    if (hist)
+        for (int i = 0; i < cap && i < (int)v.size(); ++i) hist[i] = v[i];
+    return HMG_OK;
 }
 
 hmg_status hmg_export_level(const hmg_hierarchy* h, int ref, int32_t* nbr, double* geom, double* bands, double* lam) {

@@ -171,6 +171,7 @@ struct MixedSystem {
 
 struct Hierarchy {
     mutable MixedSystem* mix = nullptr;
+    mutable std::vector<double> res_hist;   // ||r_k|| / ||b|| of the last PCG solve, k = 0 .. iters
     int device = 0;
     int fine_ref = 0, coarsest_ref = 0, nz = 0;
     double thickness = 0, w2 = 0, dz = 0;

@@ -130,6 +130,11 @@ def test_pcg_iterations(pair):
     assert it == it_o, f"iterations {it} vs oracle {it_o} (oracle history tail {hist[-3:]})"
     assert rr <= 1e-8
     assert rel(g.to_host(cfg.fine_ref, x), xo) <= 1e-6
+    # residual history (P:913-919 reports convergence histories): the same
+    # recursively updated ||r_k|| / ||b|| up to the dots' summation order
+    h = g.pcg_history()
+    assert len(h) == it + 1 and h[0] == 1.0 and h[-1] == rr
+    assert np.allclose(h, hist, rtol=1e-5, atol=1e-14)
 
 
 def test_single_level_pcg(pair):
