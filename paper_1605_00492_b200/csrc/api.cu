@@ -497,23 +497,15 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     H->rank = rank;
     H->nranks = nranks;
     H->gather_ref = dist ? gather_ref : -1;
+    // Test knobs (the only environment switches; tests/ use each one): route a
+    // one-rank hierarchy through every collective, the matrix-free operator
+    // (NEXT-2), the deferred CG x update and its CTA count, the threshold of
+    // the edge-deduplicated coupling store, and HMG_COOP_REF below.
     if (const char* e = std::getenv("HMG_FORCE_COLLECTIVES")) H->force_coll = dist && std::string(e) == "1";
-    if (const char* e = std::getenv("HMG_SWEEP")) H->use_tc_sweep = std::string(e) != "simple";
-    if (const char* e = std::getenv("HMG_SMALL")) H->use_small_sweep = std::string(e) != "0";
-    if (const char* e = std::getenv("HMG_SWEEP_ST")) H->use_st_sweep = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_OPERATOR")) H->matrix_free = std::string(e) == "free";
-    if (const char* e = std::getenv("HMG_APPLY_ST")) H->use_st_apply = std::string(e) != "0";
-    if (const char* e = std::getenv("HMG_PDL")) H->use_pdl = std::string(e) != "0";
-    if (const char* e = std::getenv("HMG_FUSE_RZ")) H->fuse_rz = std::string(e) != "0";
-    if (const char* e = std::getenv("HMG_FACT_MAX")) H->fact_max_cells = std::atoll(e);
-    if (const char* e = std::getenv("HMG_CHECK_SKIP")) H->check_skip = std::string(e) != "0";
-    if (const char* e = std::getenv("HMG_L2PF")) H->l2_prefetch_groups = std::atoi(e);
     if (const char* e = std::getenv("HMG_DEFER_X")) H->defer_x = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_X_BLOCKS")) H->x_slow_blocks = std::atoi(e);
-    if (const char* e = std::getenv("HMG_EDGE_H")) H->edge_h = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_EDGE_MIN_DOFS")) H->edge_min_dofs = std::atoll(e);
-    if (const char* e = std::getenv("HMG_RESID_ST")) H->resid_st = std::string(e) != "0";
-    if (const char* e = std::getenv("HMG_APPLY_CTAS")) H->apply_ctas_per_sm = std::atoi(e);
     {
         // Cooperative coarse tail (coarse_coop.cu): by default every level of at
         // most kCoopMaxCells cells runs in one cooperative launch -- those levels

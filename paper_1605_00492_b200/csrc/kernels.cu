@@ -569,11 +569,6 @@ inline unsigned blocks(int64_t n, int b) { return (unsigned)((n + b - 1) / b); }
 // fill the GPU; on small (coarse) levels split the layers so that the
 // sequential per-thread loop is short (these levels are latency-bound).
 unsigned vchunks(int64_t n, int nz) {
-    static const int forced = [] {
-        const char* e = std::getenv("HMG_VCHUNK_LAYERS");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (forced > 0) return (unsigned)((nz + forced - 1) / forced);
     const int64_t target = 148LL * 1024;
     int64_t c = (target + n - 1) / n;
     if (c > nz / 4) c = nz / 4;

@@ -566,8 +566,6 @@ void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const dou
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
     unsigned cap = Z ? (unsigned)((cols <= 256 && grid > (unsigned)sms) ? 2 * sms : sms) : grid;
-    if (const char* e = std::getenv("HMG_TC_PERSIST"))
-        if (std::string(e) == "0") cap = grid;
     launch_pdl(H, k_sweep_tc<Z, P, F, G, CK>, dim3(grid < cap ? grid : cap), dim3(kThreads), smem, s, maps, V, L.halo, b,
                uin, uc, ldc, L.fden, L.fg, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups);
 }
