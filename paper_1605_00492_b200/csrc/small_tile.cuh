@@ -164,6 +164,33 @@ __device__ __forceinline__ void tile_sweep(const TileSmem& S, int nz, int j, int
     __syncwarp();
 }
 
+// Back substitution of one 8-layer batch (top layer k1): delta_k = z_k - g_k
+// delta_{k+1} (delta_{nz-1} = z_{nz-1}; TOP: the batch holding nz - 1 and the
+// padding rows, the only one that needs the select), u' = u + omega delta.
+template <int TW, bool TOP>
+__device__ __forceinline__ void tile_back_batch(const TileSmem& S, int nz, int j, int k1, bool zero, double omega,
+                                                double& dl) {
+    double zz[8], gg[8], uo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int q = (k1 - i) * TW + j;
+        zz[i] = S.z[q];
+        gg[i] = S.g[q];
+        uo[i] = S.u[q];
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int k = k1 - i;
+        if (TOP)
+            dl = (k >= nz - 1) ? zz[i] : zz[i] - gg[i] * dl;
+        else
+            dl = zz[i] - gg[i] * dl;
+        uo[i] = zero ? omega * dl : uo[i] + omega * dl;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) S.u[(k1 - i) * TW + j] = uo[i];
+}
+
 // The same sweep for a CTA of kTileWarps warps on one tile: the residual pass
 // (independent per layer; issue-bound for a single warp) is split over the
 // warps by 8-layer batches, then warp 0 alone runs the serial z recurrence and
@@ -256,25 +283,12 @@ __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int wa
             }
         }
         __syncwarp();
+        // back substitution: only the top batch (layer nz - 1 and the padding
+        // rows) needs the select; below it the chain is select-free (the select
+        // costs the single chain warp ~12 cycles per layer, tools/micro/chain4.cu)
         double dl = 0.0;
-        for (int k1 = nzp - 1; k1 >= 0; k1 -= 8) {
-            double zz[8], gg[8], uo[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int q = (k1 - i) * TW + j;
-                zz[i] = S.z[q];
-                gg[i] = S.g[q];
-                uo[i] = S.u[q];
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int k = k1 - i;
-                dl = (k >= nz - 1) ? zz[i] : zz[i] - gg[i] * dl;
-                uo[i] = zero ? omega * dl : uo[i] + omega * dl;
-            }
-#pragma unroll
-            for (int i = 0; i < 8; ++i) S.u[(k1 - i) * TW + j] = uo[i];
-        }
+        tile_back_batch<TW, true>(S, nz, j, nzp - 1, zero, omega, dl);
+        for (int k1 = nzp - 9; k1 >= 0; k1 -= 8) tile_back_batch<TW, false>(S, nz, j, k1, zero, omega, dl);
         TSTAMP(p3);
         TACC(2, p2, p3);
         if (blockIdx.x == 0 && threadIdx.x == 0) TACC(3, 0, 1);
