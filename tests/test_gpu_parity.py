@@ -379,6 +379,37 @@ def test_sweep_exact_division_fallback(ref, fine):
         assert np.array_equal(g.to_host(ref, u), o.sweep(ref, bb, None if zero else u0, 2, 0.8))
 
 
+@pytest.mark.parametrize("fine,nz,edge", [(5, 16, False), (6, 64, False), (5, 64, True)])
+def test_streamed_sweep_zero_residual_columns(monkeypatch, fine, nz, edge):
+    """Streamed sweep (ref >= 5) on columns whose residual is exactly zero
+    (b = H^ u0 computed by the oracle in the kernel's own operation order): the
+    z recurrence meets +0 / -0 numerators, which leave the shared-reciprocal
+    division's checked fast path, so the warp redoes its columns with '/' and
+    must match the oracle bit for bit; also with the fused prolongation inside a
+    V-cycle, the fused <r, z> of PCG and the edge-deduplicated coupling store."""
+    if edge:
+        monkeypatch.setenv("HMG_EDGE_MIN_DOFS", "1000000")
+    cfg = hi.Config("cert", fine, 0, nz, 0.001, 1e-5)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(fine, 0, nz, 0.001, 1e-5, lam)
+    o = oracle.Hierarchy(fine, 0, nz, 0.001, 1e-5, lam)
+    u0 = hi.uniform_vector(o.shape(fine), 81)
+    bb = hi.uniform_vector(o.shape(fine), 82)
+    hu = o.apply(fine, u0)
+    bb[:, 3::41] = hu[:, 3::41]                        # exactly zero residual in these columns
+    bb[:, 200] = hu[:, 200]
+    u = g.to_device(fine, u0)
+    g.line_smooth(fine, g.to_device(fine, bb), u, 1, 0.8, False)
+    assert np.array_equal(g.to_host(fine, u), o.sweep(fine, bb, u0, 1, 0.8))
+    # inside the V-cycle (fused prolongation) and PCG (fused <r, z>)
+    z = g.to_host(fine, g.vcycle(g.to_device(fine, bb)))
+    assert np.array_equal(z, o.vcycle(bb))
+    _, it, _, st = g.pcg_solve(g.to_device(fine, bb))
+    assert st == "HMG_OK" and it == o.pcg(bb)[1]
+    g.close()
+    o.close()
+
+
 @pytest.mark.parametrize("gather_ref", [2, 3, 5])
 @pytest.mark.parametrize("force", ["0", "1"])
 def test_distributed_path_one_rank(monkeypatch, gather_ref, force):
