@@ -1,0 +1,14 @@
+# round 2 measurement set: GPU suite, smoke, default bench, reference arm, C2a/C2c/C4/C1 lines,
+# ncu launch list of the bench command, ncu full capture of the fine-level kernels
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/f_build.log 2>&1; echo "build $?"
+timeout 2400 python -m pytest tests -m gpu -q --durations=15 > gpurun_out/f_pytest.log 2>&1; echo "pytest $?"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/f_smoke.log 2>&1; echo "smoke $?"
+timeout 1200 python bench.py > gpurun_out/f_bench.json 2> gpurun_out/f_bench.err; echo "bench $?"
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/f_ref.json 2> gpurun_out/f_ref.err; echo "ref $?"
+for c in C2a C2c; do timeout 600 python bench.py --config $c --steps 30 --no-cpu-baseline > gpurun_out/f_$c.json 2> gpurun_out/f_$c.err; echo "$c $?"; done
+timeout 900 python bench.py --config C4 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/f_C4.json 2> gpurun_out/f_C4.err; echo "C4 $?"
+timeout 300 python bench.py --config C1 --no-cpu-baseline > gpurun_out/f_C1.json 2> gpurun_out/f_C1.err; echo "C1 $?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2500 --csv --log-file gpurun_out/f_launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1; echo "ncu list $?"
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_sweep_st|k_sweep_tc|k_apply_st|k_coarse_coop" -s 60 -c 14 -o gpurun_out/f_kernels_full python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/f_ncu_full.log 2>&1; echo "ncu full $?"
