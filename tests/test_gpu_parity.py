@@ -145,6 +145,23 @@ def test_single_level_pcg(pair):
     assert st == "HMG_OK" and st_o == 0 and it == it_o
 
 
+def test_pcg_maxit_zero_and_zero_rhs(pair):
+    """maxit = 0: x = x0 = 0, relres 1, 0 iterations, HMG_ERR_NOT_CONVERGED
+    (outputs filled, include/hmg.h); b = 0: x = 0 in 0 iterations, HMG_OK; the
+    residual history reports only the start."""
+    cfg, g, o, lam, b = pair
+    r = cfg.fine_ref
+    x = g.to_device(r, np.full(o.shape(r), 7.0))
+    _, it, rr, st = g.pcg_solve(g.to_device(r, b), x, maxit=0)
+    assert st == "HMG_ERR_NOT_CONVERGED" and it == 0 and rr == 1.0
+    assert np.all(g.to_host(r, x) == 0.0)
+    assert list(g.pcg_history()) == [1.0]
+    x = g.to_device(r, np.full(o.shape(r), 7.0))
+    _, it, rr, st = g.pcg_solve(g.empty(r), x)
+    assert st == "HMG_OK" and it == 0 and rr == 0.0 and np.all(g.to_host(r, x) == 0.0)
+    assert list(g.pcg_history()) == [0.0]
+
+
 def test_host_entry_point(pair):
     cfg, g, o, lam, b = pair
     x, it, rr, st = g.pcg_solve_host(b)
