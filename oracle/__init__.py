@@ -55,6 +55,8 @@ def _load():
             i64p = ctypes.POINTER(ctypes.c_int64)
             lib.ora_build.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                       ctypes.c_double, P, ctypes.POINTER(P)]
+            lib.ora_build_ex.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                         ctypes.c_double, ctypes.c_double, P, ctypes.POINTER(P)]
             lib.ora_free.argtypes = [P]
             lib.ora_free.restype = None
             lib.ora_ncells.argtypes = [P, ctypes.c_int]
@@ -147,13 +149,16 @@ def thomas(D, U, r) -> np.ndarray:
 class Hierarchy:
     """Oracle hierarchy ref ``fine_ref`` -> ``coarsest_ref`` (O1-O4)."""
 
-    def __init__(self, fine_ref: int, coarsest_ref: int, nz: int, thickness: float, w2: float, lam):
+    def __init__(self, fine_ref: int, coarsest_ref: int, nz: int, thickness: float, w2: float, lam,
+                 omega_n: float = 0.0):
+        """omega_n: the buoyancy term omega_N = (dt/2) N of Eq. 5 (reading R24);
+        0 = BASELINE's operator."""
         lib = _load()
         self.fine_ref, self.coarsest_ref, self.nz = fine_ref, coarsest_ref, nz
-        self.thickness, self.w2 = thickness, w2
+        self.thickness, self.w2, self.omega_n = thickness, w2, omega_n
         lam = _f64(lam)
         h = ctypes.c_void_p()
-        _check(lib.ora_build(fine_ref, coarsest_ref, nz, thickness, w2, _ptr(lam), ctypes.byref(h)))
+        _check(lib.ora_build_ex(fine_ref, coarsest_ref, nz, thickness, w2, omega_n, _ptr(lam), ctypes.byref(h)))
         self._h = h
 
     def close(self):

@@ -236,6 +236,7 @@ typedef struct {
 typedef struct ora_h {
     int fine_ref, coarsest_ref, nz;
     double thickness, w2, dz;
+    double sn;          /* 1 + omega_N^2 (reading R24; 1 without buoyancy) */
     ora_level lev[16];  /* indexed by ref */
 } ora_h;
 
@@ -279,7 +280,9 @@ static void geometry(ora_level* L) {
 }
 
 /* O4 assembly (reading R4; Eq. 8 at P:598-606 with two-point lumped
- * couplings): vertical Vc = ((w2*area)*lamf)/dz, horizontal
+ * couplings): vertical Vc = (((w2*area)*lamf)/dz)/(1 + omega_N^2) (the
+ * buoyancy factor of Eq. 8, reading R24; exactly ((w2*area)*lamf)/dz for
+ * omega_N = 0), horizontal
  * Hc_j = (((w2*len_j)*dz)*lamf)/cd_j, face factor lamf = 0.5*(lam_a+lam_b)
  * (reading R3), diagonal = vol + couplings, u.n = 0 at top/bottom. */
 static void assemble(ora_h* h, ora_level* L) {
@@ -294,11 +297,11 @@ static void assemble(ora_h* h, ora_level* L) {
             double vc_dn = 0.0, vc_up = 0.0;
             if (k > 0) {
                 double lamf = 0.5 * (L->lam[(int64_t)(k - 1) * n + c] + lam_kc);
-                vc_dn = ((w2 * L->area[c]) * lamf) / dz;
+                vc_dn = (((w2 * L->area[c]) * lamf) / dz) / h->sn;
             }
             if (k < nz - 1) {
                 double lamf = 0.5 * (lam_kc + L->lam[(int64_t)(k + 1) * n + c]);
-                vc_up = ((w2 * L->area[c]) * lamf) / dz;
+                vc_up = (((w2 * L->area[c]) * lamf) / dz) / h->sn;
             }
             double hc[3];
             for (int j = 0; j < 3; j++) {
@@ -331,8 +334,17 @@ void ora_free(ora_h* h) {
     free(h);
 }
 
+int ora_build_ex(int fine_ref, int coarsest_ref, int nz, double thickness, double w2, double omega_n,
+                 const double* lam_fine, ora_h** out);
+
 int ora_build(int fine_ref, int coarsest_ref, int nz, double thickness, double w2,
               const double* lam_fine, ora_h** out) {
+    return ora_build_ex(fine_ref, coarsest_ref, nz, thickness, w2, 0.0, lam_fine, out);
+}
+
+/* omega_N = (dt/2) N, the buoyancy frequency term of Eq. 5. */
+int ora_build_ex(int fine_ref, int coarsest_ref, int nz, double thickness, double w2, double omega_n,
+                 const double* lam_fine, ora_h** out) {
     *out = NULL;
     if (fine_ref < 0 || fine_ref > 10) { snprintf(ora_msg, sizeof ora_msg, "fine_ref"); return ORA_ERR_ARG; }
     if (coarsest_ref < 0 || coarsest_ref > fine_ref) { snprintf(ora_msg, sizeof ora_msg, "coarsest_ref"); return ORA_ERR_ARG; }
@@ -340,10 +352,12 @@ int ora_build(int fine_ref, int coarsest_ref, int nz, double thickness, double w
     if (!(thickness > 0)) { snprintf(ora_msg, sizeof ora_msg, "thickness"); return ORA_ERR_ARG; }
     if (!(w2 >= 0)) { snprintf(ora_msg, sizeof ora_msg, "w2"); return ORA_ERR_ARG; }
     if (!lam_fine) { snprintf(ora_msg, sizeof ora_msg, "lam"); return ORA_ERR_ARG; }
+    if (!(omega_n >= 0) || !isfinite(omega_n)) { snprintf(ora_msg, sizeof ora_msg, "omega_n"); return ORA_ERR_ARG; }
     ora_h* h = (ora_h*)zalloc(sizeof(ora_h));
     if (!h) return ORA_ERR_OOM;
     h->fine_ref = fine_ref; h->coarsest_ref = coarsest_ref; h->nz = nz;
     h->thickness = thickness; h->w2 = w2;
+    h->sn = 1.0 + omega_n * omega_n;
     h->dz = thickness / nz;
     int st = base_mesh(&h->lev[0].mesh);
     if (st) { ora_free(h); return st; }
@@ -789,6 +803,8 @@ static void rt0_gram(const ora_level* L, int64_t c, double G[3][3]) {
 /*                        + U_z[k+1]) - U_z[k]   (absent U_z skipped)     */
 /*  divT:  (D^T P)_h[k][e] = P[k][a] - P[k][b];                           */
 /*         (D^T P)_z[i][c] = P[i-1][c] - P[i][c]                          */
+/*  (with buoyancy, reading R24: the vertical mass times 1 + omega_N^2    */
+/*   and its lumped inverse divided by it)                                 */
 /*  mass:  (M2 U)_h[k][e] = t_a/(dz lam_a) + t_b/(dz lam_b),              */
 /*         t_c = ((g0 U_h[E0] + g1 U_h[E1]) + g2 U_h[E2]),                */
 /*         g_l = (s_j s_l) G^c_{j l}, j = the slot of e in c;              */
@@ -860,7 +876,7 @@ static void mixed_mass(const ora_h* h, const ora_edges* E, const double* Uh, con
             double v = dg * Uz[(int64_t)(i - 1) * n + c];
             if (i - 1 >= 1) v = v + ((dz / 6.0) / slo) * Uz[(int64_t)(i - 2) * n + c];
             if (i + 1 <= nz - 1) v = v + ((dz / 6.0) / shi) * Uz[(int64_t)i * n + c];
-            yz[(int64_t)(i - 1) * n + c] = v;
+            yz[(int64_t)(i - 1) * n + c] = v * h->sn;   /* M~2z = (1 + omega_N^2) M2z (Eq. 5) */
         }
 }
 
@@ -881,7 +897,7 @@ static void mixed_lumped_inv(const ora_h* h, const ora_edges* E, const double* U
     for (int i = 1; i <= nz - 1; i++)
         for (int64_t c = 0; c < n; c++) {
             double lamf = 0.5 * (L->lam[(int64_t)(i - 1) * n + c] + L->lam[(int64_t)i * n + c]);
-            double il = (L->area[c] * lamf) / dz;
+            double il = ((L->area[c] * lamf) / dz) / h->sn;      /* the lumping of M~2z */
             yz[(int64_t)(i - 1) * n + c] = Uz[(int64_t)(i - 1) * n + c] * il;
         }
 }

@@ -292,3 +292,65 @@ def test_gmres_cgs_loses_orthogonality_cgs2_keeps_it():
         assert orth2 <= 1000 * EPS, (name, orth2)
         assert orth1 >= loss_cgs, (name, orth1)
         h.close()
+
+
+@pytest.mark.parametrize("omega_n", [0.5, 1.0, 3.0])
+def test_buoyancy_scales_the_vertical_terms(c0, omega_n):
+    """Reading R24 (Eq. 5; Eq. 8): with buoyancy eliminated,
+    M~2 = M2h (+) (1 + omega_N^2) M2z, so the vertical velocity mass is scaled by
+    1 + omega_N^2 -- exactly, the horizontal one untouched -- and the pressure
+    operator's vertical couplings are divided by it (exactly: the same quotient
+    divided once more), the horizontal ones and the pressure mass untouched."""
+    cfg, h0, lam, L0 = c0
+    sn = 1.0 + omega_n * omega_n
+    h = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, omega_n=omega_n)
+    for ref in range(cfg.coarsest_ref, cfg.fine_ref + 1):
+        A, B = h0.level(ref), h.level(ref)
+        assert np.array_equal(B["U"], A["U"] / sn)
+        assert np.array_equal(B["H"], A["H"])
+        # diagonal: volume + the scaled vertical + the horizontal couplings, in R4's order
+        nz, n = cfg.nz, A["area"].shape[0]
+        vol = A["area"] * (cfg.thickness / nz)
+        vup = -B["U"]
+        d = np.tile(vol, (nz, 1))
+        d[1:] = d[1:] + vup[:-1]
+        d[:-1] = d[:-1] + vup[:-1]
+        for j in range(3):
+            d = d - A["H"][j]
+        assert np.array_equal(B["D"], d)
+    _, N = h.mixed_sizes()
+    x = hi.uniform_vector(N, 91)
+    ne = h.mixed_sizes()[0]
+    Uh, Uz, P = h.mixed_split(x)
+    mh0, mz0 = h0.mixed_part("mass", Uh, Uz)
+    mh, mz = h.mixed_part("mass", Uh, Uz)
+    assert np.array_equal(mh, mh0) and np.array_equal(mz, mz0 * sn)
+    lh0, lz0 = h0.mixed_part("lumped_inv", Uh, Uz)
+    lh, lz = h.mixed_part("lumped_inv", Uh, Uz)
+    assert np.array_equal(lh, lh0)
+    assert np.max(np.abs(lz - lz0 / sn)) <= 2 * EPS * np.max(np.abs(lz0 / sn))
+    h.close()
+
+
+@pytest.mark.parametrize("omega_n", [0.5, 2.0])
+def test_buoyant_lumped_schur_complement_is_the_helmholtz_operator(c0, omega_n):
+    """With buoyancy the lumped Schur complement M3 + omega^2 D L~^-1 D^T of the
+    mixed system is the hierarchy's operator H^(omega_N) of Eq. 8 -- the two
+    are computed by different code (mixed system vs band assembly) -- and
+    GMRES(30) with the Schur preconditioner converges in a few iterations."""
+    cfg, h0, lam, L = c0
+    h = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, omega_n=omega_n)
+    nz, n = cfg.nz, L["nbr"].shape[0]
+    for seed in (4, 5):
+        P = _rand((nz, n), seed)
+        th, tz = h.mixed_part("divT", P=P)
+        lh, lz = h.mixed_part("lumped_inv", th, tz)
+        s = (L["area"] * h.thickness / nz)[None, :] * P + cfg.w2 * h.mixed_part("div", lh, lz)
+        ref = h.apply(cfg.fine_ref, P)
+        assert np.max(np.abs(s - ref)) <= 64 * EPS * np.max(np.abs(ref))
+    _, N = h.mixed_sizes()
+    F = hi.uniform_vector(N, 51)
+    x, it, rel, hist, st = h.mixed_gmres(F, rtol=1e-5)
+    assert st == 0 and it <= 30 and rel <= 1e-5
+    assert np.linalg.norm(F - h.mixed_apply(x)) / np.linalg.norm(F) == pytest.approx(rel, rel=1e-10)
+    h.close()
