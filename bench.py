@@ -419,6 +419,19 @@ def run_hmg(args, ws, rank, local):
                  "unknowns": unknowns, "gmres_iterations": it_m, "status": st_m, "final_relres": rr_m,
                  "solve_ms": ms_m, "ms_per_iteration": ms_m / max(it_m, 1),
                  "unknowns_per_s_per_iteration": unknowns * it_m / (ms_m * 1e-3), "time_share": share}
+        # with buoyancy (reading R24): omega_N = 1, i.e. the vertical velocity mass
+        # doubled and the pressure operator's vertical couplings halved
+        hb = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, device=local, omega_n=1.0)
+        hb.mixed_gmres(Fd, Xd, rtol=1e-5, restart=30, maxit=300, params=params)
+        barrier()
+        e0.record(stream)
+        _, it_b, rr_b, st_b = hb.mixed_gmres(Fd, Xd, rtol=1e-5, restart=30, maxit=300, params=params)
+        e1.record(stream)
+        barrier()
+        mixed["with_buoyancy"] = {"omega_N": 1.0, "gmres_iterations": it_b, "status": st_b, "final_relres": rr_b,
+                                  "solve_ms": e0.elapsed_time(e1)}
+        hb.close()
+        del hb
         del Fd, Xd
         if rank == 0 and not args.no_cpu_baseline:
             # the oracle beside it: one preconditioner application + mixed apply on the

@@ -114,6 +114,18 @@ hmg_status hmg_build_hierarchy_dist(int fine_ref, int coarsest_ref, int nlayers,
                                     double w2, const double* lam_host, int device,
                                     const hmg_dist* dist, hmg_hierarchy** out);
 
+/* As hmg_build_hierarchy / hmg_build_hierarchy_dist (dist = NULL: one GPU) with
+ * the buoyancy term omega_n = omega_N = (dt/2) N >= 0 of Eq. 5 (
+ * DESIGN.md reading R24): eliminating buoyancy scales the vertical velocity
+ * mass by 1 + omega_N^2, so the pressure operator's vertical couplings are
+ * divided by it (Eq. 8: ((w2*area)*lamf/dz) / (1 + omega_N^2)) and the mixed
+ * system (hmg_mixed_*) uses M~2 = M2h (+) (1 + omega_N^2) M2z and the matching
+ * lumped mass.  omega_n = 0 is exactly hmg_build_hierarchy.  The matrix-free
+ * operator (HMG_OPERATOR=free) supports omega_n = 0 only (HMG_ERR_INVALID_ARG). */
+hmg_status hmg_build_hierarchy_ex(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
+                                  double omega_n, const double* lam_host, int device, const hmg_dist* dist,
+                                  hmg_hierarchy** out);
+
 /* ncclGetUniqueId into id_out[128] (call on rank 0, broadcast the bytes). */
 hmg_status hmg_nccl_unique_id(unsigned char* id_out);
 

@@ -86,6 +86,7 @@ def load_library():
         "hmg_profile_select": [P, I, I],
         "hmg_profile_query": [P, I, I, pI64, pD],
         "hmg_build_hierarchy_dist": [I, I, I, D, D, P, I, P, ctypes.POINTER(P)],
+        "hmg_build_hierarchy_ex": [I, I, I, D, D, D, P, I, P, ctypes.POINTER(P)],
         "hmg_nccl_unique_id": [P],
         "hmg_partition_plan": [I, I, I, I, pI64, pI64, pI64, pI, pI64, P, P, P, P, P, P, P],
         "hmg_mixed_layout": [P, pI64, pI64, pI64, pI64, pI64],
@@ -230,10 +231,11 @@ class Hierarchy:
     """Device hierarchy ref ``fine_ref`` -> ``coarsest_ref`` (hmg_build_hierarchy)."""
 
     def __init__(self, fine_ref: int, coarsest_ref: int, nlayers: int, thickness: float, w2: float,
-                 lam, device: int = 0, dist=None):
+                 lam, device: int = 0, dist=None, omega_n: float = 0.0):
         """dist = (rank, nranks, nccl_id_bytes, gather_ref) for one rank of a
         distributed hierarchy; lam is then this rank's owned part of the finest
-        level when gather_ref < fine_ref."""
+        level when gather_ref < fine_ref.  omega_n: the buoyancy term of Eq. 5
+        (hmg_build_hierarchy_ex; 0 = BASELINE's operator)."""
         lib = load_library()
         lam = np.ascontiguousarray(np.asarray(lam, dtype=np.float64))
         n = 20 * 4 ** fine_ref if 0 <= fine_ref <= 10 else 0
@@ -242,20 +244,23 @@ class Hierarchy:
         if lam.size != nlayers * n:
             raise ValueError(f"lam: expected {nlayers} x {n} values, got shape {lam.shape}")
         h = ctypes.c_void_p()
-        if dist is None:
+        if dist is None and omega_n == 0.0:
             _check(lib.hmg_build_hierarchy(fine_ref, coarsest_ref, nlayers, thickness, w2,
                                            lam.ctypes.data_as(ctypes.c_void_p), device, ctypes.byref(h)))
+        elif dist is None:
+            _check(lib.hmg_build_hierarchy_ex(fine_ref, coarsest_ref, nlayers, thickness, w2, omega_n,
+                                              lam.ctypes.data_as(ctypes.c_void_p), device, None, ctypes.byref(h)))
         else:
             rank, nranks, nid, gref = dist
             self._nid = ctypes.create_string_buffer(bytes(nid), 128)
             d = _Dist(rank, nranks, ctypes.cast(self._nid, ctypes.c_void_p), gref)
-            _check(lib.hmg_build_hierarchy_dist(fine_ref, coarsest_ref, nlayers, thickness, w2,
-                                                lam.ctypes.data_as(ctypes.c_void_p), device, ctypes.byref(d),
-                                                ctypes.byref(h)))
+            _check(lib.hmg_build_hierarchy_ex(fine_ref, coarsest_ref, nlayers, thickness, w2, omega_n,
+                                              lam.ctypes.data_as(ctypes.c_void_p), device, ctypes.byref(d),
+                                              ctypes.byref(h)))
         self.dist = dist
         self._h = h
         self.fine_ref, self.coarsest_ref, self.nz = fine_ref, coarsest_ref, nlayers
-        self.thickness, self.w2, self.device = thickness, w2, device
+        self.thickness, self.w2, self.device, self.omega_n = thickness, w2, device, omega_n
 
     def close(self):
         if getattr(self, "_h", None):

@@ -440,7 +440,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
 // ---------------------------------------------------------------------------
 // Hierarchy construction (single GPU, or one rank of a distributed hierarchy).
 // ---------------------------------------------------------------------------
-hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
+hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2, double omega_n,
                       const double* lam_host, int device, const hmg_dist* dist, hmg_hierarchy** out) {
     g_err.clear();
     if (!out) return fail(HMG_ERR_INVALID_ARG, "out: null pointer");
@@ -453,6 +453,8 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
         return fail(HMG_ERR_INVALID_ARG, "nlayers: must be in [1, 256], got " + std::to_string(nlayers));
     if (!(thickness > 0) || !std::isfinite(thickness)) return fail(HMG_ERR_INVALID_ARG, "thickness: must be > 0 and finite");
     if (!(w2 >= 0) || !std::isfinite(w2)) return fail(HMG_ERR_INVALID_ARG, "w2: must be >= 0 and finite");
+    if (!(omega_n >= 0) || !std::isfinite(omega_n))
+        return fail(HMG_ERR_INVALID_ARG, "omega_n: must be >= 0 and finite");
     if (!lam_host) return fail(HMG_ERR_INVALID_ARG, "lam_host: null pointer");
     int rank = 0, nranks = 1, gather_ref = fine_ref;
     if (dist) {
@@ -494,6 +496,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     H->thickness = thickness;
     H->w2 = w2;
     H->dz = thickness / nlayers;
+    H->sn = 1.0 + omega_n * omega_n;
     H->rank = rank;
     H->nranks = nranks;
     H->gather_ref = dist ? gather_ref : -1;
@@ -503,6 +506,10 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
     // the edge-deduplicated coupling store, and HMG_COOP_REF below.
     if (const char* e = std::getenv("HMG_FORCE_COLLECTIVES")) H->force_coll = dist && std::string(e) == "1";
     if (const char* e = std::getenv("HMG_OPERATOR")) H->matrix_free = std::string(e) == "free";
+    if (H->matrix_free && H->sn != 1.0) {
+        delete H;
+        return fail(HMG_ERR_INVALID_ARG, "omega_n: the matrix-free operator (HMG_OPERATOR=free) needs omega_n = 0");
+    }
     if (const char* e = std::getenv("HMG_DEFER_X")) H->defer_x = std::string(e) != "0";
     if (const char* e = std::getenv("HMG_X_BLOCKS")) H->x_slow_blocks = std::atoi(e);
     if (const char* e = std::getenv("HMG_EDGE_MIN_DOFS")) H->edge_min_dofs = std::atoll(e);
@@ -1045,13 +1052,19 @@ const char* hmg_last_error(void) { return g_err.c_str(); }
 
 hmg_status hmg_build_hierarchy(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
                                const double* lam_host, int device, hmg_hierarchy** out) {
-    return build_impl(fine_ref, coarsest_ref, nlayers, thickness, w2, lam_host, device, nullptr, out);
+    return build_impl(fine_ref, coarsest_ref, nlayers, thickness, w2, 0.0, lam_host, device, nullptr, out);
+}
+
+hmg_status hmg_build_hierarchy_ex(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
+                                  double omega_n, const double* lam_host, int device, const hmg_dist* dist,
+                                  hmg_hierarchy** out) {
+    return build_impl(fine_ref, coarsest_ref, nlayers, thickness, w2, omega_n, lam_host, device, dist, out);
 }
 
 hmg_status hmg_build_hierarchy_dist(int fine_ref, int coarsest_ref, int nlayers, double thickness, double w2,
                                     const double* lam_host, int device, const hmg_dist* dist, hmg_hierarchy** out) {
     if (!dist) return fail(HMG_ERR_INVALID_ARG, "dist: null pointer");
-    return build_impl(fine_ref, coarsest_ref, nlayers, thickness, w2, lam_host, device, dist, out);
+    return build_impl(fine_ref, coarsest_ref, nlayers, thickness, w2, 0.0, lam_host, device, dist, out);
 }
 
 hmg_status hmg_nccl_unique_id(unsigned char* id_out) {

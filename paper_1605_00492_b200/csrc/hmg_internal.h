@@ -175,6 +175,7 @@ struct Hierarchy {
     int device = 0;
     int fine_ref = 0, coarsest_ref = 0, nz = 0;
     double thickness = 0, w2 = 0, dz = 0;
+    double sn = 1.0;            // 1 + omega_N^2: the buoyancy factor of Eq. 5 / Eq. 8 (reading R24)
     std::vector<DevLevel> lev;  // index = ref
     // PCG workspace on the finest level
     double *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *p2 = nullptr;

@@ -54,7 +54,7 @@ __global__ void k_coarsen_lam(const double* __restrict__ lf, int64_t ldf, double
 
 __global__ void k_assemble(int64_t n, int64_t ld, int nz, const int32_t* __restrict__ nbr,
                            const double* __restrict__ geom, const double* __restrict__ lam,
-                           double w2, double dz, double* __restrict__ bands) {
+                           double w2, double dz, double sn, double* __restrict__ bands) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int k = blockIdx.y;
     if (c >= n) return;
@@ -63,8 +63,9 @@ __global__ void k_assemble(int64_t n, int64_t ld, int nz, const int32_t* __restr
     const double vol = area * dz;
     const double lk = lam[i];
     double vdn = 0.0, vup = 0.0;
-    if (k > 0) vdn = ((w2 * area) * (0.5 * (lam[i - ld] + lk))) / dz;
-    if (k < nz - 1) vup = ((w2 * area) * (0.5 * (lk + lam[i + ld]))) / dz;
+    // vertical couplings divided by 1 + omega_N^2 (Eq. 8; reading R24; exact for sn = 1)
+    if (k > 0) vdn = (((w2 * area) * (0.5 * (lam[i - ld] + lk))) / dz) / sn;
+    if (k < nz - 1) vup = (((w2 * area) * (0.5 * (lk + lam[i + ld]))) / dz) / sn;
     double hc[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
@@ -662,7 +663,7 @@ void launch_edge_h(const Hierarchy& H, const DevLevel& L, int64_t nedges, cudaSt
 
 void launch_assemble(const Hierarchy& H, const DevLevel& L, cudaStream_t s) {
     dim3 g(blocks(L.n, 256), H.nz);
-    k_assemble<<<g, 256, 0, s>>>(L.n, L.ld, H.nz, L.nbr, L.geom, L.lam, H.w2, H.dz, L.bands);
+    k_assemble<<<g, 256, 0, s>>>(L.n, L.ld, H.nz, L.nbr, L.geom, L.lam, H.w2, H.dz, H.sn, L.bands);
     ++H.launches;
 }
 

@@ -42,6 +42,7 @@ struct MixView {
     int nz;
     int64_t n, ld, ne, ldh, off_z, off_p;
     double dz, om;
+    double sn;                          // 1 + omega_N^2 (reading R24)
     const int32_t* __restrict__ eca;    // [ldh] lower cell a
     const int32_t* __restrict__ ecb;    // [ldh] upper cell b
     const int32_t* __restrict__ ee;     // [6][ldh] edges of a's slots 0..2, then b's
@@ -66,6 +67,7 @@ MixView view(const Hierarchy& H) {
     v.off_p = M.off_p;
     v.dz = H.dz;
     v.om = M.omega;
+    v.sn = H.sn;
     v.eca = M.eca;
     v.ecb = M.ecb;
     v.ee = M.ee;
@@ -98,7 +100,7 @@ __global__ void k_mixed_il(MixView V, const double* __restrict__ geom, const int
         const double ar = V.area[t];
         for (int i = 1; i <= V.nz - 1; ++i) {
             const double lamf = 0.5 * (V.lam[(i - 1) * V.ld + t] + V.lam[i * V.ld + t]);
-            IL[V.off_z + (i - 1) * V.ld + t] = (ar * lamf) / V.dz;
+            IL[V.off_z + (i - 1) * V.ld + t] = ((ar * lamf) / V.dz) / V.sn;   // lumping of M~2z (R24)
         }
     }
 }
@@ -154,6 +156,7 @@ __global__ void __launch_bounds__(kMixBlock) k_mixed_apply_zp(MixView V, const d
         double v = dg * W[(i - 1) * ld];
         if (i - 1 >= 1) v = v + ((dz / 6.0) / slo) * W[(i - 2) * ld];
         if (i + 1 <= nz - 1) v = v + ((dz / 6.0) / shi) * W[i * ld];
+        v = v * V.sn;                                  // M~2z = (1 + omega_N^2) M2z (Eq. 5)
         y[V.off_z + (i - 1) * ld + c] = v - V.om * (P[(i - 1) * ld] - P[i * ld]);
     }
     const int32_t E0 = V.ce[c], E1 = V.ce[ld + c], E2 = V.ce[2 * ld + c];

@@ -183,3 +183,44 @@ def test_full_size_c2b_mixed():
     assert st == "HMG_OK" and st_o == 0 and it == it_o, (it, it_o, rr, rr_o)
     g.close()
     o.close()
+
+
+@pytest.mark.parametrize("name", ["C0", "C2b_r4", "C4_r3"])
+@pytest.mark.parametrize("omega_n", [0.5, 2.0])
+def test_buoyancy_bitwise(name, omega_n):
+    """Buoyancy (reading R24; hmg_build_hierarchy_ex): the hierarchy's bands on
+    every level, the V-cycle, the mixed apply and the Schur preconditioner are
+    bitwise the oracle's; PCG and GMRES (both Gram-Schmidt variants) take the
+    oracle's iteration counts."""
+    cfg = CASES[name]
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, omega_n=omega_n)
+    o = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, omega_n=omega_n)
+    for ref in range(cfg.coarsest_ref, cfg.fine_ref + 1):
+        G, O = g.export_level(ref), o.level(ref)
+        assert np.array_equal(G["D"], O["D"]) and np.array_equal(G["U"], O["U"]) and np.array_equal(G["H"], O["H"])
+    r = cfg.fine_ref
+    bd = g.to_device(r, b)
+    assert np.array_equal(g.to_host(r, g.vcycle(bd)), o.vcycle(b))
+    _, it, _, st = g.pcg_solve(bd)
+    assert st == "HMG_OK" and it == o.pcg(b)[1]
+    _, N = o.mixed_sizes()
+    F = hi.uniform_vector(N, 69)
+    Fd = g.mixed_to_device(F)
+    assert np.array_equal(g.mixed_to_host(g.mixed_apply(Fd)), o.mixed_apply(F))
+    assert np.array_equal(g.mixed_to_host(g.mixed_precond(Fd)), o.mixed_precond(F))
+    for gs in (2, 1):
+        _, itm, rrm, stm = g.mixed_gmres(Fd, rtol=1e-5, gs_passes=gs)
+        _, itm_o, _, _, stm_o = o.mixed_gmres(F, rtol=1e-5, gs_passes=gs)
+        assert stm == "HMG_OK" and stm_o == 0 and itm == itm_o, (gs, itm, itm_o)
+    g.close()
+    o.close()
+
+
+def test_buoyancy_argument_errors(monkeypatch):
+    lam, _ = hi.make_inputs(CASES["C0"])
+    with pytest.raises(HmgError, match="omega_n"):
+        Hierarchy(2, 0, 8, 0.01, 1e-4, lam, omega_n=-1.0)
+    monkeypatch.setenv("HMG_OPERATOR", "free")
+    with pytest.raises(HmgError, match="omega_n"):
+        Hierarchy(2, 0, 8, 0.01, 1e-4, lam, omega_n=1.0)
