@@ -221,12 +221,15 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     const int col = warp * 32 + lane;
     const int64_t c = c0 + col;
     const bool live = c < ncol;
+    // reads of lanes past the last column (a partial tile; c may exceed ld) use
+    // the last column instead: results of those lanes are never stored
+    const int64_t cr = live ? c : ncol - 1;
     int s = 0;
     uint32_t ph = 0;
     // ---- forward: row interchanges and L multipliers, y into x ----
     double w[KL + 1];
 #pragma unroll
-    for (int q = 0; q <= KL; ++q) w[q] = (q < m) ? bvec[(int64_t)q * ld + c] : 0.0;
+    for (int q = 0; q <= KL; ++q) w[q] = (q < m) ? bvec[(int64_t)q * ld + cr] : 0.0;
     for (int k = 0; k < nf; ++k) {
         ptx::mbar_wait(&full[s], ph);
         const unsigned char* st = stages + (size_t)s * C::BYTES;
@@ -286,14 +289,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 #pragma unroll
     for (int q = 0; q <= KV; ++q) {
         const int idx = m - 1 - KV + q;
-        u[q] = idx >= 0 ? x[(int64_t)idx * ld + c] : 0.0;
+        u[q] = idx >= 0 ? x[(int64_t)idx * ld + cr] : 0.0;
     }
     constexpr int YQ = 2 * GB * ((kYQ + 2 * GB - 1) / (2 * GB));   // prefetch distance, a multiple of GB
     double yq[YQ];      // y(j - KV - 1 - d), d steps ahead
 #pragma unroll
     for (int d = 0; d < YQ; ++d) {
         const int idx = m - 1 - KV - 1 - d;
-        yq[d] = idx >= 0 ? x[(int64_t)idx * ld + c] : 0.0;
+        yq[d] = idx >= 0 ? x[(int64_t)idx * ld + cr] : 0.0;
     }
     for (int q0 = 0; q0 < nb; q0 += YQ / GB) {
 #pragma unroll
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
                     const int d = qq * GB + g;
                     u[0] = yq[d];
                     const int idx = j - KV - 1 - YQ;
-                    yq[d] = idx >= 0 ? x[(int64_t)idx * ld + c] : 0.0;
+                    yq[d] = idx >= 0 ? x[(int64_t)idx * ld + cr] : 0.0;
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&empty[s]);
@@ -383,11 +386,12 @@ __global__ void __launch_bounds__(kBandThreads, 1)
         return;
     }
     const int64_t c = c0 + lane;
+    const int64_t cr = c < ncol ? c : ncol - 1;   // partial tile: read a valid column, never store
     double w[BW];   // w[q] = x(i - KL + q)
 #pragma unroll
     for (int q = 0; q < BW; ++q) {
         const int j = q - KL;
-        w[q] = (j >= 0 && j < m) ? xin[(int64_t)j * ld + c] : 0.0;
+        w[q] = (j >= 0 && j < m) ? xin[(int64_t)j * ld + cr] : 0.0;
     }
     for (int i = 0; i < m; ++i) {
         const int s = i % S;

@@ -9,7 +9,7 @@ pivot rows (an integer decision taken in the same precision on both sides),
 the LU factors, the solutions, the products and the DG1 <-> DG0 transfers
 (P:645-648).  Shapes: the NLO column operator (m = 384, kl = ku = 13,
 P:1099-1106) and small / asymmetric / degenerate bands; column counts that
-span several 32-column tiles with a ragged tail; at full size (81,920 columns,
+span several tiles with a ragged tail (also past ld, 128-column solve tiles); at full size (81,920 columns,
 BASELINE-scale NLO problem N2) sampled columns against the oracle.
 """
 import numpy as np
@@ -36,7 +36,7 @@ def oracle_column(ab, c):
     return np.ascontiguousarray(ab[:, :, c].T)
 
 
-SHAPES = [(384, 13, 13, 100), (48, 13, 13, 70), (13, 13, 13, 33), (5, 13, 13, 40), (1, 13, 13, 32),
+SHAPES = [(384, 13, 13, 100), (384, 13, 13, 200), (48, 13, 13, 70), (13, 13, 13, 33), (5, 13, 13, 40), (1, 13, 13, 32),
           (64, 1, 1, 97), (40, 3, 5, 65), (30, 5, 2, 31), (17, 0, 0, 40), (7, 2, 2, 64)]
 
 
