@@ -37,9 +37,40 @@
 #include "sm100_ptx.cuh"
 #include "mf_ops.cuh"
 
+// Probe builds (tools/micro/st_probe.py only; never the product library):
+// HMG_PROBE_NORES / NOCHAIN drop consumer work, NOHALO / NOBWD / NOEDGE drop
+// parts of the data movement -- results are wrong, the timing says what bounds.
+#if defined(HMG_PROBE_NOHALO) || defined(HMG_PROBE_NOBWD) || defined(HMG_PROBE_NOEDGE) || defined(HMG_PROBE_NOMOVE)
+#define HMG_PROBE_NOCHAIN
+#endif
+#ifdef HMG_PROBE_NOMOVE
+#define HMG_PROBE_NOHALO
+#define HMG_PROBE_NOBWD
+#define HMG_PROBE_NOEDGE
+#endif
+#ifndef HMG_ST_G
+#define HMG_ST_G 2
+#endif
+#ifdef HMG_PROBE_NOHALO
+constexpr bool kProbeHalo = false;
+#else
+constexpr bool kProbeHalo = true;
+#endif
+#ifdef HMG_PROBE_NOBWD
+constexpr bool kProbeBwd = false;
+#else
+constexpr bool kProbeBwd = true;
+#endif
+#ifdef HMG_PROBE_NOEDGE
+constexpr bool kProbeEdge = false;
+#else
+constexpr bool kProbeEdge = true;
+#endif
+
 namespace hmg {
 
 CUtensorMap make_tensor_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes);
+CUtensorMap make_store_map(double* base, int64_t ld, int64_t width, int64_t rows, int box_x, int G);
 extern thread_local std::string g_launch_error;
 
 namespace {
@@ -49,12 +80,17 @@ constexpr int kConsumerWarps = kTile / 32;
 constexpr int kThreads = kTile + 32;       // + one producer warp
 constexpr int kMfWarps = kTile / 32;       // matrix-free: warps forming the couplings of each stage
 constexpr int kThreadsMf = kThreads + 32 * kMfWarps;
+constexpr int kThreadsSplit = kThreads + 32;  // stored bands, non-zero guess: + a gather warp for the halos
+// threads of one CTA: the gather warp takes the off-tile cp.async gathers off
+// the producer warp, whose TMA issue is on the sweep's critical path
+__host__ __device__ constexpr int st_threads(bool zero, bool mf) { return mf ? kThreadsMf : zero ? kThreads : kThreadsSplit; }
 constexpr int kBack = 8;                   // layers per backward stage
 constexpr int kUcRow = 64;                 // forward u_c rows: 32 parents of the tile + the next 32 (so the
                                            // tile and halo parts of u_c share the row stride kHaloMax)
 
 #ifdef HMG_TIMING
-__device__ long long g_st_timing[8];   // CTA 0, thread 0: [0] total, [1] forward wait, [2] backward wait, [3] tiles
+__device__ long long g_st_timing[12];  // CTA 0, thread 0: [0] total, [1] forward wait, [2] backward wait, [3] tiles;
+                                       // producer lane 0: [8] total, [9] waiting for free slots, [10] stages
 #endif
 
 __device__ __forceinline__ bool pivot_ok(double den) { return den > 0.0 && den <= DBL_MAX; }
@@ -68,6 +104,7 @@ struct StMaps {
     CUtensorMap ucf;    // box kTile/4 x (G + 1)   (PROLONG)
     CUtensorMap ucb;    // box kTile/4 x 8         (PROLONG)
     CUtensorMap bb;     // box kTile x 8: backward b rows (DOT)
+    CUtensorMap uo;     // box kTile x 8: u' rows stored from the backward stage (extent: the level's n columns)
 };
 
 // Doubles of one ring stage and the offsets of its parts.  Forward stage:
@@ -108,14 +145,14 @@ struct StOp {
 };
 
 template <bool ZERO, bool PROLONG, bool MF, int G, bool CHK, bool DOT = false, bool EH = false>
-__global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
+__global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
     k_sweep_st(const __grid_constant__ StMaps maps, LevelView L, StOp op, TileHalo th, EdgeTiles et,
                const double* __restrict__ bvec,
                const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc, double* __restrict__ uout,
                double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols, int pf_groups,
                double* __restrict__ partial) {
     extern __shared__ __align__(1024) unsigned char smraw[];
-    __shared__ double dred[kThreads / 32];
+    __shared__ double dred[kThreadsSplit / 32];
     static_assert(!(EH && (ZERO || MF)), "edge store: general stored-band sweeps only");
     constexpr StLayout SL = st_layout(ZERO, PROLONG, MF, G, DOT, EH);
     double dotacc = 0.0;                               // DOT: this thread's sum of b_k u'_k
@@ -125,6 +162,8 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
     constexpr bool HALO = !ZERO || MF;       // off-tile neighbour values needed
     constexpr int HS = MF ? kHaloMax : kTile;   // stride of the halo rows of u
     constexpr bool FLAT = !MF && !ZERO;         // neighbours read at per-tile offsets
+    constexpr bool SPLIT = !MF && !ZERO;        // halo gathers issued by their own warp
+    constexpr bool TSTORE = !ZERO;              // u' rows written back by TMA from the backward stage
     static_assert(kUcRow == kHaloMax, "u_c tile and halo rows share one stride");
     const int nz = L.nz;
     const int64_t ld = L.ld;
@@ -141,7 +180,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
     ptx::pdl_trigger();                                // the next kernel may start its prologue
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&full[s], SPLIT ? 2 : 1);   // producer (+ gather warp)
             ptx::mbar_init(&empty[s], kConsumerWarps);
             ptx::mbar_init(&mid[s], kMfWarps);
         }
@@ -223,6 +262,55 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 if (mlane == 0) ptx::mbar_arrive(&mid[s]);
             }
         }
+    } else if (SPLIT && warp == kConsumerWarps + 1) {
+        // ============ gather warp: off-tile u values and gathered couplings ============
+        // Per forward stage: cp.async of the <= 64 halo u values and the <= 32
+        // gathered edge couplings of each layer; the stage's full barrier counts
+        // this warp's arrival after its copies are registered with it.
+        int s = 0;
+        uint32_t phase = 0;
+        auto advance = [&]() {
+            if (++s == S) {
+                s = 0;
+                phase ^= 1u;
+            }
+        };
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int hcount = th.count[tile];
+            const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
+            const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
+            const int ehc = EH ? et.hcount[tile] : 0;
+            const int32_t eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
+            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+                ptx::mbar_wait(&empty[s], phase ^ 1u);
+                double* st = stages + (size_t)s * SL.stage;
+                if (kProbeHalo) {
+                    for (int kk = 0; kk < G; ++kk) {
+                        const int k = gi * G + kk;
+                        if (k >= nz) break;
+                        if (EH && lane < ehc)
+                            ptx::cp_async8(st + SL.eh + kk * kEdgeRow + kEdgeRange + lane,
+                                           et.H + (int64_t)k * et.ldE + eh0);
+                        const double* src = uin + (int64_t)k * ld;
+                        if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane, src + h0);
+                        if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane + 32, src + h1);
+                        if (PROLONG) {
+                            const double* srcc = uc + (int64_t)k * ldc;
+                            if (lane < hcount) ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane, srcc + (h0 >> 2));
+                            if (lane + 32 < hcount)
+                                ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane + 32, srcc + (h1 >> 2));
+                        }
+                    }
+                    ptx::cp_async_arrive(&full[s]);
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full[s]);
+            }
+            for (int m = nchunks - 1; m >= 0; --m, advance()) {   // backward stages: one arrival each
+                ptx::mbar_wait(&empty[s], phase ^ 1u);
+                if (lane == 0) ptx::mbar_arrive(&full[s]);
+            }
+        }
     } else if (warp == kConsumerWarps) {
         // ======================= producer warp =======================
         const uint64_t pol_stream = ptx::policy_evict_first();
@@ -241,28 +329,31 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 phase ^= 1u;
             }
         };
+#ifdef HMG_TIMING
+        long long p0 = clock64(), pw = 0, pn = 0, ph = 0;
+#endif
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int x = tile * kTile, xc = x / 4;
-            const int hcount = HALO ? th.count[tile] : 0;
+            const int hcount = HALO && !SPLIT ? th.count[tile] : 0;
             const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
             const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
-            // edge store: the tile's contiguous edge range and its gathered edges
+            // edge store: the tile's contiguous edge range (its gathered edges: gather warp)
             const int32_t ee0 = EH ? et.e0[tile] : 0;
             const uint32_t ebytes = EH ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
-            const int ehc = EH ? et.hcount[tile] : 0;
-            const int32_t eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
+#ifdef HMG_TIMING
+                long long q0 = clock64();
+#endif
                 ptx::mbar_wait(&empty[s], phase ^ 1u);
+#ifdef HMG_TIMING
+                pw += clock64() - q0;
+                ++pn;
+#endif
                 double* st = stages + (size_t)s * SL.stage;
-                if (EH) {
-                    for (int kk = 0; kk < G; ++kk) {
-                        const int k = gi * G + kk;
-                        if (k >= nz) break;
-                        if (lane < ehc) ptx::cp_async8(st + SL.eh + kk * kEdgeRow + kEdgeRange + lane,
-                                                       et.H + (int64_t)k * et.ldE + eh0);
-                    }
-                }
-                if (HALO) {
+#ifdef HMG_TIMING
+                const long long q1 = clock64();
+#endif
+                if (HALO && !SPLIT && kProbeHalo) {
                     for (int kk = 0; kk < G; ++kk) {          // off-tile neighbours of the G layers
                         const int k = gi * G + kk;
                         if (k >= nz) break;
@@ -286,6 +377,9 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     ptx::cp_async_arrive(&full[s]);
                 }
                 __syncwarp();
+#ifdef HMG_TIMING
+                ph += clock64() - q1;
+#endif
                 if (lane == 0) {
                     if (pf_groups > 0 && gi + pf_groups < ngroups) {   // L2 prefetch a few stages ahead
                         const int gp = gi + pf_groups;
@@ -298,8 +392,8 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     }
                     int nl = nz - gi * G;
                     nl = nl < G ? nl : G;
-                    ptx::mbar_arrive_expect_tx(&full[s], fwd_bytes + (EH ? (uint32_t)nl * ebytes : 0u));
-                    if (EH)
+                    ptx::mbar_arrive_expect_tx(&full[s], fwd_bytes + (EH && kProbeEdge ? (uint32_t)nl * ebytes : 0u));
+                    if (EH && kProbeEdge)
                         for (int kk = 0; kk < nl; ++kk)
                             ptx::bulk_g2s(st + SL.eh + kk * kEdgeRow, et.H + (int64_t)(gi * G + kk) * et.ldE + ee0,
                                           ebytes, &full[s]);
@@ -313,9 +407,16 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 }
             }
             for (int m = nchunks - 1; m >= 0; --m, advance()) {   // u rows again for the back substitution
+#ifdef HMG_TIMING
+                long long q0 = clock64();
+#endif
                 ptx::mbar_wait(&empty[s], phase ^ 1u);
+#ifdef HMG_TIMING
+                pw += clock64() - q0;
+#endif
                 double* st = stages + (size_t)s * SL.stage;
-                if (lane == 0) {
+                if (lane == 0 && !kProbeBwd) ptx::mbar_arrive(&full[s]);
+                if (lane == 0 && kProbeBwd) {
                     ptx::mbar_arrive_expect_tx(&full[s], bwd_bytes);
                     ptx::tma_load_2d_hint(st, &maps.ub, x, m * kBack, &full[s], pol_stream);
                     if (PROLONG) ptx::tma_load_2d_hint(st + kBack * kTile, &maps.ucb, xc, m * kBack, &full[s], pol_stream);
@@ -323,12 +424,21 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                 }
             }
         }
+#ifdef HMG_TIMING
+        if (blockIdx.x == 0 && lane == 0) {
+            g_st_timing[8] = clock64() - p0;
+            g_st_timing[9] = pw;
+            g_st_timing[10] = pn;
+            g_st_timing[11] = ph;
+        }
+#endif
     } else {
         // ======================= consumer warps: one column per thread =======================
         const int j = threadIdx.x;
         const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
         const uint32_t gcol = 2u * (uint32_t)nz;   // g_k at TMEM columns 2nz + 2k, z_k at 2k
         const double ydz = MF ? div_recip(op.dz) : 0.0;   // exact redo only
+        int pend = -1;                                     // TSTORE: slot whose store may still read it
         int s = 0;
         uint32_t phase = 0;
         auto advance = [&]() {
@@ -454,8 +564,19 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         acc = acc + H1 * NBRF(kk, 1, l1);
                         acc = acc + H2 * NBRF(kk, 2, l2);
                         r = bk - acc;
+#if defined(HMG_PROBE_NORES) || defined(HMG_PROBE_NOCHAIN)
+                        r = bk;   // probe build only: no residual work in the consumers (wrong results)
+#endif
                         um = uk;
                     }
+#ifdef HMG_PROBE_NOCHAIN
+                    if (IN) {   // probe build only: no Thomas chain (wrong results, same data movement)
+                        ptx::tmem_st_f64(tl + 2u * (uint32_t)k, r);
+                        ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, Uk);
+                        zprev = r;
+                        gprev = Uk;
+                    } else
+#endif
                     if (IN) {
                         const double num = r - Um * zprev;
                         const double den = Dk - Um * gprev;
@@ -493,7 +614,11 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
 #endif
             // Rare: a quotient left the fast path's exact range.  The warp redoes
             // its columns' forward pass from global memory with '/'.
+#ifdef HMG_PROBE_NOREDO
+            if (false) {
+#else
             if (__any_sync(0xffffffffu, slow && valid)) {
+#endif
                 const int32_t g0 = L.nbr[cv], g1 = L.nbr[ld + cv], g2 = L.nbr[2 * ld + cv];
                 auto GU = [&](int kk, int64_t cell) -> double {
                     double v = uin[(int64_t)kk * ld + cell];
@@ -591,7 +716,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                     ptx::tmem_ld_8f64(tl + 2u * (uint32_t)(k0 - kBack), zn);
                     ptx::tmem_ld_8f64(tl + gcol + 2u * (uint32_t)(k0 - kBack), gn);
                 }
-                const double* su = nullptr;
+                double* su = nullptr;
                 if (!ZERO) {
 #ifdef HMG_TIMING
                     long long w0 = clock64();
@@ -613,8 +738,9 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         if (PROLONG) uo = uo + su[kBack * kTile + i * (kTile / 4) + (j >> 2)];
                         o = uo + omega * dl;
                     }
+                    if (TSTORE) su[i * kTile + j] = o;     // u_old's place in the stage
                     if (valid) {
-                        uo_row[(int64_t)k * ld] = o;
+                        if (!TSTORE) uo_row[(int64_t)k * ld] = o;
                         if (DOT) dotacc = dotacc + su[kBack * kTile + i * kTile + j] * o;
                     }
                 };
@@ -637,7 +763,34 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
                         finish(i, k);
                     }
                 }
-                if (!ZERO) {
+                if (TSTORE) {
+                    // the chunk's 8 u' rows go out as one TMA box from the stage (clipped
+                    // to the level's n columns and nz rows); thread 0 releases the slot
+                    // once the copy has read it -- the previous chunk's here, this tile's
+                    // last before the next tile's forward stages need the ring
+                    ptx::fence_proxy_async_smem();
+                    ptx::named_bar_sync(1, kTile);
+                    if (warp == 0) {
+                        if (lane == 0) {
+                            ptx::tma_store_2d(&maps.uo, tile * kTile, k0, su);
+                            ptx::bulk_commit_group();
+                            if (pend >= 0) {
+                                ptx::bulk_wait_group_read<1>();
+                                ptx::mbar_arrive(&empty[pend]);
+                            }
+                            if (m == 0) {
+                                ptx::bulk_wait_group_read<0>();
+                                ptx::mbar_arrive(&empty[s]);
+                            }
+                        }
+                        pend = m == 0 ? -1 : s;
+                        __syncwarp();
+                    } else {
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&empty[s]);
+                    }
+                    advance();
+                } else if (!ZERO) {
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&empty[s]);
                     advance();
@@ -655,6 +808,7 @@ __global__ void __launch_bounds__(MF ? kThreadsMf : kThreads, 2)
             tbk += clock64() - tfw0;
 #endif
         }
+        if (TSTORE && threadIdx.x == 0) ptx::bulk_wait_group<0>();   // the u' rows are written before exit
     }
 #ifdef HMG_TIMING
     if (warp < kConsumerWarps && blockIdx.x == 0 && threadIdx.x == 0) {
@@ -729,6 +883,7 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
         maps.ucb = make_tensor_map(uc, C.ld, nz, kTile / 4, kBack, 1);
     }
     if (DOT) maps.bb = make_tensor_map(b, L.ld, nz, kTile, kBack, 1);
+    if (!Z) maps.uo = make_store_map(uout, L.ld, L.n, nz, kTile, kBack);
     const StOp op{L.lam, L.geom, H.w2, H.dz};
     // persistent grid: as many rounds of tiles as the resident CTAs need, with the
     // tiles dealt evenly (ref 6: 640 tiles -> 214 CTAs x 3 instead of 296 CTAs
@@ -736,7 +891,7 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
     const unsigned cap = (unsigned)((two ? 2 : 1) * sms);
     const unsigned rounds = (ntiles + cap - 1) / cap;
     const unsigned grid = (ntiles + rounds - 1) / rounds;
-    launch_pdl(H, k_sweep_st<Z, P, M, G, CK, DOT, EH>, dim3(grid), dim3(M ? kThreadsMf : kThreads), smem, s, maps, V,
+    launch_pdl(H, k_sweep_st<Z, P, M, G, CK, DOT, EH>, dim3(grid), dim3(st_threads(Z, M)), smem, s, maps, V,
                op, L.halo, L.edge, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups,
                H.partials);
     return (int)grid;
@@ -744,7 +899,7 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
 
 #ifdef HMG_TIMING
 }  // namespace
-extern "C" void hmg_debug_st_timing(long long* out) { cudaMemcpyFromSymbol(out, g_st_timing, sizeof(long long) * 8); }
+extern "C" void hmg_debug_st_timing(long long* out) { cudaMemcpyFromSymbol(out, g_st_timing, sizeof(long long) * 12); }
 namespace {
 #endif
 
@@ -802,7 +957,7 @@ void launch_sweep_st(const Hierarchy& H, const DevLevel& L, const double* b, con
             if (L.g_safe && uc)
                 launch_st<false, true, false, 2, false, false, true>(H, L, b, uin, uc, uout, omega, s);
             else if (L.g_safe)
-                launch_st<false, false, false, 2, false, false, true>(H, L, b, uin, nullptr, uout, omega, s);
+                launch_st<false, false, false, HMG_ST_G, false, false, true>(H, L, b, uin, nullptr, uout, omega, s);
             else if (uc)
                 launch_st<false, true, false, 2, true, false, true>(H, L, b, uin, uc, uout, omega, s);
             else

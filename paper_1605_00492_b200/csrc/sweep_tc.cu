@@ -476,10 +476,10 @@ EncodeFn encode_fn() {
 // Map over `planes` consecutive layer-major [rows][ld] fp64 arrays (planes = 1:
 // 2-D, else 3-D with plane stride rows*ld); box = box_x cells x G layers x planes.
 // Out-of-range box elements (tail tile, layers >= rows) are zero-filled.
-CUtensorMap encode_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes) {
+CUtensorMap encode_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes, int64_t width) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
-    const cuuint64_t dims[3] = {(cuuint64_t)ld, (cuuint64_t)rows, (cuuint64_t)planes};
+    const cuuint64_t dims[3] = {(cuuint64_t)(width > 0 ? width : ld), (cuuint64_t)rows, (cuuint64_t)planes};
     const cuuint64_t strides[2] = {(cuuint64_t)(ld * sizeof(double)), (cuuint64_t)(rows * ld * sizeof(double))};
     const cuuint32_t box[3] = {(cuuint32_t)box_x, (cuuint32_t)G, (cuuint32_t)planes};
     const cuuint32_t estr[3] = {1, 1, 1};
@@ -496,21 +496,26 @@ struct MapKey {
     const double* base;
     int64_t ld, rows;
     int box_x, G, planes;
+    int64_t width;
     bool operator==(const MapKey& o) const {
-        return base == o.base && ld == o.ld && rows == o.rows && box_x == o.box_x && G == o.G && planes == o.planes;
+        return base == o.base && ld == o.ld && rows == o.rows && box_x == o.box_x && G == o.G && planes == o.planes &&
+               width == o.width;
     }
 };
-CUtensorMap make_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes = 1) {
+// width > 0: the map's row extent (columns past it are neither read nor
+// written), else the row stride ld
+CUtensorMap make_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes = 1,
+                     int64_t width = 0) {
     constexpr int kCache = 128;
     static thread_local MapKey keys[kCache];
     static thread_local CUtensorMap maps[kCache];
     static thread_local int used = 0, next = 0;
-    const MapKey k{base, ld, rows, box_x, G, planes};
+    const MapKey k{base, ld, rows, box_x, G, planes, width};
     for (int i = 0; i < used; ++i)
         if (keys[i] == k) return maps[i];
     const int slot = used < kCache ? used++ : (next++ % kCache);
     keys[slot] = k;
-    maps[slot] = encode_map(base, ld, rows, box_x, G, planes);
+    maps[slot] = encode_map(base, ld, rows, box_x, G, planes, width);
     return maps[slot];
 }
 
@@ -574,6 +579,9 @@ void launch_tc(const Hierarchy& H, const DevLevel& L, const double* b, const dou
 
 CUtensorMap make_tensor_map(const double* base, int64_t ld, int64_t rows, int box_x, int G, int planes) {
     return make_map(base, ld, rows, box_x, G, planes);
+}
+CUtensorMap make_store_map(double* base, int64_t ld, int64_t width, int64_t rows, int box_x, int G) {
+    return make_map(base, ld, rows, box_x, G, 1, width);
 }
 
 #ifdef HMG_TIMING

@@ -5,14 +5,16 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 import paper_1605_00492_b200.binding as B
 from paper_1605_00492_b200 import build as pb
-lib = os.path.join(HERE, "libhmg_timing.so")
-cmd = [pb.NVCC, *pb.ARCH, *[f for f in pb.FLAGS if f not in ("-Xptxas", "-v")], "-DHMG_TIMING", "-shared",
+extra = sys.argv[1:]          # e.g. -DHMG_PROBE_NOMOVE
+lib = os.path.join(HERE, f"libhmg_timing{len(extra)}.so")
+cmd = [pb.NVCC, *pb.ARCH, *[f for f in pb.FLAGS if f not in ("-Xptxas", "-v")], "-DHMG_TIMING", *extra, "-shared",
        *[os.path.join(pb.CSRC, s) for s in pb.SOURCES], "-o", lib, "-ldl"]
 subprocess.check_call(cmd)
 B._LIB_PATH = lib
 import torch
 import hmg_inputs as hi
 from paper_1605_00492_b200 import Hierarchy
+print(" ".join(extra) or "normal")
 for ref in (7, 6, 5):
     cfg = hi.Config("t", ref, ref - 1 if ref > 5 else 4, 64, 0.001, 1e-5)
     lam, b = hi.make_inputs(cfg)
@@ -23,10 +25,10 @@ for ref in (7, 6, 5):
     for _ in range(3):
         g.line_smooth(ref, bd, u, 1, om, False)
     torch.cuda.synchronize()
-    t = (ctypes.c_longlong * 8)()
+    t = (ctypes.c_longlong * 12)()
     B.load_library().hmg_debug_st_timing(t)
     tot, wf, wb, nt, tf, tb, tws = t[0], t[1], t[2], t[3], t[4], t[5], t[6]
     print(f"ref {ref}: tiles/CTA {nt}, total {tot} cyc = {tot/1965:.1f} us, per tile {tot/max(nt,1)/1965:.1f} us; "
           f"waiting fwd {wf/tot:.0%} bwd {wb/tot:.0%}; forward phase {tf/max(nt,1)/64:.0f} cyc/layer "
-          f"(of which waiting {wf/max(nt,1)/64:.0f}), back phase incl. redo check {tb/max(nt,1)/64:.0f} cyc/layer, of which slow check + TMEM store wait {tws/max(nt,1)/64:.0f}")
+          f"(of which waiting {wf/max(nt,1)/64:.0f}), back phase incl. redo check {tb/max(nt,1)/64:.0f} cyc/layer, of which slow check + TMEM store wait {tws/max(nt,1)/64:.0f}; producer: {t[8]} cyc, waiting for free slots {t[9]/max(t[8],1):.0%}, forward stages {t[10]} ({(t[8]-t[9])/max(t[10],1):.0f} busy cyc per forward stage incl. backward issue, of which halo gathers {t[11]/max(t[10],1):.0f})")
     g.close()
