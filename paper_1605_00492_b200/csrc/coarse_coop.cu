@@ -36,13 +36,17 @@ constexpr int kCoopLevels = 5;
 
 #ifdef HMG_TIMING
 __device__ long long g_coop_timing[512];
-__device__ int g_coop_ntiming;
-#define CSTAMP()                                                              \
+__device__ int g_coop_label[512];
+// label: 0 start, 1 operands loaded, 2 tile sweep done, 3 grid barrier passed, 4 coarsest sweeps done
+#define CSTAMP(lbl)                                                           \
     do {                                                                      \
-        if (blockIdx.x == 0 && threadIdx.x == 0 && nst < 512) g_coop_timing[nst++] = clock64(); \
+        if (blockIdx.x == 0 && threadIdx.x == 0 && nst < 512) {               \
+            g_coop_label[nst] = (lbl);                                        \
+            g_coop_timing[nst++] = clock64();                                 \
+        }                                                                     \
     } while (0)
 #else
-#define CSTAMP() do {} while (0)
+#define CSTAMP(lbl) do {} while (0)
 #endif   // levels top..coarsest handled (index = ref - coarsest)
 
 struct CoopLevel {
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
 #ifdef HMG_TIMING
     int nst = 0;
 #endif
-    CSTAMP();
+    CSTAMP(0);
     uint32_t phase = 0;
     int loaded_l = -1, loaded_tile = -1;               // which tile's bands/factors are in shared memory
 
@@ -198,10 +202,20 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         res_b = bl;
         res_u = u;
     };
+    // A CTA with several tiles of a level visits them in alternating order from
+    // one step to the next, so the tile it finished last (operands resident in
+    // shared memory) is the first of the next step.
+    bool rev = false;
+    auto my_tiles = [&](const CoopLevel& L) {
+        rev = !rev;
+        return L.ntiles > (int)blockIdx.x ? (L.ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    };
     // one damped sweep of level l from iterate uin (nullptr: zero guess) to uout, all tiles
     auto sweep_step = [&](int l, const double* bl, const double* uin, double* uout) {
         const CoopLevel& L = LV[l];
-        for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
+        const int cnt = my_tiles(L);
+        for (int i = 0; i < cnt; ++i) {
+            const int t = (int)blockIdx.x + (int)gridDim.x * (rev ? cnt - 1 - i : i);
             const int64_t c = (int64_t)t * TW + j;
             int l0, l1, l2;
             slots(L, c, l0, l1, l2);
@@ -209,9 +223,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
             load_vectors(L, t, bl, uin);
             load_static(l, t);
             cp_wait();
-            CSTAMP();
+            CSTAMP(1);
             tile_sweep_cta<TW>(S, nz, warp, j, l0, l1, l2, uin == nullptr, P.omega, jlane && c < L.V.n);
-            CSTAMP();
+            CSTAMP(2);
             store_own(uout, L, c);
             resident(t, bl, uout);
         }
@@ -228,11 +242,13 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
             double* dst = (c_in == L.wa) ? L.wb : L.wa;
             sweep_step(l, bl, c_in, dst);
             grid.sync();
-            CSTAMP();
+            CSTAMP(3);
             c_in = dst;
         }
         cur[l] = c_in;
-        for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
+        const int cnt = my_tiles(L);
+        for (int i = 0; i < cnt; ++i) {
+            const int t = (int)blockIdx.x + (int)gridDim.x * (rev ? cnt - 1 - i : i);
             const int64_t c = (int64_t)t * TW + j;
             int l0, l1, l2;
             slots(L, c, l0, l1, l2);
@@ -241,7 +257,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
             load_static(l, t);
             cp_wait();
             resident(t, bl, c_in);
-            CSTAMP();
+            CSTAMP(1);
             tile_residuals_cta<TW>(S, nz, warp, j, l0, l1, l2, c_in == nullptr);   // r = b - H^ u (r = b from zero)
             __syncthreads();
             // b_c[k][p] = ((r0 + r1) + r2) + r3 over the children 4p..4p+3: thread = (parent, layer phase)
@@ -255,7 +271,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
                 }
         }
         grid.sync();
-        CSTAMP();
+        CSTAMP(3);
     }
     // ---- coarsest level: n_coarse sweeps from zero ----
     {
@@ -273,10 +289,10 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
                 cp_rows(sb, bl, L.V.ld, 0, TW);
                 load_static(l, 0);
                 cp_wait();
-                CSTAMP();
+                CSTAMP(1);
                 for (int s = 0; s < P.n_coarse; ++s)
                     tile_sweep_cta<TW>(S, nz, warp, j, l0, l1, l2, s == 0, P.omega, jlane && c < L.V.n);
-                CSTAMP();
+                CSTAMP(4);
                 store_own(out, L, c);
                 resident(0, bl, out);
             }
@@ -290,7 +306,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
             }
         }
         grid.sync();
-        CSTAMP();
+        CSTAMP(3);
     }
     // ---- up leg: prolongation fused into the first postsmoothing sweep ----
     for (int l = P.coarsest + 1; l <= P.top; ++l) {
@@ -301,7 +317,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         const double* c_in = cur[l];                   // presmoothed iterate (nullptr: zero)
         // first step: u = c_in + P u_c formed in shared memory for the tile and its halo
         double* dst = (P.nu_post <= 1) ? out : ((c_in == L.wa) ? L.wb : L.wa);
-        for (int t = blockIdx.x; t < L.ntiles; t += gridDim.x) {
+        const int cnt = my_tiles(L);
+        for (int i = 0; i < cnt; ++i) {
+            const int t = (int)blockIdx.x + (int)gridDim.x * (rev ? cnt - 1 - i : i);
             const int64_t c = (int64_t)t * TW + j;
             const bool valid = c < L.V.n;
             int l0, l1, l2;
@@ -330,20 +348,20 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
                 }
             }
             __syncthreads();
-            CSTAMP();
+            CSTAMP(1);
             if (P.nu_post > 0) tile_sweep_cta<TW>(S, nz, warp, j, l0, l1, l2, false, P.omega, jlane && valid);
-            CSTAMP();
+            CSTAMP(2);
             store_own(dst, L, c);
             resident(t, bl, dst);
         }
         grid.sync();
-        CSTAMP();
+        CSTAMP(3);
         const double* prev = dst;
         for (int s = 1; s < P.nu_post; ++s) {
             double* d2 = (s == P.nu_post - 1) ? out : ((prev == L.wa) ? L.wb : L.wa);
             sweep_step(l, bl, prev, d2);
             grid.sync();
-            CSTAMP();
+            CSTAMP(3);
             prev = d2;
         }
     }
@@ -352,8 +370,9 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
 #ifdef HMG_TIMING
 }  // namespace
 extern "C" void hmg_debug_coop_timing(long long* out) { cudaMemcpyFromSymbol(out, g_coop_timing, sizeof(long long) * 512); }
+extern "C" void hmg_debug_coop_labels(int* out) { cudaMemcpyFromSymbol(out, g_coop_label, sizeof(int) * 512); }
 extern "C" void hmg_debug_tile_phase(unsigned long long* out) {
-    cudaMemcpyFromSymbol(out, g_tile_phase, sizeof(unsigned long long) * 4);
+    cudaMemcpyFromSymbol(out, g_tile_phase, sizeof(unsigned long long) * 5);
 }
 extern "C" unsigned long long hmg_debug_tile_slow() {
     unsigned long long v = 0;

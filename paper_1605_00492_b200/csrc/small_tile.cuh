@@ -23,7 +23,7 @@ constexpr int kHaloW = kSmallHaloMax;  // width of the halo plane (<= 32 off-til
 
 #ifdef HMG_TIMING
 __device__ unsigned long long g_tile_slow_count;   // diagnostics: exact-division redos
-__device__ unsigned long long g_tile_phase[4];     // CTA 0 thread 0: residual pass, forward, backward cycles; calls
+__device__ unsigned long long g_tile_phase[5];     // CTA 0 thread 0: residual pass, forward, backward cycles; calls; forward waits
 #define TSTAMP(v) long long v = clock64()
 #define TACC(i, a, b) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_tile_phase[i] += (unsigned long long)((b) - (a)); } while (0)
 #else
@@ -229,19 +229,72 @@ __device__ __forceinline__ void tile_residuals_cta(const TileSmem& S, int nz, in
     }
 }
 
+// NB residual rows k0 .. k0 + NB - 1 into S.z (as tile_residuals_cta's batches)
+template <int TW, int NB>
+__device__ __forceinline__ void tile_residual_rows(const TileSmem& S, int nz, int nzp, int j, int k0, int l0, int l1,
+                                                   int l2, bool zero) {
+    double r[NB];
+    if (zero) {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) r[i] = S.b[(k0 + i) * TW + j];
+    } else {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+            const int k = k0 + i;
+            const int q = k * TW + j;
+            const int qm = k > 0 ? q - TW : q;          // in-range address; term skipped at k = 0
+            const int qp = k < nzp - 1 ? q + TW : q;
+            double acc = S.D[q] * S.u[q];
+            const double lo = S.U[qm] * S.u[qm];
+            const double hi = S.U[q] * S.u[qp];
+            acc = (k > 0) ? acc + lo : acc;
+            acc = (k < nz - 1) ? acc + hi : acc;
+            acc = acc + S.H0[q] * tile_nb<TW>(S, k, l0);
+            acc = acc + S.H1[q] * tile_nb<TW>(S, k, l1);
+            acc = acc + S.H2[q] * tile_nb<TW>(S, k, l2);
+            r[i] = S.b[q] - acc;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < NB; ++i) S.z[(k0 + i) * TW + j] = r[i];
+}
+
+// Named barriers 1 .. 15 hand residual batch b (8 layers) from the warp that
+// formed it to the chain warp: the overlapped form below serves nzp <= 128.
+constexpr int kOverlapMaxLayers = 128;
+__device__ __forceinline__ void named_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
 template <int TW = kTileW>
 __device__ __forceinline__ void tile_sweep_cta(const TileSmem& S, int nz, int warp, int j, int l0, int l1, int l2,
                                                bool zero, double omega, bool valid) {
     const int nzp = (nz + 7) & ~7;
+    const int nb = nzp / 8;
+    // The residual rows are independent per layer, the z recurrence is serial:
+    // with nzp <= 128 the rows are formed WHILE warp 0 runs the recurrence --
+    // batch 0 by all four warps (two layers each), batches 1 .. nb-1 by warps
+    // 1-3 in turn, each released to warp 0 by its own named barrier.
+    const bool overlap = nzp <= kOverlapMaxLayers && kTileWarps == 4;
     TSTAMP(p0);
-    tile_residuals_cta<TW>(S, nz, warp, j, l0, l1, l2, zero);
-    __syncthreads();
+    if (overlap) {
+        tile_residual_rows<TW, 2>(S, nz, nzp, j, 2 * warp, l0, l1, l2, zero);
+        __syncthreads();
+        if (warp > 0)
+            for (int bt = warp; bt < nb; bt += kTileWarps - 1) {
+                tile_residual_rows<TW, 8>(S, nz, nzp, j, 8 * bt, l0, l1, l2, zero);
+                named_arrive(bt, 64);
+            }
+    } else {
+        tile_residuals_cta<TW>(S, nz, warp, j, l0, l1, l2, zero);
+        __syncthreads();
+    }
     TSTAMP(p1);
     TACC(0, p0, p1);
     if (warp == 0) {
         bool slow = false;
         double zprev = 0.0;
         for (int k0 = 0; k0 < nzp; k0 += 8) {
+            if (overlap && k0 > 0) named_sync(k0 / 8, 64);   // residual batch k0 / 8 is formed
             double rr[8], um[8], dd[8], yy[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {

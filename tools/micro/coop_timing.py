@@ -38,12 +38,19 @@ n = next((i for i in range(1, 512) if v[i] == 0 or v[i] < v[i - 1]), 512)
 d = [v[i] - v[i - 1] for i in range(1, n)]
 print("stamps", n, "total cycles", v[n - 1] - v[0], f"= {(v[n - 1] - v[0]) / 1.965e3:.1f} us at 1965 MHz")
 print(" ".join(str(x) for x in d))
+lb = (ctypes.c_int * 512)()
+B.load_library().hmg_debug_coop_labels(lb)
+names = {1: "operand loads (incl. previous stores)", 2: "tile sweeps", 3: "to grid barrier passed", 4: "coarsest sweeps"}
+for key, nm in names.items():
+    tot = sum(d[i - 1] for i in range(1, n) if lb[i] == key)
+    cnt = sum(1 for i in range(1, n) if lb[i] == key)
+    print(f"  {nm}: {cnt} x, {tot} cyc = {tot / 1.965e3:.1f} us")
 f = B.load_library().hmg_debug_tile_slow
 f.restype = ctypes.c_ulonglong
 print("exact-division redos over 3 V-cycles (all CTAs):", f())
 
-ph = (ctypes.c_ulonglong * 4)()
+ph = (ctypes.c_ulonglong * 5)()
 B.load_library().hmg_debug_tile_phase(ph)
 n = max(ph[3], 1)
 print(f"tile_sweep_cta calls (CTA 0) {ph[3]}: residual pass {ph[0] / n:.0f} cyc, forward chain {ph[1] / n:.0f} cyc, "
-      f"backward {ph[2] / n:.0f} cyc per call")
+      f"backward {ph[2] / n:.0f} cyc per call; forward waiting for residual batches {ph[4] / n:.0f}")
