@@ -159,12 +159,32 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
             ptx::cp_async16(dst + k * w + 2 * ch, v + k * ld + col0 + 2 * ch);
         }
     };
+    // Tile metadata (the column's neighbour slots, the halo cell list) of the
+    // (level, tile) last visited, kept in registers: a CTA that owns one tile of
+    // a level reads it from global memory once per level, not once per step
+    // (three dependent L2 round trips at the start of every step otherwise).
+    const CoopLevel* m_lev = nullptr;
+    int m_t = -1, m_hcount = 0;
+    uint32_t m_loc = 0;
+    int32_t m_hc = 0;
+    auto meta = [&](const CoopLevel& L, int t) {
+        if (m_lev == &L && m_t == t) return;
+        const int64_t c = (int64_t)t * TW + j;
+        const uint32_t loc = L.sh.loc[c < L.V.n ? c : L.V.n - 1];
+        const int hcount = L.sh.count[t];
+        const int32_t hc = L.sh.cells[t * kSmallHaloMax + lane];   // slots past hcount: unused
+        m_loc = loc;
+        m_hcount = hcount;
+        m_hc = lane < hcount ? hc : 0;
+        m_lev = &L;
+        m_t = t;
+    };
     // off-tile neighbour values of v (cell >> shift) into the plane dst: lane h
     // of every warp gathers halo cell h, warps split the layers
     auto cp_halo = [&](double* dst, const double* v, const CoopLevel& L, int t, int shift, int64_t ldv) {
-        const int hcount = L.sh.count[t];
-        if (lane < hcount) {
-            const int32_t hc = L.sh.cells[t * kSmallHaloMax + lane] >> shift;
+        meta(L, t);
+        if (lane < m_hcount) {
+            const int32_t hc = m_hc >> shift;
             for (int k = warp; k < nz; k += kTileWarps) ptx::cp_async8(dst + k * kHaloW + lane, v + k * ldv + hc);
         }
     };
@@ -176,11 +196,11 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         if (jlane && c < L.V.n)
             for (int k = warp; k < nz; k += kTileWarps) dst[k * L.V.ld + c] = su[k * TW + j];
     };
-    auto slots = [&](const CoopLevel& L, int64_t c, int& l0, int& l1, int& l2) {
-        const uint32_t loc = L.sh.loc[c < L.V.n ? c : L.V.n - 1];
-        l0 = loc & 0xff;
-        l1 = (loc >> 8) & 0xff;
-        l2 = (loc >> 16) & 0xff;
+    auto slots = [&](const CoopLevel& L, int64_t c, int& l0, int& l1, int& l2) {   // c = t * TW + j
+        meta(L, (int)(c / TW));
+        l0 = m_loc & 0xff;
+        l1 = (m_loc >> 8) & 0xff;
+        l2 = (m_loc >> 16) & 0xff;
     };
     // What the vector planes hold: sb = tile res_t of res_b, su = the same tile
     // of res_u (the iterate this CTA last wrote or read for it).  A CTA that
@@ -336,7 +356,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
             load_static(l, t);
             cp_wait();
             // u + P u_c, the addition of the prolongation (0 + u_c from a zero iterate)
-            const int hcount = L.sh.count[t];
+            meta(L, t);
+            const int hcount = m_hcount;
             for (int k = warp; k < nz; k += kTileWarps) {
                 if (jlane) {
                     const double v = c_in ? su[k * TW + j] : 0.0;
