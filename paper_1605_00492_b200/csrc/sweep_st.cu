@@ -89,6 +89,8 @@ constexpr int kUcRow = 64;                 // forward u_c rows: 32 parents of th
                                            // tile and halo parts of u_c share the row stride kHaloMax)
 
 #ifdef HMG_TIMING
+__device__ unsigned long long g_cta_ns[2 * 1024];   // per CTA: globaltimer at start and end
+__device__ unsigned g_cta_sm[1024];
 __device__ long long g_st_timing[12];  // CTA 0, thread 0: [0] total, [1] forward wait, [2] backward wait, [3] tiles;
                                        // producer lane 0: [8] total, [9] waiting for free slots, [10] stages
 #endif
@@ -178,6 +180,16 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
     double* stages = reinterpret_cast<double*>(smraw + 1024);
 
     ptx::pdl_trigger();                                // the next kernel may start its prologue
+#ifdef HMG_TIMING
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_cta_ns[2 * blockIdx.x] = t;
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_cta_sm[blockIdx.x] = sm;
+    }
+#endif
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             ptx::mbar_init(&full[s], SPLIT ? 2 : 1);   // producer (+ gather warp)
@@ -465,6 +477,11 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                 l1 = (loc >> 8) & 0xff;
                 l2 = (loc >> 16) & 0xff;
             }
+#ifdef HMG_PROBE_NOCONFLICT
+            l0 = j;
+            l1 = (j + 1) & 127;
+            l2 = (j + 2) & 127;
+#endif
             // FLAT: stage offsets of the three neighbours' u at row 0 (tile row or halo row)
             const int no0 = l0 < kTile ? SL.u + l0 : SL.hu + (l0 - kTile);
             const int no1 = l1 < kTile ? SL.u + l1 : SL.hu + (l1 - kTile);
@@ -480,6 +497,11 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                 eo1 = (el >> 8) & 0xff;
                 eo2 = (el >> 16) & 0xff;
             }
+#ifdef HMG_PROBE_NOCONFLICT   // probe build only: lane-aligned gathers (wrong results, same instructions)
+            eo0 = j;
+            eo1 = j + 128;
+            eo2 = (j + 64) & 255;
+#endif
             ColumnGeom cg{};
 
             // Thomas forward elimination, reading R6 order (as k_sweep_tc's `layer`)
@@ -833,6 +855,13 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
         partial[blockIdx.x] = t;
     }
     if (warp == 0) ptx::tmem_dealloc(tbase, tmem_cols);
+#ifdef HMG_TIMING
+    if (threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_cta_ns[2 * blockIdx.x + 1] = t;
+    }
+#endif
 }
 
 uint32_t st_tmem_cols(int nz) {
@@ -900,6 +929,10 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
 #ifdef HMG_TIMING
 }  // namespace
 extern "C" void hmg_debug_st_timing(long long* out) { cudaMemcpyFromSymbol(out, g_st_timing, sizeof(long long) * 12); }
+extern "C" void hmg_debug_st_cta(unsigned long long* ns, unsigned* sm) {
+    cudaMemcpyFromSymbol(ns, g_cta_ns, sizeof(unsigned long long) * 2048);
+    cudaMemcpyFromSymbol(sm, g_cta_sm, sizeof(unsigned) * 1024);
+}
 namespace {
 #endif
 

@@ -31,4 +31,20 @@ for ref in (7, 6, 5):
     print(f"ref {ref}: tiles/CTA {nt}, total {tot} cyc = {tot/1965:.1f} us, per tile {tot/max(nt,1)/1965:.1f} us; "
           f"waiting fwd {wf/tot:.0%} bwd {wb/tot:.0%}; forward phase {tf/max(nt,1)/64:.0f} cyc/layer "
           f"(of which waiting {wf/max(nt,1)/64:.0f}), back phase incl. redo check {tb/max(nt,1)/64:.0f} cyc/layer, of which slow check + TMEM store wait {tws/max(nt,1)/64:.0f}; producer: {t[8]} cyc, waiting for free slots {t[9]/max(t[8],1):.0%}, forward stages {t[10]} ({(t[8]-t[9])/max(t[10],1):.0f} busy cyc per forward stage incl. backward issue, of which halo gathers {t[11]/max(t[10],1):.0f})")
+    ns = (ctypes.c_ulonglong * 2048)()
+    sm = (ctypes.c_uint * 1024)()
+    B.load_library().hmg_debug_st_cta(ns, sm)
+    ncta = next(i for i in range(1024) if ns[2 * i] == 0)
+    st = [ns[2 * i] for i in range(ncta)]
+    en = [ns[2 * i + 1] for i in range(ncta)]
+    t0 = min(st)
+    dur = sorted(en[i] - st[i] for i in range(ncta))
+    print(f"  CTAs {ncta}: start spread {(max(st) - t0) / 1e3:.1f} us, end spread {(max(en) - min(en)) / 1e3:.1f} us, "
+          f"kernel span {(max(en) - t0) / 1e3:.1f} us; CTA durations min {dur[0] / 1e3:.1f} median {dur[ncta // 2] / 1e3:.1f} "
+          f"max {dur[-1] / 1e3:.1f} us")
+    from collections import Counter
+    per_sm = Counter(sm[i] for i in range(ncta))
+    lone = [i for i in range(ncta) if per_sm[sm[i]] == 1]
+    if lone:
+        print(f"  {len(lone)} CTAs alone on their SM: durations {sorted(round((en[i] - st[i]) / 1e3, 1) for i in lone)[:6]} us")
     g.close()
