@@ -166,12 +166,18 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
     constexpr bool FLAT = !MF && !ZERO;         // neighbours read at per-tile offsets
     constexpr bool SPLIT = !MF && !ZERO;        // halo gathers issued by their own warp
     constexpr bool TSTORE = !ZERO;              // u' rows written back by TMA from the backward stage
+    // IL: tile p's forward elimination interleaved with tile p - 1's back
+    // substitution (see the consumers); stored bands and a non-zero guess
+    constexpr bool IL = SPLIT;
+    constexpr int kGpc = kBack / G;             // forward groups per 8-layer chunk
+    static_assert(kBack % G == 0, "a chunk holds whole groups");
     static_assert(kUcRow == kHaloMax, "u_c tile and halo rows share one stride");
     const int nz = L.nz;
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
     const int nchunks = ZERO ? 0 : (nz + kBack - 1) / kBack;
     const int ntiles = (int)((L.n + kTile - 1) / kTile);
+    const int ntc = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;   // my tiles
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
     uint64_t* empty = full + S;
@@ -287,40 +293,55 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                 phase ^= 1u;
             }
         };
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int hcount = th.count[tile];
-            const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
-            const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
-            const int ehc = EH ? et.hcount[tile] : 0;
-            const int32_t eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
-            for (int gi = 0; gi < ngroups; ++gi, advance()) {
-                ptx::mbar_wait(&empty[s], phase ^ 1u);
-                double* st = stages + (size_t)s * SL.stage;
-                if (kProbeHalo) {
-                    for (int kk = 0; kk < G; ++kk) {
-                        const int k = gi * G + kk;
-                        if (k >= nz) break;
-                        if (EH && lane < ehc)
-                            ptx::cp_async8(st + SL.eh + kk * kEdgeRow + kEdgeRange + lane,
-                                           et.H + (int64_t)k * et.ldE + eh0);
-                        const double* src = uin + (int64_t)k * ld;
-                        if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane, src + h0);
-                        if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane + 32, src + h1);
-                        if (PROLONG) {
-                            const double* srcc = uc + (int64_t)k * ldc;
-                            if (lane < hcount) ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane, srcc + (h0 >> 2));
-                            if (lane + 32 < hcount)
-                                ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane + 32, srcc + (h1 >> 2));
-                        }
-                    }
-                    ptx::cp_async_arrive(&full[s]);
-                }
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&full[s]);
+        // stage order of the interleaved schedule (IL, see the consumers): pass p
+        // takes, per 8-layer chunk, tile p - 1's backward stage, then tile p's
+        // forward stages of those layers
+        for (int p = 0; p <= ntc; ++p) {
+            const bool hasF = p < ntc, hasB = p > 0;
+            const int tile = (int)blockIdx.x + p * (int)gridDim.x;
+            int hcount = 0, ehc = 0;
+            int32_t h0 = 0, h1 = 0, eh0 = 0;
+            if (hasF) {
+                hcount = th.count[tile];
+                h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
+                h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
+                ehc = EH ? et.hcount[tile] : 0;
+                eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
             }
-            for (int m = nchunks - 1; m >= 0; --m, advance()) {   // backward stages: one arrival each
-                ptx::mbar_wait(&empty[s], phase ^ 1u);
-                if (lane == 0) ptx::mbar_arrive(&full[s]);
+            for (int ch = 0; ch < nchunks; ++ch) {
+                if (hasB) {                                    // backward stage: one arrival
+                    ptx::mbar_wait(&empty[s], phase ^ 1u);
+                    if (lane == 0) ptx::mbar_arrive(&full[s]);
+                    advance();
+                }
+                if (!hasF) continue;
+                const int g1 = (ch + 1) * kGpc < ngroups ? (ch + 1) * kGpc : ngroups;
+                for (int gi = ch * kGpc; gi < g1; ++gi, advance()) {
+                    ptx::mbar_wait(&empty[s], phase ^ 1u);
+                    double* st = stages + (size_t)s * SL.stage;
+                    if (kProbeHalo) {
+                        for (int kk = 0; kk < G; ++kk) {
+                            const int k = gi * G + kk;
+                            if (k >= nz) break;
+                            if (EH && lane < ehc)
+                                ptx::cp_async8(st + SL.eh + kk * kEdgeRow + kEdgeRange + lane,
+                                               et.H + (int64_t)k * et.ldE + eh0);
+                            const double* src = uin + (int64_t)k * ld;
+                            if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane, src + h0);
+                            if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane + 32, src + h1);
+                            if (PROLONG) {
+                                const double* srcc = uc + (int64_t)k * ldc;
+                                if (lane < hcount)
+                                    ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane, srcc + (h0 >> 2));
+                                if (lane + 32 < hcount)
+                                    ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane + 32, srcc + (h1 >> 2));
+                            }
+                        }
+                        ptx::cp_async_arrive(&full[s]);
+                    }
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&full[s]);
+                }
             }
         }
     } else if (warp == kConsumerWarps) {
@@ -344,96 +365,112 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
 #ifdef HMG_TIMING
         long long p0 = clock64(), pw = 0, pn = 0, ph = 0;
 #endif
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        // one forward stage (group gi of the tile at column x)
+        auto fwd_stage = [&](int tile, int gi, int hcount, int32_t h0, int32_t h1, int32_t ee0, uint32_t ebytes) {
             const int x = tile * kTile, xc = x / 4;
-            const int hcount = HALO && !SPLIT ? th.count[tile] : 0;
-            const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
-            const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
-            // edge store: the tile's contiguous edge range (its gathered edges: gather warp)
-            const int32_t ee0 = EH ? et.e0[tile] : 0;
-            const uint32_t ebytes = EH ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
-            for (int gi = 0; gi < ngroups; ++gi, advance()) {
 #ifdef HMG_TIMING
-                long long q0 = clock64();
+            long long q0 = clock64();
 #endif
-                ptx::mbar_wait(&empty[s], phase ^ 1u);
+            ptx::mbar_wait(&empty[s], phase ^ 1u);
 #ifdef HMG_TIMING
-                pw += clock64() - q0;
-                ++pn;
+            pw += clock64() - q0;
+            ++pn;
 #endif
-                double* st = stages + (size_t)s * SL.stage;
-#ifdef HMG_TIMING
-                const long long q1 = clock64();
-#endif
-                if (HALO && !SPLIT && kProbeHalo) {
-                    for (int kk = 0; kk < G; ++kk) {          // off-tile neighbours of the G layers
-                        const int k = gi * G + kk;
-                        if (k >= nz) break;
-                        if (!ZERO) {
-                            const double* src = uin + (int64_t)k * ld;
-                            if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane, src + h0);
-                            if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane + 32, src + h1);
-                        }
-                        if (PROLONG) {
-                            const double* srcc = uc + (int64_t)k * ldc;
-                            if (lane < hcount) ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane, srcc + (h0 >> 2));
-                            if (lane + 32 < hcount)
-                                ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane + 32, srcc + (h1 >> 2));
-                        }
-                        if (MF) {
-                            const double* srcl = op.lam + (int64_t)k * ld;
-                            if (lane < hcount) ptx::cp_async8(st + SL.hlam + kk * kHaloMax + lane, srcl + h0);
-                            if (lane + 32 < hcount) ptx::cp_async8(st + SL.hlam + kk * kHaloMax + lane + 32, srcl + h1);
-                        }
+            double* st = stages + (size_t)s * SL.stage;
+            if (HALO && !SPLIT && kProbeHalo) {
+                for (int kk = 0; kk < G; ++kk) {          // off-tile neighbours of the G layers
+                    const int k = gi * G + kk;
+                    if (k >= nz) break;
+                    if (!ZERO) {
+                        const double* src = uin + (int64_t)k * ld;
+                        if (lane < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane, src + h0);
+                        if (lane + 32 < hcount) ptx::cp_async8(st + SL.hu + kk * HS + lane + 32, src + h1);
                     }
-                    ptx::cp_async_arrive(&full[s]);
+                    if (PROLONG) {
+                        const double* srcc = uc + (int64_t)k * ldc;
+                        if (lane < hcount) ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane, srcc + (h0 >> 2));
+                        if (lane + 32 < hcount)
+                            ptx::cp_async8(st + SL.huc + kk * kHaloMax + lane + 32, srcc + (h1 >> 2));
+                    }
+                    if (MF) {
+                        const double* srcl = op.lam + (int64_t)k * ld;
+                        if (lane < hcount) ptx::cp_async8(st + SL.hlam + kk * kHaloMax + lane, srcl + h0);
+                        if (lane + 32 < hcount) ptx::cp_async8(st + SL.hlam + kk * kHaloMax + lane + 32, srcl + h1);
+                    }
                 }
-                __syncwarp();
-#ifdef HMG_TIMING
-                ph += clock64() - q1;
-#endif
-                if (lane == 0) {
-                    if (pf_groups > 0 && gi + pf_groups < ngroups) {   // L2 prefetch a few stages ahead
-                        const int gp = gi + pf_groups;
-                        if (MF)
-                            ptx::tma_prefetch_2d(&maps.lam, x, gp * G);
-                        else
-                            ptx::tma_prefetch_3d(&maps.bands, x, gp * G, 0);
-                        ptx::tma_prefetch_2d(&maps.b, x, gp * G);
-                        if (!ZERO) ptx::tma_prefetch_2d(&maps.uf, x, gp * G);
-                    }
-                    int nl = nz - gi * G;
-                    nl = nl < G ? nl : G;
-                    ptx::mbar_arrive_expect_tx(&full[s], fwd_bytes + (EH && kProbeEdge ? (uint32_t)nl * ebytes : 0u));
-                    if (EH && kProbeEdge)
-                        for (int kk = 0; kk < nl; ++kk)
-                            ptx::bulk_g2s(st + SL.eh + kk * kEdgeRow, et.H + (int64_t)(gi * G + kk) * et.ldE + ee0,
-                                          ebytes, &full[s]);
+                ptx::cp_async_arrive(&full[s]);
+            }
+            __syncwarp();
+            if (lane == 0) {
+                if (pf_groups > 0 && gi + pf_groups < ngroups) {   // L2 prefetch a few stages ahead
+                    const int gp = gi + pf_groups;
                     if (MF)
-                        ptx::tma_load_2d_hint(st + SL.op, &maps.lam, x, gi * G, &full[s], pol_stream);
+                        ptx::tma_prefetch_2d(&maps.lam, x, gp * G);
                     else
-                        ptx::tma_load_3d_hint(st + SL.op, &maps.bands, x, gi * G, 0, &full[s], pol_stream);
-                    ptx::tma_load_2d_hint(st + SL.b, &maps.b, x, gi * G, &full[s], DOT ? pol_keep : pol_stream);
-                    if (!ZERO) ptx::tma_load_2d_hint(st + SL.u, &maps.uf, x, gi * G, &full[s], pol_keep);
-                    if (PROLONG) ptx::tma_load_2d_hint(st + SL.uc, &maps.ucf, xc, gi * G, &full[s], pol_keep);
+                        ptx::tma_prefetch_3d(&maps.bands, x, gp * G, 0);
+                    ptx::tma_prefetch_2d(&maps.b, x, gp * G);
+                    if (!ZERO) ptx::tma_prefetch_2d(&maps.uf, x, gp * G);
+                }
+                int nl = nz - gi * G;
+                nl = nl < G ? nl : G;
+                ptx::mbar_arrive_expect_tx(&full[s], fwd_bytes + (EH && kProbeEdge ? (uint32_t)nl * ebytes : 0u));
+                if (EH && kProbeEdge)
+                    for (int kk = 0; kk < nl; ++kk)
+                        ptx::bulk_g2s(st + SL.eh + kk * kEdgeRow, et.H + (int64_t)(gi * G + kk) * et.ldE + ee0,
+                                      ebytes, &full[s]);
+                if (MF)
+                    ptx::tma_load_2d_hint(st + SL.op, &maps.lam, x, gi * G, &full[s], pol_stream);
+                else
+                    ptx::tma_load_3d_hint(st + SL.op, &maps.bands, x, gi * G, 0, &full[s], pol_stream);
+                ptx::tma_load_2d_hint(st + SL.b, &maps.b, x, gi * G, &full[s], DOT ? pol_keep : pol_stream);
+                if (!ZERO) ptx::tma_load_2d_hint(st + SL.u, &maps.uf, x, gi * G, &full[s], pol_keep);
+                if (PROLONG) ptx::tma_load_2d_hint(st + SL.uc, &maps.ucf, xc, gi * G, &full[s], pol_keep);
+            }
+            advance();
+        };
+        // one backward stage: the u rows (u_c, b) of chunk m of the tile at column x, again
+        auto bwd_stage = [&](int tile, int m) {
+            const int x = tile * kTile, xc = x / 4;
+#ifdef HMG_TIMING
+            long long q0 = clock64();
+#endif
+            ptx::mbar_wait(&empty[s], phase ^ 1u);
+#ifdef HMG_TIMING
+            pw += clock64() - q0;
+#endif
+            double* st = stages + (size_t)s * SL.stage;
+            if (lane == 0 && !kProbeBwd) ptx::mbar_arrive(&full[s]);
+            if (lane == 0 && kProbeBwd) {
+                ptx::mbar_arrive_expect_tx(&full[s], bwd_bytes);
+                ptx::tma_load_2d_hint(st, &maps.ub, x, m * kBack, &full[s], pol_stream);
+                if (PROLONG) ptx::tma_load_2d_hint(st + kBack * kTile, &maps.ucb, xc, m * kBack, &full[s], pol_stream);
+                if (DOT) ptx::tma_load_2d_hint(st + kBack * kTile, &maps.bb, x, m * kBack, &full[s], pol_stream);
+            }
+            advance();
+        };
+        if (IL) {
+            for (int p = 0; p <= ntc; ++p) {
+                const bool hasF = p < ntc, hasB = p > 0;
+                const int tile = (int)blockIdx.x + p * (int)gridDim.x;
+                const int32_t ee0 = EH && hasF ? et.e0[tile] : 0;
+                const uint32_t ebytes = EH && hasF ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
+                for (int ch = 0; ch < nchunks; ++ch) {
+                    if (hasB) bwd_stage(tile - (int)gridDim.x, nchunks - 1 - ch);
+                    if (!hasF) continue;
+                    const int g1 = (ch + 1) * kGpc < ngroups ? (ch + 1) * kGpc : ngroups;
+                    for (int gi = ch * kGpc; gi < g1; ++gi) fwd_stage(tile, gi, 0, 0, 0, ee0, ebytes);
                 }
             }
-            for (int m = nchunks - 1; m >= 0; --m, advance()) {   // u rows again for the back substitution
-#ifdef HMG_TIMING
-                long long q0 = clock64();
-#endif
-                ptx::mbar_wait(&empty[s], phase ^ 1u);
-#ifdef HMG_TIMING
-                pw += clock64() - q0;
-#endif
-                double* st = stages + (size_t)s * SL.stage;
-                if (lane == 0 && !kProbeBwd) ptx::mbar_arrive(&full[s]);
-                if (lane == 0 && kProbeBwd) {
-                    ptx::mbar_arrive_expect_tx(&full[s], bwd_bytes);
-                    ptx::tma_load_2d_hint(st, &maps.ub, x, m * kBack, &full[s], pol_stream);
-                    if (PROLONG) ptx::tma_load_2d_hint(st + kBack * kTile, &maps.ucb, xc, m * kBack, &full[s], pol_stream);
-                    if (DOT) ptx::tma_load_2d_hint(st + kBack * kTile, &maps.bb, x, m * kBack, &full[s], pol_stream);
-                }
+        } else {
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int hcount = HALO && !SPLIT ? th.count[tile] : 0;
+                const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
+                const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
+                // edge store: the tile's contiguous edge range (its gathered edges: gather warp)
+                const int32_t ee0 = EH ? et.e0[tile] : 0;
+                const uint32_t ebytes = EH ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
+                for (int gi = 0; gi < ngroups; ++gi) fwd_stage(tile, gi, hcount, h0, h1, ee0, ebytes);
+                for (int m = nchunks - 1; m >= 0; --m) bwd_stage(tile, m);   // u rows again for the back substitution
             }
         }
 #ifdef HMG_TIMING
@@ -448,7 +485,8 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
         // ======================= consumer warps: one column per thread =======================
         const int j = threadIdx.x;
         const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
-        const uint32_t gcol = 2u * (uint32_t)nz;   // g_k at TMEM columns 2nz + 2k, z_k at 2k
+        const int nzp = nchunks * kBack;           // layers rounded up to whole chunks (>= nz)
+        const uint32_t gcol = 2u * (uint32_t)(ZERO ? nz : nzp);   // g at TMEM columns gcol + 2 slot, z at 2 slot
         const double ydz = MF ? div_recip(op.dz) : 0.0;   // exact redo only
         int pend = -1;                                     // TSTORE: slot whose store may still read it
         int s = 0;
@@ -462,16 +500,90 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
 #ifdef HMG_TIMING
         tt0 = clock64();
 #endif
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        // IL schedule.  Pass p runs tile p's forward elimination and, chunk by
+        // chunk (8 layers, top-down), tile p - 1's back substitution: before the
+        // forward stages of layers 8c .. 8c+7, the back substitution of chunk
+        // nchunks-1-c.  The (z, g) of layer k sit in TMEM slot k for even passes
+        // and nzp - 1 - k for odd ones, so the forward pass writes each slot just
+        // after the back substitution of the previous tile has read it: two
+        // tiles' recurrences share one tile's TMEM, the loads stay continuous
+        // through the back substitution, and its u' rows are written while the
+        // next tile streams in.
+        int btile = 0;
+        bool bvalid = false, bodd = false;
+        double bdl = 0.0;
+        const int mtop_il = nchunks - 1;
+        auto bwd_chunk = [&](int m) {
+            const int k0 = m * kBack;
+            const int kt = (k0 + kBack - 1 < nz - 1) ? k0 + kBack - 1 : nz - 1;
+            const uint32_t sb = bodd ? (uint32_t)(nzp - kBack - k0) : (uint32_t)k0;
+            uint32_t zr[16], gr[16];
+            ptx::tmem_ld_8f64(tl + 2u * sb, zr);
+            ptx::tmem_ld_8f64(tl + gcol + 2u * sb, gr);
+            ptx::mbar_wait(&full[s], phase);
+            double* su = stages + (size_t)s * SL.stage;
+            ptx::tmem_wait_ld();
+            double zv[kBack], gv[kBack];                   // by layer k0 + i
+#pragma unroll
+            for (int i = 0; i < kBack; ++i) {
+                const int q = bodd ? kBack - 1 - i : i;
+                zv[i] = ptx::f64_from(zr[2 * q], zr[2 * q + 1]);
+                gv[i] = ptx::f64_from(gr[2 * q], gr[2 * q + 1]);
+            }
+            auto finish = [&](int i) {
+                double uo = su[i * kTile + j];
+                if (PROLONG) uo = uo + su[kBack * kTile + i * (kTile / 4) + (j >> 2)];
+                const double o = uo + omega * bdl;
+                su[i * kTile + j] = o;
+                if (DOT && bvalid) dotacc = dotacc + su[kBack * kTile + i * kTile + j] * o;
+            };
+            if (m < mtop_il) {                         // full chunk, every layer below nz - 1
+#pragma unroll
+                for (int i = kBack - 1; i >= 0; --i) {
+                    bdl = zv[i] - gv[i] * bdl;
+                    finish(i);
+                }
+            } else {
+#pragma unroll
+                for (int i = kBack - 1; i >= 0; --i) {
+                    const int k = k0 + i;
+                    if (k > kt) continue;
+                    bdl = (k == nz - 1) ? zv[i] : zv[i] - gv[i] * bdl;
+                    finish(i);
+                }
+            }
+            ptx::fence_proxy_async_smem();
+            ptx::named_bar_sync(1, kTile);
+            if (warp == 0) {
+                if (lane == 0) {
+                    ptx::tma_store_2d(&maps.uo, btile * kTile, k0, su);
+                    ptx::bulk_commit_group();
+                    ptx::bulk_wait_group_read<0>();
+                    ptx::mbar_arrive(&empty[s]);
+                }
+                __syncwarp();
+            } else {
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&empty[s]);
+            }
+            advance();
+        };
+        const int npass = IL ? ntc + 1 : ntc;
+        for (int pass = 0; pass < npass; ++pass) {
+            const int tile = (int)blockIdx.x + pass * (int)gridDim.x;
+            const bool hasF = pass < ntc, hasB = IL && pass > 0;
+            const bool fodd = IL && (pass & 1);
+            // TMEM slot of layer k of this pass's tile
+            auto fslot = [&](int k) -> uint32_t { return (uint32_t)(fodd ? nzp - 1 - k : k); };
 #ifdef HMG_TIMING
             ++ntl;
             tfw0 = clock64();
 #endif
             const int64_t c = (int64_t)tile * kTile + j;
-            const bool valid = c < L.n;
+            const bool valid = hasF && c < L.n;
             const int64_t cv = valid ? c : L.n - 1;
             int l0 = 0, l1 = 0, l2 = 0;
-            if (HALO) {
+            if (HALO && hasF) {
                 const uint32_t loc = th.loc[cv];
                 l0 = loc & 0xff;
                 l1 = (loc >> 8) & 0xff;
@@ -491,7 +603,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
             const int nc1 = l1 < kTile ? SL.uc + (l1 >> 2) : SL.huc + (l1 - kTile);
             const int nc2 = l2 < kTile ? SL.uc + (l2 >> 2) : SL.huc + (l2 - kTile);
             int eo0 = 0, eo1 = 0, eo2 = 0;                 // the faces' offsets in an edge row
-            if (EH) {
+            if (EH && hasF) {
                 const uint32_t el = et.loc[cv];
                 eo0 = el & 0xff;
                 eo1 = (el >> 8) & 0xff;
@@ -521,12 +633,16 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                     if (has_g) g = div_fast(Uk, den, y, slow);
                 }
                 ok = ok && pivot_ok(den);
-                ptx::tmem_st_f64(tl + 2u * (uint32_t)k, z);
-                if (has_g) ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, g);
+                ptx::tmem_st_f64(tl + 2u * fslot(k), z);
+                if (has_g) ptx::tmem_st_f64(tl + gcol + 2u * fslot(k), g);
                 zprev = z;
                 gprev = g;
             };
-            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+            for (int ch = 0; ch < (IL ? nchunks : 1); ++ch) {
+            if (hasB) bwd_chunk(nchunks - 1 - ch);
+            const int ga = IL ? ch * kGpc : 0;
+            const int gb = !hasF ? ga : !IL ? ngroups : ((ch + 1) * kGpc < ngroups ? (ch + 1) * kGpc : ngroups);
+            for (int gi = ga; gi < gb; ++gi, advance()) {
 #ifdef HMG_TIMING
                 long long w0 = clock64();
 #endif
@@ -593,8 +709,8 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                     }
 #ifdef HMG_PROBE_NOCHAIN
                     if (IN) {   // probe build only: no Thomas chain (wrong results, same data movement)
-                        ptx::tmem_st_f64(tl + 2u * (uint32_t)k, r);
-                        ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, Uk);
+                        ptx::tmem_st_f64(tl + 2u * fslot(k), r);
+                        ptx::tmem_st_f64(tl + gcol + 2u * fslot(k), Uk);
                         zprev = r;
                         gprev = Uk;
                     } else
@@ -608,8 +724,8 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                         // g_k were established at build time (k_pivot_check)
                         const double g = CHK ? div_fast(Uk, den, y, slow) : div_fast_unchecked(Uk, den, y);
                         if (CHK) ok = ok && pivot_ok(den);
-                        ptx::tmem_st_f64(tl + 2u * (uint32_t)k, z);
-                        ptx::tmem_st_f64(tl + gcol + 2u * (uint32_t)k, g);
+                        ptx::tmem_st_f64(tl + 2u * fslot(k), z);
+                        ptx::tmem_st_f64(tl + gcol + 2u * fslot(k), g);
                         zprev = z;
                         gprev = g;
                     } else {
@@ -630,6 +746,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&empty[s]);
             }
+            }   // chunks
 #ifdef HMG_TIMING
             tfw += clock64() - tfw0;
             tfw0 = clock64();
@@ -639,7 +756,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
 #ifdef HMG_PROBE_NOREDO
             if (false) {
 #else
-            if (__any_sync(0xffffffffu, slow && valid)) {
+            if (__any_sync(0xffffffffu, slow && valid)) {   // (valid implies this pass has a forward tile)
 #endif
                 const int32_t g0 = L.nbr[cv], g1 = L.nbr[ld + cv], g2 = L.nbr[2 * ld + cv];
                 auto GU = [&](int kk, int64_t cell) -> double {
@@ -696,6 +813,13 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
             }
             if (valid && !ok) atomicMin(bad, ((unsigned long long)ref << 40) | (unsigned long long)c);
             ptx::tmem_wait_st();
+            if (IL) {                                  // this tile's back substitution: next pass
+                btile = tile;
+                bvalid = valid;
+                bodd = fodd;
+                bdl = 0.0;
+                continue;
+            }
 #ifdef HMG_TIMING
             tws += clock64() - tfw0;
 #endif
