@@ -1,0 +1,4 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
+timeout 600 python tools/micro/st_probe.py normal
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
+timeout 600 python tools/micro/fine_kernels.py
