@@ -501,6 +501,29 @@ def test_streamed_kernels_layer_counts(nz):
     o.close()
 
 
+@pytest.mark.parametrize("nz", [9, 60, 65, 100])
+def test_interleaved_sweep_multi_tile_layer_counts(nz):
+    """The interleaved schedule of the streamed sweep (k_sweep_st):
+    on ref 6 (640 tiles, three per CTA) every CTA runs forward passes with the
+    mirrored TMEM slots (odd passes) and back substitutions of a previous tile
+    between them; layer counts with a partial top chunk (9, 60, 65, 100), one and
+    two CTAs per SM.  Sweeps, the V-cycle (fused prolongation) and PCG (fused
+    <r, z>) against the oracle."""
+    cfg = hi.Config("il", 6, 4, nz, 0.001, 1e-5)
+    lam, b = hi.make_inputs(cfg)
+    g = Hierarchy(6, 4, nz, 0.001, 1e-5, lam)
+    o = oracle.Hierarchy(6, 4, nz, 0.001, 1e-5, lam)
+    x = hi.uniform_vector(b.shape, 23)
+    u = g.to_device(6, x)
+    g.line_smooth(6, g.to_device(6, b), u, 3, 0.8, False)
+    assert np.array_equal(g.to_host(6, u), o.sweep(6, b, x, 3, 0.8))
+    assert np.array_equal(g.to_host(6, g.vcycle(g.to_device(6, b))), o.vcycle(b, 2, 2, 20, 0.8))
+    _, it, _, st = g.pcg_solve(g.to_device(6, b))
+    assert st == "HMG_OK" and it == o.pcg(b)[1]
+    g.close()
+    o.close()
+
+
 @pytest.mark.parametrize("nz", [64, 128])
 def test_edge_store_forced_on_small_levels(monkeypatch, nz):
     """The edge-deduplicated coupling store is built only on
