@@ -36,7 +36,7 @@ namespace {
 
 constexpr int kTile = kSweepTile;
 constexpr int kConsumerWarps = kTile / 32;
-constexpr int kThreads = kTile + 32;
+constexpr int kThreads = kTile + 64;   // + a producer warp (TMA) and a gather warp (off-tile cp.async)
 
 struct ApMaps {
     CUtensorMap bands;  // 3-D box kTile x G x 5 (x 2: D, U with the edge store)
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     ptx::pdl_trigger();
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&full[s], 2);   // producer + gather warp
             ptx::mbar_init(&empty[s], kConsumerWarps);
         }
         ptx::fence_mbar_init();
@@ -108,18 +108,13 @@ __global__ void __launch_bounds__(kThreads, 3)
             phase ^= 1u;
         }
     };
-    if (warp == kConsumerWarps) {
-        // ======================= producer warp =======================
-        const uint64_t pol = ptx::policy_evict_first();
-        const uint32_t bytes = (uint32_t)(sizeof(double) * ((EH ? 2 : 5) * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile +
-                                                            (RESID ? G * kTile : 0)));
+    if (warp == kConsumerWarps + 1) {
+        // ============ gather warp: off-tile operands and gathered couplings ============
+        // (issued here, not by the producer, whose TMA issue is on the critical path)
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-            const int x = tile * kTile;
             const int hcount = th.count[tile];
             const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
             const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
-            const int32_t ee0 = EH ? et.e0[tile] : 0;
-            const uint32_t ebytes = EH ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
             const int ehc = EH ? et.hcount[tile] : 0;
             const int32_t eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
@@ -141,6 +136,21 @@ __global__ void __launch_bounds__(kThreads, 3)
                 }
                 ptx::cp_async_arrive(&full[s]);
                 __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full[s]);
+            }
+        }
+    } else if (warp == kConsumerWarps) {
+        // ======================= producer warp =======================
+        const uint64_t pol = ptx::policy_evict_first();
+        const uint32_t bytes = (uint32_t)(sizeof(double) * ((EH ? 2 : 5) * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile +
+                                                            (RESID ? G * kTile : 0)));
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int x = tile * kTile;
+            const int32_t ee0 = EH ? et.e0[tile] : 0;
+            const uint32_t ebytes = EH ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
+            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+                ptx::mbar_wait(&empty[s], phase ^ 1u);
+                double* st = stages + (size_t)s * AL.stage;
                 if (lane == 0) {
                     int nl = nz - gi * G;
                     nl = nl < G ? nl : G;
