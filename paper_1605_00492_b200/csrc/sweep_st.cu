@@ -127,9 +127,9 @@ __host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool m
     L.u = L.b + G * kTile;
     L.uc = L.u + (zero ? 0 : (G + 1) * kTile);
     L.hu = L.uc + (prolong ? (G + 1) * kUcRow : 0);
-    // halo rows of u: kHaloMax apart (a neighbour's row stride, tile or halo, is
-    // precomputed per column)
-    L.huc = L.hu + (zero ? 0 : G * kHaloMax);
+    // halo rows of u: stride kTile where no prolongation / matrix-free parts use
+    // them, so a neighbour is read at (tile or halo offset) + kk * kTile alike
+    L.huc = L.hu + (zero ? 0 : G * (mf ? kHaloMax : kTile));
     L.hlam = L.huc + (prolong ? G * kHaloMax : 0);
     L.eh = L.hlam + (mf ? G * kHaloMax : 0);
     L.fwd = L.eh + (eh ? G * kEdgeRow : 0);
@@ -137,10 +137,6 @@ __host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool m
     L.stage = L.fwd > L.bwd ? L.fwd : L.bwd;
     return L;
 }
-
-// Barrier header in front of the ring: full, empty, mid barriers of S stages and
-// the TMEM address slot, rounded up to the TMA alignment of the stages.
-__host__ __device__ constexpr uint32_t st_header_bytes(int S) { return (uint32_t)((3 * 8 * S + 16 + 127) / 128 * 128); }
 
 // Operator of one launch: the level's stored bands (view) or, matrix-free,
 // its coefficient and geometry.
@@ -157,9 +153,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc, double* __restrict__ uout,
                double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols, int pf_groups,
                double* __restrict__ partial) {
-    // 128-byte alignment (TMA): with 1024 the DOT variants' static reduction array
-    // padded the block to 1 KB of static shared memory, and two CTAs no longer fit an SM
-    extern __shared__ __align__(128) unsigned char smraw[];
+    extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ double dred[kThreadsSplit / 32];
     static_assert(!(EH && (ZERO || MF)), "edge store: general stored-band sweeps only");
     constexpr StLayout SL = st_layout(ZERO, PROLONG, MF, G, DOT, EH);
@@ -168,7 +162,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
     long long tt0 = 0, wf = 0, wb = 0, ntl = 0, tfw = 0, tbk = 0, tfw0 = 0, tws = 0;
 #endif
     constexpr bool HALO = !ZERO || MF;       // off-tile neighbour values needed
-    constexpr int HS = kHaloMax;                // stride of the halo rows of u
+    constexpr int HS = MF ? kHaloMax : kTile;   // stride of the halo rows of u
     constexpr bool FLAT = !MF && !ZERO;         // neighbours read at per-tile offsets
     constexpr bool SPLIT = !MF && !ZERO;        // halo gathers issued by their own warp
     constexpr bool TSTORE = !ZERO;              // u' rows written back by TMA from the backward stage
@@ -189,7 +183,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
     uint64_t* empty = full + S;
     uint64_t* mid = empty + S;                        // matrix-free: the stage's band rows are formed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mid + S);
-    double* stages = reinterpret_cast<double*>(smraw + st_header_bytes(S));
+    double* stages = reinterpret_cast<double*>(smraw + 1024);
 
     ptx::pdl_trigger();                                // the next kernel may start its prologue
 #ifdef HMG_TIMING
@@ -604,9 +598,6 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
             const int no0 = l0 < kTile ? SL.u + l0 : SL.hu + (l0 - kTile);
             const int no1 = l1 < kTile ? SL.u + l1 : SL.hu + (l1 - kTile);
             const int no2 = l2 < kTile ? SL.u + l2 : SL.hu + (l2 - kTile);
-            const int ns0 = l0 < kTile ? kTile : HS;       // their row strides
-            const int ns1 = l1 < kTile ? kTile : HS;
-            const int ns2 = l2 < kTile ? kTile : HS;
             // PROLONG: offsets of the neighbours' u_c (parent in the tile's rows, or halo row)
             const int nc0 = l0 < kTile ? SL.uc + (l0 >> 2) : SL.huc + (l0 - kTile);
             const int nc1 = l1 < kTile ? SL.uc + (l1 >> 2) : SL.huc + (l1 - kTile);
@@ -678,7 +669,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                 };
                 auto NBRF = [&](int kk, int q, int l) -> double {   // neighbour q (slot l) of the column
                     if (FLAT) {
-                        double v = st[q == 0 ? no0 + kk * ns0 : q == 1 ? no1 + kk * ns1 : no2 + kk * ns2];
+                        double v = st[(q == 0 ? no0 : q == 1 ? no1 : no2) + kk * kTile];
                         if (PROLONG) v = v + st[(q == 0 ? nc0 : q == 1 ? nc1 : nc2) + kk * kUcRow];
                         return v;
                     }
@@ -1013,11 +1004,10 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
     const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
     const bool two = cols <= 256;                  // two CTAs' Thomas state fit one SM's tensor memory
-    // two CTAs: half the SM's 228 KB less each CTA's 1 KB reservation and static shared memory
-    const size_t budget = two ? 114 * 1024 - 1024 - 128 : 220 * 1024;
-    int S = 32;
-    while (S > 2 && st_header_bytes(S) + sizeof(double) * (size_t)S * SL.stage > budget) --S;
-    size_t smem = st_header_bytes(S) + sizeof(double) * (size_t)S * SL.stage;
+    const size_t budget = two ? 110 * 1024 : 220 * 1024;
+    int S = (int)((budget - 1024) / (sizeof(double) * SL.stage));
+    S = S < 2 ? 2 : (S > 32 ? 32 : S);
+    size_t smem = 1024 + sizeof(double) * (size_t)S * SL.stage;
     const size_t floor_smem = two ? 80 * 1024 : 120 * 1024;   // never a third CTA per SM (TMEM)
     if (smem < floor_smem) smem = floor_smem;
     static bool attr = false;
