@@ -1,4 +1,4 @@
-# round 2 measurement set (rerun after the interleaved sweep, gather warps): GPU suite, smoke, default bench, reference arm, C2a/C2c/C4/C1 lines,
+# round 2 measurement set (rerun: interleaved sweep, gather warps): GPU suite, smoke, default bench, reference arm, C2a/C2c/C4/C1 lines,
 # ncu launch list of the bench command, ncu full capture of the fine-level kernels
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
