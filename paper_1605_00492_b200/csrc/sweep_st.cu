@@ -13,15 +13,20 @@
 //    its TMA ring and, with the fused prolongation, leaves two stages.  Here
 //    the u rows travel in the ring like every other operand: a forward stage
 //    carries G layers of the bands and b, G + 1 layers of u (layer k + 1 of the
-//    own column is needed at layer k) and the <= 64 off-tile neighbours; after
-//    the tile's forward stages, backward stages bring the u rows again,
-//    8 layers at a time in descending order, for u' = u_old + omega delta.
-//    That re-read is an L2 hit: the forward copies of u use an evict_last
-//    policy and the streamed-once bands an evict_first policy.
-//  * CTAs are persistent (two per SM), each looping over tiles; the producer
-//    warp streams the next tile's forward stages while the consumers finish
-//    the current tile's back substitution.
-//  * The Thomas state (z_k, g_k) of a column stays in tensor memory.
+//    own column is needed at layer k) and the <= 64 off-tile neighbours; a
+//    backward stage brings 8 layers of u again for u' = u_old + omega delta.
+//    That re-read is mostly an L2 hit: the forward copies of u use an
+//    evict_last policy and the streamed-once bands an evict_first policy.
+//  * Warp roles: 4 consumer warps (thread = column), a producer warp issuing
+//    the TMA copies, and (stored bands, non-zero guess) a gather warp issuing
+//    the off-tile cp.async gathers; the stage's full barrier counts both.
+//  * CTAs are persistent (two per SM at nz <= 64).  With stored bands and a
+//    non-zero guess (IL) pass p runs tile p's forward elimination and, one
+//    8-layer chunk at a time, tile p - 1's back substitution; the Thomas state
+//    (z_k, g_k) sits in tensor memory at slot k on even passes and nzp - 1 - k
+//    on odd ones, so each slot is rewritten right after it was read.  The ring
+//    keeps streaming through the back substitution, and the u' rows of a chunk
+//    leave by one TMA store from its backward stage.
 // HBM traffic per dof: u, b, D, U, H0, H1, H2 read once, u' written once
 // (64 B/dof; + 2 B/dof of u_c with the fused prolongation).
 #include <cuda.h>
