@@ -89,6 +89,10 @@ __global__ void __launch_bounds__(kThreads, 3)
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
     uint64_t* empty = full + S;
     double* stages = reinterpret_cast<double*>(smraw + 1024);
+#ifdef HMG_CHECKED
+    int* tags = reinterpret_cast<int*>(smraw + 896);   // checked builds: stage sequence numbers (S <= 32)
+    int pseq = 0, cseq = 0;
+#endif
     ptx::pdl_trigger();
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -117,6 +121,8 @@ __global__ void __launch_bounds__(kThreads, 3)
             const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
             const int ehc = EH ? et.hcount[tile] : 0;
             const int32_t eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
+            HMG_DCHECK(hcount <= kHaloMax && h0 >= 0 && h0 < ld && h1 >= 0 && h1 < ld);
+            HMG_DCHECK(ehc <= kEdgeHalo && eh0 >= 0 && (!EH || eh0 < et.ldE));
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
                 ptx::mbar_wait(&empty[s], phase ^ 1u);
                 double* st = stages + (size_t)s * AL.stage;
@@ -150,6 +156,10 @@ __global__ void __launch_bounds__(kThreads, 3)
             const uint32_t ebytes = EH ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
                 ptx::mbar_wait(&empty[s], phase ^ 1u);
+#ifdef HMG_CHECKED
+                if (lane == 0) tags[s] = pseq;
+                ++pseq;
+#endif
                 double* st = stages + (size_t)s * AL.stage;
                 if (lane == 0) {
                     int nl = nz - gi * G;
@@ -177,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             const int l0 = loc & 0xff, l1 = (loc >> 8) & 0xff, l2 = (loc >> 16) & 0xff;
             // stage offsets of the neighbours' x (p_old) at row 0; their z lies at the same
             // offset + (AL.z - AL.x) (tile and halo rows of z both sit that far after x's)
+            HMG_DCHECK(l0 < kTile + kHaloMax && l1 < kTile + kHaloMax && l2 < kTile + kHaloMax);
             const int ox0 = l0 < kTile ? AL.x + l0 : AL.hx + (l0 - kTile);
             const int ox1 = l1 < kTile ? AL.x + l1 : AL.hx + (l1 - kTile);
             const int ox2 = l2 < kTile ? AL.x + l2 : AL.hx + (l2 - kTile);
@@ -187,9 +198,14 @@ __global__ void __launch_bounds__(kThreads, 3)
                 eo1 = (el >> 8) & 0xff;
                 eo2 = (el >> 16) & 0xff;
             }
+            HMG_DCHECK(eo0 < kEdgeRow && eo1 < kEdgeRow && eo2 < kEdgeRow);
             double xm = 0.0, Um = 0.0;
             for (int gi = 0; gi < ngroups; ++gi, advance()) {
                 ptx::mbar_wait(&full[s], phase);
+#ifdef HMG_CHECKED
+                HMG_DCHECK(tags[s] == cseq);
+                ++cseq;
+#endif
                 const double* st = stages + (size_t)s * AL.stage;
                 const double* sx = st + AL.x;
                 const double* sz = st + AL.z;

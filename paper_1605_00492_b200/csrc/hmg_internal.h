@@ -14,6 +14,25 @@ namespace hmg {
 
 constexpr int kMaxLayers = 256;   // Thomas state for a column lives in shared memory
 constexpr int kMaxRef = 10;
+// Checked builds (-DHMG_CHECKED, tools/checked_probe.py; never the product
+// library): device-side bounds checks on gathered indices and a sequence tag
+// on every ring stage (the producer writes the stage's number, the consumers
+// check it) -- the stand-in for compute-sanitizer, which the GPU pool refuses.
+#ifdef HMG_CHECKED
+#define HMG_DCHECK(c)                                                                              \
+    do {                                                                                           \
+        if (!(c)) {                                                                                \
+            printf("HMG_CHECKED: %s failed (%s:%d) block %d thread %d\n", #c, __FILE__, __LINE__, \
+                   (int)blockIdx.x, (int)threadIdx.x);                                            \
+            __trap();                                                                              \
+        }                                                                                          \
+    } while (0)
+#else
+#define HMG_DCHECK(c) \
+    do {              \
+    } while (0)
+#endif
+
 constexpr int kSweepTile = 128;   // columns per CTA of the TMA/TMEM sweep (sweep_tc.cu)
 constexpr int kHaloMax = 64;
 constexpr int64_t kFactMaxCells = 148 * 128;

@@ -189,6 +189,15 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
     uint64_t* mid = empty + S;                        // matrix-free: the stage's band rows are formed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mid + S);
     double* stages = reinterpret_cast<double*>(smraw + 1024);
+#ifdef HMG_CHECKED
+    int* tags = reinterpret_cast<int*>(smraw + 896);   // checked builds: stage sequence numbers (S <= 32)
+    int pseq = 0, cseq = 0;
+#define ST_TAG_SET() do { if (lane == 0) tags[s] = pseq; ++pseq; } while (0)
+#define ST_TAG_CHECK() do { HMG_DCHECK(tags[s] == cseq); ++cseq; } while (0)
+#else
+#define ST_TAG_SET() do {} while (0)
+#define ST_TAG_CHECK() do {} while (0)
+#endif
 
     ptx::pdl_trigger();                                // the next kernel may start its prologue
 #ifdef HMG_TIMING
@@ -312,6 +321,8 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                 h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
                 ehc = EH ? et.hcount[tile] : 0;
                 eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
+                HMG_DCHECK(hcount <= kHaloMax && h0 >= 0 && h0 < ld && h1 >= 0 && h1 < ld);
+                HMG_DCHECK(ehc <= kEdgeHalo && eh0 >= 0 && (!EH || eh0 < et.ldE));
             }
             for (int ch = 0; ch < nchunks; ++ch) {
                 if (hasB) {                                    // backward stage: one arrival
@@ -377,6 +388,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
             long long q0 = clock64();
 #endif
             ptx::mbar_wait(&empty[s], phase ^ 1u);
+            ST_TAG_SET();
 #ifdef HMG_TIMING
             pw += clock64() - q0;
             ++pn;
@@ -440,6 +452,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
             long long q0 = clock64();
 #endif
             ptx::mbar_wait(&empty[s], phase ^ 1u);
+            ST_TAG_SET();
 #ifdef HMG_TIMING
             pw += clock64() - q0;
 #endif
@@ -526,6 +539,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
             ptx::tmem_ld_8f64(tl + 2u * sb, zr);
             ptx::tmem_ld_8f64(tl + gcol + 2u * sb, gr);
             ptx::mbar_wait(&full[s], phase);
+            ST_TAG_CHECK();
             double* su = stages + (size_t)s * SL.stage;
             ptx::tmem_wait_ld();
             double zv[kBack], gv[kBack];                   // by layer k0 + i
@@ -600,6 +614,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
             l2 = (j + 2) & 127;
 #endif
             // FLAT: stage offsets of the three neighbours' u at row 0 (tile row or halo row)
+            HMG_DCHECK(l0 < kTile + kHaloMax && l1 < kTile + kHaloMax && l2 < kTile + kHaloMax);
             const int no0 = l0 < kTile ? SL.u + l0 : SL.hu + (l0 - kTile);
             const int no1 = l1 < kTile ? SL.u + l1 : SL.hu + (l1 - kTile);
             const int no2 = l2 < kTile ? SL.u + l2 : SL.hu + (l2 - kTile);
@@ -619,6 +634,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
             eo1 = j + 128;
             eo2 = (j + 64) & 255;
 #endif
+            HMG_DCHECK(eo0 < kEdgeRow && eo1 < kEdgeRow && eo2 < kEdgeRow);
             ColumnGeom cg{};
 
             // Thomas forward elimination, reading R6 order (as k_sweep_tc's `layer`)
@@ -652,6 +668,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                 long long w0 = clock64();
 #endif
                 ptx::mbar_wait(MF ? &mid[s] : &full[s], phase);
+                ST_TAG_CHECK();
 #ifdef HMG_TIMING
                 wf += clock64() - w0;
 #endif
@@ -873,6 +890,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                     long long w0 = clock64();
 #endif
                     ptx::mbar_wait(MF ? &mid[s] : &full[s], phase);
+                    ST_TAG_CHECK();
 #ifdef HMG_TIMING
                     wb += clock64() - w0;
 #endif
