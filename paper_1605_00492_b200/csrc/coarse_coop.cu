@@ -173,6 +173,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) k_coarse_coop(const __grid_co
         const uint32_t loc = L.sh.loc[c < L.V.n ? c : L.V.n - 1];
         const int hcount = L.sh.count[t];
         const int32_t hc = L.sh.cells[t * kSmallHaloMax + lane];   // slots past hcount: unused
+        HMG_DCHECK(hcount <= kSmallHaloMax && (lane >= hcount || (hc >= 0 && hc < L.V.ld)));
+        HMG_DCHECK((loc & 0xff) < TW + kHaloW && ((loc >> 8) & 0xff) < TW + kHaloW && ((loc >> 16) & 0xff) < TW + kHaloW);
         m_loc = loc;
         m_hcount = hcount;
         m_hc = lane < hcount ? hc : 0;
