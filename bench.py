@@ -47,6 +47,29 @@ UNIT = "dof/s"
 # Algorithmic bytes per dof of each kernel class
 BYTES_PER_DOF = {"sweep": 64.0, "sweep_zero": 32.0, "sweep_prolong": 66.0, "apply": 56.0, "apply_pupdate": 72.0,
                  "resid_restrict": 58.0}
+# The streamed kernels (general sweep with or without the fused prolongation,
+# apply, streamed residual + restriction; not the apply with the p update) do not read D:
+# their consumers re-form D_k from the prism volume and the streamed couplings
+# (DESIGN 7.7), 8 B/dof less than the per-cell store's figure above.
+D_REFORMED = 8.0
+
+
+def store_bytes(es: dict) -> dict:
+    """Bytes per dof each fine-level kernel class actually reads and writes on a
+    level with edge-store flags `es` (hmg_edge_store): the edge-deduplicated
+    couplings save 12 B/dof, the re-formed diagonal 8."""
+    bpd = dict(BYTES_PER_DOF)
+    for k in ("sweep", "sweep_prolong", "apply"):
+        bpd[k] -= D_REFORMED
+    if es["sweep"]:
+        bpd["sweep"] -= 12.0
+        bpd["sweep_prolong"] -= 12.0
+    if es["apply"]:
+        bpd["apply"] -= 12.0
+        bpd["apply_pupdate"] -= 12.0
+    if es["resid_restrict"]:            # the streamed residual (k_apply_st): edge store and re-formed D
+        bpd["resid_restrict"] -= 12.0 + D_REFORMED
+    return bpd
 
 
 def parse():
@@ -323,17 +346,10 @@ def run_hmg(args, ws, rank, local):
 
     # ---- dominant kernel: the fused line-Jacobi sweep on the finest level ----
     # algorithmic bytes of the store the kernels actually read: with the
-    # edge-deduplicated coupling store 1.5 couplings per dof instead of 3 (12 B less)
+    # edge-deduplicated coupling store 1.5 couplings per dof instead of 3 (12 B
+    # less), and D re-formed in the streamed kernels (8 B less)
     es = h.edge_store(r)
-    bpd = dict(BYTES_PER_DOF)
-    if es["sweep"]:
-        bpd["sweep"] -= 12.0
-        bpd["sweep_prolong"] -= 12.0
-    if es["apply"]:
-        bpd["apply"] -= 12.0
-        bpd["apply_pupdate"] -= 12.0
-    if es["resid_restrict"]:
-        bpd["resid_restrict"] -= 12.0
+    bpd = store_bytes(es)
     n_sw, ms_sw = h.profile_query("sweep", r)
     avg_sw = ms_sw / max(n_sw, 1)
     dofs_local = cfg.ndofs // ws
@@ -518,10 +534,10 @@ def run_hmg(args, ws, rank, local):
                          "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": ncu_traffic(cfg.name, es["sweep"]),
-                         "store": ("edge-deduplicated couplings: u, b, D, U, 1.5 H in, u' out = 52 B/dof"
-                                   if es["sweep"] else "per-cell bands: u, b, D, U, 3 H in, u' out = 64 B/dof"),
-                         # the same launch counted with the per-cell store's 64 B/dof (the byte model of
-                         # earlier rounds), for comparison only: these bytes are not all moved
+                         "store": ("edge-deduplicated couplings, D re-formed: u, b, U, 1.5 H in, u' out = 44 B/dof"
+                                   if es["sweep"] else "per-cell couplings, D re-formed: u, b, U, 3 H in, u' out = 56 B/dof"),
+                         # the same launch counted with the canonical per-cell store's 64 B/dof (SURVEY
+                         # 8(d)), for comparison only: these bytes are not all moved
                          "per_cell_store_equivalent": {
                              "bytes_per_dof": BYTES_PER_DOF["sweep"],
                              "GB/s": BYTES_PER_DOF["sweep"] * dofs_local / (avg_sw * 1e-3) / 1e9,
@@ -589,9 +605,10 @@ def level_table(h, cfg, ws, bpd_fine, fine_ref) -> dict:
         h.profile_end()
         row = {"ref": ref, "cells": n_r, "dofs": dofs}
         es = h.edge_store(ref)
-        for key, cls, bpd in (("H", "apply", 44.0 if es["apply"] else 56.0),
+        sb = store_bytes(es)
+        for key, cls, bpd in (("H", "apply", sb["apply"]),
                               ("Hz_inv", "sweep_zero", 32.0),
-                              ("sweep", "sweep", 52.0 if es["sweep"] else 64.0)):
+                              ("sweep", "sweep", sb["sweep"])):
             nk, ms = h.profile_query(cls, ref)
             if nk:
                 us = ms * 1e3 / nk
@@ -751,8 +768,8 @@ def run_c1(args):
 
     flush = _Flush()
     ops = {
-        "apply": (lambda: h.apply_helmholtz(r, xd, yd), "apply", r, 56.0),
-        "sweep": (lambda: h.line_smooth(r, bd, ud, 1, 0.8, False), "sweep", r, 64.0),
+        "apply": (lambda: h.apply_helmholtz(r, xd, yd), "apply", r, 56.0 - D_REFORMED),
+        "sweep": (lambda: h.line_smooth(r, bd, ud, 1, 0.8, False), "sweep", r, 64.0 - D_REFORMED),
         "restrict": (lambda: h.restrict(r, xd, cd), "restrict", r, 10.0),
         "prolong": (lambda: h.prolong_add(r, cd, yd), "prolong", r, 18.0),
     }

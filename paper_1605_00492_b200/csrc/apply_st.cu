@@ -15,7 +15,13 @@
 //    written back -- the p update fused into q = H^ p; rows of both z and
 //    p_old travel in the stage.
 //  * DOT: <x, H^ x> accumulated per thread, reduced per CTA in a fixed order.
-// HBM traffic per dof: 56 B (x, bands in; y out), 72 B with the p update.
+//  * D is not streamed (except with the p update): the consumers re-form D_k
+//    from the column's prism volume and the streamed couplings in
+//    k_assemble's order (bitwise the stored diagonal), so a stage carries the
+//    U, H0, H1, H2 rows only.  The p-update variant streams D: re-forming it
+//    there measured slower (C2b 223 -> 266 us).
+// HBM traffic per dof: 48 B (x, U, H0-H2 in; y out), 72 B with the p update;
+// with the edge store 36 / 60 B.
 #include <cuda.h>
 
 #include <cstring>
@@ -39,7 +45,7 @@ constexpr int kConsumerWarps = kTile / 32;
 constexpr int kThreads = kTile + 64;   // + a producer warp (TMA) and a gather warp (off-tile cp.async)
 
 struct ApMaps {
-    CUtensorMap bands;  // 3-D box kTile x G x 5 (x 2: D, U with the edge store)
+    CUtensorMap bands;  // 3-D box kTile x G x 4: U, H0, H1, H2 (x 1, 2-D: U with the edge store); PUPD: D first
     CUtensorMap x;      // box kTile x (G + 1): x, or p_old (PUPD), or u (RESID)
     CUtensorMap z;      // box kTile x (G + 1): z (PUPD)
     CUtensorMap b;      // box kTile x G: right-hand side (RESID)
@@ -48,12 +54,13 @@ struct ApMaps {
 struct ApLayout {
     int x, z, b, hx, hz, eh, stage;
 };
-// eh: the band box carries D and U only; couplings from the edge store (one
-// row of kEdgeRow doubles per layer: contiguous range, then gathered edges)
+// eh: the band box carries U (PUPD: D, U) only; couplings from the edge store
+// (one row of kEdgeRow doubles per layer: contiguous range, then gathered edges)
+__host__ __device__ constexpr int ap_band_planes(bool pupd, bool eh) { return (eh ? 2 : 5) - (pupd ? 0 : 1); }
 __host__ __device__ constexpr ApLayout ap_layout(bool pupd, int G, bool eh = false, bool resid = false) {
     static_assert(kTile % 2 == 0, "");
     ApLayout L{};
-    L.x = (eh ? 2 : 5) * G * kTile;
+    L.x = ap_band_planes(pupd, eh) * G * kTile;
     L.z = L.x + (G + 1) * kTile;
     L.b = L.z + (pupd ? (G + 1) * kTile : 0);
     L.hx = L.b + (resid ? G * kTile : 0);
@@ -76,11 +83,14 @@ __global__ void __launch_bounds__(kThreads, 3)
     k_apply_st(const __grid_constant__ ApMaps maps, LevelView L, TileHalo th, EdgeTiles et,
                const double* __restrict__ xin,
                const double* __restrict__ zv, double* __restrict__ y, double* __restrict__ pnew,
-               double* __restrict__ partial, const PcgScalars* __restrict__ sc, int S, int64_t ldc, int64_t coff) {
+               double* __restrict__ partial, const PcgScalars* __restrict__ sc, int S, int64_t ldc, int64_t coff,
+               const double* __restrict__ geom, double dz) {
     static_assert(!(RESID && (DOT || PUPD)), "residual mode: plain operator only");
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ double red[kThreads / 32];
     constexpr ApLayout AL = ap_layout(PUPD, G, EH, RESID);
+    constexpr bool ND = !PUPD;                 // D re-formed by the consumers, not streamed
+    constexpr int NBP = ap_band_planes(PUPD, EH);
     const int nz = L.nz;
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
@@ -148,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 3)
     } else if (warp == kConsumerWarps) {
         // ======================= producer warp =======================
         const uint64_t pol = ptx::policy_evict_first();
-        const uint32_t bytes = (uint32_t)(sizeof(double) * ((EH ? 2 : 5) * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile +
+        const uint32_t bytes = (uint32_t)(sizeof(double) * (NBP * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile +
                                                             (RESID ? G * kTile : 0)));
         for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
             const int x = tile * kTile;
@@ -169,7 +179,10 @@ __global__ void __launch_bounds__(kThreads, 3)
                         for (int kk = 0; kk < nl; ++kk)
                             ptx::bulk_g2s(st + AL.eh + kk * kEdgeRow, et.H + (int64_t)(gi * G + kk) * et.ldE + ee0,
                                           ebytes, &full[s]);
-                    ptx::tma_load_3d_hint(st, &maps.bands, x, gi * G, 0, &full[s], pol);
+                    if (NBP == 1)
+                        ptx::tma_load_2d_hint(st, &maps.bands, x, gi * G, &full[s], pol);
+                    else
+                        ptx::tma_load_3d_hint(st, &maps.bands, x, gi * G, 0, &full[s], pol);
                     if (RESID) ptx::tma_load_2d_hint(st + AL.b, &maps.b, x, gi * G, &full[s], pol);
                     ptx::tma_load_2d(st + AL.x, &maps.x, x, gi * G, &full[s]);
                     if (PUPD) ptx::tma_load_2d(st + AL.z, &maps.z, x, gi * G, &full[s]);
@@ -184,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             const int64_t c = (int64_t)tile * kTile + j;
             const bool valid = c < L.n;
             const uint32_t loc = th.loc[valid ? c : L.n - 1];
+            const double vol = ND ? geom[valid ? c : L.n - 1] * dz : 0.0;   // k_assemble's prism volume
             const int l0 = loc & 0xff, l1 = (loc >> 8) & 0xff, l2 = (loc >> 16) & 0xff;
             // stage offsets of the neighbours' x (p_old) at row 0; their z lies at the same
             // offset + (AL.z - AL.x) (tile and halo rows of z both sit that far after x's)
@@ -230,18 +244,34 @@ __global__ void __launch_bounds__(kThreads, 3)
                     constexpr bool IN = decltype(interior)::value;
                     const int k = gi * G + kk;
                     const double* sr = st + kk * kTile + j;
-                    const double Dk = sr[0];
-                    const double Uk = sr[G * kTile];
+                    constexpr int pu = ND ? 0 : 1;     // plane of U in the stage's band rows
+                    const double Uk = sr[pu * G * kTile];
+                    const double* er = st + AL.eh + kk * kEdgeRow;
+                    const double H0 = EH ? er[eo0] : sr[(pu + 1) * G * kTile];
+                    const double H1 = EH ? er[eo1] : sr[(pu + 2) * G * kTile];
+                    const double H2 = EH ? er[eo2] : sr[(pu + 3) * G * kTile];
+                    double Dk;
+                    if (ND) {
+                        // k_assemble's diagonal vol + V_dn + V_up + H0 + H1 + H2 from the stored
+                        // U = -V_up, H_j = -(coupling) (x + (-y) is x - y exactly): bitwise D_k
+                        Dk = vol;
+                        if (IN || k > 0) Dk = Dk - Um;
+                        if (IN || k < nz - 1) Dk = Dk - Uk;
+                        Dk = Dk - H0;
+                        Dk = Dk - H1;
+                        Dk = Dk - H2;
+                    } else {
+                        Dk = sr[0];
+                    }
                     const double xk = XV(kk, j);
                     double xp = 0.0;
                     if (IN || k < nz - 1) xp = XV(kk + 1, j);
                     double acc = Dk * xk;
                     if (IN || k > 0) acc = acc + Um * xm;
                     if (IN || k < nz - 1) acc = acc + Uk * xp;
-                    const double* er = st + AL.eh + kk * kEdgeRow;
-                    acc = acc + (EH ? er[eo0] : sr[2 * G * kTile]) * XN(kk, 0);
-                    acc = acc + (EH ? er[eo1] : sr[3 * G * kTile]) * XN(kk, 1);
-                    acc = acc + (EH ? er[eo2] : sr[4 * G * kTile]) * XN(kk, 2);
+                    acc = acc + H0 * XN(kk, 0);
+                    acc = acc + H1 * XN(kk, 1);
+                    acc = acc + H2 * XN(kk, 2);
                     if (RESID) {
                         const double r = st[AL.b + kk * kTile + j] - acc;
                         const double r1 = __shfl_down_sync(0xffffffffu, r, 1);
@@ -308,7 +338,7 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     ApMaps maps;
     std::memset(&maps, 0, sizeof(maps));
     const LevelView V = L.view(nz);
-    maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, EH ? 2 : 5);
+    maps.bands = make_tensor_map(PUPD ? V.D : V.U, L.ld, nz, kTile, G, ap_band_planes(PUPD, EH));
     maps.x = make_tensor_map(x, L.ld, nz, kTile, G + 1, 1);
     if (PUPD) maps.z = make_tensor_map(z, L.ld, nz, kTile, G + 1, 1);
     if (RESID) maps.b = make_tensor_map(b, L.ld, nz, kTile, G, 1);
@@ -316,7 +346,7 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     const unsigned cap = (unsigned)((per_sm >= 3 ? 3 : 2) * sms);
     const unsigned grid = ntiles < cap ? ntiles : cap;
     launch_pdl(H, k_apply_st<DOT, PUPD, G, EH, RESID>, dim3(grid), dim3(kThreads), smem, s, maps, V, L.halo, L.edge, x,
-               z, y, pnew, H.partials, H.scal, S, ldc, coff);
+               z, y, pnew, H.partials, H.scal, S, ldc, coff, L.geom, H.dz);
     return (int)grid;
 }
 

@@ -122,13 +122,19 @@ struct StLayout {
     int op, band, b, u, uc, hu, huc, hlam, eh, fwd, bwd, stage;
 };
 // eh: the band box carries D and U only; the couplings come from the edge
-// store, one row of kEdgeRow doubles per layer (contiguous range, then gathered)
+// store, one row of kEdgeRow doubles per layer (contiguous range, then gathered).
+// Stored bands with a non-zero guess: the D rows are not streamed -- the
+// consumers re-form D_k from the column's prism volume and the streamed
+// couplings in k_assemble's order (st_band_planes).
+__host__ __device__ constexpr int st_band_planes(bool zero, bool mf, bool eh) {
+    return (eh ? 2 : 5) - ((!zero && !mf) ? 1 : 0);
+}
 __host__ __device__ constexpr StLayout st_layout(bool zero, bool prolong, bool mf, int G, bool dot = false,
                                                  bool eh = false) {
     StLayout L{};
     L.op = 0;                                        // band rows (stored), or lam rows (matrix-free)
     L.band = mf ? (G + 1) * kTile : 0;               // band rows as the consumers read them
-    L.b = L.band + (eh ? 2 : 5) * G * kTile;
+    L.b = L.band + st_band_planes(zero, mf, eh) * G * kTile;
     L.u = L.b + G * kTile;
     L.uc = L.u + (zero ? 0 : (G + 1) * kTile);
     L.hu = L.uc + (prolong ? (G + 1) * kUcRow : 0);
@@ -162,6 +168,10 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
     __shared__ double dred[kThreadsSplit / 32];
     static_assert(!(EH && (ZERO || MF)), "edge store: general stored-band sweeps only");
     constexpr StLayout SL = st_layout(ZERO, PROLONG, MF, G, DOT, EH);
+    // ND: D_k is not streamed but re-formed by the consumers (st_band_planes);
+    // the stage's band rows start at U
+    constexpr bool ND = !ZERO && !MF;
+    constexpr int NBP = st_band_planes(ZERO, MF, EH);
     double dotacc = 0.0;                               // DOT: this thread's sum of b_k u'_k
 #ifdef HMG_TIMING
     long long tt0 = 0, wf = 0, wb = 0, ntl = 0, tfw = 0, tbk = 0, tfw0 = 0, tws = 0;
@@ -364,7 +374,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
         // ======================= producer warp =======================
         const uint64_t pol_stream = ptx::policy_evict_first();
         const uint64_t pol_keep = ptx::policy_evict_last();
-        constexpr int op_rows = MF ? (G + 1) * kTile : (EH ? 2 : 5) * G * kTile;
+        constexpr int op_rows = MF ? (G + 1) * kTile : NBP * G * kTile;
         const uint32_t fwd_bytes =
             (uint32_t)(sizeof(double) * (op_rows + G * kTile + (ZERO ? 0 : (G + 1) * kTile) +
                                          (PROLONG ? (G + 1) * kUcRow : 0)));
@@ -423,6 +433,8 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                     const int gp = gi + pf_groups;
                     if (MF)
                         ptx::tma_prefetch_2d(&maps.lam, x, gp * G);
+                    else if (NBP == 1)
+                        ptx::tma_prefetch_2d(&maps.bands, x, gp * G);
                     else
                         ptx::tma_prefetch_3d(&maps.bands, x, gp * G, 0);
                     ptx::tma_prefetch_2d(&maps.b, x, gp * G);
@@ -437,6 +449,8 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                                       ebytes, &full[s]);
                 if (MF)
                     ptx::tma_load_2d_hint(st + SL.op, &maps.lam, x, gi * G, &full[s], pol_stream);
+                else if (NBP == 1)
+                    ptx::tma_load_2d_hint(st + SL.op, &maps.bands, x, gi * G, &full[s], pol_stream);
                 else
                     ptx::tma_load_3d_hint(st + SL.op, &maps.bands, x, gi * G, 0, &full[s], pol_stream);
                 ptx::tma_load_2d_hint(st + SL.b, &maps.b, x, gi * G, &full[s], DOT ? pol_keep : pol_stream);
@@ -636,6 +650,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
 #endif
             HMG_DCHECK(eo0 < kEdgeRow && eo1 < kEdgeRow && eo2 < kEdgeRow);
             ColumnGeom cg{};
+            const double vol = ND ? op.geom[cv] * op.dz : 0.0;   // k_assemble's prism volume
 
             // Thomas forward elimination, reading R6 order (as k_sweep_tc's `layer`)
             double um = 0.0, Um = 0.0, gprev = 0.0, zprev = 0.0, vdn = 0.0;
@@ -703,12 +718,26 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                     constexpr bool IN = decltype(interior)::value;
                     const int k = gi * G + kk;
                     const double* sr = st + SL.band + kk * kTile + j;
-                    const double Dk = sr[0];
-                    const double Uk = sr[G * kTile];
+                    constexpr int pu = ND ? 0 : 1;     // plane of U in the stage's band rows
+                    const double Uk = sr[pu * G * kTile];
                     const double* er = st + SL.eh + kk * kEdgeRow;
-                    const double H0 = EH ? er[eo0] : sr[2 * G * kTile];
-                    const double H1 = EH ? er[eo1] : sr[3 * G * kTile];
-                    const double H2 = EH ? er[eo2] : sr[4 * G * kTile];
+                    const double H0 = EH ? er[eo0] : sr[(pu + 1) * G * kTile];
+                    const double H1 = EH ? er[eo1] : sr[(pu + 2) * G * kTile];
+                    const double H2 = EH ? er[eo2] : sr[(pu + 3) * G * kTile];
+                    double Dk;
+                    if (ND) {
+                        // k_assemble's diagonal: vol + V_dn + V_up + H0 + H1 + H2 with the
+                        // stored U = -V_up, H_j = -(coupling): x + (-y) is x - y exactly
+                        double d = vol;
+                        if (IN || k > 0) d = d - Um;
+                        if (IN || k < nz - 1) d = d - Uk;
+                        d = d - H0;
+                        d = d - H1;
+                        d = d - H2;
+                        Dk = d;
+                    } else {
+                        Dk = sr[0];
+                    }
                     const double bk = st[SL.b + kk * kTile + j];
                     double r;
                     if (ZERO) {
@@ -1045,7 +1074,7 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
     if (M)
         maps.lam = make_tensor_map(L.lam, L.ld, nz, kTile, G + 1, 1);
     else
-        maps.bands = make_tensor_map(V.D, L.ld, nz, kTile, G, EH ? 2 : 5);
+        maps.bands = make_tensor_map(!Z ? V.U : V.D, L.ld, nz, kTile, G, st_band_planes(Z, M, EH));
     maps.b = make_tensor_map(b, L.ld, nz, kTile, G, 1);
     if (!Z) {
         maps.uf = make_tensor_map(uin, L.ld, nz, kTile, G + 1, 1);

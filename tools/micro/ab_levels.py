@@ -27,6 +27,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "--build":   # build the libraries here,
     sys.exit(0)
 rev = sys.argv[1] if len(sys.argv) > 1 else "work"
 zero = len(sys.argv) > 2 and sys.argv[2] == "zero"      # time the zero-guess sweep instead
+app = len(sys.argv) > 2 and sys.argv[2] == "apply"     # time the operator apply instead
 B._LIB_PATH = lib_for(rev)
 import torch
 import hmg_inputs as hi
@@ -39,14 +40,19 @@ for r in (7, 6, 5):
     n = hi.ncells(r)
     bd = g.to_device(r, hi.uniform_vector((64, n), 5))
     u = g.to_device(r, hi.uniform_vector((64, n), 3))
+    def one():
+        if app:
+            g.apply_helmholtz(r, u, bd)
+        else:
+            g.line_smooth(r, bd, u, 1, 0.8, zero)
     for _ in range(3):
-        g.line_smooth(r, bd, u, 1, 0.8, zero)
+        one()
     torch.cuda.synchronize()
     g.profile_begin()
     for _ in range(20):
-        g.line_smooth(r, bd, u, 1, 0.8, zero)
+        one()
     torch.cuda.synchronize()
     g.profile_end()
-    k, ms = g.profile_query("sweep_zero" if zero else "sweep", r)
+    k, ms = g.profile_query("apply" if app else "sweep_zero" if zero else "sweep", r)
     out.append(f"ref {r} {ms * 1e3 / k:.1f} us")
-print(rev, "zero" if zero else "", os.environ.get("HMG_ZERO_ST", ""), " | ".join(out))
+print(rev, "apply" if app else "zero" if zero else "", os.environ.get("HMG_ZERO_ST", ""), " | ".join(out))
