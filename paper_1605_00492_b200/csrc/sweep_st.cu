@@ -27,8 +27,12 @@
 //    on odd ones, so each slot is rewritten right after it was read.  The ring
 //    keeps streaming through the back substitution, and the u' rows of a chunk
 //    leave by one TMA store from its backward stage.
-// HBM traffic per dof: u, b, D, U, H0, H1, H2 read once, u' written once
-// (64 B/dof; + 2 B/dof of u_c with the fused prolongation).
+//  * D is not streamed: the consumers re-form D_k = ((((vol - U_{k-1}) - U_k)
+//    - H0) - H1) - H2 from the column's prism volume and the streamed
+//    couplings, k_assemble's sum term by term, so bitwise the stored D.
+// HBM traffic per dof: u, b, U, H0, H1, H2 read once, u' written once
+// (56 B/dof; the per-cell store's 64 of SURVEY 8(d) less D; 44 with the edge
+// store; + 2 B/dof of u_c with the fused prolongation).
 #include <cuda.h>
 
 #include <cfloat>
