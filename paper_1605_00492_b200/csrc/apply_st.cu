@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                const double* __restrict__ xin,
                const double* __restrict__ zv, double* __restrict__ y, double* __restrict__ pnew,
                double* __restrict__ partial, const PcgScalars* __restrict__ sc, int S, int64_t ldc, int64_t coff,
-               const double* __restrict__ geom, double dz) {
+               const double* __restrict__ geom, double dz, int nsplit) {
     static_assert(!(RESID && (DOT || PUPD)), "residual mode: plain operator only");
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ double red[kThreads / 32];
@@ -95,6 +95,9 @@ __global__ void __launch_bounds__(kThreads, 3)
     const int64_t ld = L.ld;
     const int ngroups = (nz + G - 1) / G;
     const int ntiles = (int)((L.n + kTile - 1) / kTile);
+    // work unit = (tile, one of nsplit contiguous layer ranges): small levels split
+    // their columns' layers so that every resident CTA has work (launch_ap)
+    const int nunits = ntiles * nsplit;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     uint64_t* full = reinterpret_cast<uint64_t*>(smraw);
     uint64_t* empty = full + S;
@@ -125,7 +128,9 @@ __global__ void __launch_bounds__(kThreads, 3)
     if (warp == kConsumerWarps + 1) {
         // ============ gather warp: off-tile operands and gathered couplings ============
         // (issued here, not by the producer, whose TMA issue is on the critical path)
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
+            const int tile = un / nsplit, part = un - tile * nsplit;
+            const int ga = part * ngroups / nsplit, gb = (part + 1) * ngroups / nsplit;
             const int hcount = th.count[tile];
             const int32_t h0 = lane < hcount ? th.cells[tile * kHaloMax + lane] : 0;
             const int32_t h1 = lane + 32 < hcount ? th.cells[tile * kHaloMax + lane + 32] : 0;
@@ -133,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             const int32_t eh0 = EH && lane < ehc ? et.hcells[tile * kEdgeHalo + lane] : 0;
             HMG_DCHECK(hcount <= kHaloMax && h0 >= 0 && h0 < ld && h1 >= 0 && h1 < ld);
             HMG_DCHECK(ehc <= kEdgeHalo && eh0 >= 0 && (!EH || eh0 < et.ldE));
-            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+            for (int gi = ga; gi < gb; ++gi, advance()) {
                 ptx::mbar_wait(&empty[s], phase ^ 1u);
                 double* st = stages + (size_t)s * AL.stage;
                 for (int kk = 0; kk < G; ++kk) {
@@ -160,11 +165,13 @@ __global__ void __launch_bounds__(kThreads, 3)
         const uint64_t pol = ptx::policy_evict_first();
         const uint32_t bytes = (uint32_t)(sizeof(double) * (NBP * G * kTile + (PUPD ? 2 : 1) * (G + 1) * kTile +
                                                             (RESID ? G * kTile : 0)));
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
+            const int tile = un / nsplit, part = un - tile * nsplit;
+            const int ga = part * ngroups / nsplit, gb = (part + 1) * ngroups / nsplit;
             const int x = tile * kTile;
             const int32_t ee0 = EH ? et.e0[tile] : 0;
             const uint32_t ebytes = EH ? (uint32_t)(sizeof(double) * et.ne[tile]) : 0u;
-            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+            for (int gi = ga; gi < gb; ++gi, advance()) {
                 ptx::mbar_wait(&empty[s], phase ^ 1u);
 #ifdef HMG_CHECKED
                 if (lane == 0) tags[s] = pseq;
@@ -193,7 +200,9 @@ __global__ void __launch_bounds__(kThreads, 3)
         // ======================= consumers: one column per thread =======================
         const int j = threadIdx.x;
         const double beta = PUPD ? sc->beta : 0.0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
+            const int tile = un / nsplit, part = un - tile * nsplit;
+            const int ga = part * ngroups / nsplit, gb = (part + 1) * ngroups / nsplit;
             const int64_t c = (int64_t)tile * kTile + j;
             const bool valid = c < L.n;
             const uint32_t loc = th.loc[valid ? c : L.n - 1];
@@ -214,7 +223,12 @@ __global__ void __launch_bounds__(kThreads, 3)
             }
             HMG_DCHECK(eo0 < kEdgeRow && eo1 < kEdgeRow && eo2 < kEdgeRow);
             double xm = 0.0, Um = 0.0;
-            for (int gi = 0; gi < ngroups; ++gi, advance()) {
+            if (ga > 0) {   // a unit starting above layer 0: x (p) and U of the layer below
+                const int64_t i = (int64_t)(ga * G - 1) * ld + (valid ? c : L.n - 1);
+                xm = PUPD ? zv[i] + beta * xin[i] : xin[i];
+                Um = L.U[i];
+            }
+            for (int gi = ga; gi < gb; ++gi, advance()) {
                 ptx::mbar_wait(&full[s], phase);
 #ifdef HMG_CHECKED
                 HMG_DCHECK(tags[s] == cseq);
@@ -323,8 +337,18 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, H.device);
     // resident CTAs per SM (shared memory split evenly): three for the p-update
     // and residual variants (more consumer warps: C2b 244 -> 225 us and 183 -> 172
-    // us), two for the plain apply (C1 19.0 against 20.3 us with three)
-    const int per_sm = (PUPD || RESID) ? H.apply_ctas_per_sm : 2;
+    // us), two for the plain apply.  A level with at most 1.5 tiles per SM
+    // (ref <= 5: C1's 160 tiles) runs three per SM and splits each column's
+    // layers into nsplit contiguous ranges, one work unit each, so that every
+    // resident CTA streams (C1: 320 units of 32 layers instead of 160 tiles on
+    // 148 SMs).
+    const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
+    const int ngroups = (nz + G - 1) / G;
+    const bool small = 2 * ntiles <= 3u * (unsigned)sms;
+    int nsplit = small ? (int)((3u * (unsigned)sms) / (ntiles > 0 ? ntiles : 1u)) : 1;
+    nsplit = nsplit < 1 ? 1 : (nsplit > 4 ? 4 : nsplit);
+    nsplit = nsplit > ngroups ? ngroups : nsplit;
+    const int per_sm = small ? 3 : (PUPD || RESID) ? H.apply_ctas_per_sm : 2;
     const size_t budget = (size_t)(per_sm >= 3 ? 72 : 110) * 1024;
     int S = (int)((budget - 1024) / (sizeof(double) * AL.stage));
     S = S < 2 ? 2 : (S > 32 ? 32 : S);
@@ -342,11 +366,11 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     maps.x = make_tensor_map(x, L.ld, nz, kTile, G + 1, 1);
     if (PUPD) maps.z = make_tensor_map(z, L.ld, nz, kTile, G + 1, 1);
     if (RESID) maps.b = make_tensor_map(b, L.ld, nz, kTile, G, 1);
-    const unsigned ntiles = (unsigned)((L.n + kTile - 1) / kTile);
+    const unsigned nunits = ntiles * (unsigned)nsplit;
     const unsigned cap = (unsigned)((per_sm >= 3 ? 3 : 2) * sms);
-    const unsigned grid = ntiles < cap ? ntiles : cap;
+    const unsigned grid = nunits < cap ? nunits : cap;
     launch_pdl(H, k_apply_st<DOT, PUPD, G, EH, RESID>, dim3(grid), dim3(kThreads), smem, s, maps, V, L.halo, L.edge, x,
-               z, y, pnew, H.partials, H.scal, S, ldc, coff, L.geom, H.dz);
+               z, y, pnew, H.partials, H.scal, S, ldc, coff, L.geom, H.dz, nsplit);
     return (int)grid;
 }
 

@@ -1,5 +1,10 @@
-python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1
-python tools/micro/st_probe.py normal
-python tools/micro/st_probe.py normal -DHMG_ST_G=4
-python tools/micro/st_probe.py normal -DHMG_ST_G=3
-python tools/micro/st_timing.py -DHMG_ST_G=4
+# cooperative coarse tail: per-tile static blocks by bulk copies (A/B against f8da31a), GPU suite
+set -x
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/r02v_build.log 2>&1; echo "build $?"
+summ() { python -c "import json,sys;d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]);print(sys.argv[1], round(d['ms_per_step'],3), d['clocks']['sm_mhz'], d['clocks']['reasons'], d['multigrid_breakdown']['vcycle_us_per_level'], d['time_share']['coarse_tail'])" $1; }
+for rep in 1 2; do
+  timeout 600 python tools/micro/bench_with_lib.py tools/micro/libhmg_f8da31a.so --steps 30 --no-cpu-baseline > gpurun_out/r02v_old$rep.json 2>/dev/null; summ gpurun_out/r02v_old$rep.json
+  timeout 600 python bench.py --steps 30 --no-cpu-baseline > gpurun_out/r02v_new$rep.json 2>/dev/null; summ gpurun_out/r02v_new$rep.json
+done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/r02v_pytest.log 2>&1; echo "pytest $?"
+tail -2 gpurun_out/r02v_pytest.log
