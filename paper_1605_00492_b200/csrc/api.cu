@@ -224,6 +224,7 @@ double* run_sweeps(const Hierarchy& H, const DevLevel& L, const double* b, doubl
             !H.matrix_free && H.use_tc_sweep && sweep_st_supported(H, L)) {
             // the preconditioner's last sweep: <r, z> = <b, u'> accumulated on the fly
             ProfScope ps(H, kKSweep, L.ref, s);
+            fin_begin(H, H.rz_op);
             H.rz_parts = launch_sweep_st_dot(H, L, b, cur, dst, omega, s);
             H.rz_req = false;
         } else {
@@ -328,6 +329,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     // x/r update reads b and writes x = 0 + alpha p, r = b - alpha q (the same
     // arithmetic as from x = 0, r = b)
     const double* r0 = b;
+    fin_begin(H, kFinBB);
     launch_dot(H, F, r0, r0, s);
     launch_finalize(H, kFinBB, s);
     HMG_TRY(check_launch());
@@ -346,11 +348,13 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     auto precond_dot = [&](const double* r, double* z, int op) {
         H.rz_req = H.fuse_rz;
         H.rz_parts = 0;
+        H.rz_op = op;
         precond(r, z);
         H.rz_req = false;
         if (H.rz_parts > 0) {
             finalize_parts(H, H.rz_parts, op, s);
         } else {
+            fin_begin(H, op);
             launch_dot(H, F, r, z, s);
             launch_finalize(H, op, s);
         }
@@ -386,6 +390,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
             launch_apply_pupdate_dot(H, F, zb, pc, pn, H.q, s);
             pc = pn;
         }
+        fin_begin(H, kFinRR);
         if (H.defer_x) {
             launch_update_part(H, F, 1, it == 1, x, pc, b, s);   // r = r - alpha q (b - alpha q), partial <r, r>
             H.px.pending = true;

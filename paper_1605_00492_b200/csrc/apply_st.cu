@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 3)
                const double* __restrict__ xin,
                const double* __restrict__ zv, double* __restrict__ y, double* __restrict__ pnew,
                double* __restrict__ partial, const PcgScalars* __restrict__ sc, int S, int64_t ldc, int64_t coff,
-               const double* __restrict__ geom, double dz, int nsplit) {
+               const double* __restrict__ geom, double dz, int nsplit, FinArgs fin) {
     static_assert(!(RESID && (DOT || PUPD)), "residual mode: plain operator only");
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ double red[kThreads / 32];
@@ -325,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, 3)
             for (int w = 0; w < kThreads / 32; ++w) t = t + red[w];
             partial[blockIdx.x] = t;
         }
+        fin_fused(fin, partial);   // the last CTA: alpha = rho / <p, q> (fused finalize)
     }
 }
 
@@ -370,7 +371,7 @@ int launch_ap(const Hierarchy& H, const DevLevel& L, const double* x, const doub
     const unsigned cap = (unsigned)((per_sm >= 3 ? 3 : 2) * sms);
     const unsigned grid = nunits < cap ? nunits : cap;
     launch_pdl(H, k_apply_st<DOT, PUPD, G, EH, RESID>, dim3(grid), dim3(kThreads), smem, s, maps, V, L.halo, L.edge, x,
-               z, y, pnew, H.partials, H.scal, S, ldc, coff, L.geom, H.dz, nsplit);
+               z, y, pnew, H.partials, H.scal, S, ldc, coff, L.geom, H.dz, nsplit, DOT ? fin_take(H) : FinArgs());
     return (int)grid;
 }
 

@@ -154,6 +154,7 @@ struct DevLevel {
 struct PcgScalars {
     double rho, alpha, beta, pq, rr, rz, bb, tmp;
     unsigned long long bad;     // encoded (ref << 40 | column) of the first bad pivot, or ~0
+    unsigned int fin_count;     // fused finalize: CTAs of the current partial-sum launch that are done
 };
 
 // Optional per-launch CUDA-event timing (hmg_profile_*): each instrumented
@@ -233,6 +234,11 @@ struct Hierarchy {
     // sweep launch that takes it writes per-CTA partial sums and sets rz_parts
     mutable bool rz_req = false;
     mutable int rz_parts = 0;
+    mutable int rz_op = -1;           // the scalar op of that <r, z> (fused finalize)
+    // fused finalize (FinArgs): op announced for the next partial-sum launch,
+    // and whether that launch took it
+    mutable int fin_op = -1;
+    mutable bool fin_fused = false;
     bool fuse_rz = true;        // HMG_FUSE_RZ=0: separate dot kernel
     int64_t fact_max_cells = kFactMaxCells;   // levels up to this size carry precomputed Thomas factors
     bool check_skip = true;     // HMG_CHECK_SKIP=0: keep the per-layer pivot / g tests even where proven at build
@@ -384,6 +390,56 @@ struct ProfScope {
 };
 
 enum FinalizeOp { kFinPQ = 0, kFinRR = 1, kFinRZ = 2, kFinRhoInit = 3, kFinBB = 4 };
+
+// Fused finalize (one rank): a kernel that writes one partial sum per CTA into
+// `partial` also applies the PCG scalar update -- its last CTA to finish sums
+// the partials in a fixed order (one warp: strided per lane, then a fixed
+// shuffle tree) and does k_finalize's scalar op, so no single-block finalize
+// launch follows.  op < 0: not fused (k_finalize or the all-reduce follows).
+struct FinArgs {
+    int op = -1;
+    PcgScalars* sc = nullptr;
+    PcgScalars* pub = nullptr;   // mapped host copy for the scalars the host reads
+};
+// The FinArgs of the next partial-sum launch: finalize_parts' op when the sum
+// needs no all-reduce (pcg_impl announces it with fin_begin before the launch;
+// the launch takes it with fin_take, and finalize_parts then launches nothing)
+FinArgs fin_take(const Hierarchy& H);
+void fin_begin(const Hierarchy& H, int op);
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void pcg_scalar_op(PcgScalars* sc, int op, double S) {
+    switch (op) {
+        case kFinPQ: sc->pq = S; sc->alpha = sc->rho / S; break;
+        case kFinRR: sc->rr = S; break;
+        case kFinRZ: sc->rz = S; sc->beta = S / sc->rho; sc->rho = S; break;
+        case kFinRhoInit: sc->rho = S; break;
+        case kFinBB: sc->bb = S; break;
+    }
+}
+// Every thread of the CTA calls it after the CTA's partial was stored by thread 0.
+__device__ __forceinline__ void fin_fused(const FinArgs& f, const double* partial) {
+    if (f.op < 0) return;
+    __shared__ unsigned s_last;
+    __syncthreads();
+    const unsigned nb = gridDim.x * gridDim.y;
+    if (threadIdx.x == 0) {
+        __threadfence();                               // this CTA's partial before its arrival
+        s_last = atomicAdd(&f.sc->fin_count, 1u) == nb - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x >= 32) return;
+    __threadfence();
+    double v = 0.0;
+    for (unsigned i = threadIdx.x; i < nb; i += 32) v = v + __ldcg(partial + i);
+    for (int off = 16; off > 0; off >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, off);
+    if (threadIdx.x == 0) {
+        f.sc->fin_count = 0;
+        pcg_scalar_op(f.sc, f.op, v);
+        if (f.pub) *f.pub = *f.sc;
+    }
+}
+#endif
 
 // multi-GPU helpers (kernels.cu)
 void launch_halo_pack(const Hierarchy& H, const DevLevel& L, const double* v, cudaStream_t s);

@@ -457,7 +457,8 @@ __device__ __forceinline__ VecRange vec_range(int nz) {
 }
 
 __global__ void __launch_bounds__(kVecBlock) k_dot(const double* __restrict__ a, const double* __restrict__ b,
-                                                   int64_t n, int64_t ld, int nz, double* __restrict__ partial) {
+                                                   int64_t n, int64_t ld, int nz, double* __restrict__ partial,
+                                                   FinArgs fin) {
     __shared__ double red[kVecBlock / 32];
     const VecRange v = vec_range(nz);
     double s = 0.0;
@@ -474,6 +475,7 @@ __global__ void __launch_bounds__(kVecBlock) k_dot(const double* __restrict__ a,
         }
     const double tot = block_sum(s, red);
     if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = tot;
+    fin_fused(fin, partial);
 }
 
 // FIRST: the first iteration from x = 0, r = b -- reads b instead of r and does
@@ -484,8 +486,8 @@ template <bool FIRST, int PART = 0>
 __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x, double* __restrict__ r,
                                                          const double* __restrict__ p, const double* __restrict__ q,
                                                          const double* __restrict__ rin, int64_t n, int64_t ld, int nz,
-                                                         const PcgScalars* __restrict__ sc,
-                                                         double* __restrict__ partial) {
+                                                         const PcgScalars* sc, double* __restrict__ partial,
+                                                         FinArgs fin = FinArgs()) {
     __shared__ double red[kVecBlock / 32];
     const double alpha = sc->alpha;
     const VecRange v = vec_range(nz);
@@ -517,17 +519,10 @@ __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x,
     if (PART == 2) return;
     const double tot = block_sum(s, red);
     if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = tot;
+    fin_fused(fin, partial);
 }
 
-__device__ __forceinline__ void scalar_op(PcgScalars* sc, int op, double S) {
-    switch (op) {
-        case kFinPQ: sc->pq = S; sc->alpha = sc->rho / S; break;
-        case kFinRR: sc->rr = S; break;
-        case kFinRZ: sc->rz = S; sc->beta = S / sc->rho; sc->rho = S; break;
-        case kFinRhoInit: sc->rho = S; break;
-        case kFinBB: sc->bb = S; break;
-    }
-}
+__device__ __forceinline__ void scalar_op(PcgScalars* sc, int op, double S) { pcg_scalar_op(sc, op, S); }
 
 // pub: non-null for the scalars the host reads (||b||^2, ||r||^2 with the
 // singular-pivot flag): the updated struct is also written to mapped pinned
@@ -618,7 +613,29 @@ ProfScope::~ProfScope() {
 
 // Sum of the per-block partials into the PCG scalar `op`; across ranks
 // (multi-GPU) the rank-local totals are all-reduced first.
+FinArgs fin_take(const Hierarchy& H) {
+    FinArgs f;
+    if (H.fin_op >= 0) {
+        f.op = H.fin_op;
+        f.sc = H.scal;
+        f.pub = (f.op == kFinBB || f.op == kFinRR) ? H.scal_pub : nullptr;
+        H.fin_fused = true;
+    }
+    H.fin_op = -1;
+    return f;
+}
+
+void fin_begin(const Hierarchy& H, int op) {
+    H.fin_op = (!H.comm || (H.nranks == 1 && !H.force_coll)) ? op : -1;
+    H.fin_fused = false;
+}
+
 void finalize_parts(const Hierarchy& H, int nparts, int op, cudaStream_t s) {
+    H.fin_op = -1;
+    if (H.fin_fused) {                 // the partial-sum launch finalized itself
+        H.fin_fused = false;
+        return;
+    }
     PcgScalars* pub = (op == kFinBB || op == kFinRR) ? H.scal_pub : nullptr;
     if (!H.comm || (H.nranks == 1 && !H.force_coll)) {
         k_finalize<<<1, kFinThreads, 0, s>>>(H.partials, nparts, op, H.scal, pub);
@@ -685,6 +702,7 @@ void launch_apply(const Hierarchy& H, const DevLevel& L, const double* x, double
 void launch_apply_dot(const Hierarchy& H, const DevLevel& L, const double* x, double* y, cudaStream_t s) {
     ProfScope ps(H, kKApply, L.ref, s);
     if (!H.matrix_free && apply_st_supported(H, L)) {
+        fin_begin(H, kFinPQ);
         const int n = launch_apply_st(H, L, x, y, true, s);
         finalize_parts(H, n, kFinPQ, s);
         return;
@@ -736,6 +754,7 @@ void launch_apply_pupdate_dot(const Hierarchy& H, const DevLevel& L, const doubl
                               double* q, cudaStream_t s) {
     ProfScope ps(H, kKApplyP, L.ref, s);
     if (!H.matrix_free && apply_st_supported(H, L)) {
+        fin_begin(H, kFinPQ);
         const int n = launch_apply_pupdate_st(H, L, z, pold, pnew, q, s);
         finalize_parts(H, n, kFinPQ, s);
         return;
@@ -790,7 +809,7 @@ dim3 vec_grid(int64_t n, int nz) {
 
 void launch_dot(const Hierarchy& H, const DevLevel& L, const double* a, const double* b, cudaStream_t s) {
     ProfScope ps(H, kKVector, H.fine_ref, s);
-    k_dot<<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(a, b, L.n, L.ld, H.nz, H.partials);
+    k_dot<<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(a, b, L.n, L.ld, H.nz, H.partials, fin_take(H));
     ++H.launches;
 }
 
@@ -856,7 +875,7 @@ void launch_update_p(const Hierarchy& H, const DevLevel& L, double* p, const dou
 void launch_update_xr(const Hierarchy& H, const DevLevel& L, double* x, const double* p, cudaStream_t s) {
     ProfScope ps(H, kKVector, H.fine_ref, s);
     k_update_xr<false><<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(x, H.r, p, H.q, nullptr, L.n, L.ld, H.nz, H.scal,
-                                                                 H.partials);
+                                                                 H.partials, fin_take(H));
     ++H.launches;
 }
 
@@ -888,8 +907,11 @@ void launch_update_part(const Hierarchy& H, const DevLevel& L, int part, bool fi
                         const double* b, cudaStream_t s) {
     ProfScope ps(H, kKVector, H.fine_ref, s);
     const dim3 g = vec_grid(L.n, H.nz);
-    if (part == 1 && first) k_update_xr<true, 1><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
-    if (part == 1 && !first) k_update_xr<false, 1><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
+    if (part == 1) {
+        const FinArgs f = fin_take(H);
+        if (first) k_update_xr<true, 1><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials, f);
+        else k_update_xr<false, 1><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials, f);
+    }
     if (part == 2 && first) k_update_xr<true, 2><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
     if (part == 2 && !first) k_update_xr<false, 2><<<g, kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal, H.partials);
     if (part == 3) {
@@ -904,7 +926,7 @@ void launch_update_xr_first(const Hierarchy& H, const DevLevel& L, double* x, co
                             cudaStream_t s) {
     ProfScope ps(H, kKVector, H.fine_ref, s);
     k_update_xr<true><<<vec_grid(L.n, H.nz), kVecBlock, 0, s>>>(x, H.r, p, H.q, b, L.n, L.ld, H.nz, H.scal,
-                                                                H.partials);
+                                                                H.partials, fin_take(H));
     ++H.launches;
 }
 

@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                const double* __restrict__ bvec,
                const double* __restrict__ uin, const double* __restrict__ uc, int64_t ldc, double* __restrict__ uout,
                double omega, int ref, unsigned long long* __restrict__ bad, int S, uint32_t tmem_cols, int pf_groups,
-               double* __restrict__ partial) {
+               double* __restrict__ partial, FinArgs fin) {
     extern __shared__ __align__(1024) unsigned char smraw[];
     __shared__ double dred[kThreadsSplit / 32];
     static_assert(!(EH && (ZERO || MF)), "edge store: general stored-band sweeps only");
@@ -1035,6 +1035,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
         partial[blockIdx.x] = t;
     }
     if (warp == 0) ptx::tmem_dealloc(tbase, tmem_cols);
+    if (DOT) fin_fused(fin, partial);   // the last CTA: beta, rho from <r, z> (fused finalize)
 #ifdef HMG_TIMING
     if (threadIdx.x == 0) {
         unsigned long long t;
@@ -1102,7 +1103,7 @@ int launch_st(const Hierarchy& H, const DevLevel& L, const double* b, const doub
     const unsigned grid = (ntiles + rounds - 1) / rounds;
     launch_pdl(H, k_sweep_st<Z, P, M, G, CK, DOT, EH>, dim3(grid), dim3(st_threads(Z, M)), smem, s, maps, V,
                op, L.halo, L.edge, b, uin, uc, ldc, uout, omega, L.ref, &H.scal->bad, S, cols, H.l2_prefetch_groups,
-               H.partials);
+               H.partials, DOT ? fin_take(H) : FinArgs());
     return (int)grid;
 }
 
