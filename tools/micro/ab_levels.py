@@ -9,6 +9,8 @@ import paper_1605_00492_b200.binding as B
 from paper_1605_00492_b200 import build as pb
 
 def lib_for(rev):
+    if rev.endswith(".so"):                                 # a library built elsewhere (e.g. with -D flags)
+        return os.path.abspath(rev)
     if rev == "work":
         return os.path.join(ROOT, "paper_1605_00492_b200", "libhmg.so")
     out = os.path.join(HERE, f"libhmg_{rev}.so")

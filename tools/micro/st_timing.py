@@ -6,16 +6,18 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
 import paper_1605_00492_b200.binding as B
 from paper_1605_00492_b200 import build as pb
 extra = sys.argv[1:]          # e.g. -DHMG_PROBE_NOMOVE
+REFS = [int(r) for r in os.environ.get("REFS", "7,6,5").split(",")]   # one level per process: clean CTA stamps
 lib = os.path.join(HERE, f"libhmg_timing{len(extra)}.so")
 cmd = [pb.NVCC, *pb.ARCH, *[f for f in pb.FLAGS if f not in ("-Xptxas", "-v")], "-DHMG_TIMING", *extra, "-shared",
        *[os.path.join(pb.CSRC, s) for s in pb.SOURCES], "-o", lib, "-ldl"]
-subprocess.check_call(cmd)
+if not os.path.exists(lib) or os.environ.get("REBUILD"):
+    subprocess.check_call(cmd)
 B._LIB_PATH = lib
 import torch
 import hmg_inputs as hi
 from paper_1605_00492_b200 import Hierarchy
 print(" ".join(extra) or "normal")
-for ref in (7, 6, 5):
+for ref in REFS:
     cfg = hi.Config("t", ref, ref - 1 if ref > 5 else 4, 64, 0.001, 1e-5)
     lam, b = hi.make_inputs(cfg)
     g = Hierarchy(ref, cfg.coarsest_ref, 64, 0.001, 1e-5, lam)
@@ -39,6 +41,8 @@ for ref in (7, 6, 5):
     en = [ns[2 * i + 1] for i in range(ncta)]
     t0 = min(st)
     dur = sorted(en[i] - st[i] for i in range(ncta))
+    print("  start offsets (us, sorted):", [round((x - t0) / 1e3, 2) for x in sorted(st)][::max(1, ncta // 16)])
+    print("  end offsets (us, sorted):", [round((x - t0) / 1e3, 2) for x in sorted(en)][::max(1, ncta // 16)])
     print(f"  CTAs {ncta}: start spread {(max(st) - t0) / 1e3:.1f} us, end spread {(max(en) - min(en)) / 1e3:.1f} us, "
           f"kernel span {(max(en) - t0) / 1e3:.1f} us; CTA durations min {dur[0] / 1e3:.1f} median {dur[ncta // 2] / 1e3:.1f} "
           f"max {dur[-1] / 1e3:.1f} us")
