@@ -452,6 +452,38 @@ def test_distributed_path_one_rank(monkeypatch, gather_ref, force):
     o.close()
 
 
+def test_pcg_fused_finalize_deterministic_and_equal_to_unfused(monkeypatch):
+    """The fused finalize (the last CTA of each partial-sum kernel applies the
+    CG scalar update, DESIGN 7 k_update_xr row): two solves on one hierarchy give
+    bitwise the same x and residual history (fixed reduction order, the CTA
+    counter reset after every launch); a one-rank hierarchy through the
+    unfused path (k_finalize + the NCCL all-reduce, HMG_FORCE_COLLECTIVES=1)
+    reaches the same iterate up to the partial sums' order, with the oracle's
+    iteration count on both."""
+    from paper_1605_00492_b200 import nccl_unique_id
+    cfg = hi.Config("fin", 5, 0, 16, 0.01, 1e-3)
+    lam, b = hi.make_inputs(cfg)
+    o = oracle.Hierarchy(5, 0, 16, 0.01, 1e-3, lam)
+    it_o = o.pcg(b)[1]
+    g = Hierarchy(5, 0, 16, 0.01, 1e-3, lam)
+    bd = g.to_device(5, b)
+    runs = []
+    for _ in range(2):
+        x, it, rr, st = g.pcg_solve(bd)
+        assert st == "HMG_OK" and it == it_o
+        runs.append((g.to_host(5, x), g.pcg_history()))
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+    monkeypatch.setenv("HMG_FORCE_COLLECTIVES", "1")
+    gd = Hierarchy(5, 0, 16, 0.01, 1e-3, lam, dist=(0, 1, nccl_unique_id(), 3))
+    xd, itd, rrd, std = gd.pcg_solve(gd.to_device(5, b))
+    assert std == "HMG_OK" and itd == it_o
+    assert rel(gd.to_host(5, xd), runs[0][0]) <= 1e-12
+    assert np.allclose(gd.pcg_history(), runs[0][1], rtol=1e-10, atol=0)
+    g.close()
+    gd.close()
+    o.close()
+
+
 @pytest.mark.parametrize("w2", [1e-4, 1e-290])
 def test_matrix_free_operator(monkeypatch, w2):
     """NEXT-2 matrix-free store (HMG_OPERATOR=free): couplings recomputed from
