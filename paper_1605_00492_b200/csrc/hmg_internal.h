@@ -247,16 +247,19 @@ struct Hierarchy {
     // selects the reference-layout sweep kernel, HMG_SMALL=0 disables the
     // small-level kernel, HMG_L2PF sets the streamed sweep's L2 prefetch
     // distance in ring stages, HMG_TAIL_REF the one-launch coarse tail
-    bool use_tc_sweep = true;
-    bool use_st_sweep = true;
-    bool use_pdl = true;        // HMG_PDL=0: plain stream-ordered launches instead of programmatic dependent launch
-    bool use_st_apply = true;   // HMG_APPLY_ST=0: thread-per-column k_apply_t instead of k_apply_st
-    bool matrix_free = false;   // operator applies recompute the couplings from lam + geometry (NEXT-2)   // HMG_SWEEP_ST=0: non-zero-guess sweeps by k_sweep_tc instead of k_sweep_st
+    // Fixed choices of the measured design (DESIGN.md 7.1a lists the alternatives
+    // that were measured; only the test knobs of README.md are read from the
+    // environment, in build_impl).
+    bool use_tc_sweep = true;   // TMEM/TMA sweeps (k_sweep_tc, k_sweep_st) instead of thread-per-column k_sweep
+    bool use_st_sweep = true;   // non-zero-guess sweeps by the streamed k_sweep_st
+    bool use_pdl = true;        // programmatic dependent launch of the persistent kernels
+    bool use_st_apply = true;   // streamed k_apply_st instead of thread-per-column k_apply_t
+    bool matrix_free = false;   // operator applies recompute the couplings from lam + geometry (NEXT-2; HMG_OPERATOR=free)
     bool use_small_sweep = true;
-    bool edge_h = true;         // HMG_EDGE_H=0: streamed sweeps read the per-cell H bands
+    bool edge_h = true;         // edge-deduplicated couplings on levels of >= edge_min_dofs (HMG_EDGE_MIN_DOFS)
     int64_t edge_min_dofs = 16LL << 20;
-    bool resid_st = true;
-    int apply_ctas_per_sm = 3;  // HMG_APPLY_CTAS=2: two CTAs per SM for the p-update / residual applies too       // HMG_RESID_ST=0: residual + restriction by k_resid_restrict on edge-store levels too   // levels with fewer dofs keep the per-cell bands (HMG_EDGE_MIN_DOFS)
+    bool resid_st = true;       // residual + restriction by the streamed apply on edge-store levels
+    int apply_ctas_per_sm = 3;  // CTAs per SM of the p-update and residual applies
     int l2_prefetch_groups = 0;   // measured: the ring alone is as fast at ref 7 and faster at ref 6
 };
 
