@@ -329,18 +329,27 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
     // x/r update reads b and writes x = 0 + alpha p, r = b - alpha q (the same
     // arithmetic as from x = 0, r = b)
     const double* r0 = b;
-    fin_begin(H, kFinBB);
-    launch_dot(H, F, r0, r0, s);
-    launch_finalize(H, kFinBB, s);
-    HMG_TRY(check_launch());
-    HMG_CUDA(cudaStreamSynchronize(s));
-    const double bn = std::sqrt(H.scal_host->bb);
-    H.res_hist.assign(1, bn == 0.0 ? 0.0 : 1.0);
-    if (bn == 0.0 || maxit == 0) {            // x = x0 = 0 (and r = b: relres 1 when b != 0)
-        HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
-        if (bn == 0.0) return HMG_OK;
-        *relres = 1.0;
-        return fail(HMG_ERR_NOT_CONVERGED, "not converged after 0 iterations (relres 1)");
+    // ||b||: on one rank the first r update sums <b, b> beside <r, r> (fused
+    // finalize), so the solve starts without a dot and a host round trip; b = 0
+    // is then recognised at the first convergence read (x reset to 0)
+    const bool solo = !H.comm || (H.nranks == 1 && !H.force_coll);
+    const bool bb_late = solo && maxit > 0;
+    double bn = -1.0;
+    H.res_hist.clear();
+    if (!bb_late) {
+        fin_begin(H, kFinBB);
+        launch_dot(H, F, r0, r0, s);
+        launch_finalize(H, kFinBB, s);
+        HMG_TRY(check_launch());
+        HMG_CUDA(cudaStreamSynchronize(s));
+        bn = std::sqrt(H.scal_host->bb);
+        H.res_hist.assign(1, bn == 0.0 ? 0.0 : 1.0);
+        if (bn == 0.0 || maxit == 0) {            // x = x0 = 0 (and r = b: relres 1 when b != 0)
+            HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
+            if (bn == 0.0) return HMG_OK;
+            *relres = 1.0;
+            return fail(HMG_ERR_NOT_CONVERGED, "not converged after 0 iterations (relres 1)");
+        }
     }
     // <r, z> after each preconditioner application: fused into its last sweep
     // when that is a streamed fine-level sweep (a fixed-order per-CTA sum, like
@@ -390,7 +399,7 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
             launch_apply_pupdate_dot(H, F, zb, pc, pn, H.q, s);
             pc = pn;
         }
-        fin_begin(H, kFinRR);
+        fin_begin(H, it == 1 && bb_late ? kFinRRBB : kFinRR);
         if (H.defer_x) {
             launch_update_part(H, F, 1, it == 1, x, pc, b, s);   // r = r - alpha q (b - alpha q), partial <r, r>
             H.px.pending = true;
@@ -418,6 +427,18 @@ hmg_status pcg_impl(const Hierarchy& H, const hmg_mg_params* p, int single_sweep
         if (H.scal_host->bad != ~0ull) {
             H.px.pending = false;
             return check_bad(H, s);
+        }
+        if (bn < 0.0) {                            // the first read: ||b|| (bb_late)
+            bn = std::sqrt(H.scal_host->bb);
+            H.res_hist.assign(1, bn == 0.0 ? 0.0 : 1.0);
+            if (bn == 0.0) {                       // b = 0: x = x0 = 0 (the iteration's scalars were 0/0)
+                H.px.pending = false;
+                HMG_CUDA(cudaMemset2DAsync(x, sizeof(double) * F.ld, 0, sizeof(double) * F.n, H.nz, s));
+                HMG_CUDA(cudaStreamSynchronize(s));
+                *iters = 0;
+                *relres = 0.0;
+                return HMG_OK;
+            }
         }
         const double rn = std::sqrt(H.scal_host->rr);
         *iters = it;
@@ -871,7 +892,7 @@ hmg_status build_impl(int fine_ref, int coarsest_ref, int nlayers, double thickn
         BCUDA(cudaMalloc(v, fb));
         BCUDA(cudaMemset(*v, 0, fb));
     }
-    H->npartials = partials_needed(F.n, nlayers) + 148 * 8 + 64;
+    H->npartials = 2 * partials_needed(F.n, nlayers) + 148 * 8 + 64;   // x 2: the first r update's <r, r> and <b, b>
     BCUDA(cudaMalloc(&H->partials, sizeof(double) * H->npartials));
     {
         int lo = 0, hi = 0;

@@ -392,7 +392,9 @@ struct ProfScope {
     ~ProfScope();
 };
 
-enum FinalizeOp { kFinPQ = 0, kFinRR = 1, kFinRZ = 2, kFinRhoInit = 3, kFinBB = 4 };
+// kFinRRBB: the first r update's two sums, <r, r> in partial[0, nb) and <b, b>
+// in partial[nb, 2 nb) (fused finalize only)
+enum FinalizeOp { kFinPQ = 0, kFinRR = 1, kFinRZ = 2, kFinRhoInit = 3, kFinBB = 4, kFinRRBB = 5 };
 
 // Fused finalize (one rank): a kernel that writes one partial sum per CTA into
 // `partial` also applies the PCG scalar update -- its last CTA to finish sums
@@ -433,12 +435,20 @@ __device__ __forceinline__ void fin_fused(const FinArgs& f, const double* partia
     __syncthreads();
     if (!s_last || threadIdx.x >= 32) return;
     __threadfence();
-    double v = 0.0;
+    double v = 0.0, w = 0.0;
     for (unsigned i = threadIdx.x; i < nb; i += 32) v = v + __ldcg(partial + i);
+    if (f.op == kFinRRBB)
+        for (unsigned i = threadIdx.x; i < nb; i += 32) w = w + __ldcg(partial + nb + i);
     for (int off = 16; off > 0; off >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, off);
+    for (int off = 16; off > 0; off >>= 1) w = w + __shfl_down_sync(0xffffffffu, w, off);
     if (threadIdx.x == 0) {
         f.sc->fin_count = 0;
-        pcg_scalar_op(f.sc, f.op, v);
+        if (f.op == kFinRRBB) {
+            f.sc->rr = v;
+            f.sc->bb = w;
+        } else {
+            pcg_scalar_op(f.sc, f.op, v);
+        }
         if (f.pub) *f.pub = *f.sc;
     }
 }

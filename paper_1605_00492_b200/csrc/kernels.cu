@@ -488,10 +488,12 @@ __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x,
                                                          const double* __restrict__ rin, int64_t n, int64_t ld, int nz,
                                                          const PcgScalars* sc, double* __restrict__ partial,
                                                          FinArgs fin = FinArgs()) {
-    __shared__ double red[kVecBlock / 32];
+    __shared__ double red[kVecBlock / 32], red2[kVecBlock / 32];
     const double alpha = sc->alpha;
     const VecRange v = vec_range(nz);
-    double s = 0.0;
+    // FIRST with kFinRRBB: <b, b> as well (the PCG's ||b||, no separate dot)
+    const bool with_bb = FIRST && PART != 2 && fin.op == kFinRRBB;
+    double s = 0.0, sb = 0.0;
     for (int k = v.k0; k < v.k1; ++k)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -507,6 +509,10 @@ __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x,
                 }
                 if (PART != 2) {
                     double2 rr = *reinterpret_cast<const double2*>((FIRST ? rin : r) + i);
+                    if (with_bb) {
+                        sb = sb + rr.x * rr.x;
+                        sb = sb + rr.y * rr.y;
+                    }
                     const double2 qq = *reinterpret_cast<const double2*>(q + i);
                     rr.x = rr.x - alpha * qq.x;
                     rr.y = rr.y - alpha * qq.y;
@@ -519,6 +525,10 @@ __global__ void __launch_bounds__(kVecBlock) k_update_xr(double* __restrict__ x,
     if (PART == 2) return;
     const double tot = block_sum(s, red);
     if (threadIdx.x == 0) partial[blockIdx.y * gridDim.x + blockIdx.x] = tot;
+    if (with_bb) {
+        const double totb = block_sum(sb, red2);
+        if (threadIdx.x == 0) partial[gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = totb;
+    }
     fin_fused(fin, partial);
 }
 
@@ -618,7 +628,7 @@ FinArgs fin_take(const Hierarchy& H) {
     if (H.fin_op >= 0) {
         f.op = H.fin_op;
         f.sc = H.scal;
-        f.pub = (f.op == kFinBB || f.op == kFinRR) ? H.scal_pub : nullptr;
+        f.pub = (f.op == kFinBB || f.op == kFinRR || f.op == kFinRRBB) ? H.scal_pub : nullptr;
         H.fin_fused = true;
     }
     H.fin_op = -1;
