@@ -548,6 +548,11 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
         int btile = 0;
         bool bvalid = false, bodd = false;
         double bdl = 0.0;
+        // the last pass has only back-substitution chunks: there thread 0 releases
+        // a chunk's slot once the NEXT chunk's store is issued (the stores overlap
+        // instead of each waiting for its copy to read the stage)
+        bool blazy = false;
+        int bpend = -1;
         const int mtop_il = nchunks - 1;
         auto bwd_chunk = [&](int m) {
             const int k0 = m * kBack;
@@ -595,9 +600,21 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
                 if (lane == 0) {
                     ptx::tma_store_2d(&maps.uo, btile * kTile, k0, su);
                     ptx::bulk_commit_group();
-                    ptx::bulk_wait_group_read<0>();
-                    ptx::mbar_arrive(&empty[s]);
+                    if (!blazy) {
+                        ptx::bulk_wait_group_read<0>();
+                        ptx::mbar_arrive(&empty[s]);
+                    } else {
+                        if (bpend >= 0) {
+                            ptx::bulk_wait_group_read<1>();
+                            ptx::mbar_arrive(&empty[bpend]);
+                        }
+                        if (m == 0) {
+                            ptx::bulk_wait_group_read<0>();
+                            ptx::mbar_arrive(&empty[s]);
+                        }
+                    }
                 }
+                bpend = (blazy && m != 0) ? s : -1;
                 __syncwarp();
             } else {
                 __syncwarp();
@@ -610,6 +627,7 @@ __global__ void __launch_bounds__(st_threads(ZERO, MF), 2)
             const int tile = (int)blockIdx.x + pass * (int)gridDim.x;
             const bool hasF = pass < ntc, hasB = IL && pass > 0;
             const bool fodd = IL && (pass & 1);
+            blazy = !hasF;
             // TMEM slot of layer k of this pass's tile
             auto fslot = [&](int k) -> uint32_t { return (uint32_t)(fodd ? nzp - 1 - k : k); };
 #ifdef HMG_TIMING
