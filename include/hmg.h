@@ -197,7 +197,8 @@ hmg_status hmg_vcycle(const hmg_hierarchy* h, const hmg_mg_params* p, const doub
  * recursively updated residual.  b, x: device [nlayers][ld_fine].
  *  iters   number of H^ applications performed
  *  relres  final ||r||/||b||
- * Synchronises `stream` once per iteration (8-byte convergence read).
+ * Synchronises `stream` once per iteration (a mapped-memory read of ||r|| -- and,
+ * in the first, of ||b||, which one rank sums in the first r update).
  * Returns HMG_ERR_NOT_CONVERGED (x, iters, relres filled) after maxit. */
 hmg_status hmg_pcg_solve(const hmg_hierarchy* h, const hmg_mg_params* p, const double* b, double* x,
                          double rtol, int maxit, int* iters, double* relres, void* stream);
