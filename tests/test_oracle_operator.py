@@ -149,3 +149,32 @@ def test_ref0_closed_form_spectrum():
                 expect = (1 - (1 - 0.8 * lam_ / tau) ** s) / lam_
                 assert np.allclose(us, expect * v, rtol=0, atol=1e-11 * abs(expect))
     h.close()
+
+
+@pytest.mark.parametrize("omega_n", [0.0, 1.0])
+def test_diagonal_reforms_from_couplings_bitwise(omega_n):
+    """The identity the streamed GPU kernels rely on (DESIGN 7.7): with the
+    stored U_k = -V_up,k and H_j = -(coupling j), the assembled diagonal is,
+    bit for bit, ((((vol - U_{k-1}) - U_k) - H0) - H1) - H2 with vol = area * dz
+    (the k > 0 / k < nz - 1 terms dropped at the ends): V_dn at layer k is the
+    same expression as V_up at layer k - 1, and x + (-y) is x - y in IEEE
+    arithmetic.  Also with buoyancy (reading R24), on every level."""
+    cfg = hi.Config("dref", 3, 0, 9, 0.01, 1e-3)
+    lam, _ = hi.make_inputs(cfg)
+    h = oracle.Hierarchy(cfg.fine_ref, cfg.coarsest_ref, cfg.nz, cfg.thickness, cfg.w2, lam, omega_n=omega_n)
+    dz = cfg.thickness / cfg.nz
+    for ref in range(cfg.coarsest_ref, cfg.fine_ref + 1):
+        L = h.level(ref)
+        U, H = L["U"], L["H"]
+        vol = L["area"] * dz
+        for k in range(cfg.nz):
+            d = vol.copy()
+            if k > 0:
+                d = d - U[k - 1]
+            if k < cfg.nz - 1:
+                d = d - U[k]
+            d = d - H[0, k]
+            d = d - H[1, k]
+            d = d - H[2, k]
+            assert np.array_equal(d, L["D"][k]), f"ref {ref} layer {k}"
+    h.close()
